@@ -1,0 +1,214 @@
+/* geojoin_b200 — C ABI of the B200-native probe side of the adaptive
+ * geospatial join (arXiv 1802.09488).
+ *
+ * This is the drop-in boundary for ONE path of the reference C++ library
+ * `geojoin` (paths below are relative to the reference's proj/ directory):
+ *
+ *   points -> leaf cell id      cell_from_point            src/cell_id.cpp:82-95
+ *   cell id -> tagged entry     Act::probe / probe_batch   src/act.cpp:248-270,310-315
+ *                               detail::ProbeBatchFn       include/geojoin/act.hpp:270-283
+ *   entry -> references         Act::for_each_reference    include/geojoin/act.hpp:169-196
+ *   candidates -> PIP refine    pip_test                   src/geometry.cpp:184-204
+ *   emit / count / stats        run_join, join_exact,      src/join.cpp:88-140,237-247
+ *                               join_approx,
+ *                               join_count_per_polygon,    src/join.cpp:255-285
+ *                               accumulate_probe_stats     src/join.cpp:287-290
+ *
+ * Everything is plain C: pointers and sizes, no C++/torch types.  The index
+ * is built OFFLINE by the reference's own build_index (src/join.cpp:152-235)
+ * or read from its GJX1 bundle file (src/join.cpp:316-381); this library
+ * copies it into one GPU's HBM and runs the probe path there.  There is no CPU
+ * fallback: every entry point needs a CUDA device and fails with
+ * GJ_CUDA_ERROR otherwise.
+ *
+ * Threading: a gj_index is immutable after creation (like the reference's
+ * IndexBundle, include/geojoin/join.hpp:86-88).  A gj_session owns one CUDA
+ * stream plus scratch buffers and must not be used by two threads at once;
+ * any number of sessions may share one index.
+ */
+#ifndef GEOJOIN_B200_H_
+#define GEOJOIN_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(_WIN32)
+#define GJ_API
+#else
+#define GJ_API __attribute__((visibility("default")))
+#endif
+
+/* Status codes.  The reference signals the same conditions with exceptions;
+ * include/geojoin_gpu.hpp re-throws the matching types. */
+typedef enum {
+  GJ_OK = 0,
+  GJ_INVALID_POINT = 1,    /* std::invalid_argument, src/cell_id.cpp:83-85 */
+  GJ_INVALID_ARGUMENT = 2, /* bad handle / size / mode */
+  GJ_CORRUPT_INDEX = 3,    /* CorruptionError: src/act.cpp:141-153,269,654-716 */
+  GJ_UNKNOWN_POLYGON = 4,  /* CorruptionError, src/join.cpp:111-114 */
+  GJ_CUDA_ERROR = 5,
+  GJ_CAPACITY = 6,         /* caller-provided output buffer too small */
+  GJ_IO_ERROR = 7
+} gj_status;
+
+/* Join mode.  GJ_MODE_BUNDLE takes the mode negotiated at build time, as
+ * join_count_per_polygon does (src/join.cpp:257). */
+typedef enum { GJ_MODE_BUNDLE = 0, GJ_MODE_APPROX = 1, GJ_MODE_EXACT = 2 } gj_mode;
+
+typedef struct gj_index gj_index;
+typedef struct gj_session gj_session;
+
+/* Borrowed host views of a built reference index: the fields of
+ * ActProbeView (include/geojoin/act.hpp:108-116), Act::node_count() /
+ * lookup_table() (act.hpp:213-214), ActConfig::k_max (act.hpp:34),
+ * BuildReport::mode (join.hpp:66) and IndexBundle::polygons() flattened to
+ * CSR (join.hpp:90).  Nothing is retained after gj_index_create returns. */
+typedef struct {
+  const uint64_t* arena;      /* node n (1-based) at [(n-1)*256, n*256) */
+  uint64_t node_count;
+  const uint32_t* lut;        /* records [t, id*t, c, id*c] */
+  uint64_t lut_len;
+  uint64_t roots[8];          /* node id per face, 0 = none */
+  uint64_t prefixes[8];
+  uint64_t prefix_bits[8];    /* multiples of 8, <= 56 */
+  int32_t k_max;              /* 8, 16, ..., 56 or 60 */
+  int32_t approx_mode;        /* 1 when the bundle was negotiated approx */
+  uint64_t n_polygons;
+  const uint32_t* polygon_ids;/* bundle order, ids < 2^30 */
+  const uint64_t* vtx_off;    /* n_polygons + 1 */
+  const double* vtx_latlng;   /* (lat, lng) pairs, ring not closed */
+} gj_index_desc;
+
+typedef struct {
+  uint64_t node_count;
+  uint64_t lut_len;
+  uint64_t n_polygons;
+  uint64_t n_ids;             /* length of the id table (count slots) */
+  uint64_t device_bytes;      /* HBM held by this index */
+  int32_t k_max;
+  int32_t approx_mode;
+  int32_t device;
+  int32_t dir_level;          /* grid level resolved by the shared-memory directory */
+  int32_t dir_width;          /* directory window, cells */
+  int32_t dir_height;
+  int32_t dir_dict_len;       /* distinct terminal entries referenced by it */
+  int32_t ids_dense;          /* 1 when id == slot for every polygon */
+} gj_index_info;
+
+/* JoinStats (include/geojoin/join.hpp:77-84), in this order. */
+typedef struct {
+  uint64_t probes;
+  uint64_t pip_tests;
+  uint64_t false_hits;
+  uint64_t solely_true_hits;
+  uint64_t refinement_entered;
+  uint64_t candidate_refs;
+} gj_stats;
+
+GJ_API const char* gj_last_error(void);
+GJ_API int gj_device_count(void);
+
+/* ---- index -------------------------------------------------------------
+ * gj_index_create validates once what the reference checks lazily or at load
+ * time (Act::load / rebuild_derived, src/act.cpp:654-716; check_record,
+ * src/act.cpp:141-153): face block ranges, the node graph being a forest of
+ * depth <= ceil((k_max - prefix_bits)/8), every lookup-table record in
+ * bounds.  After that the kernels run check-free.  `device` < 0 = current. */
+GJ_API int gj_index_create(const gj_index_desc* desc, int device, gj_index** out);
+
+/* Reads the reference's GJX1 bundle file (IndexBundle::save,
+ * src/join.cpp:316-339, wrapping the ACT1 snapshot, src/act.cpp:600-622)
+ * straight into HBM without constructing the reference's Act. */
+GJ_API int gj_index_load_file(const char* gjx1_path, int device, gj_index** out);
+
+GJ_API void gj_index_destroy(gj_index* ix);
+GJ_API int gj_index_get_info(const gj_index* ix, gj_index_info* info);
+
+/* The id table: sorted unique polygon ids (the bundle's plus every id the
+ * trie can emit).  Per-polygon count arrays below are indexed by position
+ * in this table; `ids` must hold info.n_ids values. */
+GJ_API int gj_index_ids(const gj_index* ix, uint32_t* ids);
+
+/* ---- session ------------------------------------------------------------ */
+GJ_API int gj_session_create(gj_index* ix, gj_session** out);
+GJ_API void gj_session_destroy(gj_session* s);
+/* The CUDA stream (cudaStream_t) the session launches on. */
+GJ_API void* gj_session_stream(gj_session* s);
+
+/* Pinned host memory for the *_host entry points (plain cudaHostAlloc). */
+GJ_API void* gj_host_alloc(size_t bytes);
+GJ_API void gj_host_free(void* p);
+
+/* ---- probe only: the ProbeBatchFn contract (act.hpp:270-276) at scale ----
+ * out[i] is bitwise Act::probe(cell_from_point(p_i, k_max/2)); misses are 0.
+ * An invalid point returns GJ_INVALID_POINT with the first bad index. */
+GJ_API int gj_probe_points_host(gj_session* s, const double* latlng, uint64_t n,
+                                uint64_t* out_entries, uint64_t* bad_index);
+/* out[i] is bitwise Act::probe(CellId{raw[i]}) for ids already discretised
+ * at level k_max/2 (all 8 face values accepted, as in the batch kernels). */
+GJ_API int gj_probe_cells_host(gj_session* s, const uint64_t* raw_ids, uint64_t n,
+                               uint64_t* out_entries);
+
+/* ---- streaming join: per-polygon counts (+ first id per point) ----------
+ * ≙ join_count_per_polygon / run_join with a counting emit.
+ *   counts[n_ids]   ADDED to (caller zeroes); slot order = gj_index_ids.
+ *   stats           optional JoinStats, ADDED to.
+ *   out_first_id[n] optional: the first emitted polygon id of point i in the
+ *                   reference's emit order, GJ_NO_MATCH if none; bit 31
+ *                   (GJ_MORE_FLAG) set when the point emitted more pairs —
+ *                   those are appended to the overflow list.
+ *   out_first_id    ... GJ_DEFERRED marks a point whose pairs (zero or more)
+ *                   are ALL in the overflow list: in exact mode a point with
+ *                   candidate references is resolved by the refine kernel.
+ *   overflow        optional (point_index, polygon_id) records for every pair
+ *                   not held inline by out_first_id, sorted by point index and
+ *                   then by the reference's emit order.  overflow->count
+ *                   returns the number produced; GJ_CAPACITY if it exceeds
+ *                   the capacity.
+ * base_index offsets reported point indices (join.cpp:66-67). */
+#define GJ_NO_MATCH 0xFFFFFFFFu
+#define GJ_DEFERRED 0xFFFFFFFEu
+#define GJ_MORE_FLAG 0x80000000u
+
+typedef struct {
+  uint64_t* point_index; /* capacity records */
+  uint32_t* polygon_id;
+  uint64_t capacity;
+  uint64_t count;        /* out */
+} gj_overflow;
+
+GJ_API int gj_join_count_host(gj_session* s, const double* latlng, uint64_t n,
+                              uint64_t base_index, int mode, uint64_t* counts,
+                              gj_stats* stats, uint32_t* out_first_id,
+                              gj_overflow* overflow, uint64_t* bad_index);
+
+/* Same with points already resident in HBM (device pointers; asynchronous on
+ * the session stream unless `sync` != 0).  d_counts/d_stats are device
+ * arrays (u64[n_ids], u64[6]) that are ADDED to; d_first_id may be NULL.
+ * Errors (invalid point, unknown polygon) are latched in the session and
+ * returned by gj_session_sync. */
+GJ_API int gj_join_count_device(gj_session* s, const double* d_latlng, uint64_t n,
+                                int mode, uint64_t* d_counts, uint64_t* d_stats,
+                                uint32_t* d_first_id, int sync);
+GJ_API int gj_session_sync(gj_session* s, uint64_t* bad_index);
+/* Number of kernels this session has launched so far. */
+GJ_API uint64_t gj_session_launches(const gj_session* s);
+
+/* ---- materialised join: ≙ join_exact / join_approx ----------------------
+ * Pairs in the reference's order (ascending point index, references in index
+ * order, join.hpp:125-127) as CSR: row_ptr[n+1], polygon_id[row_ptr[n]].
+ * Two calls: gj_join_pairs_host runs the join and keeps the result in the
+ * session; gj_pairs_copy copies it out. */
+GJ_API int gj_join_pairs_host(gj_session* s, const double* latlng, uint64_t n,
+                              int mode, uint64_t* n_pairs, gj_stats* stats,
+                              uint64_t* bad_index);
+GJ_API int gj_pairs_copy(gj_session* s, uint64_t* row_ptr, uint32_t* polygon_id);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GEOJOIN_B200_H_ */

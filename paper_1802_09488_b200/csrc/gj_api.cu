@@ -1,0 +1,619 @@
+// C ABI of geojoin_b200 (include/geojoin_b200.h): sessions, kernel launch
+// plumbing and the host-buffer pipelines (H2D / kernels / D2H overlapped on
+// three streams).
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <numeric>
+
+#include "gj_host.hpp"
+#include "gj_kernels.cuh"
+
+namespace gj {
+
+const std::string& last_error();
+int create_index(const gj_index_desc& d, int device, gj_index** out);
+int load_index_file(const char* path, int device, gj_index** out);
+
+namespace {
+
+constexpr uint64_t kMaxLaunchPoints = 1ull << 31;  // task/point indices are u32
+constexpr size_t kScratchBudget = 3ull << 30;      // per-chunk task + overflow scratch
+
+size_t align16(size_t v) { return (v + 15) & ~size_t{15}; }
+
+struct SmemPlan {
+  uint32_t dict_off, hist_off, hist_rep;
+  size_t total;
+};
+
+SmemPlan plan_smem(const gj_index& ix) {
+  SmemPlan p{};
+  size_t at = align16(std::max<size_t>(ix.dev.dir.n_table * 4, 16));
+  const size_t limit = ix.smem_optin > 2048 ? ix.smem_optin - 1024 : 0;
+  if (ix.dev.dir.n_dict <= 4096 && at + align16(ix.dev.dir.n_dict * 8) <= limit) {
+    p.dict_off = static_cast<uint32_t>(at);
+    at += align16(ix.dev.dir.n_dict * 8);
+  } else {
+    p.dict_off = 0xFFFFFFFFu;
+  }
+  p.hist_off = static_cast<uint32_t>(at);
+  const size_t room = std::min<size_t>(limit > at ? limit - at : 0, 64 << 10);
+  uint32_t rep = 32;
+  while (rep && static_cast<size_t>(ix.dev.n_ids) * rep * 4 > room) rep >>= 1;
+  p.hist_rep = ix.dev.n_ids ? rep : 0;
+  at += static_cast<size_t>(ix.dev.n_ids) * p.hist_rep * 4;
+  p.total = at;
+  return p;
+}
+
+template <bool kIds, bool kStats>
+int launch_join_variant(gj_session* s, const JoinParams& jp, const SmemPlan& sp) {
+  const gj_index& ix = *s->ix;
+  auto kernel = join_kernel<kIds, kStats>;
+  GJ_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(sp.total)));
+  int occ = 0;
+  GJ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kJoinThreads, sp.total));
+  if (occ < 1) {
+    set_error("join kernel does not fit on an SM");
+    return GJ_CUDA_ERROR;
+  }
+  const uint64_t tile = static_cast<uint64_t>(kJoinThreads) * kPointsPerThread;
+  const uint64_t n_tiles = (jp.n + tile - 1) / tile;
+  const unsigned grid = static_cast<unsigned>(
+      std::max<uint64_t>(1, std::min<uint64_t>(n_tiles, static_cast<uint64_t>(ix.sm_count) * occ)));
+  kernel<<<grid, kJoinThreads, sp.total, s->stream>>>(ix.dev, jp);
+  ++s->launches;
+  GJ_CUDA(cudaGetLastError());
+  return GJ_OK;
+}
+
+int reset_status(gj_session* s, DevStatus* d_status) {
+  static const DevStatus init{kNoBadIndex, 0, 0, 0, 0};
+  GJ_CUDA(cudaMemcpyAsync(d_status, &init, sizeof init, cudaMemcpyHostToDevice, s->stream));
+  return GJ_OK;
+}
+
+struct JoinRequest {
+  const double2* d_pts;
+  uint64_t n;
+  uint64_t base_index;
+  bool exact;
+  bool want_stats;
+  unsigned long long* d_counts;
+  unsigned long long* d_stats;
+  uint32_t* d_first_id;  // null = counts only
+  DevStatus* d_status;
+  uint64_t ovf_cap;      // records available in the session overflow buffers
+  uint64_t task_cap;
+  uint8_t* d_task_pass;  // pairs mode
+};
+
+// Enqueue K1 (+ bucket + K2 in exact mode) on the session stream.
+int enqueue_join(gj_session* s, const JoinRequest& rq) {
+  gj_index& ix = *s->ix;
+  if (rq.n > kMaxLaunchPoints) {
+    set_error("more than 2^31 points in one launch");
+    return GJ_INVALID_ARGUMENT;
+  }
+  const uint32_t n_ids = ix.dev.n_ids;
+  int rc = reset_status(s, rq.d_status);
+  if (rc != GJ_OK) return rc;
+  const SmemPlan sp = plan_smem(ix);
+
+  JoinParams jp{};
+  jp.pts = rq.d_pts;
+  jp.n = rq.n;
+  jp.base_index = rq.base_index;
+  jp.counts = rq.d_counts;
+  jp.stats = rq.want_stats ? rq.d_stats : nullptr;
+  jp.first_id = rq.d_first_id;
+  jp.ovf_point = s->d_ovf_point.as<uint64_t>();
+  jp.ovf_id = s->d_ovf_id.as<uint32_t>();
+  jp.ovf_ord = s->d_ovf_ord.as<uint32_t>();
+  jp.ovf_cap = rq.d_first_id ? rq.ovf_cap : 0;
+  jp.task_point = s->d_task_point.as<uint32_t>();
+  jp.task_slot = s->d_task_slot.as<uint32_t>();
+  jp.task_ord = s->d_task_ord.as<uint32_t>();
+  jp.task_cap = rq.exact ? rq.task_cap : 0;
+  jp.task_per_slot = s->d_task_per_slot.as<uint32_t>();
+  jp.status = rq.d_status;
+  jp.smem_dict_off = sp.dict_off;
+  jp.smem_hist_off = sp.hist_off;
+  jp.hist_rep = sp.hist_rep;
+  jp.exact = rq.exact ? 1 : 0;
+
+  RefinePlan pl{};
+  if (rq.exact) {
+    GJ_CUDA(s->d_task_per_slot.reserve(static_cast<size_t>(n_ids + 1) * 4));
+    GJ_CUDA(s->d_scan_a.reserve(static_cast<size_t>(n_ids + 2) * 4 * 3 + 16));
+    jp.task_per_slot = s->d_task_per_slot.as<uint32_t>();
+    GJ_CUDA(cudaMemsetAsync(jp.task_per_slot, 0, static_cast<size_t>(n_ids + 1) * 4, s->stream));
+    uint32_t* base = s->d_scan_a.as<uint32_t>();
+    pl.task_per_slot = jp.task_per_slot;
+    pl.slot_task_off = base;
+    pl.slot_unit_off = base + (n_ids + 1);
+    pl.slot_cursor = base + 2 * (n_ids + 1);
+    pl.unit_counter = base + 3 * (n_ids + 1);
+  }
+
+  if (rq.d_first_id) {
+    rc = rq.want_stats ? launch_join_variant<true, true>(s, jp, sp) : launch_join_variant<true, false>(s, jp, sp);
+  } else {
+    rc = rq.want_stats ? launch_join_variant<false, true>(s, jp, sp) : launch_join_variant<false, false>(s, jp, sp);
+  }
+  if (rc != GJ_OK) return rc;
+
+  if (rq.exact && n_ids) {
+    plan_units_kernel<<<1, 1024, 0, s->stream>>>(pl, n_ids);
+    const unsigned blocks = static_cast<unsigned>(ix.sm_count) * 8u;
+    scatter_tasks_kernel<<<blocks, 256, 0, s->stream>>>(pl, jp.task_slot, rq.d_status, jp.task_cap,
+                                                        s->d_task_sorted.as<uint32_t>());
+    RefineParams rp{};
+    rp.pts = rq.d_pts;
+    rp.base_index = rq.base_index;
+    rp.task_point = jp.task_point;
+    rp.task_ord = jp.task_ord;
+    rp.task_sorted = s->d_task_sorted.as<uint32_t>();
+    rp.counts = rq.d_counts;
+    rp.ovf_point = jp.ovf_point;
+    rp.ovf_id = jp.ovf_id;
+    rp.ovf_ord = jp.ovf_ord;
+    rp.ovf_cap = jp.ovf_cap;
+    rp.task_pass = rq.d_task_pass;
+    rp.status = rq.d_status;
+    rp.want_ids = rq.d_first_id ? 1 : 0;
+    refine_kernel<<<blocks, kRefineThreads, 0, s->stream>>>(ix.dev, pl, rp);
+    s->launches += 3;
+    GJ_CUDA(cudaGetLastError());
+  }
+  return GJ_OK;
+}
+
+int reserve_tasks(gj_session* s, uint64_t cap) {
+  GJ_CUDA(s->d_task_point.reserve(cap * 4 + 16));
+  GJ_CUDA(s->d_task_slot.reserve(cap * 4 + 16));
+  GJ_CUDA(s->d_task_ord.reserve(cap * 4 + 16));
+  GJ_CUDA(s->d_task_sorted.reserve(cap * 4 + 16));
+  return GJ_OK;
+}
+
+int reserve_overflow(gj_session* s, uint64_t cap) {
+  GJ_CUDA(s->d_ovf_point.reserve(cap * 8 + 16));
+  GJ_CUDA(s->d_ovf_id.reserve(cap * 4 + 16));
+  GJ_CUDA(s->d_ovf_ord.reserve(cap * 4 + 16));
+  return GJ_OK;
+}
+
+int status_to_code(const DevStatus& st, uint64_t* bad_index) {
+  if (st.flags & kErrInvalidPoint) {
+    if (bad_index) *bad_index = st.bad_index;
+    set_error("cell_from_point: invalid coordinate");
+    return GJ_INVALID_POINT;
+  }
+  if (st.flags & kErrUnknownPolygon) {
+    if (bad_index) *bad_index = st.bad_index;
+    set_error("index references unknown polygon");
+    return GJ_UNKNOWN_POLYGON;
+  }
+  if (st.flags & (kErrOverflowCap | kErrTaskCap)) {
+    set_error("device scratch capacity exceeded");
+    return GJ_CAPACITY;
+  }
+  return GJ_OK;
+}
+
+bool resolve_exact(const gj_index& ix, int mode, bool* exact) {
+  switch (mode) {
+    case GJ_MODE_BUNDLE:
+      *exact = !ix.info.approx_mode;
+      return true;
+    case GJ_MODE_APPROX:
+      *exact = false;
+      return true;
+    case GJ_MODE_EXACT:
+      *exact = true;
+      return true;
+    default:
+      return false;
+  }
+}
+
+struct OverflowSink {
+  std::vector<uint64_t> point;
+  std::vector<uint32_t> id, ord;
+};
+
+// The chunked host pipeline shared by gj_join_count_host and
+// gj_join_pairs_host.
+int run_host_join(gj_session* s, const double* latlng, uint64_t n, uint64_t base_index, bool exact,
+                  uint64_t* counts, gj_stats* stats, uint32_t* out_first_id, OverflowSink* sink,
+                  uint64_t* bad_index) {
+  gj_index& ix = *s->ix;
+  GJ_CUDA(cudaSetDevice(ix.device));
+  const uint32_t n_ids = ix.dev.n_ids;
+  const bool want_ids = out_first_id != nullptr;
+  const uint64_t max_cand = std::max<uint64_t>(1, ix.max_cand_refs);
+  const uint64_t max_refs = std::max<uint64_t>(1, ix.max_refs);
+  // Worst-case scratch per point decides the chunk size.
+  uint64_t per_point = 16 + (want_ids ? 4 : 0);
+  if (exact) per_point += max_cand * 17;
+  if (want_ids) per_point += max_refs * 16;
+  uint64_t chunk = std::min<uint64_t>(8ull << 20, std::max<uint64_t>(4096, kScratchBudget / per_point));
+  chunk = std::min<uint64_t>(chunk, std::max<uint64_t>(n, 1));
+  const uint64_t task_cap = exact ? chunk * max_cand : 0;
+  const uint64_t ovf_cap = want_ids ? chunk * max_refs : 0;
+  if (task_cap >= (1ull << 32)) {
+    set_error("candidate task capacity exceeds 2^32");
+    return GJ_INVALID_ARGUMENT;
+  }
+  int rc;
+  if (exact && (rc = reserve_tasks(s, task_cap)) != GJ_OK) return rc;
+  if (want_ids && (rc = reserve_overflow(s, ovf_cap)) != GJ_OK) return rc;
+  for (int b = 0; b < 3; ++b) {
+    GJ_CUDA(s->d_points[b].reserve(chunk * 16));
+    if (want_ids) GJ_CUDA(s->d_first_id[b].reserve(chunk * 4));
+  }
+  GJ_CUDA(s->d_counts.reserve(static_cast<size_t>(n_ids + 1) * 8));
+  GJ_CUDA(s->d_stats.reserve(6 * 8));
+  GJ_CUDA(cudaMemsetAsync(s->d_counts.ptr, 0, static_cast<size_t>(n_ids + 1) * 8, s->stream));
+  GJ_CUDA(cudaMemsetAsync(s->d_stats.ptr, 0, 6 * 8, s->stream));
+
+  // With ids or exact mode every chunk shares the task/overflow scratch, so
+  // a chunk must be fully drained before the next kernel starts; the H2D of
+  // the next chunk still overlaps.  Counting in approx mode pipelines freely.
+  const bool serial = want_ids || exact;
+  const uint64_t n_chunks = (n + chunk - 1) / chunk;
+  int final_rc = GJ_OK;
+  DevStatus worst{kNoBadIndex, 0, 0, 0, 0};
+
+  auto drain = [&](uint64_t c) -> int {  // chunk c finished on the device?
+    const int b = static_cast<int>(c % 3);
+    GJ_CUDA(cudaEventSynchronize(s->ev_done[b]));
+    const DevStatus& st = s->h_status[b];
+    worst.flags |= st.flags;
+    worst.bad_index = std::min(worst.bad_index, st.bad_index);
+    if (sink && st.overflow_count && !(st.flags & kErrOverflowCap)) {
+      const size_t at = sink->point.size();
+      const size_t m = st.overflow_count;
+      sink->point.resize(at + m);
+      sink->id.resize(at + m);
+      sink->ord.resize(at + m);
+      GJ_CUDA(cudaMemcpyAsync(sink->point.data() + at, s->d_ovf_point.ptr, m * 8, cudaMemcpyDeviceToHost, s->stream));
+      GJ_CUDA(cudaMemcpyAsync(sink->id.data() + at, s->d_ovf_id.ptr, m * 4, cudaMemcpyDeviceToHost, s->stream));
+      GJ_CUDA(cudaMemcpyAsync(sink->ord.data() + at, s->d_ovf_ord.ptr, m * 4, cudaMemcpyDeviceToHost, s->stream));
+      GJ_CUDA(cudaStreamSynchronize(s->stream));
+    }
+    return GJ_OK;
+  };
+
+  for (uint64_t c = 0; c < n_chunks; ++c) {
+    const int b = static_cast<int>(c % 3);
+    const uint64_t begin = c * chunk;
+    const uint64_t len = std::min(chunk, n - begin);
+    // buffer b is free once the kernel of chunk c-3 is done (and its ids copied)
+    if (c >= 3) {
+      GJ_CUDA(cudaStreamWaitEvent(s->copy_in, s->ev_done[b], 0));
+      if (!serial && (rc = drain(c - 3)) != GJ_OK) return rc;
+    }
+    GJ_CUDA(cudaMemcpyAsync(s->d_points[b].ptr, latlng + 2 * begin, len * 16, cudaMemcpyHostToDevice, s->copy_in));
+    GJ_CUDA(cudaEventRecord(s->ev_in[b], s->copy_in));
+    if (serial && c >= 1 && (rc = drain(c - 1)) != GJ_OK) return rc;
+    GJ_CUDA(cudaStreamWaitEvent(s->stream, s->ev_in[b], 0));
+    if (want_ids && c >= 3) GJ_CUDA(cudaStreamWaitEvent(s->stream, s->ev_out[b], 0));
+
+    JoinRequest rq{};
+    rq.d_pts = s->d_points[b].as<double2>();
+    rq.n = len;
+    rq.base_index = base_index + begin;
+    rq.exact = exact;
+    rq.want_stats = stats != nullptr;
+    rq.d_counts = s->d_counts.as<unsigned long long>();
+    rq.d_stats = s->d_stats.as<unsigned long long>();
+    rq.d_first_id = want_ids ? s->d_first_id[b].as<uint32_t>() : nullptr;
+    rq.d_status = s->d_status.as<DevStatus>() + b;
+    rq.ovf_cap = ovf_cap;
+    rq.task_cap = task_cap;
+    if ((rc = enqueue_join(s, rq)) != GJ_OK) return rc;
+    GJ_CUDA(cudaMemcpyAsync(&s->h_status[b], rq.d_status, sizeof(DevStatus), cudaMemcpyDeviceToHost, s->stream));
+    GJ_CUDA(cudaEventRecord(s->ev_done[b], s->stream));
+    if (want_ids) {
+      GJ_CUDA(cudaStreamWaitEvent(s->copy_out, s->ev_done[b], 0));
+      GJ_CUDA(cudaMemcpyAsync(out_first_id + begin, s->d_first_id[b].ptr, len * 4, cudaMemcpyDeviceToHost, s->copy_out));
+      GJ_CUDA(cudaEventRecord(s->ev_out[b], s->copy_out));
+    }
+  }
+  // drain what is still in flight
+  const uint64_t first_pending = serial ? (n_chunks ? n_chunks - 1 : 0) : (n_chunks > 3 ? n_chunks - 3 : 0);
+  for (uint64_t c = first_pending; c < n_chunks; ++c) {
+    if ((rc = drain(c)) != GJ_OK) return rc;
+  }
+  GJ_CUDA(cudaStreamSynchronize(s->copy_out));
+  GJ_CUDA(cudaStreamSynchronize(s->stream));
+
+  final_rc = status_to_code(worst, bad_index);
+  if (final_rc != GJ_OK) return final_rc;  // like the reference's throw: no partial results
+
+  std::vector<unsigned long long> h_counts(n_ids + 1);
+  unsigned long long h_stats[6];
+  GJ_CUDA(cudaMemcpy(h_counts.data(), s->d_counts.ptr, static_cast<size_t>(n_ids) * 8, cudaMemcpyDeviceToHost));
+  GJ_CUDA(cudaMemcpy(h_stats, s->d_stats.ptr, sizeof h_stats, cudaMemcpyDeviceToHost));
+  if (counts) {
+    for (uint32_t i = 0; i < n_ids; ++i) counts[i] += h_counts[i];
+  }
+  if (stats) {
+    stats->probes += h_stats[0];
+    stats->pip_tests += h_stats[1];
+    stats->false_hits += h_stats[2];
+    stats->solely_true_hits += h_stats[3];
+    stats->refinement_entered += h_stats[4];
+    stats->candidate_refs += h_stats[5];
+  }
+  return GJ_OK;
+}
+
+}  // namespace
+}  // namespace gj
+
+using namespace gj;
+
+extern "C" {
+
+const char* gj_last_error(void) { return last_error().c_str(); }
+
+int gj_device_count(void) {
+  int n = 0;
+  return cudaGetDeviceCount(&n) == cudaSuccess ? n : 0;
+}
+
+int gj_index_create(const gj_index_desc* desc, int device, gj_index** out) {
+  if (!desc) return GJ_INVALID_ARGUMENT;
+  return create_index(*desc, device, out);
+}
+
+int gj_index_load_file(const char* path, int device, gj_index** out) {
+  return load_index_file(path, device, out);
+}
+
+void gj_index_destroy(gj_index* ix) {
+  if (!ix) return;
+  cudaSetDevice(ix->device);
+  delete ix;
+}
+
+int gj_index_get_info(const gj_index* ix, gj_index_info* info) {
+  if (!ix || !info) return GJ_INVALID_ARGUMENT;
+  *info = ix->info;
+  return GJ_OK;
+}
+
+int gj_index_ids(const gj_index* ix, uint32_t* ids) {
+  if (!ix || (!ids && !ix->ids.empty())) return GJ_INVALID_ARGUMENT;
+  std::copy(ix->ids.begin(), ix->ids.end(), ids);
+  return GJ_OK;
+}
+
+int gj_session_create(gj_index* ix, gj_session** out) {
+  if (!ix || !out) return GJ_INVALID_ARGUMENT;
+  *out = nullptr;
+  GJ_CUDA(cudaSetDevice(ix->device));
+  std::unique_ptr<gj_session> s(new gj_session);
+  s->ix = ix;
+  GJ_CUDA(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+  GJ_CUDA(cudaStreamCreateWithFlags(&s->copy_in, cudaStreamNonBlocking));
+  GJ_CUDA(cudaStreamCreateWithFlags(&s->copy_out, cudaStreamNonBlocking));
+  for (int b = 0; b < 3; ++b) {
+    GJ_CUDA(cudaEventCreateWithFlags(&s->ev_in[b], cudaEventDisableTiming));
+    GJ_CUDA(cudaEventCreateWithFlags(&s->ev_done[b], cudaEventDisableTiming));
+    GJ_CUDA(cudaEventCreateWithFlags(&s->ev_out[b], cudaEventDisableTiming));
+  }
+  GJ_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&s->h_status), 4 * sizeof(DevStatus), cudaHostAllocDefault));
+  GJ_CUDA(s->d_status.reserve(4 * sizeof(DevStatus)));
+  GJ_CUDA(s->d_task_per_slot.reserve(static_cast<size_t>(ix->dev.n_ids + 1) * 4));
+  *out = s.release();
+  return GJ_OK;
+}
+
+void gj_session_destroy(gj_session* s) {
+  if (!s) return;
+  cudaSetDevice(s->ix->device);
+  cudaStreamSynchronize(s->stream);
+  cudaStreamSynchronize(s->copy_in);
+  cudaStreamSynchronize(s->copy_out);
+  for (int b = 0; b < 3; ++b) {
+    if (s->ev_in[b]) cudaEventDestroy(s->ev_in[b]);
+    if (s->ev_done[b]) cudaEventDestroy(s->ev_done[b]);
+    if (s->ev_out[b]) cudaEventDestroy(s->ev_out[b]);
+  }
+  if (s->h_status) cudaFreeHost(s->h_status);
+  cudaStreamDestroy(s->stream);
+  cudaStreamDestroy(s->copy_in);
+  cudaStreamDestroy(s->copy_out);
+  delete s;
+}
+
+void* gj_session_stream(gj_session* s) { return s ? s->stream : nullptr; }
+uint64_t gj_session_launches(const gj_session* s) { return s ? s->launches : 0; }
+
+void* gj_host_alloc(size_t bytes) {
+  void* p = nullptr;
+  if (cudaHostAlloc(&p, bytes ? bytes : 1, cudaHostAllocDefault) != cudaSuccess) {
+    cuda_fail(cudaGetLastError(), "cudaHostAlloc");
+    return nullptr;
+  }
+  return p;
+}
+
+void gj_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
+int gj_probe_points_host(gj_session* s, const double* latlng, uint64_t n, uint64_t* out_entries,
+                         uint64_t* bad_index) {
+  if (!s || (n && (!latlng || !out_entries))) return GJ_INVALID_ARGUMENT;
+  gj_index& ix = *s->ix;
+  GJ_CUDA(cudaSetDevice(ix.device));
+  const uint64_t chunk = 4ull << 20;
+  GJ_CUDA(s->d_points[0].reserve(std::min(chunk, std::max<uint64_t>(n, 1)) * 16));
+  GJ_CUDA(s->d_entries.reserve(std::min(chunk, std::max<uint64_t>(n, 1)) * 8));
+  DevStatus* d_status = s->d_status.as<DevStatus>() + 3;
+  int rc = reset_status(s, d_status);
+  if (rc != GJ_OK) return rc;
+  const size_t smem = align16(std::max<size_t>(ix.dev.dir.n_table * 4, 16));
+  GJ_CUDA(cudaFuncSetAttribute(probe_points_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(smem)));
+  for (uint64_t begin = 0; begin < n; begin += chunk) {
+    const uint64_t len = std::min(chunk, n - begin);
+    GJ_CUDA(cudaMemcpyAsync(s->d_points[0].ptr, latlng + 2 * begin, len * 16, cudaMemcpyHostToDevice, s->stream));
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((len + 255) / 256, ix.sm_count * 4ull));
+    probe_points_kernel<<<grid, 256, smem, s->stream>>>(ix.dev, s->d_points[0].as<double2>(), len, begin,
+                                                        s->d_entries.as<uint64_t>(), d_status);
+    ++s->launches;
+    GJ_CUDA(cudaGetLastError());
+    GJ_CUDA(cudaMemcpyAsync(out_entries + begin, s->d_entries.ptr, len * 8, cudaMemcpyDeviceToHost, s->stream));
+    GJ_CUDA(cudaStreamSynchronize(s->stream));
+  }
+  GJ_CUDA(cudaMemcpyAsync(&s->h_status[3], d_status, sizeof(DevStatus), cudaMemcpyDeviceToHost, s->stream));
+  GJ_CUDA(cudaStreamSynchronize(s->stream));
+  return status_to_code(s->h_status[3], bad_index);
+}
+
+int gj_probe_cells_host(gj_session* s, const uint64_t* raw_ids, uint64_t n, uint64_t* out_entries) {
+  if (!s || (n && (!raw_ids || !out_entries))) return GJ_INVALID_ARGUMENT;
+  gj_index& ix = *s->ix;
+  GJ_CUDA(cudaSetDevice(ix.device));
+  const uint64_t chunk = 4ull << 20;
+  GJ_CUDA(s->d_points[0].reserve(std::min(chunk, std::max<uint64_t>(n, 1)) * 16));
+  GJ_CUDA(s->d_entries.reserve(std::min(chunk, std::max<uint64_t>(n, 1)) * 8));
+  for (uint64_t begin = 0; begin < n; begin += chunk) {
+    const uint64_t len = std::min(chunk, n - begin);
+    GJ_CUDA(cudaMemcpyAsync(s->d_points[0].ptr, raw_ids + begin, len * 8, cudaMemcpyHostToDevice, s->stream));
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((len + 255) / 256, ix.sm_count * 8ull));
+    probe_cells_kernel<<<grid, 256, 0, s->stream>>>(ix.dev, s->d_points[0].as<uint64_t>(), len,
+                                                    s->d_entries.as<uint64_t>());
+    ++s->launches;
+    GJ_CUDA(cudaGetLastError());
+    GJ_CUDA(cudaMemcpyAsync(out_entries + begin, s->d_entries.ptr, len * 8, cudaMemcpyDeviceToHost, s->stream));
+    GJ_CUDA(cudaStreamSynchronize(s->stream));
+  }
+  return GJ_OK;
+}
+
+int gj_join_count_host(gj_session* s, const double* latlng, uint64_t n, uint64_t base_index, int mode,
+                       uint64_t* counts, gj_stats* stats, uint32_t* out_first_id, gj_overflow* overflow,
+                       uint64_t* bad_index) {
+  if (!s || (n && !latlng)) return GJ_INVALID_ARGUMENT;
+  bool exact = false;
+  if (!resolve_exact(*s->ix, mode, &exact)) return GJ_INVALID_ARGUMENT;
+  if (overflow && !out_first_id) {
+    set_error("an overflow list needs out_first_id");
+    return GJ_INVALID_ARGUMENT;
+  }
+  OverflowSink sink;
+  const int rc = run_host_join(s, latlng, n, base_index, exact, counts, stats, out_first_id,
+                               out_first_id ? &sink : nullptr, bad_index);
+  if (rc != GJ_OK) return rc;
+  if (overflow) {
+    const size_t m = sink.point.size();
+    overflow->count = m;
+    if (m > overflow->capacity) {
+      set_error("overflow list larger than the caller's capacity");
+      return GJ_CAPACITY;
+    }
+    std::vector<uint64_t> order(m);
+    std::iota(order.begin(), order.end(), 0);
+    std::sort(order.begin(), order.end(), [&](uint64_t a, uint64_t b) {
+      return sink.point[a] != sink.point[b] ? sink.point[a] < sink.point[b] : sink.ord[a] < sink.ord[b];
+    });
+    for (size_t k = 0; k < m; ++k) {
+      overflow->point_index[k] = sink.point[order[k]];
+      overflow->polygon_id[k] = sink.id[order[k]];
+    }
+  }
+  return GJ_OK;
+}
+
+int gj_join_count_device(gj_session* s, const double* d_latlng, uint64_t n, int mode, uint64_t* d_counts,
+                         uint64_t* d_stats, uint32_t* d_first_id, int sync) {
+  if (!s || (n && !d_latlng) || !d_counts) return GJ_INVALID_ARGUMENT;
+  gj_index& ix = *s->ix;
+  bool exact = false;
+  if (!resolve_exact(ix, mode, &exact)) return GJ_INVALID_ARGUMENT;
+  GJ_CUDA(cudaSetDevice(ix.device));
+  const uint64_t task_cap = exact ? n * std::max<uint64_t>(1, ix.max_cand_refs) : 0;
+  const uint64_t ovf_cap = d_first_id ? n * std::max<uint64_t>(1, ix.max_refs) : 0;
+  if (task_cap >= (1ull << 32)) {
+    set_error("candidate task capacity exceeds 2^32; split the launch");
+    return GJ_INVALID_ARGUMENT;
+  }
+  int rc;
+  if (exact && (rc = reserve_tasks(s, task_cap)) != GJ_OK) return rc;
+  if (d_first_id && (rc = reserve_overflow(s, ovf_cap)) != GJ_OK) return rc;
+  JoinRequest rq{};
+  rq.d_pts = reinterpret_cast<const double2*>(d_latlng);
+  rq.n = n;
+  rq.base_index = 0;
+  rq.exact = exact;
+  rq.want_stats = d_stats != nullptr;
+  rq.d_counts = reinterpret_cast<unsigned long long*>(d_counts);
+  rq.d_stats = reinterpret_cast<unsigned long long*>(d_stats);
+  rq.d_first_id = d_first_id;
+  rq.d_status = s->d_status.as<DevStatus>();
+  rq.ovf_cap = ovf_cap;
+  rq.task_cap = task_cap;
+  if ((rc = enqueue_join(s, rq)) != GJ_OK) return rc;
+  if (sync) return gj_session_sync(s, nullptr);
+  return GJ_OK;
+}
+
+int gj_session_sync(gj_session* s, uint64_t* bad_index) {
+  if (!s) return GJ_INVALID_ARGUMENT;
+  GJ_CUDA(cudaSetDevice(s->ix->device));
+  GJ_CUDA(cudaMemcpyAsync(&s->h_status[0], s->d_status.ptr, sizeof(DevStatus), cudaMemcpyDeviceToHost, s->stream));
+  GJ_CUDA(cudaStreamSynchronize(s->stream));
+  return status_to_code(s->h_status[0], bad_index);
+}
+
+int gj_join_pairs_host(gj_session* s, const double* latlng, uint64_t n, int mode, uint64_t* n_pairs,
+                       gj_stats* stats, uint64_t* bad_index) {
+  if (!s || (n && !latlng)) return GJ_INVALID_ARGUMENT;
+  bool exact = false;
+  if (!resolve_exact(*s->ix, mode, &exact)) return GJ_INVALID_ARGUMENT;
+  std::vector<uint32_t> first(n);
+  OverflowSink sink;
+  s->pairs_row_ptr.clear();
+  s->pairs_id.clear();
+  const int rc = run_host_join(s, latlng, n, 0, exact, nullptr, stats, first.data(), &sink, bad_index);
+  if (rc != GJ_OK) return rc;
+  // Assemble CSR in the reference's order (join.hpp:125-127): per point the
+  // inline first id (ordinal 0 of a non-deferred point) and then its
+  // overflow records by ordinal.
+  const size_t m = sink.point.size();
+  std::vector<uint64_t> order(m);
+  std::iota(order.begin(), order.end(), 0);
+  std::sort(order.begin(), order.end(), [&](uint64_t a, uint64_t b) {
+    return sink.point[a] != sink.point[b] ? sink.point[a] < sink.point[b] : sink.ord[a] < sink.ord[b];
+  });
+  s->pairs_row_ptr.assign(n + 1, 0);
+  s->pairs_id.reserve(n + m);
+  size_t k = 0;
+  for (uint64_t i = 0; i < n; ++i) {
+    s->pairs_row_ptr[i] = s->pairs_id.size();
+    const uint32_t f = first[i];
+    if (f != kNoMatch && f != kDeferred) s->pairs_id.push_back(f & ~kMoreFlag);
+    while (k < m && sink.point[order[k]] == i) s->pairs_id.push_back(sink.id[order[k++]]);
+  }
+  s->pairs_row_ptr[n] = s->pairs_id.size();
+  if (n_pairs) *n_pairs = s->pairs_id.size();
+  return GJ_OK;
+}
+
+int gj_pairs_copy(gj_session* s, uint64_t* row_ptr, uint32_t* polygon_id) {
+  if (!s || !row_ptr) return GJ_INVALID_ARGUMENT;
+  std::copy(s->pairs_row_ptr.begin(), s->pairs_row_ptr.end(), row_ptr);
+  if (polygon_id) std::copy(s->pairs_id.begin(), s->pairs_id.end(), polygon_id);
+  return GJ_OK;
+}
+
+}  // extern "C"

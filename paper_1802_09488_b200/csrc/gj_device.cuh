@@ -1,0 +1,223 @@
+// Device-side data layout and the per-point hot path (sm_100a).
+//
+// Compiled with -fmad=false: the reference's Release build contains no FMA
+// (SURVEY.md T1), and grid_coord / pip_test are rounding-sensitive.  The few
+// floating-point expressions that define results are additionally spelled
+// with explicit round-to-nearest intrinsics so their operation order is the
+// reference's regardless of compiler flags.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace gj {
+
+constexpr int kNodeSlots = 256;             // ActConfig::kFanout, act.hpp:36
+constexpr uint32_t kDirLink = 0x80000000u;  // directory code: continue in arena
+constexpr uint32_t kNoMatch = 0xFFFFFFFFu;
+constexpr uint32_t kDeferred = 0xFFFFFFFEu;
+constexpr uint32_t kMoreFlag = 0x80000000u;
+constexpr uint64_t kNoBadIndex = ~0ull;
+
+// Error bits latched in DevStatus::flags.
+constexpr uint32_t kErrInvalidPoint = 1u;
+constexpr uint32_t kErrUnknownPolygon = 2u;
+constexpr uint32_t kErrOverflowCap = 4u;
+constexpr uint32_t kErrTaskCap = 8u;
+
+// The shared-memory directory: a dense window over grid level `level`
+// (= prefix_level + 4*chunks) holding, per cell, what a trie walk reaches
+// after `chunks` node steps: a miss (0), a terminal entry (index into `dict`)
+// or the node to continue from (kDirLink | node id).  Derived from the arena
+// at index-create time; results are bitwise those of the plain walk.
+struct DevDirectory {
+  const uint32_t* table;  // [height * width], global copy
+  const uint64_t* dict;   // [n_dict], dict[0] == 0
+  uint32_t width, height;
+  uint32_t x0, y0;        // window origin in level-`level` cells
+  uint32_t n_table, n_dict;
+  int32_t shift;          // 30 - level
+  int32_t chunks;         // node steps already resolved
+};
+
+struct DevIndex {
+  const uint64_t* arena;   // payload polygon ids replaced by id-table slots
+  const uint32_t* lut;     // records [t, slot*t, c, slot*c]
+  const uint32_t* ids;     // slot -> polygon id (sorted unique)
+  // closed rings per slot, x = lng, y = lat (geometry.cpp:35); len 0 = the
+  // bundle has no geometry for this id (join.cpp:111-114)
+  const uint64_t* ring_off;
+  const uint32_t* ring_len;
+  const double2* ring_xy;
+  uint64_t roots[8];
+  uint64_t prefixes[8];
+  uint32_t prefix_bits[8];
+  uint32_t n_ids;
+  int32_t k_max;
+  int32_t leaf_level;      // k_max / 2
+  int32_t prefix_level0;   // prefix_bits[0] / 2
+  int32_t ids_dense;
+  DevDirectory dir;
+};
+
+struct DevStatus {
+  unsigned long long bad_index;  // min over offending point indices
+  uint32_t flags;
+  uint32_t pad;
+  unsigned long long overflow_count;
+  unsigned long long task_count;
+};
+
+// ---------------------------------------------------------------------------
+// cellgrid: latlng.hpp:31-34, cell_id.cpp:50-56
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ bool latlng_valid(double lat, double lng) {
+  // finite and inside [-90,90] x [-180,180]; NaN and inf fail the compare
+  return fabs(lat) <= 90.0 && fabs(lng) <= 180.0;
+}
+
+// (value - lo) / span * 2^30 -> clamp below -> truncate -> clamp above, in
+// the reference's operation order with an IEEE division.
+__device__ __forceinline__ uint32_t grid_coord(double value, double lo, double span) {
+  const double scaled = __dmul_rn(__ddiv_rn(__dsub_rn(value, lo), span), 1073741824.0);
+  // __double2uint_rz saturates: negatives (and -0) give 0, like the clamp.
+  const uint32_t cell = __double2uint_rz(scaled);
+  return cell >= (1u << 30) ? (1u << 30) - 1u : cell;
+}
+
+// spread the low 4 bits of v to bit positions 0,2,4,6 (cell_id.cpp:30-37
+// restricted to one trie chunk)
+__device__ __forceinline__ uint32_t spread4(uint32_t v) {
+  v = (v | (v << 2)) & 0x33u;
+  return (v | (v << 1)) & 0x55u;
+}
+
+// Slot of trie chunk `chunk` (8 key bits = 4 grid levels below
+// prefix_level + 4*chunk): y bit above x bit in every pair
+// (cell_id.hpp:30-33).  xl/yl are the 30-bit grid coordinates, already
+// truncated to the leaf level, shifted left by 2.
+__device__ __forceinline__ uint32_t chunk_slot(uint32_t xl, uint32_t yl, int level_above) {
+  const int sh = 28 - level_above;
+  return (spread4((yl >> sh) & 0xFu) << 1) | spread4((xl >> sh) & 0xFu);
+}
+
+__device__ __forceinline__ uint64_t ld_arena(const uint64_t* p) { return __ldg(p); }
+
+// Trie descent from `node`, whose slots resolve the 4 grid levels below
+// `level_above` (act.cpp:258-268).  The index was validated at create time
+// (forest, depth bound), so the loop needs no bound of its own.
+__device__ __forceinline__ uint64_t walk_from(const DevIndex& ix, uint64_t node, int level_above,
+                                              uint32_t xl, uint32_t yl) {
+  for (;;) {
+    const uint32_t slot = chunk_slot(xl, yl, level_above);
+    const uint64_t e = ld_arena(ix.arena + (node - 1) * kNodeSlots + slot);
+    if ((e & 3u) != 0u || e == 0u) return e;
+    node = e >> 2;
+    level_above += 4;
+  }
+}
+
+// One point -> tagged entry, bitwise Act::probe(cell_from_point(p, k_max/2))
+// for face 0 (cell_from_point never sets face bits, cell_id.cpp:89-94).
+__device__ __forceinline__ uint64_t probe_point(const DevIndex& ix, const uint32_t* dir_table,
+                                                const uint64_t* dir_dict, double lat, double lng) {
+  uint32_t x = grid_coord(lng, -180.0, 360.0);
+  uint32_t y = grid_coord(lat, -90.0, 180.0);
+  const DevDirectory& d = ix.dir;
+  const uint32_t cx = (x >> d.shift) - d.x0;
+  const uint32_t cy = (y >> d.shift) - d.y0;
+  if (cx >= d.width || cy >= d.height) return 0;  // outside every indexed cell
+  const uint32_t code = dir_table[cy * d.width + cx];
+  if (code == 0) return 0;
+  if ((code & kDirLink) == 0) return dir_dict[code];
+  // truncate to the leaf level (cell_id.cpp:93-94), left-align to 32 bits
+  const uint32_t keep = ~((1u << (30 - ix.leaf_level)) - 1u);
+  return walk_from(ix, code & ~kDirLink, ix.prefix_level0 + 4 * d.chunks, (x & keep) << 2,
+                   (y & keep) << 2);
+}
+
+// Generic probe of a raw cell id on any face without the directory: the
+// scalar walk of act.cpp:248-270 (used by gj_probe_cells_host, the
+// ProbeBatchFn-shaped test hook).
+__device__ __forceinline__ uint64_t probe_raw(const DevIndex& ix, uint64_t raw) {
+  const uint32_t face = static_cast<uint32_t>(raw >> 61);
+  uint64_t node = ix.roots[face];  // faces 6,7 hold a zero root
+  if (node == 0) return 0;
+  const uint64_t key = (raw ^ (raw & (~raw + 1))) << 3;  // key_of, act.hpp:142-145
+  const uint32_t plen = ix.prefix_bits[face];
+  if (plen != 0 && (key >> (64 - plen)) != ix.prefixes[face]) return 0;
+  int shift = 56 - static_cast<int>(plen);
+  for (;;) {
+    // past the last key bit the reference's lockstep kernels would read
+    // zeros; a validated index never gets there
+    const uint32_t slot = shift >= 0 ? static_cast<uint32_t>(key >> shift) & 0xffu : 0u;
+    const uint64_t e = ld_arena(ix.arena + (node - 1) * kNodeSlots + slot);
+    if ((e & 3u) != 0u || e == 0u) return e;
+    node = e >> 2;
+    shift -= 8;
+  }
+}
+
+// Device arenas carry id-table slots in their payloads; entries handed back
+// to the caller carry the original polygon ids again (act.hpp:55-83).
+__device__ __forceinline__ uint64_t entry_slots_to_ids(const DevIndex& ix, uint64_t e) {
+  if (ix.ids_dense) return e;
+  const uint32_t tag = static_cast<uint32_t>(e) & 3u;
+  if (tag == 1u) {
+    const uint32_t p = static_cast<uint32_t>(e >> 2) & 0x7fffffffu;
+    return (static_cast<uint64_t>((ix.ids[p >> 1] << 1) | (p & 1u)) << 2) | 1u;
+  }
+  if (tag == 2u) {
+    const uint32_t a = static_cast<uint32_t>(e >> 33) & 0x7fffffffu;
+    const uint32_t b = static_cast<uint32_t>(e >> 2) & 0x7fffffffu;
+    return (static_cast<uint64_t>((ix.ids[a >> 1] << 1) | (a & 1u)) << 33) |
+           (static_cast<uint64_t>((ix.ids[b >> 1] << 1) | (b & 1u)) << 2) | 2u;
+  }
+  return e;  // sentinel or lookup-table offset
+}
+
+// ---------------------------------------------------------------------------
+// PIP refine: geometry.cpp:28-29,63-75,184-204
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double point_segment_dist_sq(double px, double py, double ax, double ay,
+                                                        double bx, double by) {
+  const double dx = __dsub_rn(bx, ax);
+  const double dy = __dsub_rn(by, ay);
+  const double len2 = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
+  double t = 0.0;
+  if (len2 > 0.0) {
+    t = __ddiv_rn(__dadd_rn(__dmul_rn(__dsub_rn(px, ax), dx), __dmul_rn(__dsub_rn(py, ay), dy)),
+                  len2);
+    t = (t < 0.0) ? 0.0 : (1.0 < t) ? 1.0 : t;  // std::clamp
+  }
+  const double cx = __dsub_rn(__dadd_rn(ax, __dmul_rn(t, dx)), px);
+  const double cy = __dsub_rn(__dadd_rn(ay, __dmul_rn(t, dy)), py);
+  return __dadd_rn(__dmul_rn(cx, cx), __dmul_rn(cy, cy));
+}
+
+// One edge's contribution to pip_test: bit 0 = on the boundary, bit 1 = the
+// rightward ray crosses it.  The boundary any() and the crossing parity are
+// order-independent, so edges may be evaluated in any order or in parallel;
+// each edge's arithmetic is the reference's.
+__device__ __forceinline__ uint32_t pip_edge(double qx, double qy, double ax, double ay, double bx,
+                                             double by) {
+  const double eps_sq = __dmul_rn(1e-12, 1e-12);  // the product, not 1e-24
+  uint32_t r = 0;
+  // Cheap exact rejection of the boundary test: a point farther than 1e-9
+  // degrees from the edge's bounding box is at distance >= 1e-9 from the
+  // segment, and rounding errors of the distance arithmetic (coordinates
+  // <= 360, ulp <= 5.7e-14) cannot bring cx^2+cy^2 from >= 1e-18 down to
+  // 1e-24, so the reference's comparison is false as well.
+  const double m = 1e-9;
+  const bool near_box = qx >= fmin(ax, bx) - m && qx <= fmax(ax, bx) + m &&
+                        qy >= fmin(ay, by) - m && qy <= fmax(ay, by) + m;
+  if (near_box && point_segment_dist_sq(qx, qy, ax, ay, bx, by) <= eps_sq) r |= 1u;
+  if ((ay > qy) != (by > qy)) {
+    const double x_cross =
+        __dadd_rn(ax, __dmul_rn(__ddiv_rn(__dsub_rn(qy, ay), __dsub_rn(by, ay)), __dsub_rn(bx, ax)));
+    if (qx < x_cross) r |= 2u;
+  }
+  return r;
+}
+
+}  // namespace gj

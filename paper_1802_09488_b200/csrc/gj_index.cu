@@ -1,0 +1,586 @@
+// Index ingestion: validate a built reference index once, derive the id
+// table, closed polygon rings and the shared-memory directory, and copy it
+// all into one GPU's HBM.  Host C++ (the reference's counterpart is host C++
+// too: Act::load / rebuild_derived, src/act.cpp:654-716, and
+// IndexBundle::load, src/join.cpp:341-381).
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <unordered_map>
+
+#include "gj_host.hpp"
+
+namespace gj {
+
+namespace {
+
+thread_local std::string g_error;
+
+constexpr uint64_t kMaxDirEntries = 36864;  // 144 KB of u32 codes
+constexpr uint64_t kMaxPolygonId = (1u << 30) - 1;
+
+struct Bitmap {
+  std::vector<uint64_t> w;
+  void ensure(uint64_t bit) {
+    const uint64_t need = bit / 64 + 1;
+    if (w.size() < need) w.resize(std::max<uint64_t>(need, w.size() * 2), 0);
+  }
+  bool test_and_set(uint64_t bit) {
+    ensure(bit);
+    const uint64_t m = 1ull << (bit & 63);
+    const bool was = (w[bit >> 6] & m) != 0;
+    w[bit >> 6] |= m;
+    return was;
+  }
+  void set(uint64_t bit) { test_and_set(bit); }
+};
+
+// De-interleave `levels` quadrant pairs (y bit above x bit,
+// cell_id.hpp:30-33) from the low 2*levels bits of v.
+void unzip_pairs(uint64_t v, int levels, uint32_t* x, uint32_t* y) {
+  uint32_t xx = 0, yy = 0;
+  for (int i = levels - 1; i >= 0; --i) {
+    const uint64_t pair = (v >> (2 * i)) & 3;
+    xx = (xx << 1) | static_cast<uint32_t>(pair & 1);
+    yy = (yy << 1) | static_cast<uint32_t>(pair >> 1);
+  }
+  *x = xx;
+  *y = yy;
+}
+
+struct Cell {
+  uint64_t node_or_entry;
+  uint32_t x, y;
+  int32_t step;  // terminals: grid level = prefix_level + 4*step
+};
+
+struct Box {
+  uint64_t x_lo = ~0ull, y_lo = ~0ull, x_hi = 0, y_hi = 0;
+  bool empty() const { return x_lo == ~0ull; }
+  void add(uint64_t xl, uint64_t yl, uint64_t xh, uint64_t yh) {
+    x_lo = std::min(x_lo, xl);
+    y_lo = std::min(y_lo, yl);
+    x_hi = std::max(x_hi, xh);
+    y_hi = std::max(y_hi, yh);
+  }
+  uint64_t area() const { return empty() ? 0 : (x_hi - x_lo + 1) * (y_hi - y_lo + 1); }
+};
+
+bool record_in_bounds(const gj_index_desc& d, uint64_t off) {  // act.cpp:141-153
+  if (off >= d.lut_len) return false;
+  const uint64_t t = d.lut[off];
+  if (off + 1 + t >= d.lut_len) return false;
+  const uint64_t c = d.lut[off + 1 + t];
+  return off + 2 + t + c <= d.lut_len;
+}
+
+struct Analysis {
+  std::vector<uint32_t> ids;
+  HostDirectory dir;
+  uint64_t max_refs = 0;       // most references behind one entry
+  uint64_t max_cand_refs = 0;  // most candidate references behind one entry
+};
+
+// One breadth-first pass per face: forest check, depth bound, record bounds,
+// id collection; for face 0 the first levels also feed the directory.
+int analyse(const gj_index_desc& d, Analysis* out) {
+  const bool k_ok = d.k_max >= 8 && d.k_max <= 60 && (d.k_max % 8 == 0 || d.k_max == 60);
+  if (!k_ok) {  // validate_act_config, act.cpp:38-42
+    set_error("k_max must be one of 8, 16, ..., 56, 60");
+    return GJ_CORRUPT_INDEX;
+  }
+  if (d.node_count > (1ull << 32) || d.lut_len > 0x7fffffffull) {
+    set_error("index header sizes out of range");
+    return GJ_CORRUPT_INDEX;
+  }
+  if (d.node_count >= (1ull << 31)) {
+    set_error("arenas of 2^31 nodes or more are not supported by the directory encoding");
+    return GJ_INVALID_ARGUMENT;
+  }
+  Bitmap visited, id_seen, record_seen;
+  visited.ensure(d.node_count + 1);
+  for (uint64_t p = 0; p < d.n_polygons; ++p) {
+    if (d.polygon_ids[p] > kMaxPolygonId) {
+      set_error("polygon id above 2^30 - 1");
+      return GJ_INVALID_ARGUMENT;
+    }
+    id_seen.set(d.polygon_ids[p]);
+  }
+  auto see_payload = [&](uint32_t payload) -> uint64_t {
+    id_seen.set(payload >> 1);
+    return (payload & 1u) ? 0 : 1;  // candidate?
+  };
+  auto check_terminal = [&](uint64_t e) -> bool {
+    switch (e & 3) {
+      case 1:
+        out->max_cand_refs = std::max(out->max_cand_refs, see_payload(static_cast<uint32_t>(e >> 2) & 0x7fffffffu));
+        out->max_refs = std::max<uint64_t>(out->max_refs, 1);
+        return true;
+      case 2:
+        out->max_cand_refs = std::max(out->max_cand_refs,
+                                      see_payload(static_cast<uint32_t>(e >> 33) & 0x7fffffffu) +
+                                          see_payload(static_cast<uint32_t>(e >> 2) & 0x7fffffffu));
+        out->max_refs = std::max<uint64_t>(out->max_refs, 2);
+        return true;
+      default: {
+        const uint64_t off = (e >> 2) & 0x7fffffffu;
+        if (!record_in_bounds(d, off)) return false;
+        if (!record_seen.test_and_set(off)) {
+          const uint32_t t = d.lut[off];
+          const uint32_t c = d.lut[off + 1 + t];
+          out->max_refs = std::max<uint64_t>(out->max_refs, static_cast<uint64_t>(t) + c);
+          out->max_cand_refs = std::max<uint64_t>(out->max_cand_refs, c);
+          for (uint32_t i = 0; i < t + c; ++i) {
+            const uint32_t id = d.lut[off + 1 + i + (i >= t ? 1 : 0)];
+            if (id > kMaxPolygonId) return false;  // kMaxPolygonId, geometry.hpp:25
+            id_seen.set(id);
+          }
+        }
+        return true;
+      }
+    }
+  };
+
+  HostDirectory& dir = out->dir;
+  for (int face = 0; face < 6; ++face) {
+    const uint64_t root = d.roots[face];
+    const uint64_t plen = d.prefix_bits[face];
+    if (root > d.node_count || plen > 56 || plen % 8 != 0) {  // act.cpp:644-647
+      set_error("face block out of range");
+      return GJ_CORRUPT_INDEX;
+    }
+    if (root == 0) continue;
+    const int max_chunks = (d.k_max - static_cast<int>(plen) + 7) / 8;
+    if (max_chunks < 1) {
+      set_error("face prefix leaves no key bits below the root");
+      return GJ_CORRUPT_INDEX;
+    }
+    const int prefix_level = static_cast<int>(plen) / 2;
+
+    // Directory bookkeeping (face 0 only; cell_from_point never leaves it).
+    bool track = face == 0;
+    std::vector<Cell> terminals;      // steps <= chosen depth
+    std::vector<Cell> frontier;       // nodes at the current depth, with cells
+    std::vector<Cell> best_links;     // frontier at the chosen depth
+    size_t best_terminals = 0;
+    Box best_box;
+    int best_chunks = 0;
+
+    uint32_t px = 0, py = 0;
+    unzip_pairs(d.prefixes[face], prefix_level, &px, &py);
+    frontier.push_back(Cell{root, px, py, 0});
+    for (int depth = 0; !frontier.empty(); ++depth) {
+      if (depth >= max_chunks) {  // act.cpp:269 / act.cpp:693-696
+        set_error("trie path longer than the maximum key length");
+        return GJ_CORRUPT_INDEX;
+      }
+      std::vector<Cell> next;
+      for (const Cell& c : frontier) {
+        const uint64_t node = c.node_or_entry;
+        if (node == 0 || node > d.node_count || visited.test_and_set(node)) {
+          set_error("node graph is not a forest");  // act.cpp:667-669
+          return GJ_CORRUPT_INDEX;
+        }
+        const uint64_t* slots = d.arena + (node - 1) * kNodeSlots;
+        for (uint32_t s = 0; s < kNodeSlots; ++s) {
+          const uint64_t e = slots[s];
+          if (e == 0) continue;
+          uint32_t sx = 0, sy = 0;
+          if (track) unzip_pairs(s, 4, &sx, &sy);
+          const Cell child{(e & 3) == 0 ? e >> 2 : e, (c.x << 4) | sx, (c.y << 4) | sy, depth + 1};
+          if ((e & 3) == 0) {
+            next.push_back(child);
+          } else {
+            if (!check_terminal(e)) {
+              set_error("lookup-table record out of bounds or polygon id above 2^30 - 1");
+              return GJ_CORRUPT_INDEX;
+            }
+            if (track) terminals.push_back(child);
+          }
+        }
+      }
+      if (track) {
+        // Window at `depth + 1` node steps: every terminal so far (scaled to
+        // this level) plus the cells of the nodes still to be expanded.
+        Box box;
+        for (const Cell& t : terminals) {
+          const int s = 4 * (depth + 1 - t.step);
+          box.add(static_cast<uint64_t>(t.x) << s, static_cast<uint64_t>(t.y) << s,
+                  ((static_cast<uint64_t>(t.x) + 1) << s) - 1, ((static_cast<uint64_t>(t.y) + 1) << s) - 1);
+        }
+        for (const Cell& l : next) box.add(l.x, l.y, l.x, l.y);
+        if (box.area() <= kMaxDirEntries) {
+          best_chunks = depth + 1;
+          best_box = box;
+          best_links = next;
+          best_terminals = terminals.size();
+        } else {
+          track = false;  // deeper windows only grow
+          terminals.resize(best_terminals);
+          terminals.shrink_to_fit();
+        }
+      }
+      frontier.swap(next);
+    }
+
+    if (face == 0 && best_chunks > 0 && !best_box.empty()) {
+      dir.chunks = best_chunks;
+      dir.level = prefix_level + 4 * best_chunks;
+      dir.x0 = static_cast<uint32_t>(best_box.x_lo);
+      dir.y0 = static_cast<uint32_t>(best_box.y_lo);
+      dir.width = static_cast<uint32_t>(best_box.x_hi - best_box.x_lo + 1);
+      dir.height = static_cast<uint32_t>(best_box.y_hi - best_box.y_lo + 1);
+      dir.table.assign(static_cast<size_t>(dir.width) * dir.height, 0u);
+      dir.dict.assign(1, 0ull);
+      std::unordered_map<uint64_t, uint32_t> code_of;
+      terminals.resize(best_terminals);
+      for (const Cell& t : terminals) {
+        auto it = code_of.find(t.node_or_entry);
+        if (it == code_of.end()) {
+          it = code_of.emplace(t.node_or_entry, static_cast<uint32_t>(dir.dict.size())).first;
+          dir.dict.push_back(t.node_or_entry);
+        }
+        const int s = 4 * (best_chunks - t.step);
+        const uint64_t bx = (static_cast<uint64_t>(t.x) << s) - dir.x0;
+        const uint64_t by = (static_cast<uint64_t>(t.y) << s) - dir.y0;
+        const uint64_t side = 1ull << s;
+        for (uint64_t yy = 0; yy < side; ++yy) {
+          uint32_t* row = dir.table.data() + (by + yy) * dir.width + bx;
+          std::fill(row, row + side, it->second);
+        }
+      }
+      for (const Cell& l : best_links) {
+        dir.table[static_cast<size_t>(l.y - dir.y0) * dir.width + (l.x - dir.x0)] =
+            kDirLink | static_cast<uint32_t>(l.node_or_entry);
+      }
+    }
+  }
+  if (dir.level > 30) {
+    set_error("directory level out of range");
+    return GJ_CORRUPT_INDEX;
+  }
+
+  // id table: sorted unique ids
+  for (uint64_t wi = 0; wi < id_seen.w.size(); ++wi) {
+    uint64_t bits = id_seen.w[wi];
+    while (bits) {
+      const int b = __builtin_ctzll(bits);
+      out->ids.push_back(static_cast<uint32_t>(wi * 64 + b));
+      bits &= bits - 1;
+    }
+  }
+  return GJ_OK;
+}
+
+template <typename T>
+int upload(DeviceBuffer& buf, const T* src, size_t count, size_t* total) {
+  const size_t bytes = std::max<size_t>(count * sizeof(T), 16);
+  GJ_CUDA(buf.reserve(bytes));
+  if (count) GJ_CUDA(cudaMemcpy(buf.ptr, src, count * sizeof(T), cudaMemcpyHostToDevice));
+  *total += bytes;
+  return GJ_OK;
+}
+
+}  // namespace
+
+void set_error(const std::string& msg) { g_error = msg; }
+const std::string& last_error() { return g_error; }
+
+int cuda_fail(cudaError_t e, const char* what) {
+  set_error(std::string(what) + ": " + cudaGetErrorString(e));
+  return GJ_CUDA_ERROR;
+}
+
+int create_index(const gj_index_desc& d, int device, gj_index** out) {
+  if (!out) return GJ_INVALID_ARGUMENT;
+  *out = nullptr;
+  if ((d.node_count && !d.arena) || (d.lut_len && !d.lut) ||
+      (d.n_polygons && (!d.polygon_ids || !d.vtx_off || !d.vtx_latlng))) {
+    set_error("null array in index description");
+    return GJ_INVALID_ARGUMENT;
+  }
+  int n_dev = 0;
+  if (cudaGetDeviceCount(&n_dev) != cudaSuccess || n_dev == 0) {
+    set_error("no CUDA device: geojoin_b200 has no CPU fallback");
+    return GJ_CUDA_ERROR;
+  }
+  if (device < 0) GJ_CUDA(cudaGetDevice(&device));
+  GJ_CUDA(cudaSetDevice(device));
+
+  Analysis an;
+  int rc = analyse(d, &an);
+  if (rc != GJ_OK) return rc;
+
+  std::unique_ptr<gj_index> ix(new gj_index);
+  ix->device = device;
+  ix->ids = std::move(an.ids);
+  ix->max_refs = an.max_refs;
+  ix->max_cand_refs = an.max_cand_refs;
+  const size_t n_ids = ix->ids.size();
+  bool dense = true;
+  for (size_t i = 0; i < n_ids; ++i) dense = dense && ix->ids[i] == i;
+
+  // Closed rings per id-table slot; the first polygon carrying an id wins
+  // (unordered_map::emplace keeps the first, join.cpp:144-150).
+  std::vector<uint64_t> ring_off(n_ids + 1, 0);
+  std::vector<uint32_t> ring_len(n_ids, 0);
+  std::vector<int64_t> first_poly(n_ids, -1);
+  for (uint64_t p = 0; p < d.n_polygons; ++p) {
+    const size_t slot =
+        std::lower_bound(ix->ids.begin(), ix->ids.end(), d.polygon_ids[p]) - ix->ids.begin();
+    if (first_poly[slot] < 0) first_poly[slot] = static_cast<int64_t>(p);
+  }
+  uint64_t total = 0;
+  for (size_t s = 0; s < n_ids; ++s) {
+    ring_off[s] = total;
+    if (first_poly[s] >= 0) {
+      const uint64_t nv = d.vtx_off[first_poly[s] + 1] - d.vtx_off[first_poly[s]];
+      if (nv > (1ull << 24)) {  // join.cpp:368-370
+        set_error("polygon vertex count out of range");
+        return GJ_CORRUPT_INDEX;
+      }
+      ring_len[s] = static_cast<uint32_t>(nv);
+      total += nv ? nv + 1 : 0;
+    }
+  }
+  ring_off[n_ids] = total;
+  std::vector<double2> ring_xy(total);
+  for (size_t s = 0; s < n_ids; ++s) {
+    if (ring_len[s] == 0) continue;
+    const uint64_t b = d.vtx_off[first_poly[s]];
+    double2* dst = ring_xy.data() + ring_off[s];
+    for (uint32_t v = 0; v <= ring_len[s]; ++v) {
+      const uint64_t src = b + (v == ring_len[s] ? 0 : v);  // v[(i + 1) % n], geometry.cpp:189
+      dst[v] = make_double2(d.vtx_latlng[2 * src + 1], d.vtx_latlng[2 * src]);  // x = lng, y = lat
+    }
+  }
+
+  size_t bytes = 0;
+  if ((rc = upload(ix->d_arena, d.arena, d.node_count * kNodeSlots, &bytes)) != GJ_OK) return rc;
+  if ((rc = upload(ix->d_lut, d.lut, d.lut_len, &bytes)) != GJ_OK) return rc;
+  if ((rc = upload(ix->d_ids, ix->ids.data(), n_ids, &bytes)) != GJ_OK) return rc;
+  if ((rc = upload(ix->d_ring_off, ring_off.data(), ring_off.size(), &bytes)) != GJ_OK) return rc;
+  if ((rc = upload(ix->d_ring_len, ring_len.data(), ring_len.size(), &bytes)) != GJ_OK) return rc;
+  if ((rc = upload(ix->d_ring_xy, ring_xy.data(), ring_xy.size(), &bytes)) != GJ_OK) return rc;
+  if ((rc = upload(ix->d_dir_table, an.dir.table.data(), an.dir.table.size(), &bytes)) != GJ_OK) return rc;
+  if ((rc = upload(ix->d_dir_dict, an.dir.dict.data(), an.dir.dict.size(), &bytes)) != GJ_OK) return rc;
+
+  DevIndex& dv = ix->dev;
+  dv.arena = ix->d_arena.as<uint64_t>();
+  dv.lut = ix->d_lut.as<uint32_t>();
+  dv.ids = ix->d_ids.as<uint32_t>();
+  dv.ring_off = ix->d_ring_off.as<uint64_t>();
+  dv.ring_len = ix->d_ring_len.as<uint32_t>();
+  dv.ring_xy = ix->d_ring_xy.as<double2>();
+  for (int f = 0; f < 8; ++f) {
+    dv.roots[f] = f < 6 ? d.roots[f] : 0;  // refresh_view, act.cpp:373-383
+    dv.prefixes[f] = f < 6 ? d.prefixes[f] : 0;
+    dv.prefix_bits[f] = f < 6 ? static_cast<uint32_t>(d.prefix_bits[f]) : 0;
+  }
+  dv.n_ids = static_cast<uint32_t>(n_ids);
+  dv.k_max = d.k_max;
+  dv.leaf_level = d.k_max / 2;
+  dv.prefix_level0 = static_cast<int>(d.prefix_bits[0]) / 2;
+  dv.ids_dense = dense ? 1 : 0;
+  dv.dir.table = ix->d_dir_table.as<uint32_t>();
+  dv.dir.dict = ix->d_dir_dict.as<uint64_t>();
+  dv.dir.width = an.dir.width;
+  dv.dir.height = an.dir.height;
+  dv.dir.x0 = an.dir.x0;
+  dv.dir.y0 = an.dir.y0;
+  dv.dir.n_table = static_cast<uint32_t>(an.dir.table.size());
+  dv.dir.n_dict = static_cast<uint32_t>(an.dir.dict.size());
+  dv.dir.shift = 30 - an.dir.level;
+  dv.dir.chunks = an.dir.chunks;
+
+  cudaDeviceProp prop{};
+  GJ_CUDA(cudaGetDeviceProperties(&prop, device));
+  ix->sm_count = prop.multiProcessorCount;
+  ix->smem_optin = prop.sharedMemPerBlockOptin;
+
+  gj_index_info& info = ix->info;
+  info.node_count = d.node_count;
+  info.lut_len = d.lut_len;
+  info.n_polygons = d.n_polygons;
+  info.n_ids = n_ids;
+  info.device_bytes = bytes;
+  info.k_max = d.k_max;
+  info.approx_mode = d.approx_mode ? 1 : 0;
+  info.device = device;
+  info.dir_level = an.dir.level;
+  info.dir_width = static_cast<int32_t>(an.dir.width);
+  info.dir_height = static_cast<int32_t>(an.dir.height);
+  info.dir_dict_len = static_cast<int32_t>(an.dir.dict.size());
+  info.ids_dense = dense ? 1 : 0;
+  *out = ix.release();
+  return GJ_OK;
+}
+
+// ---------------------------------------------------------------------------
+// GJX1 / ACT1 reader (join.cpp:316-381, act.cpp:600-652): little-endian,
+// raw arena and lookup table — mapped and copied straight to the device.
+// ---------------------------------------------------------------------------
+namespace {
+
+struct Cursor {
+  const uint8_t* p;
+  const uint8_t* end;
+  bool ok = true;
+  bool take(void* dst, size_t n) {
+    if (!ok || static_cast<size_t>(end - p) < n) {
+      ok = false;
+      return false;
+    }
+    std::memcpy(dst, p, n);
+    p += n;
+    return true;
+  }
+  uint32_t u32() {
+    uint32_t v = 0;
+    take(&v, 4);
+    return v;
+  }
+  uint64_t u64() {
+    uint64_t v = 0;
+    take(&v, 8);
+    return v;
+  }
+  double f64() {
+    double v = 0;
+    take(&v, 8);
+    return v;
+  }
+  const uint8_t* span(size_t n) {
+    if (!ok || static_cast<size_t>(end - p) < n) {
+      ok = false;
+      return nullptr;
+    }
+    const uint8_t* s = p;
+    p += n;
+    return s;
+  }
+};
+
+}  // namespace
+
+int load_index_file(const char* path, int device, gj_index** out) {
+  if (!path || !out) return GJ_INVALID_ARGUMENT;
+  *out = nullptr;
+  const int fd = ::open(path, O_RDONLY);
+  if (fd < 0) {
+    set_error(std::string("cannot open ") + path);
+    return GJ_IO_ERROR;
+  }
+  struct stat st{};
+  if (fstat(fd, &st) != 0 || st.st_size < 8) {
+    ::close(fd);
+    set_error("not a geojoin index file");
+    return GJ_CORRUPT_INDEX;
+  }
+  const size_t size = static_cast<size_t>(st.st_size);
+  void* map = mmap(nullptr, size, PROT_READ, MAP_PRIVATE, fd, 0);
+  ::close(fd);
+  if (map == MAP_FAILED) {
+    set_error("mmap failed");
+    return GJ_IO_ERROR;
+  }
+  struct Unmap {
+    void* m;
+    size_t n;
+    ~Unmap() { munmap(m, n); }
+  } unmap{map, size};
+
+  Cursor c{static_cast<const uint8_t*>(map), static_cast<const uint8_t*>(map) + size};
+  char magic[4];
+  if (!c.take(magic, 4) || std::memcmp(magic, "GJX1", 4) != 0) {
+    set_error("not a geojoin index file");
+    return GJ_CORRUPT_INDEX;
+  }
+  if (c.u32() != 1) {
+    set_error("unsupported index version");
+    return GJ_CORRUPT_INDEX;
+  }
+  gj_index_desc d{};
+  d.approx_mode = c.u32() != 0;
+  c.u32();  // precision_achieved
+  c.f64();  // precision_m
+  c.f64();  // achieved_precision_m
+  c.u64();  // memory budget
+  for (int i = 0; i < 4; ++i) c.u32();  // covering config
+  if (!c.take(magic, 4) || std::memcmp(magic, "ACT1", 4) != 0) {
+    set_error("not an ACT1 index snapshot");
+    return GJ_CORRUPT_INDEX;
+  }
+  d.k_max = static_cast<int32_t>(c.u32());
+  d.node_count = c.u64();
+  d.lut_len = c.u64();
+  if (!c.ok || d.node_count > (1ull << 32) || d.lut_len > 0x7fffffffull) {
+    set_error("snapshot header sizes out of range");
+    return GJ_CORRUPT_INDEX;
+  }
+  for (int f = 0; f < 6; ++f) {
+    d.roots[f] = c.u64();
+    d.prefixes[f] = c.u64();
+    d.prefix_bits[f] = c.u32();
+  }
+  const uint8_t* arena = c.span(d.node_count * kNodeSlots * 8);
+  const uint8_t* lut = c.span(d.lut_len * 4);
+  if (!c.ok) {
+    set_error("truncated index snapshot");
+    return GJ_CORRUPT_INDEX;
+  }
+  // The header is 200 bytes, so the arena is 8-byte aligned inside the map.
+  std::vector<uint64_t> arena_copy;
+  if (reinterpret_cast<uintptr_t>(arena) % 8 != 0) {
+    arena_copy.resize(d.node_count * kNodeSlots);
+    std::memcpy(arena_copy.data(), arena, arena_copy.size() * 8);
+    d.arena = arena_copy.data();
+  } else {
+    d.arena = reinterpret_cast<const uint64_t*>(arena);
+  }
+  std::vector<uint32_t> lut_copy;
+  if (reinterpret_cast<uintptr_t>(lut) % 4 != 0) {
+    lut_copy.resize(d.lut_len);
+    std::memcpy(lut_copy.data(), lut, lut_copy.size() * 4);
+    d.lut = lut_copy.data();
+  } else {
+    d.lut = reinterpret_cast<const uint32_t*>(lut);
+  }
+  const uint64_t n_poly = c.u64();
+  if (!c.ok || n_poly > (1ull << 30)) {
+    set_error("index polygon count out of range");
+    return GJ_CORRUPT_INDEX;
+  }
+  std::vector<uint32_t> ids(n_poly);
+  std::vector<uint64_t> off(n_poly + 1, 0);
+  std::vector<double> latlng;
+  for (uint64_t p = 0; p < n_poly; ++p) {
+    ids[p] = c.u32();
+    const uint64_t nv = c.u64();
+    if (!c.ok || nv > (1ull << 24)) {
+      set_error("polygon vertex count out of range");
+      return GJ_CORRUPT_INDEX;
+    }
+    const uint8_t* v = c.span(nv * 16);
+    if (!c.ok) {
+      set_error("truncated index file");
+      return GJ_CORRUPT_INDEX;
+    }
+    const size_t at = latlng.size();
+    latlng.resize(at + 2 * nv);
+    std::memcpy(latlng.data() + at, v, nv * 16);
+    off[p + 1] = off[p] + nv;
+  }
+  d.n_polygons = n_poly;
+  d.polygon_ids = ids.data();
+  d.vtx_off = off.data();
+  d.vtx_latlng = latlng.data();
+  return create_index(d, device, out);
+}
+
+}  // namespace gj

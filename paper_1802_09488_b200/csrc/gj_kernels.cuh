@@ -1,0 +1,498 @@
+// sm_100a kernels of the probe path.
+//
+//   K1  join_kernel        points -> cell -> directory/trie -> entry -> emit
+//                          (counts, first ids, overflow records, stats) and,
+//                          in exact mode, candidate tasks for K2
+//   K1' probe_points_kernel / probe_cells_kernel   entries only (test hooks)
+//   K2  refine_kernel      ray-crossing PIP over candidate tasks bucketed by
+//                          polygon; edges staged in shared memory per warp
+//   plan_units_kernel / scatter_tasks_kernel        bucket the tasks for K2
+//
+// All of it is HBM/L2-bound integer and fp64 scalar work; no tensor cores.
+#pragma once
+
+#include "gj_device.cuh"
+
+namespace gj {
+
+constexpr int kJoinThreads = 1024;
+constexpr int kPointsPerThread = 4;
+constexpr int kRefineThreads = 256;
+constexpr int kRefineTile = 64;  // vertices staged per warp and tile
+
+struct JoinParams {
+  const double2* pts;  // (lat, lng) pairs: .x = lat, .y = lng  (latlng.hpp:26-29)
+  uint64_t n;
+  uint64_t base_index;
+  unsigned long long* counts;  // [n_ids], added to
+  unsigned long long* stats;   // [6] or null
+  uint32_t* first_id;          // [n] or null
+  uint64_t* ovf_point;
+  uint32_t* ovf_id;
+  uint32_t* ovf_ord;
+  uint64_t ovf_cap;
+  uint32_t* task_point;
+  uint32_t* task_slot;
+  uint32_t* task_ord;
+  uint64_t task_cap;
+  uint32_t* task_per_slot;  // [n_ids]
+  DevStatus* status;
+  uint32_t smem_dict_off;   // bytes; 0xFFFFFFFF = dictionary stays in global
+  uint32_t smem_hist_off;   // bytes
+  uint32_t hist_rep;        // replicas per slot (power of two), 0 = global atomics
+  int32_t exact;
+};
+
+__device__ __forceinline__ uint32_t id_to_slot(const DevIndex& ix, uint32_t id) {
+  if (ix.ids_dense) return id;
+  uint32_t lo = 0, hi = ix.n_ids;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (__ldg(ix.ids + mid) < id) {
+      lo = mid + 1;
+    } else {
+      hi = mid;
+    }
+  }
+  return lo;  // present by construction of the id table
+}
+
+__device__ __forceinline__ void flag_error(DevStatus* st, uint32_t bit, uint64_t index) {
+  atomicOr(&st->flags, bit);
+  atomicMin(&st->bad_index, static_cast<unsigned long long>(index));
+}
+
+// Per-thread emit state of K1.
+template <bool kIds, bool kStats>
+struct Emitter {
+  const DevIndex& ix;
+  const JoinParams& jp;
+  uint32_t* s_hist;
+  uint32_t lane_rep;  // lane & (hist_rep - 1)
+  uint32_t false_hits = 0, solely_true = 0, refined = 0, cand_refs = 0;
+
+  __device__ __forceinline__ Emitter(const DevIndex& i, const JoinParams& j, uint32_t* h, uint32_t lr)
+      : ix(i), jp(j), s_hist(h), lane_rep(lr) {}
+
+  __device__ __forceinline__ void count(uint32_t slot) {
+    if (jp.hist_rep) {
+      atomicAdd(&s_hist[slot * jp.hist_rep + lane_rep], 1u);
+    } else {
+      atomicAdd(&jp.counts[slot], 1ull);
+    }
+  }
+
+  // k-th reference of an entry in the reference's emit order
+  // (act.hpp:169-196): payload = (polygon_id << 1) | interior.
+  __device__ __forceinline__ uint32_t ref_payload(uint64_t entry, uint32_t tag, uint32_t k, uint32_t off,
+                                                  uint32_t t) const {
+    if (tag == 2u) {
+      return k == 0 ? static_cast<uint32_t>(entry >> 33) & 0x7fffffffu
+                    : static_cast<uint32_t>(entry >> 2) & 0x7fffffffu;
+    }
+    // lookup-table record [t, true ids, c, candidate ids]
+    return k < t ? (__ldg(ix.lut + off + 1 + k) << 1) | 1u : (__ldg(ix.lut + off + 2 + k) << 1);
+  }
+
+  // The per-(point, entry) body of run_join, join.cpp:93-127.  Returns the
+  // first-id word for the point.
+  __device__ __forceinline__ uint32_t handle(uint64_t entry, uint64_t local) {
+    if (entry == 0) {
+      if (kStats) ++false_hits;
+      return kNoMatch;
+    }
+    const uint32_t tag = static_cast<uint32_t>(entry) & 3u;
+    if (tag == 1u) {  // one inlined payload: the overwhelmingly common case
+      const uint32_t p = static_cast<uint32_t>(entry >> 2) & 0x7fffffffu;
+      const uint32_t id = p >> 1;
+      if ((p & 1u) != 0u || !jp.exact) {
+        count(id_to_slot(ix, id));
+        if (kStats) {
+          if (p & 1u) {
+            ++solely_true;
+          } else {
+            ++refined;
+            ++cand_refs;
+          }
+        }
+        return id;
+      }
+    }
+    return handle_general(entry, tag, local);
+  }
+
+  __device__ __noinline__ uint32_t handle_general(uint64_t entry, uint32_t tag, uint64_t local) {
+    uint32_t off = 0, t = 0, n_refs;
+    if (tag == 1u) {
+      n_refs = 1;
+    } else if (tag == 2u) {
+      n_refs = 2;
+    } else {
+      off = static_cast<uint32_t>(entry >> 2) & 0x7fffffffu;
+      t = __ldg(ix.lut + off);
+      n_refs = t + __ldg(ix.lut + off + 1 + t);
+    }
+    uint32_t n_cand = 0;
+    if (tag == 1u) {
+      n_cand = 1;  // only exact-mode candidates reach here with tag 1
+    } else if (tag == 2u) {
+      n_cand = 2u - ((static_cast<uint32_t>(entry >> 33) & 1u) + (static_cast<uint32_t>(entry >> 2) & 1u));
+    } else {
+      n_cand = n_refs - t;
+    }
+    if (kStats) {
+      if (n_cand == 0) {
+        ++solely_true;
+      } else {
+        ++refined;
+        cand_refs += n_cand;
+      }
+    }
+    const bool defer = jp.exact && n_cand != 0;  // some pairs depend on K2
+    const uint32_t n_now = jp.exact ? n_refs - n_cand : n_refs;  // pairs emitted here
+
+    // overflow records: everything after the first pair, or every pair when
+    // the point is deferred
+    uint64_t ovf_base = 0;
+    uint32_t n_ovf = 0;
+    if (kIds) {
+      n_ovf = defer ? n_now : (n_now > 0 ? n_now - 1 : 0);
+      if (n_ovf) {
+        ovf_base = atomicAdd(&jp.status->overflow_count, static_cast<unsigned long long>(n_ovf));
+        if (ovf_base + n_ovf > jp.ovf_cap) {
+          atomicOr(&jp.status->flags, kErrOverflowCap);
+          n_ovf = 0;
+        }
+      }
+    }
+    uint64_t task_base = 0;
+    bool tasks_ok = false;
+    if (defer) {
+      task_base = atomicAdd(&jp.status->task_count, static_cast<unsigned long long>(n_cand));
+      tasks_ok = task_base + n_cand <= jp.task_cap;
+      if (!tasks_ok) atomicOr(&jp.status->flags, kErrTaskCap);
+    }
+
+    uint32_t first = defer ? kDeferred : kNoMatch;
+    uint32_t emitted = 0, tasks = 0;
+    for (uint32_t k = 0; k < n_refs; ++k) {
+      const uint32_t p = tag == 1u ? static_cast<uint32_t>(entry >> 2) & 0x7fffffffu
+                                   : ref_payload(entry, tag, k, off, t);
+      const uint32_t id = p >> 1;
+      const uint32_t slot = id_to_slot(ix, id);
+      if ((p & 1u) != 0u || !jp.exact) {
+        count(slot);
+        if (kIds) {
+          if (!defer && emitted == 0) {
+            first = id | (n_now > 1 ? kMoreFlag : 0u);
+          } else if (n_ovf) {
+            const uint64_t w = ovf_base + (defer ? emitted : emitted - 1);
+            jp.ovf_point[w] = jp.base_index + local;
+            jp.ovf_id[w] = id;
+            jp.ovf_ord[w] = k;
+          }
+        }
+        ++emitted;
+      } else {
+        if (__ldg(ix.ring_len + slot) == 0u) {  // join.cpp:111-114
+          flag_error(jp.status, kErrUnknownPolygon, jp.base_index + local);
+        }
+        if (tasks_ok) {
+          const uint64_t w = task_base + tasks;
+          jp.task_point[w] = static_cast<uint32_t>(local);
+          jp.task_slot[w] = slot;
+          jp.task_ord[w] = k;
+          atomicAdd(&jp.task_per_slot[slot], 1u);
+        }
+        ++tasks;
+      }
+    }
+    return first;
+  }
+};
+
+// K1.  Persistent grid (one CTA per SM slot); each CTA stages the directory
+// (and a replicated per-polygon histogram) in shared memory once, then
+// streams tiles of points: 16-byte coalesced loads, kPointsPerThread
+// independent points in flight per thread.
+template <bool kIds, bool kStats>
+__global__ void __launch_bounds__(kJoinThreads, 1)
+join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinParams jp) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint32_t* s_table = reinterpret_cast<uint32_t*>(smem);
+  const bool dict_in_smem = jp.smem_dict_off != 0xFFFFFFFFu;
+  uint64_t* s_dict = reinterpret_cast<uint64_t*>(smem + (dict_in_smem ? jp.smem_dict_off : 0));
+  uint32_t* s_hist = reinterpret_cast<uint32_t*>(smem + jp.smem_hist_off);
+  const uint32_t tid = threadIdx.x;
+
+  {  // stage directory + dictionary, clear histogram
+    const uint4* src = reinterpret_cast<const uint4*>(ix.dir.table);
+    uint4* dst = reinterpret_cast<uint4*>(s_table);
+    const uint32_t n4 = (ix.dir.n_table + 3) / 4;  // buffers are padded to 16 B
+    for (uint32_t i = tid; i < n4; i += kJoinThreads) dst[i] = __ldg(src + i);
+    if (dict_in_smem) {
+      for (uint32_t i = tid; i < ix.dir.n_dict; i += kJoinThreads) s_dict[i] = __ldg(ix.dir.dict + i);
+    }
+    const uint32_t n_hist = ix.n_ids * jp.hist_rep;
+    for (uint32_t i = tid; i < n_hist; i += kJoinThreads) s_hist[i] = 0;
+  }
+  __syncthreads();
+  const uint64_t* dict = dict_in_smem ? s_dict : ix.dir.dict;
+
+  Emitter<kIds, kStats> em(ix, jp, s_hist, (tid & 31u) & (jp.hist_rep ? jp.hist_rep - 1u : 0u));
+  uint32_t n_valid = 0;
+
+  constexpr uint64_t kTile = static_cast<uint64_t>(kJoinThreads) * kPointsPerThread;
+  const uint64_t n_tiles = (jp.n + kTile - 1) / kTile;
+  for (uint64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const uint64_t base = tile * kTile + tid;
+    double2 p[kPointsPerThread];
+#pragma unroll
+    for (int j = 0; j < kPointsPerThread; ++j) {
+      const uint64_t i = base + static_cast<uint64_t>(j) * kJoinThreads;
+      // streaming read, touched once: evict-first
+      p[j] = i < jp.n ? __ldcs(jp.pts + i) : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int j = 0; j < kPointsPerThread; ++j) {
+      const uint64_t i = base + static_cast<uint64_t>(j) * kJoinThreads;
+      if (i >= jp.n) break;
+      uint64_t entry = 0;
+      if (latlng_valid(p[j].x, p[j].y)) {
+        entry = probe_point(ix, s_table, dict, p[j].x, p[j].y);
+        ++n_valid;
+      } else {
+        flag_error(jp.status, kErrInvalidPoint, jp.base_index + i);  // cell_id.cpp:83-85
+        continue;
+      }
+      const uint32_t first = em.handle(entry, i);
+      if (kIds) __stcs(jp.first_id + i, first);
+    }
+  }
+
+  __syncthreads();
+  if (jp.hist_rep) {  // fold the replicas, one global add per non-zero slot
+    for (uint32_t s = tid; s < ix.n_ids; s += kJoinThreads) {
+      uint32_t sum = 0;
+      for (uint32_t r = 0; r < jp.hist_rep; ++r) sum += s_hist[s * jp.hist_rep + r];
+      if (sum) atomicAdd(&jp.counts[s], static_cast<unsigned long long>(sum));
+    }
+  }
+  if (kStats && jp.stats) {  // JoinStats, join.hpp:77-84
+    uint32_t v[5] = {n_valid, em.false_hits, em.solely_true, em.refined, em.cand_refs};
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
+    }
+    if ((tid & 31u) == 0) {
+      atomicAdd(&jp.stats[0], static_cast<unsigned long long>(v[0]));                      // probes
+      if (jp.exact) atomicAdd(&jp.stats[1], static_cast<unsigned long long>(v[4]));        // pip_tests
+      atomicAdd(&jp.stats[2], static_cast<unsigned long long>(v[1]));                      // false_hits
+      atomicAdd(&jp.stats[3], static_cast<unsigned long long>(v[2]));                      // solely_true_hits
+      atomicAdd(&jp.stats[4], static_cast<unsigned long long>(v[3]));                      // refinement_entered
+      atomicAdd(&jp.stats[5], static_cast<unsigned long long>(v[4]));                      // candidate_refs
+    }
+  }
+}
+
+// Entries only: bitwise Act::probe(cell_from_point(p, k_max/2)).
+__global__ void __launch_bounds__(256)
+probe_points_kernel(const __grid_constant__ DevIndex ix, const double2* __restrict__ pts, uint64_t n,
+                    uint64_t base_index, uint64_t* __restrict__ out, DevStatus* status) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint32_t* s_table = reinterpret_cast<uint32_t*>(smem);
+  for (uint32_t i = threadIdx.x; i < ix.dir.n_table; i += blockDim.x) s_table[i] = __ldg(ix.dir.table + i);
+  __syncthreads();
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const double2 p = __ldcs(pts + i);
+    uint64_t e = 0;
+    if (latlng_valid(p.x, p.y)) {
+      e = probe_point(ix, s_table, ix.dir.dict, p.x, p.y);
+    } else {
+      flag_error(status, kErrInvalidPoint, base_index + i);
+    }
+    out[i] = e;
+  }
+}
+
+// Same without the directory (plain arena walk): the cross-check that the
+// directory changes nothing, and the all-faces raw-id entry point.
+__global__ void __launch_bounds__(256)
+probe_cells_kernel(const __grid_constant__ DevIndex ix, const uint64_t* __restrict__ raw, uint64_t n,
+                   uint64_t* __restrict__ out) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    out[i] = probe_raw(ix, __ldg(raw + i));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Task bucketing for K2: tasks grouped by polygon slot, cut into units of
+// <= 32 tasks (one warp each).  Single-CTA scan over the id table.
+// ---------------------------------------------------------------------------
+struct RefinePlan {
+  const uint32_t* task_per_slot;  // [n_ids]
+  uint32_t* slot_task_off;        // [n_ids + 1]
+  uint32_t* slot_unit_off;        // [n_ids + 1]
+  uint32_t* slot_cursor;          // [n_ids]
+  uint32_t* unit_counter;         // [1] dynamic unit queue head
+};
+
+__global__ void __launch_bounds__(1024) plan_units_kernel(RefinePlan pl, uint32_t n_ids) {
+  __shared__ uint32_t s_a[1024], s_b[1024];
+  __shared__ uint32_t carry_a, carry_b;
+  const uint32_t tid = threadIdx.x;
+  if (tid == 0) {
+    carry_a = 0;
+    carry_b = 0;
+    *pl.unit_counter = 0;
+  }
+  __syncthreads();
+  for (uint32_t base = 0; base < n_ids; base += 1024) {
+    const uint32_t i = base + tid;
+    const uint32_t c = i < n_ids ? pl.task_per_slot[i] : 0u;
+    const uint32_t u = (c + 31u) / 32u;
+    s_a[tid] = c;
+    s_b[tid] = u;
+    __syncthreads();
+    for (uint32_t o = 1; o < 1024; o <<= 1) {  // Hillis-Steele inclusive scan
+      const uint32_t va = tid >= o ? s_a[tid - o] : 0u;
+      const uint32_t vb = tid >= o ? s_b[tid - o] : 0u;
+      __syncthreads();
+      s_a[tid] += va;
+      s_b[tid] += vb;
+      __syncthreads();
+    }
+    if (i < n_ids) {
+      pl.slot_task_off[i] = carry_a + s_a[tid] - c;
+      pl.slot_unit_off[i] = carry_b + s_b[tid] - u;
+      pl.slot_cursor[i] = 0;
+    }
+    __syncthreads();
+    if (tid == 1023) {
+      carry_a += s_a[1023];
+      carry_b += s_b[1023];
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    pl.slot_task_off[n_ids] = carry_a;
+    pl.slot_unit_off[n_ids] = carry_b;
+  }
+}
+
+__global__ void __launch_bounds__(256)
+scatter_tasks_kernel(RefinePlan pl, const uint32_t* __restrict__ task_slot, const DevStatus* status,
+                     uint64_t task_cap, uint32_t* __restrict__ task_sorted) {
+  const uint64_t n = min(static_cast<uint64_t>(status->task_count), task_cap);
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const uint32_t slot = task_slot[i];
+    task_sorted[pl.slot_task_off[slot] + atomicAdd(&pl.slot_cursor[slot], 1u)] = static_cast<uint32_t>(i);
+  }
+}
+
+struct RefineParams {
+  const double2* pts;
+  uint64_t base_index;
+  const uint32_t* task_point;
+  const uint32_t* task_ord;
+  const uint32_t* task_sorted;
+  unsigned long long* counts;
+  // ids mode: accepted candidates become overflow records
+  uint64_t* ovf_point;
+  uint32_t* ovf_id;
+  uint32_t* ovf_ord;
+  uint64_t ovf_cap;
+  // pairs mode: one flag per task (1 = the candidate passed)
+  uint8_t* task_pass;
+  DevStatus* status;
+  int32_t want_ids;
+};
+
+// K2.  One warp per unit (<= 32 candidate points of ONE polygon): the
+// polygon's closed ring is staged tile by tile into the warp's slice of
+// shared memory with coalesced 16-byte loads; every lane then runs its point
+// over the staged edges (broadcast reads, conflict-free).  Units are handed
+// out through an atomic queue, so warps balance by edge count on their own.
+__global__ void __launch_bounds__(kRefineThreads)
+refine_kernel(const __grid_constant__ DevIndex ix, RefinePlan pl, RefineParams rp) {
+  __shared__ double2 s_ring[kRefineThreads / 32][kRefineTile + 1];
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t warp = threadIdx.x >> 5;
+  const uint32_t n_units = pl.slot_unit_off[ix.n_ids];
+  for (;;) {
+    uint32_t unit = 0;
+    if (lane == 0) unit = atomicAdd(pl.unit_counter, 1u);
+    unit = __shfl_sync(0xffffffffu, unit, 0);
+    if (unit >= n_units) break;
+    // slot owning this unit: last slot with unit_off <= unit
+    uint32_t lo = 0, hi = ix.n_ids;
+    while (hi - lo > 1) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (__ldg(pl.slot_unit_off + mid) <= unit) {
+        lo = mid;
+      } else {
+        hi = mid;
+      }
+    }
+    const uint32_t slot = lo;
+    const uint32_t t_begin = pl.slot_task_off[slot] + (unit - pl.slot_unit_off[slot]) * 32u;
+    const uint32_t t_end = min(t_begin + 32u, pl.slot_task_off[slot + 1]);
+    const bool active = t_begin + lane < t_end;
+    uint32_t task = 0, point = 0;
+    double qx = 0.0, qy = 0.0;
+    if (active) {
+      task = rp.task_sorted[t_begin + lane];
+      point = rp.task_point[task];
+      const double2 p = __ldg(rp.pts + point);
+      qx = p.y;  // x = lng
+      qy = p.x;  // y = lat
+    }
+    const uint64_t ring = __ldg(ix.ring_off + slot);
+    const uint32_t n_edges = __ldg(ix.ring_len + slot);
+    uint32_t boundary = 0, crossings = 0;
+    for (uint32_t e0 = 0; e0 < n_edges; e0 += kRefineTile) {
+      const uint32_t n_tile = min(static_cast<uint32_t>(kRefineTile), n_edges - e0);
+      __syncwarp();
+      for (uint32_t v = lane; v <= n_tile; v += 32u) s_ring[warp][v] = __ldg(ix.ring_xy + ring + e0 + v);
+      __syncwarp();
+      if (active) {
+        for (uint32_t e = 0; e < n_tile; ++e) {
+          const double2 a = s_ring[warp][e];
+          const double2 b = s_ring[warp][e + 1];
+          const uint32_t r = pip_edge(qx, qy, a.x, a.y, b.x, b.y);
+          boundary |= r & 1u;
+          crossings ^= r >> 1;
+        }
+      }
+    }
+    const bool pass = active && n_edges != 0 && (boundary | crossings) != 0u;
+    const uint32_t pass_mask = __ballot_sync(0xffffffffu, pass);
+    if (rp.task_pass) {
+      if (active) rp.task_pass[task] = pass ? 1 : 0;
+    } else {
+      if (lane == 0 && pass_mask) {
+        atomicAdd(&rp.counts[slot], static_cast<unsigned long long>(__popc(pass_mask)));
+      }
+      if (rp.want_ids && pass_mask) {
+        unsigned long long base = 0;
+        if (lane == 0) {
+          base = atomicAdd(&rp.status->overflow_count, static_cast<unsigned long long>(__popc(pass_mask)));
+        }
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (base + __popc(pass_mask) > rp.ovf_cap) {
+          if (lane == 0) atomicOr(&rp.status->flags, kErrOverflowCap);
+        } else if (pass) {
+          const uint64_t w = base + __popc(pass_mask & ((1u << lane) - 1u));
+          rp.ovf_point[w] = rp.base_index + point;
+          rp.ovf_id[w] = __ldg(ix.ids + slot);
+          rp.ovf_ord[w] = rp.task_ord[task];
+        }
+      }
+    }
+  }
+}
+
+}  // namespace gj

@@ -1,0 +1,339 @@
+"""Host-side mirror of the reference's index/join API for the probe path,
+running on a B200 through the C ABI (include/geojoin_b200.h).
+
+Names, argument meaning and error behaviour follow the reference
+(paths relative to its proj/ directory):
+
+    IndexBundle                include/geojoin/join.hpp:86-115
+    JoinStats                  include/geojoin/join.hpp:77-84
+    join_exact / join_approx   src/join.cpp:237-247
+    join_count_per_polygon     src/join.cpp:255-285
+    accumulate_probe_stats     src/join.cpp:287-290
+    metrics_from_stats         src/join.cpp:292-307
+
+The index itself is built offline by the reference's ``build_index`` (or read
+from its ``GJX1`` file); this module only moves it to the GPU and probes it.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, fields
+
+import numpy as np
+
+from . import capi
+
+
+class InvalidArgument(ValueError):
+    """std::invalid_argument: a non-finite or out-of-range coordinate (cell_id.cpp:83-85)."""
+
+    def __init__(self, msg, index=None):
+        super().__init__(msg)
+        self.index = index
+
+
+class CorruptionError(RuntimeError):
+    """geojoin::CorruptionError (act.hpp:44-46)."""
+
+    def __init__(self, msg, index=None):
+        super().__init__(msg)
+        self.index = index
+
+
+class CapacityError(RuntimeError):
+    pass
+
+
+class CudaError(RuntimeError):
+    pass
+
+
+def _raise(rc: int, bad_index=None):
+    msg = capi.lib().gj_last_error().decode()
+    if rc == capi.GJ_INVALID_POINT:
+        raise InvalidArgument(msg, bad_index)
+    if rc in (capi.GJ_CORRUPT_INDEX, capi.GJ_UNKNOWN_POLYGON):
+        raise CorruptionError(msg, bad_index)
+    if rc == capi.GJ_INVALID_ARGUMENT:
+        raise ValueError(msg)
+    if rc == capi.GJ_CAPACITY:
+        raise CapacityError(msg)
+    if rc == capi.GJ_IO_ERROR:
+        raise OSError(msg)
+    raise CudaError(msg)
+
+
+def _check(rc: int, bad: C.c_uint64 | None = None):
+    if rc != capi.GJ_OK:
+        _raise(rc, bad.value if bad is not None else None)
+
+
+@dataclass
+class JoinStats:
+    probes: int = 0
+    pip_tests: int = 0
+    false_hits: int = 0
+    solely_true_hits: int = 0
+    refinement_entered: int = 0
+    candidate_refs: int = 0
+
+    def as_tuple(self):
+        return tuple(getattr(self, f.name) for f in fields(self))
+
+    def _add(self, s: capi.Stats):
+        for f in fields(self):
+            setattr(self, f.name, getattr(self, f.name) + int(getattr(s, f.name)))
+
+
+@dataclass
+class IndexMetrics:
+    tree_nodes: int = 0
+    false_hit_fraction: float = 0.0
+    solely_true_hit_fraction: float = 0.0
+    avg_candidates: float = 0.0
+
+
+def metrics_from_stats(stats: JoinStats, tree_nodes: int) -> IndexMetrics:
+    m = IndexMetrics(tree_nodes=tree_nodes)
+    if stats.probes > 0:
+        m.false_hit_fraction = stats.false_hits / stats.probes
+        m.solely_true_hit_fraction = stats.solely_true_hits / stats.probes
+    if stats.refinement_entered > 0:
+        m.avg_candidates = stats.candidate_refs / stats.refinement_entered
+    return m
+
+
+def _points(points) -> np.ndarray:
+    a = np.ascontiguousarray(points, dtype=np.float64)
+    if a.ndim == 1:
+        a = a.reshape(-1, 2)
+    if a.ndim != 2 or a.shape[1] != 2:
+        raise ValueError("points must be (n, 2) float64 (lat, lng) pairs")
+    return a
+
+
+def _vp(a):
+    return C.c_void_p(a.ctypes.data) if a is not None else None
+
+
+class IndexBundle:
+    """An immutable index replicated into one GPU's HBM."""
+
+    def __init__(self, handle: int):
+        self._h = C.c_void_p(handle)
+        info = capi.IndexInfo()
+        _check(capi.lib().gj_index_get_info(self._h, C.byref(info)))
+        self.info = info
+        self.ids = np.empty(info.n_ids, np.uint32)
+        _check(capi.lib().gj_index_ids(self._h, _vp(self.ids)))
+        self._session = None
+
+    def close(self):
+        if self._session is not None:
+            self._session.close()
+            self._session = None
+        if self._h:
+            capi.lib().gj_index_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @staticmethod
+    def from_arrays(arena, lut, roots, prefixes, prefix_bits, k_max: int, approx_mode: bool,
+                    polygon_ids, vtx_off, vtx_latlng, device: int = -1) -> "IndexBundle":
+        arena = np.ascontiguousarray(arena, np.uint64)
+        lut = np.ascontiguousarray(lut, np.uint32)
+        polygon_ids = np.ascontiguousarray(polygon_ids, np.uint32)
+        vtx_off = np.ascontiguousarray(vtx_off, np.uint64)
+        vtx_latlng = np.ascontiguousarray(vtx_latlng, np.float64)
+        d = capi.IndexDesc()
+        d.arena = arena.ctypes.data
+        d.node_count = len(arena) // 256
+        d.lut = lut.ctypes.data
+        d.lut_len = len(lut)
+        for f in range(8):
+            d.roots[f] = int(roots[f])
+            d.prefixes[f] = int(prefixes[f])
+            d.prefix_bits[f] = int(prefix_bits[f])
+        d.k_max = int(k_max)
+        d.approx_mode = int(bool(approx_mode))
+        d.n_polygons = len(polygon_ids)
+        d.polygon_ids = polygon_ids.ctypes.data
+        d.vtx_off = vtx_off.ctypes.data
+        d.vtx_latlng = vtx_latlng.ctypes.data
+        h = C.c_void_p()
+        _check(capi.lib().gj_index_create(C.byref(d), device, C.byref(h)))
+        return IndexBundle(h.value)
+
+    @staticmethod
+    def load(path, device: int = -1) -> "IndexBundle":
+        """IndexBundle::load (join.cpp:341-381): GJX1 file -> HBM."""
+        h = C.c_void_p()
+        _check(capi.lib().gj_index_load_file(str(path).encode(), device, C.byref(h)))
+        return IndexBundle(h.value)
+
+    @property
+    def approx(self) -> bool:
+        return bool(self.info.approx_mode)
+
+    def session(self) -> "Session":
+        if self._session is None:
+            self._session = Session(self)
+        return self._session
+
+
+class Session:
+    """One CUDA stream + scratch; not thread-safe (use one per thread)."""
+
+    def __init__(self, bundle: IndexBundle):
+        self.bundle = bundle
+        h = C.c_void_p()
+        _check(capi.lib().gj_session_create(bundle._h, C.byref(h)))
+        self._h = h
+
+    def close(self):
+        if self._h:
+            capi.lib().gj_session_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def stream(self) -> int:
+        return capi.lib().gj_session_stream(self._h)
+
+    @property
+    def launches(self) -> int:
+        return int(capi.lib().gj_session_launches(self._h))
+
+    # ---- probe ----
+    def probe_points(self, points) -> np.ndarray:
+        p = _points(points)
+        out = np.empty(len(p), np.uint64)
+        bad = C.c_uint64(0)
+        _check(capi.lib().gj_probe_points_host(self._h, _vp(p), len(p), _vp(out), C.byref(bad)), bad)
+        return out
+
+    def probe_cells(self, raw_ids) -> np.ndarray:
+        r = np.ascontiguousarray(raw_ids, np.uint64)
+        out = np.empty(len(r), np.uint64)
+        _check(capi.lib().gj_probe_cells_host(self._h, _vp(r), len(r), _vp(out)))
+        return out
+
+    # ---- streaming join ----
+    def join_count(self, points, mode=capi.GJ_MODE_BUNDLE, stats: JoinStats | None = None,
+                   want_ids: bool = False, base_index: int = 0, overflow_capacity: int | None = None):
+        """Returns (counts_by_slot u64[n_ids], first_id u32[n] | None, (ovf_point, ovf_id) | None)."""
+        p = _points(points)
+        counts = np.zeros(max(1, len(self.bundle.ids)), np.uint64)
+        cs = capi.Stats()
+        bad = C.c_uint64(0)
+        first = np.empty(len(p), np.uint32) if want_ids else None
+        ovf = None
+        ovf_pt = ovf_id = None
+        if want_ids:
+            cap = overflow_capacity if overflow_capacity is not None else max(1024, len(p) // 4)
+            while True:
+                ovf_pt = np.empty(cap, np.uint64)
+                ovf_id = np.empty(cap, np.uint32)
+                ovf = capi.Overflow(ovf_pt.ctypes.data, ovf_id.ctypes.data, cap, 0)
+                counts[:] = 0
+                cs = capi.Stats()
+                rc = capi.lib().gj_join_count_host(self._h, _vp(p), len(p), base_index, mode, _vp(counts),
+                                                   C.byref(cs) if stats is not None else None,
+                                                   _vp(first), C.byref(ovf), C.byref(bad))
+                if rc == capi.GJ_CAPACITY and ovf.count > cap and overflow_capacity is None:
+                    cap = int(ovf.count)
+                    continue
+                _check(rc, bad)
+                break
+            ovf_pt, ovf_id = ovf_pt[:ovf.count], ovf_id[:ovf.count]
+        else:
+            _check(capi.lib().gj_join_count_host(self._h, _vp(p), len(p), base_index, mode, _vp(counts),
+                                                 C.byref(cs) if stats is not None else None,
+                                                 None, None, C.byref(bad)), bad)
+        if stats is not None:
+            stats._add(cs)
+        counts = counts[:len(self.bundle.ids)]
+        return counts, first, ((ovf_pt, ovf_id) if want_ids else None)
+
+    def join_count_device(self, d_points_ptr: int, n: int, d_counts_ptr: int, mode=capi.GJ_MODE_BUNDLE,
+                          d_stats_ptr: int = 0, d_first_id_ptr: int = 0, sync: bool = False):
+        """Points already in HBM (raw device pointers, e.g. ``tensor.data_ptr()``);
+        asynchronous on ``self.stream`` unless ``sync``."""
+        _check(capi.lib().gj_join_count_device(self._h, C.c_void_p(d_points_ptr), n, mode,
+                                               C.c_void_p(d_counts_ptr),
+                                               C.c_void_p(d_stats_ptr) if d_stats_ptr else None,
+                                               C.c_void_p(d_first_id_ptr) if d_first_id_ptr else None,
+                                               int(sync)))
+
+    def sync(self):
+        bad = C.c_uint64(0)
+        _check(capi.lib().gj_session_sync(self._h, C.byref(bad)), bad)
+
+    # ---- materialised pairs ----
+    def join_pairs(self, points, mode, stats: JoinStats | None = None):
+        """(row_ptr u64[n+1], polygon_id u32[]) in the reference's emit order."""
+        p = _points(points)
+        n_pairs = C.c_uint64(0)
+        cs = capi.Stats()
+        bad = C.c_uint64(0)
+        _check(capi.lib().gj_join_pairs_host(self._h, _vp(p), len(p), mode, C.byref(n_pairs),
+                                             C.byref(cs) if stats is not None else None, C.byref(bad)), bad)
+        row_ptr = np.empty(len(p) + 1, np.uint64)
+        ids = np.empty(n_pairs.value, np.uint32)
+        _check(capi.lib().gj_pairs_copy(self._h, _vp(row_ptr), _vp(ids)))
+        if stats is not None:
+            stats._add(cs)
+        return row_ptr, ids
+
+
+def _pairs_from_csr(row_ptr: np.ndarray, ids: np.ndarray):
+    n = len(row_ptr) - 1
+    point_index = np.repeat(np.arange(n, dtype=np.uint64), np.diff(row_ptr.astype(np.int64)))
+    return point_index, ids
+
+
+def join_exact(bundle: IndexBundle, points, stats: JoinStats | None = None):
+    """join.cpp:237-241 — (point_index u64[], polygon_id u32[]) like vector<JoinPair>."""
+    return _pairs_from_csr(*bundle.session().join_pairs(points, capi.GJ_MODE_EXACT, stats))
+
+
+def join_approx(bundle: IndexBundle, points, stats: JoinStats | None = None):
+    """join.cpp:243-247."""
+    return _pairs_from_csr(*bundle.session().join_pairs(points, capi.GJ_MODE_APPROX, stats))
+
+
+def join_count_per_polygon(bundle: IndexBundle, points, threads: int = 1) -> dict[int, int]:
+    """join.cpp:255-285 — mode from the bundle; only polygons with a non-zero
+    count appear.  ``threads`` is accepted for signature parity (the GPU path
+    has no use for it; results are independent of it by contract)."""
+    counts, _, _ = bundle.session().join_count(points, capi.GJ_MODE_BUNDLE)
+    nz = np.nonzero(counts)[0]
+    return {int(bundle.ids[k]): int(counts[k]) for k in nz}
+
+
+def count_per_polygon(polygon_ids) -> dict[int, int]:
+    """join.cpp:249-253."""
+    ids, cnt = np.unique(np.asarray(polygon_ids, np.uint32), return_counts=True)
+    return {int(i): int(c) for i, c in zip(ids, cnt)}
+
+
+def accumulate_probe_stats(bundle: IndexBundle, points, stats: JoinStats) -> None:
+    """join.cpp:287-290 — probe-only pass (approx emit, nothing kept) adding into ``stats``."""
+    bundle.session().join_count(points, capi.GJ_MODE_APPROX, stats)
+
+
+def collect_metrics(bundle: IndexBundle, points) -> IndexMetrics:
+    """join.cpp:309-314."""
+    s = JoinStats()
+    accumulate_probe_stats(bundle, points, s)
+    return metrics_from_stats(s, int(bundle.info.node_count))

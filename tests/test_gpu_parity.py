@@ -1,0 +1,149 @@
+"""GPU parity tests proper: the CUDA path, called through the C ABI, against
+(a) the committed golden outputs of the compiled reference and (b) the C
+oracle run live on the same inputs.  Bit-exact: entries, pairs (order
+included), per-polygon counts and the six JoinStats counters."""
+import numpy as np
+import pytest
+
+from paper_1802_09488_b200 import capi, join
+from tests import golden_util
+
+pytestmark = pytest.mark.gpu
+
+JOIN_FIXTURES = [
+    "join_small_exact", "join_small_approx", "acceptance_exact20", "cfg1_tess5_approx60m",
+    "cfg2_tess16_approx4m", "cfg3_tess16_exact_trained", "cfg4_tess36_approx1m_k56",
+    "cfg5_stars_scaled", "kmax60_sparse_ids", "world_stars", "empty_index",
+]
+
+_cache = {}
+
+
+def setup(name):
+    if name not in _cache:
+        fx = golden_util.load(name)
+        bundle = join.IndexBundle.load(golden_util.bundle_file(name), device=0)
+        _cache.clear()  # one resident index at a time
+        _cache[name] = (fx, bundle)
+    return _cache[name]
+
+
+def pairs_from_csr(row_ptr, ids):
+    n = len(row_ptr) - 1
+    return np.repeat(np.arange(n, dtype=np.uint64), np.diff(row_ptr.astype(np.int64))), ids
+
+
+@pytest.mark.parametrize("name", JOIN_FIXTURES)
+def test_entries_match_reference(name):
+    fx, bundle = setup(name)
+    got = bundle.session().probe_points(fx["points"])
+    assert np.array_equal(got, fx["entries"])  # bitwise Act::probe(cell_from_point(p))
+
+
+@pytest.mark.parametrize("name", JOIN_FIXTURES)
+def test_cell_probe_matches_point_probe_and_oracle(name):
+    """The directory-free raw-id kernel (ProbeBatchFn contract) agrees with
+    the directory path and the oracle's scalar walk."""
+    from oracle import oracle
+    fx, bundle = setup(name)
+    k_max = int(fx["k_max"][0])
+    raw = oracle.cell_from_point(fx["points"], k_max // 2)
+    got = bundle.session().probe_cells(raw)
+    assert np.array_equal(got, fx["entries"])
+    ox = golden_util.oracle_index(fx)
+    assert np.array_equal(got[:2000], ox.probe_raw(raw[:2000]))
+
+
+@pytest.mark.parametrize("name", JOIN_FIXTURES)
+@pytest.mark.parametrize("kind", ["exact", "approx"])
+def test_pairs_match_reference(name, kind):
+    fx, bundle = setup(name)
+    mode = capi.GJ_MODE_EXACT if kind == "exact" else capi.GJ_MODE_APPROX
+    st = join.JoinStats()
+    pi, pid = pairs_from_csr(*bundle.session().join_pairs(fx["points"], mode, st))
+    epi, epid = golden_util.pairs_of(fx, kind)
+    assert np.array_equal(pi, epi)
+    assert np.array_equal(pid, epid)  # order included
+    assert st.as_tuple() == tuple(int(v) for v in fx[f"{kind}_stats"])
+
+
+@pytest.mark.parametrize("name", JOIN_FIXTURES)
+def test_counts_match_reference(name):
+    """join_count_per_polygon: mode from the bundle, zero counts dropped."""
+    fx, bundle = setup(name)
+    got = join.join_count_per_polygon(bundle, fx["points"])
+    want = {int(k): int(v) for k, v in zip(fx["count_ids"], fx["count_values"])}
+    assert got == want
+    assert bundle.approx == bool(fx["bundle_approx"][0])
+
+
+@pytest.mark.parametrize("name", JOIN_FIXTURES)
+def test_probe_stats_match_reference(name):
+    fx, bundle = setup(name)
+    st = join.JoinStats()
+    join.accumulate_probe_stats(bundle, fx["points"], st)
+    assert st.as_tuple() == tuple(int(v) for v in fx["probe_stats"])
+    assert st.false_hits + st.solely_true_hits + st.refinement_entered == st.probes
+
+
+@pytest.mark.parametrize("name", ["join_small_exact", "cfg3_tess16_exact_trained", "cfg5_stars_scaled"])
+@pytest.mark.parametrize("kind", ["exact", "approx"])
+def test_first_id_and_overflow(name, kind):
+    fx, bundle = setup(name)
+    mode = capi.GJ_MODE_EXACT if kind == "exact" else capi.GJ_MODE_APPROX
+    counts, first, (opt, oid) = bundle.session().join_count(fx["points"], mode, want_ids=True)
+    epi, epid = golden_util.pairs_of(fx, kind)
+    n = len(fx["points"])
+    inline = (first != capi.GJ_NO_MATCH) & (first != capi.GJ_DEFERRED)
+    # rebuild the pair list: inline first ids + overflow records (already sorted)
+    pts = np.concatenate([np.nonzero(inline)[0].astype(np.uint64), opt])
+    ids = np.concatenate([first[inline] & ~np.uint32(capi.GJ_MORE_FLAG), oid])
+    seq = np.concatenate([np.zeros(int(inline.sum()), np.int64), 1 + np.arange(len(opt), dtype=np.int64)])
+    order = np.lexsort((seq, pts))
+    assert np.array_equal(pts[order], epi)
+    assert np.array_equal(ids[order], epid)
+    want = np.bincount(np.searchsorted(bundle.ids, epid), minlength=len(bundle.ids))
+    assert np.array_equal(counts, want.astype(np.uint64))
+    more = (first & capi.GJ_MORE_FLAG) != 0
+    per_point = np.bincount(epi.astype(np.int64), minlength=n)
+    assert np.array_equal(more & inline, (per_point > 1) & inline)
+
+
+def test_invalid_point_reports_first_index():
+    fx, bundle = setup("join_small_exact")
+    pts = fx["points"].copy()
+    pts[777, 0] = 91.0
+    pts[4242, 1] = np.nan
+    with pytest.raises(join.InvalidArgument) as e:
+        bundle.session().probe_points(pts)
+    assert e.value.index == 777
+    with pytest.raises(join.InvalidArgument) as e:
+        join.join_count_per_polygon(bundle, pts)
+    assert e.value.index == 777
+    pts = fx["points"].copy()
+    pts[5, 1] = np.inf
+    with pytest.raises(join.InvalidArgument):
+        join.join_exact(bundle, pts)
+
+
+def test_edge_sizes():
+    fx, bundle = setup("join_small_exact")
+    s = bundle.session()
+    assert len(s.probe_points(np.zeros((0, 2)))) == 0
+    assert join.join_count_per_polygon(bundle, np.zeros((0, 2))) == {}
+    for n in (1, 7, 8, 9, 1023, 4097):  # ragged tails around batch / tile sizes
+        pi, pid = join.join_exact(bundle, fx["points"][:n])
+        epi, epid = golden_util.pairs_of(fx, "exact")
+        keep = epi < n
+        assert np.array_equal(pi, epi[keep]) and np.array_equal(pid, epid[keep])
+
+
+def test_from_arrays_equals_load_file():
+    fx, bundle = setup("cfg2_tess16_approx4m")
+    g = golden_util.parse_gjx(golden_util.gjx_bytes(fx))
+    b2 = join.IndexBundle.from_arrays(g["arena"], g["lut"], g["roots"], g["prefixes"], g["prefix_bits"],
+                                      g["k_max"], g["approx"], g["polygon_ids"], g["vtx_off"],
+                                      g["vtx_latlng"], device=0)
+    assert np.array_equal(b2.session().probe_points(fx["points"]), fx["entries"])
+    assert b2.info.node_count == bundle.info.node_count and b2.info.dir_level == bundle.info.dir_level
+    b2.close()
