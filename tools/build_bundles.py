@@ -11,7 +11,9 @@ product then reads the GJX1 file with its own loader (``gj_index_load_file``).
 """
 from __future__ import annotations
 
+import os
 import sys
+import tempfile
 import time
 import zlib
 from pathlib import Path
@@ -25,15 +27,16 @@ if str(ROOT) not in sys.path:
 from paper_1802_09488_b200 import synth  # noqa: E402
 
 CACHE = ROOT / ".cache"
+# inflated copies live outside the repo so they are not shipped to the GPU box
+SCRATCH = Path(tempfile.gettempdir()) / f"gj_bundles_{os.getuid()}"
 
 
 def bundle_paths(name: str):
-    return CACHE / f"{name}.gjx", CACHE / f"{name}.gjx.z"
+    return SCRATCH / f"{name}.gjx", CACHE / f"{name}.gjx.z"
 
 
 def have_bundle(name: str) -> bool:
-    raw, z = bundle_paths(name)
-    return raw.exists() or z.exists()
+    return bundle_paths(name)[1].exists()
 
 
 def bundle_file(name: str) -> Path:
@@ -42,7 +45,8 @@ def bundle_file(name: str) -> Path:
     if not raw.exists():
         if not z.exists():
             raise FileNotFoundError(f"no cached index {name}; run tools/build_bundles.py")
-        tmp = raw.with_suffix(".tmp")
+        SCRATCH.mkdir(exist_ok=True)
+        tmp = raw.with_suffix(f".tmp{os.getpid()}")
         tmp.write_bytes(zlib.decompress(z.read_bytes()))
         tmp.rename(raw)
     return raw
@@ -53,6 +57,7 @@ def build_bundle(name: str, polys: synth.PolygonSet, spec: synth.WorkloadSpec,
     from oracle import ref  # the reference's build_index, offline
 
     CACHE.mkdir(exist_ok=True)
+    SCRATCH.mkdir(exist_ok=True)
     raw, z = bundle_paths(name)
     cfg = ref.default_config(mode_approx=int(spec.build_approx), precision_m=spec.precision_m,
                              k_max=spec.k_max, memory_budget_bytes=spec.budget_bytes,
