@@ -237,7 +237,8 @@ def run_ours(args):
     sess = bundle.session()
     info = bundle.info
     log(f"[bench] rank {rank}: index {info.node_count} nodes, {info.device_bytes / 1e6:.0f} MB HBM, "
-        f"directory level {info.dir_level} ({info.dir_width}x{info.dir_height}, dict {info.dir_dict_len})")
+        f"directory tier 1 level {info.dir_level} ({info.dir_width}x{info.dir_height}, shared memory), "
+        f"tier 2 level {info.dir2_level} ({info.dir2_width}x{info.dir2_height}, L2), dict {info.dir_dict_len}")
 
     t0 = time.time()
     host_pts = make_points(n, rank, pinned_alloc=L.gj_host_alloc)

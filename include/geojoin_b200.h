@@ -95,7 +95,10 @@ typedef struct {
   int32_t dir_level;          /* grid level resolved by the shared-memory directory */
   int32_t dir_width;          /* directory window, cells */
   int32_t dir_height;
-  int32_t dir_dict_len;       /* distinct terminal entries referenced by it */
+  int32_t dir_dict_len;       /* terminal entries that do not fit a directory code */
+  int32_t dir2_level;         /* second, L2-resident directory tier (0 = absent) */
+  int32_t dir2_width;
+  int32_t dir2_height;
   int32_t ids_dense;          /* 1 when id == slot for every polygon */
 } gj_index_info;
 
@@ -142,6 +145,13 @@ GJ_API void* gj_session_stream(gj_session* s);
 /* Pinned host memory for the *_host entry points (plain cudaHostAlloc). */
 GJ_API void* gj_host_alloc(size_t bytes);
 GJ_API void gj_host_free(void* p);
+
+/* ---- cell ids: cell_from_point (src/cell_id.cpp:82-95) over an array ------
+ * out_raw[i] is bitwise cell_from_point(p_i, level).raw; an invalid point
+ * returns GJ_INVALID_POINT, a level outside [0, 30] GJ_INVALID_ARGUMENT
+ * (both std::invalid_argument in the reference). */
+GJ_API int gj_cells_from_points_host(gj_session* s, const double* latlng, uint64_t n,
+                                     int level, uint64_t* out_raw, uint64_t* bad_index);
 
 /* ---- probe only: the ProbeBatchFn contract (act.hpp:270-276) at scale ----
  * out[i] is bitwise Act::probe(cell_from_point(p_i, k_max/2)); misses are 0.

@@ -39,17 +39,20 @@ def up_to_date() -> bool:
     return all(d.stat().st_mtime <= t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, defines=(), out: Path | None = None) -> Path:
+    """Default: the product library.  ``defines``/``out`` build tuning variants
+    (tools/k1_sweep.py) next to it."""
+    target = out or LIB
+    if out is None and not force and up_to_date():
         return LIB
-    cmd = [nvcc(), *NVCC_FLAGS, *(["-Xptxas", "-v"] if verbose else []),
-           "-o", str(LIB), *[str(CSRC / f) for f in SOURCES]]
+    cmd = [nvcc(), *NVCC_FLAGS, *(["-Xptxas", "-v"] if verbose else []), *[f"-D{d}" for d in defines],
+           "-o", str(target), *[str(CSRC / f) for f in SOURCES]]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError("nvcc failed:\n" + res.stdout + res.stderr)
     if verbose:
         print(res.stderr)
-    return LIB
+    return target
 
 
 if __name__ == "__main__":

@@ -22,7 +22,7 @@ GJ_MORE_FLAG = 0x80000000
 EXPORTS = [
     "gj_last_error", "gj_device_count", "gj_index_create", "gj_index_load_file", "gj_index_destroy",
     "gj_index_get_info", "gj_index_ids", "gj_session_create", "gj_session_destroy", "gj_session_stream",
-    "gj_host_alloc", "gj_host_free", "gj_probe_points_host", "gj_probe_cells_host",
+    "gj_host_alloc", "gj_host_free", "gj_cells_from_points_host", "gj_probe_points_host", "gj_probe_cells_host",
     "gj_join_count_host", "gj_join_count_device", "gj_session_sync", "gj_session_launches",
     "gj_join_pairs_host", "gj_pairs_copy",
 ]
@@ -45,7 +45,8 @@ class IndexInfo(C.Structure):
         ("n_ids", C.c_uint64), ("device_bytes", C.c_uint64),
         ("k_max", C.c_int32), ("approx_mode", C.c_int32), ("device", C.c_int32),
         ("dir_level", C.c_int32), ("dir_width", C.c_int32), ("dir_height", C.c_int32),
-        ("dir_dict_len", C.c_int32), ("ids_dense", C.c_int32),
+        ("dir_dict_len", C.c_int32), ("dir2_level", C.c_int32), ("dir2_width", C.c_int32),
+        ("dir2_height", C.c_int32), ("ids_dense", C.c_int32),
     ]
 
 
@@ -97,6 +98,8 @@ def lib():
         L.gj_session_launches.argtypes = [C.c_void_p]
         L.gj_session_sync.argtypes = [C.c_void_p, C.POINTER(C.c_uint64)]
         L.gj_probe_points_host.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p, C.POINTER(C.c_uint64)]
+        L.gj_cells_from_points_host.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_int, C.c_void_p,
+                                                C.POINTER(C.c_uint64)]
         L.gj_probe_cells_host.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_void_p]
         L.gj_join_count_host.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.c_int, C.c_void_p,
                                          C.POINTER(Stats), C.c_void_p, C.POINTER(Overflow), C.POINTER(C.c_uint64)]

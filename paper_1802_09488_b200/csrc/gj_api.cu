@@ -23,7 +23,7 @@ constexpr size_t kScratchBudget = 3ull << 30;      // per-chunk task + overflow 
 size_t align16(size_t v) { return (v + 15) & ~size_t{15}; }
 
 struct SmemPlan {
-  uint32_t dict_off, hist_off, hist_rep;
+  uint32_t queue_off, hist_off, hist_rep;
   size_t total;
 };
 
@@ -31,12 +31,8 @@ SmemPlan plan_smem(const gj_index& ix) {
   SmemPlan p{};
   size_t at = align16(std::max<size_t>(ix.dev.dir.n_table * 4, 16));
   const size_t limit = ix.smem_optin > 2048 ? ix.smem_optin - 1024 : 0;
-  if (ix.dev.dir.n_dict <= 4096 && at + align16(ix.dev.dir.n_dict * 8) <= limit) {
-    p.dict_off = static_cast<uint32_t>(at);
-    at += align16(ix.dev.dir.n_dict * 8);
-  } else {
-    p.dict_off = 0xFFFFFFFFu;
-  }
+  p.queue_off = static_cast<uint32_t>(at);
+  at += static_cast<size_t>(kJoinThreads / 32) * kQueueCap * sizeof(uint2);
   p.hist_off = static_cast<uint32_t>(at);
   const size_t room = std::min<size_t>(limit > at ? limit - at : 0, 64 << 10);
   uint32_t rep = 32;
@@ -47,10 +43,10 @@ SmemPlan plan_smem(const gj_index& ix) {
   return p;
 }
 
-template <bool kIds, bool kStats>
+template <bool kIds, bool kStats, bool kDense>
 int launch_join_variant(gj_session* s, const JoinParams& jp, const SmemPlan& sp) {
   const gj_index& ix = *s->ix;
-  auto kernel = join_kernel<kIds, kStats>;
+  auto kernel = join_kernel<kIds, kStats, kDense>;
   GJ_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(sp.total)));
   int occ = 0;
@@ -119,7 +115,7 @@ int enqueue_join(gj_session* s, const JoinRequest& rq) {
   jp.task_cap = rq.exact ? rq.task_cap : 0;
   jp.task_per_slot = s->d_task_per_slot.as<uint32_t>();
   jp.status = rq.d_status;
-  jp.smem_dict_off = sp.dict_off;
+  jp.smem_queue_off = sp.queue_off;
   jp.smem_hist_off = sp.hist_off;
   jp.hist_rep = sp.hist_rep;
   jp.exact = rq.exact ? 1 : 0;
@@ -138,10 +134,16 @@ int enqueue_join(gj_session* s, const JoinRequest& rq) {
     pl.unit_counter = base + 3 * (n_ids + 1);
   }
 
-  if (rq.d_first_id) {
-    rc = rq.want_stats ? launch_join_variant<true, true>(s, jp, sp) : launch_join_variant<true, false>(s, jp, sp);
-  } else {
-    rc = rq.want_stats ? launch_join_variant<false, true>(s, jp, sp) : launch_join_variant<false, false>(s, jp, sp);
+  const int variant = (rq.d_first_id ? 4 : 0) | (rq.want_stats ? 2 : 0) | (ix.dev.ids_dense ? 1 : 0);
+  switch (variant) {
+    case 0: rc = launch_join_variant<false, false, false>(s, jp, sp); break;
+    case 1: rc = launch_join_variant<false, false, true>(s, jp, sp); break;
+    case 2: rc = launch_join_variant<false, true, false>(s, jp, sp); break;
+    case 3: rc = launch_join_variant<false, true, true>(s, jp, sp); break;
+    case 4: rc = launch_join_variant<true, false, false>(s, jp, sp); break;
+    case 5: rc = launch_join_variant<true, false, true>(s, jp, sp); break;
+    case 6: rc = launch_join_variant<true, true, false>(s, jp, sp); break;
+    default: rc = launch_join_variant<true, true, true>(s, jp, sp); break;
   }
   if (rc != GJ_OK) return rc;
 
@@ -472,6 +474,37 @@ int gj_probe_points_host(gj_session* s, const double* latlng, uint64_t n, uint64
     ++s->launches;
     GJ_CUDA(cudaGetLastError());
     GJ_CUDA(cudaMemcpyAsync(out_entries + begin, s->d_entries.ptr, len * 8, cudaMemcpyDeviceToHost, s->stream));
+    GJ_CUDA(cudaStreamSynchronize(s->stream));
+  }
+  GJ_CUDA(cudaMemcpyAsync(&s->h_status[3], d_status, sizeof(DevStatus), cudaMemcpyDeviceToHost, s->stream));
+  GJ_CUDA(cudaStreamSynchronize(s->stream));
+  return status_to_code(s->h_status[3], bad_index);
+}
+
+int gj_cells_from_points_host(gj_session* s, const double* latlng, uint64_t n, int level, uint64_t* out_raw,
+                              uint64_t* bad_index) {
+  if (!s || (n && (!latlng || !out_raw))) return GJ_INVALID_ARGUMENT;
+  if (level < 0 || level > 30) {  // cell_id.cpp:86-88
+    set_error("cell_from_point: level out of range");
+    return GJ_INVALID_ARGUMENT;
+  }
+  gj_index& ix = *s->ix;
+  GJ_CUDA(cudaSetDevice(ix.device));
+  const uint64_t chunk = 4ull << 20;
+  GJ_CUDA(s->d_points[0].reserve(std::min(chunk, std::max<uint64_t>(n, 1)) * 16));
+  GJ_CUDA(s->d_entries.reserve(std::min(chunk, std::max<uint64_t>(n, 1)) * 8));
+  DevStatus* d_status = s->d_status.as<DevStatus>() + 3;
+  int rc = reset_status(s, d_status);
+  if (rc != GJ_OK) return rc;
+  for (uint64_t begin = 0; begin < n; begin += chunk) {
+    const uint64_t len = std::min(chunk, n - begin);
+    GJ_CUDA(cudaMemcpyAsync(s->d_points[0].ptr, latlng + 2 * begin, len * 16, cudaMemcpyHostToDevice, s->stream));
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((len + 255) / 256, ix.sm_count * 8ull));
+    cells_kernel<<<grid, 256, 0, s->stream>>>(s->d_points[0].as<double2>(), len, level, begin,
+                                              s->d_entries.as<uint64_t>(), d_status);
+    ++s->launches;
+    GJ_CUDA(cudaGetLastError());
+    GJ_CUDA(cudaMemcpyAsync(out_raw + begin, s->d_entries.ptr, len * 8, cudaMemcpyDeviceToHost, s->stream));
     GJ_CUDA(cudaStreamSynchronize(s->stream));
   }
   GJ_CUDA(cudaMemcpyAsync(&s->h_status[3], d_status, sizeof(DevStatus), cudaMemcpyDeviceToHost, s->stream));

@@ -13,7 +13,11 @@
 namespace gj {
 
 constexpr int kNodeSlots = 256;             // ActConfig::kFanout, act.hpp:36
-constexpr uint32_t kDirLink = 0x80000000u;  // directory code: continue in arena
+// Directory codes (u32): 0 = miss; bit 31 = continue the walk at node
+// (code & 0x7fffffff); bit 30 = one inlined payload ((polygon_id << 1) |
+// interior, ids below 2^29) in the low 30 bits; anything else indexes `dict`.
+constexpr uint32_t kDirLink = 0x80000000u;
+constexpr uint32_t kDirInline = 0x40000000u;
 constexpr uint32_t kNoMatch = 0xFFFFFFFFu;
 constexpr uint32_t kDeferred = 0xFFFFFFFEu;
 constexpr uint32_t kMoreFlag = 0x80000000u;
@@ -32,10 +36,9 @@ constexpr uint32_t kErrTaskCap = 8u;
 // at index-create time; results are bitwise those of the plain walk.
 struct DevDirectory {
   const uint32_t* table;  // [height * width], global copy
-  const uint64_t* dict;   // [n_dict], dict[0] == 0
   uint32_t width, height;
   uint32_t x0, y0;        // window origin in level-`level` cells
-  uint32_t n_table, n_dict;
+  uint32_t n_table;       // 0 = tier absent
   int32_t shift;          // 30 - level
   int32_t chunks;         // node steps already resolved
 };
@@ -57,7 +60,14 @@ struct DevIndex {
   int32_t leaf_level;      // k_max / 2
   int32_t prefix_level0;   // prefix_bits[0] / 2
   int32_t ids_dense;
+  // Two directory tiers over the same trie: `dir` is staged into shared
+  // memory by K1, `dir2` (deeper, optional) stays in global memory and is
+  // small enough to live in L2.  `dict` holds the terminal entries that do
+  // not fit a 32-bit code (two payloads, lookup-table offsets).
   DevDirectory dir;
+  DevDirectory dir2;
+  const uint64_t* dict;  // [n_dict], dict[0] == 0
+  uint32_t n_dict;
 };
 
 struct DevStatus {
@@ -83,6 +93,59 @@ __device__ __forceinline__ uint32_t grid_coord(double value, double lo, double s
   // __double2uint_rz saturates: negatives (and -0) give 0, like the clamp.
   const uint32_t cell = __double2uint_rz(scaled);
   return cell >= (1u << 30) ? (1u << 30) - 1u : cell;
+}
+
+// grid_coord for both axes without the division in the common case.
+//
+// Reference value: cell = trunc(s), s = RN(d / span) * 2^30, d = RN(v - lo).
+// Here p = RN(d * R) with R = RN(2^30 / span), so |p - s| <= 3.01 * 2^-53 * 2^30
+// < 3.6e-7.  Adding 2^31 puts p in [2^31, 2^32), where the double's 52
+// mantissa bits ARE the fixed-point number k = RN(p * 2^21) (|k 2^-21 - p| <=
+// 2^-22): integer part k >> 21, 21 fraction bits below.  Hence
+// |k 2^-21 - s| < 6.0e-7 = 1.26 * 2^-21, and whenever the fraction field f
+// satisfies 2 <= f <= 2^21 - 3 the integer part equals trunc(s) exactly
+// (and is < 2^30, so the upper clamp cannot bind).
+// Otherwise (probability 5 * 2^-21 per axis, and always for points on a grid
+// line or on the +90/+180 edge) the caller falls back to grid_coord().
+__device__ __forceinline__ bool grid_xy_fast(double lat, double lng, uint32_t* x, uint32_t* y) {
+  const double rx = 1073741824.0 / 360.0;  // RN(2^30 / 360), folded at compile time
+  const double ry = 1073741824.0 / 180.0;
+  const double tx = __dadd_rn(__dmul_rn(__dsub_rn(lng, -180.0), rx), 2147483648.0);
+  const double ty = __dadd_rn(__dmul_rn(__dsub_rn(lat, -90.0), ry), 2147483648.0);
+  const uint32_t xl = static_cast<uint32_t>(__double2loint(tx)), xh = static_cast<uint32_t>(__double2hiint(tx));
+  const uint32_t yl = static_cast<uint32_t>(__double2loint(ty)), yh = static_cast<uint32_t>(__double2hiint(ty));
+  *x = __funnelshift_l(xl, xh, 11);  // (hi << 11) | (lo >> 21): exponent bits fall off, bit 31 stays 0
+  *y = __funnelshift_l(yl, yh, 11);
+  const uint32_t fx = ((xl & 0x1FFFFFu) - 2u), fy = ((yl & 0x1FFFFFu) - 2u);
+  return max(fx, fy) <= 0x1FFFFFu - 4u;  // both fractions inside [2, 2^21 - 3]
+}
+
+// Both grid coordinates of a valid point, bit-exact (fast path + fallback).
+__device__ __forceinline__ void grid_xy(double lat, double lng, uint32_t* x, uint32_t* y) {
+  if (!grid_xy_fast(lat, lng, x, y)) {  // within 2^-20 of a cell boundary: do the division
+    *x = grid_coord(lng, -180.0, 360.0);
+    *y = grid_coord(lat, -90.0, 180.0);
+  }
+}
+
+// spread_bits (cell_id.cpp:30-37): bit i of the low 30 bits moves to bit 2i.
+__device__ __forceinline__ uint64_t spread_bits(uint64_t v) {
+  v = (v | (v << 16)) & 0x0000ffff0000ffffull;
+  v = (v | (v << 8)) & 0x00ff00ff00ff00ffull;
+  v = (v | (v << 4)) & 0x0f0f0f0f0f0f0f0full;
+  v = (v | (v << 2)) & 0x3333333333333333ull;
+  v = (v | (v << 1)) & 0x5555555555555555ull;
+  return v;
+}
+
+// cell_from_point (cell_id.cpp:82-95) for a valid point and level in [0, 30].
+__device__ __forceinline__ uint64_t cell_from_point(double lat, double lng, int level) {
+  uint32_t x, y;
+  grid_xy(lat, lng, &x, &y);
+  const uint64_t pos60 = (spread_bits(y) << 1) | spread_bits(x);
+  const uint64_t leaf = (pos60 << 1) | 1ull;
+  const uint64_t marker = 1ull << (60 - 2 * level);
+  return (leaf & ~(marker - 1) & ~marker) | marker;
 }
 
 // spread the low 4 bits of v to bit positions 0,2,4,6 (cell_id.cpp:30-37
@@ -117,23 +180,33 @@ __device__ __forceinline__ uint64_t walk_from(const DevIndex& ix, uint64_t node,
   }
 }
 
-// One point -> tagged entry, bitwise Act::probe(cell_from_point(p, k_max/2))
-// for face 0 (cell_from_point never sets face bits, cell_id.cpp:89-94).
-__device__ __forceinline__ uint64_t probe_point(const DevIndex& ix, const uint32_t* dir_table,
-                                                const uint64_t* dir_dict, double lat, double lng) {
-  uint32_t x = grid_coord(lng, -180.0, 360.0);
-  uint32_t y = grid_coord(lat, -90.0, 180.0);
-  const DevDirectory& d = ix.dir;
+// Directory lookup: the code of the level-`d` cell holding grid point (x, y).
+__device__ __forceinline__ uint32_t dir_code(const DevDirectory& d, const uint32_t* table, uint32_t x,
+                                             uint32_t y) {
   const uint32_t cx = (x >> d.shift) - d.x0;
   const uint32_t cy = (y >> d.shift) - d.y0;
   if (cx >= d.width || cy >= d.height) return 0;  // outside every indexed cell
-  const uint32_t code = dir_table[cy * d.width + cx];
+  return table[cy * d.width + cx];
+}
+
+// One point -> tagged entry, bitwise Act::probe(cell_from_point(p, k_max/2))
+// for face 0 (cell_from_point never sets face bits, cell_id.cpp:89-94).
+__device__ __forceinline__ uint64_t probe_point(const DevIndex& ix, const uint32_t* dir_table, double lat,
+                                                double lng) {
+  uint32_t x, y;
+  grid_xy(lat, lng, &x, &y);
+  uint32_t code = dir_code(ix.dir, dir_table, x, y);
+  int chunks = ix.dir.chunks;
+  if ((code & kDirLink) && ix.dir2.n_table) {
+    code = dir_code(ix.dir2, ix.dir2.table, x, y);
+    chunks = ix.dir2.chunks;
+  }
   if (code == 0) return 0;
-  if ((code & kDirLink) == 0) return dir_dict[code];
+  if ((code >> 30) == 1u) return (static_cast<uint64_t>(code & 0x3FFFFFFFu) << 2) | 1u;  // make_one
+  if ((code & kDirLink) == 0) return __ldg(ix.dict + code);
   // truncate to the leaf level (cell_id.cpp:93-94), left-align to 32 bits
   const uint32_t keep = ~((1u << (30 - ix.leaf_level)) - 1u);
-  return walk_from(ix, code & ~kDirLink, ix.prefix_level0 + 4 * d.chunks, (x & keep) << 2,
-                   (y & keep) << 2);
+  return walk_from(ix, code & ~kDirLink, ix.prefix_level0 + 4 * chunks, (x & keep) << 2, (y & keep) << 2);
 }
 
 // Generic probe of a raw cell id on any face without the directory: the

@@ -52,7 +52,6 @@ struct HostDirectory {
   int chunks = 0;  // node steps folded in
   uint32_t x0 = 0, y0 = 0, width = 0, height = 0;
   std::vector<uint32_t> table;
-  std::vector<uint64_t> dict;
 };
 
 }  // namespace gj
@@ -62,7 +61,7 @@ struct gj_index {
   gj::DevIndex dev{};
   gj_index_info info{};
   std::vector<uint32_t> ids;  // slot -> polygon id
-  gj::DeviceBuffer d_arena, d_lut, d_ids, d_ring_off, d_ring_len, d_ring_xy, d_dir_table, d_dir_dict;
+  gj::DeviceBuffer d_arena, d_lut, d_ids, d_ring_off, d_ring_len, d_ring_xy, d_dir_table, d_dir_dict, d_dir2_table;
   int sm_count = 0;
   size_t smem_optin = 0;
   uint64_t max_refs = 0;       // most references behind one reachable entry

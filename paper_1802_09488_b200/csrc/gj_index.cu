@@ -21,7 +21,8 @@ namespace {
 
 thread_local std::string g_error;
 
-constexpr uint64_t kMaxDirEntries = 36864;  // 144 KB of u32 codes
+constexpr uint64_t kMaxDirEntries = 32768;         // 128 KB of u32 codes (shared memory)
+constexpr uint64_t kMaxDir2Entries = 16ull << 20;  // 64 MB of u32 codes (stays in the 126 MB L2)
 constexpr uint64_t kMaxPolygonId = (1u << 30) - 1;
 
 struct Bitmap {
@@ -81,7 +82,9 @@ bool record_in_bounds(const gj_index_desc& d, uint64_t off) {  // act.cpp:141-15
 
 struct Analysis {
   std::vector<uint32_t> ids;
-  HostDirectory dir;
+  HostDirectory dir;           // shared-memory tier
+  HostDirectory dir2;          // global-memory (L2-resident) tier, deeper; may be empty
+  std::vector<uint64_t> dict;  // terminal entries that do not fit a directory code
   uint64_t max_refs = 0;       // most references behind one entry
   uint64_t max_cand_refs = 0;  // most candidate references behind one entry
 };
@@ -163,13 +166,17 @@ int analyse(const gj_index_desc& d, Analysis* out) {
     const int prefix_level = static_cast<int>(plen) / 2;
 
     // Directory bookkeeping (face 0 only; cell_from_point never leaves it).
+    // Two windows are kept: the deepest one small enough for shared memory
+    // and the deepest one small enough to stay L2-resident in global memory.
     bool track = face == 0;
-    std::vector<Cell> terminals;      // steps <= chosen depth
-    std::vector<Cell> frontier;       // nodes at the current depth, with cells
-    std::vector<Cell> best_links;     // frontier at the chosen depth
-    size_t best_terminals = 0;
-    Box best_box;
-    int best_chunks = 0;
+    std::vector<Cell> terminals;  // steps <= the deepest window still tracked
+    std::vector<Cell> frontier;   // nodes at the current depth, with cells
+    struct Snapshot {
+      int chunks = 0;
+      Box box;
+      std::vector<Cell> links;  // frontier at that depth
+      size_t n_terminals = 0;
+    } snap1, snap2;
 
     uint32_t px = 0, py = 0;
     unzip_pairs(d.prefixes[face], prefix_level, &px, &py);
@@ -214,53 +221,63 @@ int analyse(const gj_index_desc& d, Analysis* out) {
                   ((static_cast<uint64_t>(t.x) + 1) << s) - 1, ((static_cast<uint64_t>(t.y) + 1) << s) - 1);
         }
         for (const Cell& l : next) box.add(l.x, l.y, l.x, l.y);
-        if (box.area() <= kMaxDirEntries) {
-          best_chunks = depth + 1;
-          best_box = box;
-          best_links = next;
-          best_terminals = terminals.size();
+        if (box.area() <= kMaxDirEntries) snap1 = Snapshot{depth + 1, box, next, terminals.size()};
+        if (box.area() <= kMaxDir2Entries) {
+          snap2 = Snapshot{depth + 1, box, next, terminals.size()};
         } else {
           track = false;  // deeper windows only grow
-          terminals.resize(best_terminals);
+          terminals.resize(snap2.n_terminals);
           terminals.shrink_to_fit();
         }
       }
       frontier.swap(next);
     }
 
-    if (face == 0 && best_chunks > 0 && !best_box.empty()) {
-      dir.chunks = best_chunks;
-      dir.level = prefix_level + 4 * best_chunks;
-      dir.x0 = static_cast<uint32_t>(best_box.x_lo);
-      dir.y0 = static_cast<uint32_t>(best_box.y_lo);
-      dir.width = static_cast<uint32_t>(best_box.x_hi - best_box.x_lo + 1);
-      dir.height = static_cast<uint32_t>(best_box.y_hi - best_box.y_lo + 1);
-      dir.table.assign(static_cast<size_t>(dir.width) * dir.height, 0u);
-      dir.dict.assign(1, 0ull);
+    if (face == 0) {
       std::unordered_map<uint64_t, uint32_t> code_of;
-      terminals.resize(best_terminals);
-      for (const Cell& t : terminals) {
-        auto it = code_of.find(t.node_or_entry);
-        if (it == code_of.end()) {
-          it = code_of.emplace(t.node_or_entry, static_cast<uint32_t>(dir.dict.size())).first;
-          dir.dict.push_back(t.node_or_entry);
+      out->dict.assign(1, 0ull);
+      auto fill = [&](const Snapshot& sn, HostDirectory& hd) {
+        if (sn.chunks == 0 || sn.box.empty()) return;
+        hd.chunks = sn.chunks;
+        hd.level = prefix_level + 4 * sn.chunks;
+        hd.x0 = static_cast<uint32_t>(sn.box.x_lo);
+        hd.y0 = static_cast<uint32_t>(sn.box.y_lo);
+        hd.width = static_cast<uint32_t>(sn.box.x_hi - sn.box.x_lo + 1);
+        hd.height = static_cast<uint32_t>(sn.box.y_hi - sn.box.y_lo + 1);
+        hd.table.assign(static_cast<size_t>(hd.width) * hd.height, 0u);
+        for (size_t ti = 0; ti < sn.n_terminals; ++ti) {
+          const Cell& t = terminals[ti];
+          auto it = code_of.find(t.node_or_entry);
+          if (it == code_of.end()) {
+            const uint64_t e = t.node_or_entry;
+            uint32_t code;
+            if ((e & 3) == 1 && ((e >> 2) & 0x7fffffffu) < kDirInline) {
+              code = kDirInline | static_cast<uint32_t>((e >> 2) & 0x3fffffffu);  // payload inlined
+            } else {
+              code = static_cast<uint32_t>(out->dict.size());
+              out->dict.push_back(e);
+            }
+            it = code_of.emplace(e, code).first;
+          }
+          const int s = 4 * (sn.chunks - t.step);
+          const uint64_t bx = (static_cast<uint64_t>(t.x) << s) - hd.x0;
+          const uint64_t by = (static_cast<uint64_t>(t.y) << s) - hd.y0;
+          const uint64_t side = 1ull << s;
+          for (uint64_t yy = 0; yy < side; ++yy) {
+            uint32_t* row = hd.table.data() + (by + yy) * hd.width + bx;
+            std::fill(row, row + side, it->second);
+          }
         }
-        const int s = 4 * (best_chunks - t.step);
-        const uint64_t bx = (static_cast<uint64_t>(t.x) << s) - dir.x0;
-        const uint64_t by = (static_cast<uint64_t>(t.y) << s) - dir.y0;
-        const uint64_t side = 1ull << s;
-        for (uint64_t yy = 0; yy < side; ++yy) {
-          uint32_t* row = dir.table.data() + (by + yy) * dir.width + bx;
-          std::fill(row, row + side, it->second);
+        for (const Cell& l : sn.links) {
+          hd.table[static_cast<size_t>(l.y - hd.y0) * hd.width + (l.x - hd.x0)] =
+              kDirLink | static_cast<uint32_t>(l.node_or_entry);
         }
-      }
-      for (const Cell& l : best_links) {
-        dir.table[static_cast<size_t>(l.y - dir.y0) * dir.width + (l.x - dir.x0)] =
-            kDirLink | static_cast<uint32_t>(l.node_or_entry);
-      }
+      };
+      fill(snap1, dir);
+      if (snap2.chunks > snap1.chunks) fill(snap2, out->dir2);
     }
   }
-  if (dir.level > 30) {
+  if (dir.level > 30 || out->dir2.level > 30) {
     set_error("directory level out of range");
     return GJ_CORRUPT_INDEX;
   }
@@ -368,7 +385,8 @@ int create_index(const gj_index_desc& d, int device, gj_index** out) {
   if ((rc = upload(ix->d_ring_len, ring_len.data(), ring_len.size(), &bytes)) != GJ_OK) return rc;
   if ((rc = upload(ix->d_ring_xy, ring_xy.data(), ring_xy.size(), &bytes)) != GJ_OK) return rc;
   if ((rc = upload(ix->d_dir_table, an.dir.table.data(), an.dir.table.size(), &bytes)) != GJ_OK) return rc;
-  if ((rc = upload(ix->d_dir_dict, an.dir.dict.data(), an.dir.dict.size(), &bytes)) != GJ_OK) return rc;
+  if ((rc = upload(ix->d_dir_dict, an.dict.data(), an.dict.size(), &bytes)) != GJ_OK) return rc;
+  if ((rc = upload(ix->d_dir2_table, an.dir2.table.data(), an.dir2.table.size(), &bytes)) != GJ_OK) return rc;
 
   DevIndex& dv = ix->dev;
   dv.arena = ix->d_arena.as<uint64_t>();
@@ -387,16 +405,20 @@ int create_index(const gj_index_desc& d, int device, gj_index** out) {
   dv.leaf_level = d.k_max / 2;
   dv.prefix_level0 = static_cast<int>(d.prefix_bits[0]) / 2;
   dv.ids_dense = dense ? 1 : 0;
-  dv.dir.table = ix->d_dir_table.as<uint32_t>();
-  dv.dir.dict = ix->d_dir_dict.as<uint64_t>();
-  dv.dir.width = an.dir.width;
-  dv.dir.height = an.dir.height;
-  dv.dir.x0 = an.dir.x0;
-  dv.dir.y0 = an.dir.y0;
-  dv.dir.n_table = static_cast<uint32_t>(an.dir.table.size());
-  dv.dir.n_dict = static_cast<uint32_t>(an.dir.dict.size());
-  dv.dir.shift = 30 - an.dir.level;
-  dv.dir.chunks = an.dir.chunks;
+  auto set_dir = [](DevDirectory& dd, const HostDirectory& hd, const uint32_t* table) {
+    dd.table = table;
+    dd.width = hd.width;
+    dd.height = hd.height;
+    dd.x0 = hd.x0;
+    dd.y0 = hd.y0;
+    dd.n_table = static_cast<uint32_t>(hd.table.size());
+    dd.shift = 30 - hd.level;
+    dd.chunks = hd.chunks;
+  };
+  set_dir(dv.dir, an.dir, ix->d_dir_table.as<uint32_t>());
+  set_dir(dv.dir2, an.dir2, ix->d_dir2_table.as<uint32_t>());
+  dv.dict = ix->d_dir_dict.as<uint64_t>();
+  dv.n_dict = static_cast<uint32_t>(an.dict.size());
 
   cudaDeviceProp prop{};
   GJ_CUDA(cudaGetDeviceProperties(&prop, device));
@@ -415,7 +437,10 @@ int create_index(const gj_index_desc& d, int device, gj_index** out) {
   info.dir_level = an.dir.level;
   info.dir_width = static_cast<int32_t>(an.dir.width);
   info.dir_height = static_cast<int32_t>(an.dir.height);
-  info.dir_dict_len = static_cast<int32_t>(an.dir.dict.size());
+  info.dir_dict_len = static_cast<int32_t>(an.dict.size());
+  info.dir2_level = an.dir2.table.empty() ? 0 : an.dir2.level;
+  info.dir2_width = static_cast<int32_t>(an.dir2.width);
+  info.dir2_height = static_cast<int32_t>(an.dir2.height);
   info.ids_dense = dense ? 1 : 0;
   *out = ix.release();
   return GJ_OK;

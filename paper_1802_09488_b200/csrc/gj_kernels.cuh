@@ -15,8 +15,20 @@
 
 namespace gj {
 
-constexpr int kJoinThreads = 1024;
-constexpr int kPointsPerThread = 4;
+// Tunables (overridable with -D for tools/k1_sweep.py).
+#ifndef GJ_JOIN_THREADS
+#define GJ_JOIN_THREADS 1024
+#endif
+#ifndef GJ_JOIN_MIN_BLOCKS
+#define GJ_JOIN_MIN_BLOCKS 1
+#endif
+#ifndef GJ_PPT
+#define GJ_PPT 4
+#endif
+constexpr int kJoinThreads = GJ_JOIN_THREADS;
+constexpr int kPointsPerThread = GJ_PPT;
+// open-point queue entries per warp: < 32 left over + up to 32 per point slot of a tile
+constexpr int kQueueCap = 32 * (kPointsPerThread + 1);
 constexpr int kRefineThreads = 256;
 constexpr int kRefineTile = 64;  // vertices staged per warp and tile
 
@@ -37,7 +49,7 @@ struct JoinParams {
   uint64_t task_cap;
   uint32_t* task_per_slot;  // [n_ids]
   DevStatus* status;
-  uint32_t smem_dict_off;   // bytes; 0xFFFFFFFF = dictionary stays in global
+  uint32_t smem_queue_off;  // bytes: per-warp open-point queues
   uint32_t smem_hist_off;   // bytes
   uint32_t hist_rep;        // replicas per slot (power of two), 0 = global atomics
   int32_t exact;
@@ -63,29 +75,55 @@ __device__ __forceinline__ void flag_error(DevStatus* st, uint32_t bit, uint64_t
 }
 
 // Per-thread emit state of K1.
-template <bool kIds, bool kStats>
+template <bool kIds, bool kStats, bool kDense>
 struct Emitter {
   const DevIndex& ix;
   const JoinParams& jp;
   uint32_t* s_hist;
-  uint32_t lane_rep;  // lane & (hist_rep - 1)
+  uint32_t hist_rep, lane_rep;  // replicas per slot, lane & (hist_rep - 1)
+  bool exact;
   uint32_t false_hits = 0, solely_true = 0, refined = 0, cand_refs = 0;
 
-  __device__ __forceinline__ Emitter(const DevIndex& i, const JoinParams& j, uint32_t* h, uint32_t lr)
-      : ix(i), jp(j), s_hist(h), lane_rep(lr) {}
+  __device__ __forceinline__ Emitter(const DevIndex& i, const JoinParams& j, uint32_t* h, uint32_t lane)
+      : ix(i), jp(j), s_hist(h), hist_rep(j.hist_rep), lane_rep(lane & (j.hist_rep ? j.hist_rep - 1u : 0u)),
+        exact(j.exact != 0) {}
+
+  __device__ __forceinline__ uint32_t slot_of(uint32_t id) const { return kDense ? id : id_to_slot(ix, id); }
 
   __device__ __forceinline__ void count(uint32_t slot) {
-    if (jp.hist_rep) {
-      atomicAdd(&s_hist[slot * jp.hist_rep + lane_rep], 1u);
+#ifdef GJ_EXP_NO_HIST  // timing experiment: results are wrong
+    return;
+#endif
+    if (hist_rep) {
+      atomicAdd(&s_hist[slot * hist_rep + lane_rep], 1u);
     } else {
       atomicAdd(&jp.counts[slot], 1ull);
     }
+  }
+
+  // One inlined payload ((polygon_id << 1) | interior) that emits right here:
+  // a true hit, or a candidate in approximate mode (join.cpp:100-108).
+  __device__ __forceinline__ bool emits_now(uint32_t payload) const { return (payload & 1u) != 0u || !exact; }
+
+  __device__ __forceinline__ uint32_t emit_single(uint32_t payload) {
+    const uint32_t id = payload >> 1;
+    count(slot_of(id));
+    if (kStats) {
+      if (payload & 1u) {
+        ++solely_true;
+      } else {
+        ++refined;
+        ++cand_refs;
+      }
+    }
+    return id;
   }
 
   // k-th reference of an entry in the reference's emit order
   // (act.hpp:169-196): payload = (polygon_id << 1) | interior.
   __device__ __forceinline__ uint32_t ref_payload(uint64_t entry, uint32_t tag, uint32_t k, uint32_t off,
                                                   uint32_t t) const {
+    if (tag == 1u) return static_cast<uint32_t>(entry >> 2) & 0x7fffffffu;
     if (tag == 2u) {
       return k == 0 ? static_cast<uint32_t>(entry >> 33) & 0x7fffffffu
                     : static_cast<uint32_t>(entry >> 2) & 0x7fffffffu;
@@ -94,50 +132,31 @@ struct Emitter {
     return k < t ? (__ldg(ix.lut + off + 1 + k) << 1) | 1u : (__ldg(ix.lut + off + 2 + k) << 1);
   }
 
-  // The per-(point, entry) body of run_join, join.cpp:93-127.  Returns the
-  // first-id word for the point.
-  __device__ __forceinline__ uint32_t handle(uint64_t entry, uint64_t local) {
-    if (entry == 0) {
-      if (kStats) ++false_hits;
-      return kNoMatch;
-    }
-    const uint32_t tag = static_cast<uint32_t>(entry) & 3u;
-    if (tag == 1u) {  // one inlined payload: the overwhelmingly common case
+  // The per-(point, entry) body of run_join, join.cpp:93-127, for a
+  // non-sentinel entry.  Returns the first-id word of the point.
+  __device__ __forceinline__ uint32_t handle(uint64_t entry, uint32_t local) {
+    if ((static_cast<uint32_t>(entry) & 3u) == 1u) {
       const uint32_t p = static_cast<uint32_t>(entry >> 2) & 0x7fffffffu;
-      const uint32_t id = p >> 1;
-      if ((p & 1u) != 0u || !jp.exact) {
-        count(id_to_slot(ix, id));
-        if (kStats) {
-          if (p & 1u) {
-            ++solely_true;
-          } else {
-            ++refined;
-            ++cand_refs;
-          }
-        }
-        return id;
-      }
+      if (emits_now(p)) return emit_single(p);
     }
-    return handle_general(entry, tag, local);
+    return handle_general(entry, local);
   }
 
-  __device__ __noinline__ uint32_t handle_general(uint64_t entry, uint32_t tag, uint64_t local) {
-    uint32_t off = 0, t = 0, n_refs;
+  // Everything else: two payloads, lookup-table records, exact-mode
+  // candidates (tasks for K2) and the overflow list.  Cold.
+  __device__ __noinline__ uint32_t handle_general(uint64_t entry, uint32_t local) {
+    const uint32_t tag = static_cast<uint32_t>(entry) & 3u;
+    uint32_t off = 0, t = 0, n_refs, n_cand;
     if (tag == 1u) {
       n_refs = 1;
+      n_cand = 1;  // only exact-mode candidates get here with one payload
     } else if (tag == 2u) {
       n_refs = 2;
+      n_cand = 2u - ((static_cast<uint32_t>(entry >> 33) & 1u) + (static_cast<uint32_t>(entry >> 2) & 1u));
     } else {
       off = static_cast<uint32_t>(entry >> 2) & 0x7fffffffu;
       t = __ldg(ix.lut + off);
       n_refs = t + __ldg(ix.lut + off + 1 + t);
-    }
-    uint32_t n_cand = 0;
-    if (tag == 1u) {
-      n_cand = 1;  // only exact-mode candidates reach here with tag 1
-    } else if (tag == 2u) {
-      n_cand = 2u - ((static_cast<uint32_t>(entry >> 33) & 1u) + (static_cast<uint32_t>(entry >> 2) & 1u));
-    } else {
       n_cand = n_refs - t;
     }
     if (kStats) {
@@ -148,8 +167,8 @@ struct Emitter {
         cand_refs += n_cand;
       }
     }
-    const bool defer = jp.exact && n_cand != 0;  // some pairs depend on K2
-    const uint32_t n_now = jp.exact ? n_refs - n_cand : n_refs;  // pairs emitted here
+    const bool defer = exact && n_cand != 0;                  // some pairs depend on K2
+    const uint32_t n_now = exact ? n_refs - n_cand : n_refs;  // pairs emitted here
 
     // overflow records: everything after the first pair, or every pair when
     // the point is deferred
@@ -176,11 +195,10 @@ struct Emitter {
     uint32_t first = defer ? kDeferred : kNoMatch;
     uint32_t emitted = 0, tasks = 0;
     for (uint32_t k = 0; k < n_refs; ++k) {
-      const uint32_t p = tag == 1u ? static_cast<uint32_t>(entry >> 2) & 0x7fffffffu
-                                   : ref_payload(entry, tag, k, off, t);
+      const uint32_t p = ref_payload(entry, tag, k, off, t);
       const uint32_t id = p >> 1;
-      const uint32_t slot = id_to_slot(ix, id);
-      if ((p & 1u) != 0u || !jp.exact) {
+      const uint32_t slot = slot_of(id);
+      if (emits_now(p)) {
         count(slot);
         if (kIds) {
           if (!defer && emitted == 0) {
@@ -199,7 +217,7 @@ struct Emitter {
         }
         if (tasks_ok) {
           const uint64_t w = task_base + tasks;
-          jp.task_point[w] = static_cast<uint32_t>(local);
+          jp.task_point[w] = local;
           jp.task_slot[w] = slot;
           jp.task_ord[w] = k;
           atomicAdd(&jp.task_per_slot[slot], 1u);
@@ -211,63 +229,183 @@ struct Emitter {
   }
 };
 
-// K1.  Persistent grid (one CTA per SM slot); each CTA stages the directory
-// (and a replicated per-polygon histogram) in shared memory once, then
-// streams tiles of points: 16-byte coalesced loads, kPointsPerThread
-// independent points in flight per thread.
-template <bool kIds, bool kStats>
-__global__ void __launch_bounds__(kJoinThreads, 1)
+// K1.  Persistent grid (one CTA per SM slot); each CTA stages the first
+// directory tier (and a replicated per-polygon histogram) in shared memory
+// once, then streams tiles of points: 16-byte coalesced loads,
+// kPointsPerThread independent points in flight per thread.  A tile runs in
+// three phases of decreasing population:
+//   1. all points (warp-uniform): cell coordinates, shared-memory directory,
+//      emit when it resolves to one payload;
+//   2. points under a directory link: one independent gather each into the
+//      second, L2-resident directory tier — all gathers of the tile are
+//      issued before any is consumed;
+//   3. the remainder: dependent 8-byte gathers down the arena, dictionary and
+//      lookup-table entries, exact-mode candidates.
+template <bool kIds, bool kStats, bool kDense>
+__global__ void __launch_bounds__(kJoinThreads, GJ_JOIN_MIN_BLOCKS)
 join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinParams jp) {
   extern __shared__ __align__(16) unsigned char smem[];
   uint32_t* s_table = reinterpret_cast<uint32_t*>(smem);
-  const bool dict_in_smem = jp.smem_dict_off != 0xFFFFFFFFu;
-  uint64_t* s_dict = reinterpret_cast<uint64_t*>(smem + (dict_in_smem ? jp.smem_dict_off : 0));
   uint32_t* s_hist = reinterpret_cast<uint32_t*>(smem + jp.smem_hist_off);
   const uint32_t tid = threadIdx.x;
 
-  {  // stage directory + dictionary, clear histogram
+  {  // stage the directory, clear the histogram
     const uint4* src = reinterpret_cast<const uint4*>(ix.dir.table);
     uint4* dst = reinterpret_cast<uint4*>(s_table);
     const uint32_t n4 = (ix.dir.n_table + 3) / 4;  // buffers are padded to 16 B
     for (uint32_t i = tid; i < n4; i += kJoinThreads) dst[i] = __ldg(src + i);
-    if (dict_in_smem) {
-      for (uint32_t i = tid; i < ix.dir.n_dict; i += kJoinThreads) s_dict[i] = __ldg(ix.dir.dict + i);
-    }
     const uint32_t n_hist = ix.n_ids * jp.hist_rep;
     for (uint32_t i = tid; i < n_hist; i += kJoinThreads) s_hist[i] = 0;
   }
   __syncthreads();
-  const uint64_t* dict = dict_in_smem ? s_dict : ix.dir.dict;
 
-  Emitter<kIds, kStats> em(ix, jp, s_hist, (tid & 31u) & (jp.hist_rep ? jp.hist_rep - 1u : 0u));
+  Emitter<kIds, kStats, kDense> em(ix, jp, s_hist, tid & 31u);
   uint32_t n_valid = 0;
 
-  constexpr uint64_t kTile = static_cast<uint64_t>(kJoinThreads) * kPointsPerThread;
-  const uint64_t n_tiles = (jp.n + kTile - 1) / kTile;
-  for (uint64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-    const uint64_t base = tile * kTile + tid;
+  // loop invariants in registers
+  const uint32_t dir_w = ix.dir.width, dir_h = ix.dir.height, dir_x0 = ix.dir.x0, dir_y0 = ix.dir.y0;
+  const int dir_shift = ix.dir.shift;
+  const bool has_dir2 = ix.dir2.n_table != 0;
+  const uint32_t* __restrict__ table2 = ix.dir2.table;
+  const uint32_t d2_w = ix.dir2.width, d2_h = ix.dir2.height, d2_x0 = ix.dir2.x0, d2_y0 = ix.dir2.y0;
+  const int d2_shift = ix.dir2.shift;
+  const int walk_level = ix.prefix_level0 + 4 * (has_dir2 ? ix.dir2.chunks : ix.dir.chunks);
+  const uint32_t leaf_keep = ~((1u << (30 - ix.leaf_level)) - 1u);  // cell_id.cpp:93-94
+  const double2* __restrict__ pts = jp.pts;
+  uint32_t* __restrict__ first_id = jp.first_id;
+  const uint32_t n = static_cast<uint32_t>(jp.n);  // <= 2^31 per launch
+
+  // per-warp queue of open points: (point index, directory code)
+  const uint32_t lane = tid & 31u;
+  const uint32_t lane_lt = (1u << lane) - 1u;
+  uint2* s_queue = reinterpret_cast<uint2*>(smem + jp.smem_queue_off) + (tid >> 5) * kQueueCap;
+  uint32_t q_count = 0;  // warp-uniform
+
+  // Phase 3 for one open point: arena descent (dependent 8-byte gathers),
+  // dictionary entries, exact-mode candidates.
+  auto resolve_open = [&](uint32_t i, uint32_t c) {
+    uint64_t entry;
+    if (c & kDirLink) {
+      const double2 q = __ldg(pts + i);  // cheaper to re-read than to queue the coordinates
+      uint32_t x, y;
+      grid_xy(q.x, q.y, &x, &y);
+      entry = walk_from(ix, c & ~kDirLink, walk_level, (x & leaf_keep) << 2, (y & leaf_keep) << 2);
+    } else if (c & kDirInline) {
+      entry = (static_cast<uint64_t>(c & 0x3FFFFFFFu) << 2) | 1u;  // exact-mode candidate
+    } else {
+      entry = __ldg(ix.dict + c);
+    }
+    uint32_t first = kNoMatch;
+    if (entry == 0) {
+      if (kStats) ++em.false_hits;
+    } else {
+      first = em.handle(entry, i);
+    }
+    if (kIds) __stcs(first_id + i, first);
+  };
+
+  constexpr uint32_t kTile = kJoinThreads * kPointsPerThread;
+  const uint32_t n_tiles = (n + kTile - 1) / kTile;
+  for (uint32_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const uint32_t base = tile * kTile + tid;
+    const bool full = n - tile * kTile >= kTile;
     double2 p[kPointsPerThread];
+    uint32_t code[kPointsPerThread], gx[kPointsPerThread], gy[kPointsPerThread];
 #pragma unroll
     for (int j = 0; j < kPointsPerThread; ++j) {
-      const uint64_t i = base + static_cast<uint64_t>(j) * kJoinThreads;
-      // streaming read, touched once: evict-first
-      p[j] = i < jp.n ? __ldcs(jp.pts + i) : make_double2(0.0, 0.0);
+      const uint32_t i = base + j * kJoinThreads;
+      // streaming read, touched once: evict-first; out-of-range lanes get an invalid point
+      p[j] = (full || i < n) ? __ldcs(pts + i) : make_double2(1e300, 1e300);
     }
+    // ---- phase 1: shared-memory directory ----
 #pragma unroll
     for (int j = 0; j < kPointsPerThread; ++j) {
-      const uint64_t i = base + static_cast<uint64_t>(j) * kJoinThreads;
-      if (i >= jp.n) break;
-      uint64_t entry = 0;
+      const uint32_t i = base + j * kJoinThreads;
+      uint32_t first = kNoMatch;
+      code[j] = 0;
       if (latlng_valid(p[j].x, p[j].y)) {
-        entry = probe_point(ix, s_table, dict, p[j].x, p[j].y);
         ++n_valid;
-      } else {
+        uint32_t x, y;
+        grid_xy(p[j].x, p[j].y, &x, &y);
+        const uint32_t cx = (x >> dir_shift) - dir_x0;
+        const uint32_t cy = (y >> dir_shift) - dir_y0;
+        uint32_t c = 0;
+        if (cx < dir_w && cy < dir_h) c = s_table[cy * dir_w + cx];
+        if ((c >> 30) == 1u && em.emits_now(c & 0x3FFFFFFFu)) {
+          first = em.emit_single(c & 0x3FFFFFFFu);
+        } else if (c == 0) {
+          if (kStats) ++em.false_hits;
+        } else {
+          code[j] = c;
+          gx[j] = x;
+          gy[j] = y;
+        }
+      } else if (full || i < n) {
         flag_error(jp.status, kErrInvalidPoint, jp.base_index + i);  // cell_id.cpp:83-85
-        continue;
       }
-      const uint32_t first = em.handle(entry, i);
-      if (kIds) __stcs(jp.first_id + i, first);
+      if (kIds && code[j] == 0 && (full || i < n)) __stcs(first_id + i, first);
     }
+#ifdef GJ_EXP_PHASE1_ONLY  // timing experiment: results are wrong
+    continue;
+#endif
+    // ---- phase 2: second directory tier (one gather per linked point) ----
+    if (has_dir2) {
+      uint32_t c2[kPointsPerThread];
+#pragma unroll
+      for (int j = 0; j < kPointsPerThread; ++j) {
+        c2[j] = code[j];
+        if (code[j] & kDirLink) {
+          const uint32_t cx = (gx[j] >> d2_shift) - d2_x0;
+          const uint32_t cy = (gy[j] >> d2_shift) - d2_y0;
+          c2[j] = (cx < d2_w && cy < d2_h) ? __ldg(table2 + cy * d2_w + cx) : 0u;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < kPointsPerThread; ++j) {
+        if ((code[j] & kDirLink) == 0) continue;
+        const uint32_t c = c2[j];
+        const uint32_t i = base + j * kJoinThreads;
+        if ((c >> 30) == 1u && em.emits_now(c & 0x3FFFFFFFu)) {
+          const uint32_t first = em.emit_single(c & 0x3FFFFFFFu);
+          if (kIds) __stcs(first_id + i, first);
+          code[j] = 0;
+        } else if (c == 0) {
+          if (kStats) ++em.false_hits;
+          if (kIds) __stcs(first_id + i, kNoMatch);
+          code[j] = 0;
+        } else {
+          code[j] = c;
+        }
+      }
+    }
+    // ---- phase 3, deferred: what is still open goes to this warp's queue ----
+    // Few points get here (directory links into deep boundary nodes,
+    // dictionary entries, exact-mode candidates).  Running them where they
+    // occur would drag all 32 lanes through the long path for one or two
+    // active ones, so they are compacted per warp and drained 32 at a time.
+#pragma unroll
+    for (int j = 0; j < kPointsPerThread; ++j) {
+      const bool open = code[j] != 0;
+      const uint32_t mask = __ballot_sync(0xffffffffu, open);
+      if (open) {
+        s_queue[q_count + __popc(mask & lane_lt)] = make_uint2(base + j * kJoinThreads, code[j]);
+      }
+      q_count += __popc(mask);
+    }
+#ifdef GJ_EXP_NO_PHASE3  // timing experiment: results are wrong
+    q_count = 0;
+#endif
+    __syncwarp();
+    while (q_count >= 32u) {
+      q_count -= 32u;
+      const uint2 item = s_queue[q_count + lane];
+      __syncwarp();
+      resolve_open(item.x, item.y);
+    }
+  }
+  if (lane < q_count) {  // the last, partial batch
+    const uint2 item = s_queue[lane];
+    resolve_open(item.x, item.y);
   }
 
   __syncthreads();
@@ -285,12 +423,12 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
       for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
     }
     if ((tid & 31u) == 0) {
-      atomicAdd(&jp.stats[0], static_cast<unsigned long long>(v[0]));                      // probes
-      if (jp.exact) atomicAdd(&jp.stats[1], static_cast<unsigned long long>(v[4]));        // pip_tests
-      atomicAdd(&jp.stats[2], static_cast<unsigned long long>(v[1]));                      // false_hits
-      atomicAdd(&jp.stats[3], static_cast<unsigned long long>(v[2]));                      // solely_true_hits
-      atomicAdd(&jp.stats[4], static_cast<unsigned long long>(v[3]));                      // refinement_entered
-      atomicAdd(&jp.stats[5], static_cast<unsigned long long>(v[4]));                      // candidate_refs
+      atomicAdd(&jp.stats[0], static_cast<unsigned long long>(v[0]));                // probes
+      if (jp.exact) atomicAdd(&jp.stats[1], static_cast<unsigned long long>(v[4]));  // pip_tests
+      atomicAdd(&jp.stats[2], static_cast<unsigned long long>(v[1]));                // false_hits
+      atomicAdd(&jp.stats[3], static_cast<unsigned long long>(v[2]));                // solely_true_hits
+      atomicAdd(&jp.stats[4], static_cast<unsigned long long>(v[3]));                // refinement_entered
+      atomicAdd(&jp.stats[5], static_cast<unsigned long long>(v[4]));                // candidate_refs
     }
   }
 }
@@ -308,11 +446,28 @@ probe_points_kernel(const __grid_constant__ DevIndex ix, const double2* __restri
     const double2 p = __ldcs(pts + i);
     uint64_t e = 0;
     if (latlng_valid(p.x, p.y)) {
-      e = probe_point(ix, s_table, ix.dir.dict, p.x, p.y);
+      e = probe_point(ix, s_table, p.x, p.y);
     } else {
       flag_error(status, kErrInvalidPoint, base_index + i);
     }
     out[i] = e;
+  }
+}
+
+// cell_from_point over an array (cell_id.cpp:82-95).
+__global__ void __launch_bounds__(256)
+cells_kernel(const double2* __restrict__ pts, uint64_t n, int level, uint64_t base_index,
+             uint64_t* __restrict__ out, DevStatus* status) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const double2 p = __ldcs(pts + i);
+    uint64_t raw = 0;
+    if (latlng_valid(p.x, p.y)) {
+      raw = cell_from_point(p.x, p.y, level);
+    } else {
+      flag_error(status, kErrInvalidPoint, base_index + i);
+    }
+    out[i] = raw;
   }
 }
 

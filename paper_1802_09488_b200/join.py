@@ -214,6 +214,16 @@ class Session:
     def launches(self) -> int:
         return int(capi.lib().gj_session_launches(self._h))
 
+    # ---- cell ids ----
+    def cells_from_points(self, points, level: int) -> np.ndarray:
+        """cell_from_point over an array (cell_id.cpp:82-95)."""
+        p = _points(points)
+        out = np.empty(len(p), np.uint64)
+        bad = C.c_uint64(0)
+        _check(capi.lib().gj_cells_from_points_host(self._h, _vp(p), len(p), int(level), _vp(out),
+                                                    C.byref(bad)), bad)
+        return out
+
     # ---- probe ----
     def probe_points(self, points) -> np.ndarray:
         p = _points(points)

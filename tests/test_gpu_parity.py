@@ -147,3 +147,49 @@ def test_from_arrays_equals_load_file():
     assert np.array_equal(b2.session().probe_points(fx["points"]), fx["entries"])
     assert b2.info.node_count == bundle.info.node_count and b2.info.dir_level == bundle.info.dir_level
     b2.close()
+
+
+def test_cell_ids_match_reference_fixture():
+    """cell_from_point: KATs, seed 0x5eed0001 cases, clamps and grid-line points."""
+    fx = golden_util.load("cells")
+    _, bundle = setup("join_small_exact")
+    s = bundle.session()
+    assert np.array_equal(s.cells_from_points(fx["points"], 24), fx["raw_l24"])
+    assert np.array_equal(s.cells_from_points(fx["points"], 30), fx["raw_l30"])
+    for level in (0, 1, 5, 12, 22, 30):
+        sel = fx["levels"] == level
+        if sel.any():
+            assert np.array_equal(s.cells_from_points(fx["points"][sel], level), fx["raw"][sel])
+    # literal KATs (test_cellgrid.cpp:25-33, SURVEY.md §8c)
+    assert int(s.cells_from_points([[0.0, 0.0]], 1)[0]) == (0b11 << 59) | (1 << 58)
+    assert int(s.cells_from_points([[12.3, 45.6]], 0)[0]) == 1 << 60
+    assert int(s.cells_from_points([[40.7, -74.0]], 24)[0]) == 0x1358F7810DB39000
+    with pytest.raises(ValueError):
+        s.cells_from_points([[0.0, 0.0]], 31)
+    with pytest.raises(join.InvalidArgument):
+        s.cells_from_points([[0.0, 181.0]], 5)
+
+
+def test_cell_ids_adversarial_grid_lines_vs_oracle():
+    """The division-free fast path must fall back exactly where truncation
+    could differ: points on grid lines of every level and a few ulps around
+    them, plus dense random points, bit-exact against the C oracle."""
+    from oracle import oracle
+    _, bundle = setup("join_small_exact")
+    s = bundle.session()
+    rng = np.random.default_rng(0xC311)
+    pts = []
+    for level in (30, 29, 24, 20, 16, 8):
+        k = rng.integers(0, (1 << level) + 1, 40000)
+        lat = k / float(1 << level) * 180.0 - 90.0
+        lng = k[::-1] / float(1 << level) * 360.0 - 180.0
+        for ulps in (0, 1, 2, 3, -1, -2, -3):
+            a, o = lat.copy(), lng.copy()
+            for _ in range(abs(ulps)):
+                a = np.nextafter(a, np.inf if ulps > 0 else -np.inf)
+                o = np.nextafter(o, np.inf if ulps > 0 else -np.inf)
+            pts.append(np.stack([np.clip(a, -90.0, 90.0), np.clip(o, -180.0, 180.0)], axis=1))
+    pts.append(np.stack([rng.uniform(-90, 90, 2_000_000), rng.uniform(-180, 180, 2_000_000)], axis=1))
+    pts.append(np.stack([rng.uniform(40.5, 40.95, 2_000_000), rng.uniform(-74.25, -73.70, 2_000_000)], axis=1))
+    pts = np.concatenate(pts)
+    assert np.array_equal(s.cells_from_points(pts, 30), oracle.cell_from_point(pts, 30))

@@ -1,0 +1,103 @@
+"""Tuning harness for K1 (join_kernel): builds variants of the library with -D
+switches and times the device-resident join of BASELINE config 2 for each.
+
+    python tools/k1_sweep.py build      # here (CPU): cross-compile all variants
+    python tools/k1_sweep.py run [N]    # on the GPU box: time them
+
+Variants whose name starts with ``exp_`` drop work (wrong results) and exist
+only to attribute time to phases."""
+from __future__ import annotations
+
+import ctypes
+import json
+import sys
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+from paper_1802_09488_b200 import _build  # noqa: E402
+
+OUT = ROOT / "tools" / "_variants"
+VARIANTS = {
+    "base": [],
+    "t512_b2": ["GJ_JOIN_THREADS=512", "GJ_JOIN_MIN_BLOCKS=2"],
+    "ppt2": ["GJ_PPT=2"],
+    "ppt3": ["GJ_PPT=3"],
+    "ppt6": ["GJ_PPT=6"],
+    "exp_phase1_only": ["GJ_EXP_PHASE1_ONLY"],
+    "exp_no_phase3": ["GJ_EXP_NO_PHASE3"],
+    "exp_no_hist": ["GJ_EXP_NO_HIST"],
+}
+
+
+def build_all():
+    OUT.mkdir(exist_ok=True)
+    for name, defs in VARIANTS.items():
+        t0 = time.time()
+        _build.build(defines=defs, out=OUT / f"lib_{name}.so")
+        print(f"built {name} in {time.time() - t0:.1f}s")
+
+
+def run_all(n_points: int):
+    import numpy as np
+    import torch
+
+    from paper_1802_09488_b200 import capi, join, synth
+    from tools import build_bundles
+
+    path = build_bundles.bundle_file(build_bundles.workload_name(2))
+    pts = synth.uniform_points(n_points, synth.seed_for(2, 2))
+    d_pts = torch.from_numpy(pts).cuda()
+    results = {}
+    ref_counts = None
+    for name in VARIANTS:
+        lib = OUT / f"lib_{name}.so"
+        if not lib.exists():
+            continue
+        capi._LIB = None
+        _build.LIB = lib
+        capi._build.LIB = lib
+        bundle = join.IndexBundle.load(path, device=0)
+        sess = bundle.session()
+        d_counts = torch.zeros(len(bundle.ids), dtype=torch.int64, device="cuda")
+        d_first = torch.empty(n_points, dtype=torch.int32, device="cuda")
+        stream = torch.cuda.ExternalStream(sess.stream)
+
+        def step():
+            sess.join_count_device(d_pts.data_ptr(), n_points, d_counts.data_ptr(), capi.GJ_MODE_APPROX,
+                                   d_first_id_ptr=d_first.data_ptr())
+        for _ in range(3):
+            step()
+        sess.sync()
+        d_counts.zero_()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 10
+        with torch.cuda.stream(stream):
+            e0.record()
+            for _ in range(reps):
+                step()
+            e1.record()
+        sess.sync()
+        ms = e0.elapsed_time(e1) / reps
+        counts = d_counts.cpu().numpy() // reps
+        ok = None
+        if not name.startswith("exp_"):
+            if ref_counts is None:
+                ref_counts = counts
+            ok = bool(np.array_equal(counts, ref_counts))
+        results[name] = {"ms": ms, "gpts": n_points / ms / 1e6, "counts_ok": ok}
+        print(f"{name:28s} {ms:8.4f} ms  {n_points / ms / 1e6:8.1f} Gpts/s  counts_ok={ok}", flush=True)
+        sess.close()
+        bundle.close()
+    (ROOT / "gpurun_out").mkdir(exist_ok=True)
+    (ROOT / "gpurun_out" / "k1_sweep.json").write_text(json.dumps(results, indent=1))
+
+
+if __name__ == "__main__":
+    if sys.argv[1] == "build":
+        build_all()
+    else:
+        run_all(int(sys.argv[2]) if len(sys.argv) > 2 else 100_000_000)
