@@ -35,8 +35,8 @@ constexpr uint32_t kErrTaskCap = 8u;
 // or the node to continue from (kDirLink | node id).  Derived from the arena
 // at index-create time; results are bitwise those of the plain walk.
 struct DevDirectory {
-  const uint32_t* table;  // [height * width], global copy
-  uint32_t width, height;
+  const uint32_t* table;  // [(height + 1) * pitch], last column and row all miss
+  uint32_t width, height, pitch;  // pitch = width + 1
   uint32_t x0, y0;        // window origin in level-`level` cells
   uint32_t n_table;       // 0 = tier absent
   int32_t shift;          // 30 - level
@@ -183,10 +183,11 @@ __device__ __forceinline__ uint64_t walk_from(const DevIndex& ix, uint64_t node,
 // Directory lookup: the code of the level-`d` cell holding grid point (x, y).
 __device__ __forceinline__ uint32_t dir_code(const DevDirectory& d, const uint32_t* table, uint32_t x,
                                              uint32_t y) {
-  const uint32_t cx = (x >> d.shift) - d.x0;
-  const uint32_t cy = (y >> d.shift) - d.y0;
-  if (cx >= d.width || cy >= d.height) return 0;  // outside every indexed cell
-  return table[cy * d.width + cx];
+  // cells left of / below the window wrap to huge values: both sides clamp
+  // into the all-miss padding
+  const uint32_t cx = min((x >> d.shift) - d.x0, d.width);
+  const uint32_t cy = min((y >> d.shift) - d.y0, d.height);
+  return table[cy * d.pitch + cx];
 }
 
 // One point -> tagged entry, bitwise Act::probe(cell_from_point(p, k_max/2))

@@ -50,7 +50,7 @@ struct DeviceBuffer {
 struct HostDirectory {
   int level = 0;   // grid level the table resolves
   int chunks = 0;  // node steps folded in
-  uint32_t x0 = 0, y0 = 0, width = 0, height = 0;
+  uint32_t x0 = 0, y0 = 0, width = 0, height = 0, pitch = 0;
   std::vector<uint32_t> table;
 };
 

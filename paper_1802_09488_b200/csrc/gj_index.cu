@@ -244,7 +244,10 @@ int analyse(const gj_index_desc& d, Analysis* out) {
         hd.y0 = static_cast<uint32_t>(sn.box.y_lo);
         hd.width = static_cast<uint32_t>(sn.box.x_hi - sn.box.x_lo + 1);
         hd.height = static_cast<uint32_t>(sn.box.y_hi - sn.box.y_lo + 1);
-        hd.table.assign(static_cast<size_t>(hd.width) * hd.height, 0u);
+        // one extra all-miss column and row: lookups clamp into them instead
+        // of testing the window bounds
+        hd.pitch = hd.width + 1;
+        hd.table.assign(static_cast<size_t>(hd.pitch) * (hd.height + 1), 0u);
         for (size_t ti = 0; ti < sn.n_terminals; ++ti) {
           const Cell& t = terminals[ti];
           auto it = code_of.find(t.node_or_entry);
@@ -264,12 +267,12 @@ int analyse(const gj_index_desc& d, Analysis* out) {
           const uint64_t by = (static_cast<uint64_t>(t.y) << s) - hd.y0;
           const uint64_t side = 1ull << s;
           for (uint64_t yy = 0; yy < side; ++yy) {
-            uint32_t* row = hd.table.data() + (by + yy) * hd.width + bx;
+            uint32_t* row = hd.table.data() + (by + yy) * hd.pitch + bx;
             std::fill(row, row + side, it->second);
           }
         }
         for (const Cell& l : sn.links) {
-          hd.table[static_cast<size_t>(l.y - hd.y0) * hd.width + (l.x - hd.x0)] =
+          hd.table[static_cast<size_t>(l.y - hd.y0) * hd.pitch + (l.x - hd.x0)] =
               kDirLink | static_cast<uint32_t>(l.node_or_entry);
         }
       };
@@ -377,6 +380,11 @@ int create_index(const gj_index_desc& d, int device, gj_index** out) {
     }
   }
 
+  if (an.dir.table.empty()) {  // no tree on face 0: the window is just its all-miss padding
+    an.dir = HostDirectory{};
+    an.dir.pitch = 1;
+    an.dir.table.assign(1, 0u);
+  }
   size_t bytes = 0;
   if ((rc = upload(ix->d_arena, d.arena, d.node_count * kNodeSlots, &bytes)) != GJ_OK) return rc;
   if ((rc = upload(ix->d_lut, d.lut, d.lut_len, &bytes)) != GJ_OK) return rc;
@@ -409,6 +417,7 @@ int create_index(const gj_index_desc& d, int device, gj_index** out) {
     dd.table = table;
     dd.width = hd.width;
     dd.height = hd.height;
+    dd.pitch = hd.pitch;
     dd.x0 = hd.x0;
     dd.y0 = hd.y0;
     dd.n_table = static_cast<uint32_t>(hd.table.size());

@@ -74,215 +74,236 @@ __device__ __forceinline__ void flag_error(DevStatus* st, uint32_t bit, uint64_t
   atomicMin(&st->bad_index, static_cast<unsigned long long>(index));
 }
 
-// Per-thread emit state of K1.
-template <bool kIds, bool kStats, bool kDense>
-struct Emitter {
-  const DevIndex& ix;
-  const JoinParams& jp;
-  uint32_t* s_hist;
-  uint32_t hist_rep, lane_rep;  // replicas per slot, lane & (hist_rep - 1)
-  bool exact;
-  uint32_t false_hits = 0, solely_true = 0, refined = 0, cand_refs = 0;
+// ---------------------------------------------------------------------------
+// Shared memory by 32-bit shared-window address and predicated memory
+// operations.  K1's hot path is straight-line code: conditional loads, atomics
+// and stores are predicated instructions, not branches.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint32_t lds32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ uint2 lds64(uint32_t addr) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts64_if(uint32_t addr, uint32_t x, uint32_t y, bool pred) {
+  asm volatile("{ .reg .pred p; setp.ne.u32 p, %3, 0; @p st.shared.v2.u32 [%0], {%1, %2}; }" ::"r"(addr), "r"(x),
+               "r"(y), "r"(static_cast<uint32_t>(pred))
+               : "memory");
+}
+__device__ __forceinline__ void red_inc_shared_if(uint32_t addr, bool pred) {
+  asm volatile("{ .reg .pred p; setp.ne.u32 p, %1, 0; @p red.shared.add.u32 [%0], 1; }" ::"r"(addr),
+               "r"(static_cast<uint32_t>(pred))
+               : "memory");
+}
+__device__ __forceinline__ uint32_t ldg32_if(const uint32_t* p, bool pred, uint32_t otherwise) {
+  uint32_t v;
+  asm volatile("{ .reg .pred p; setp.ne.u32 p, %3, 0; mov.u32 %0, %2; @p ld.global.nc.u32 %0, [%1]; }"
+               : "=r"(v)
+               : "l"(p), "r"(otherwise), "r"(static_cast<uint32_t>(pred)));
+  return v;
+}
+__device__ __forceinline__ void stcs32_if(uint32_t* p, uint32_t v, bool pred) {
+  asm volatile("{ .reg .pred p; setp.ne.u32 p, %2, 0; @p st.global.cs.u32 [%0], %1; }" ::"l"(p), "r"(v),
+               "r"(static_cast<uint32_t>(pred))
+               : "memory");
+}
 
-  __device__ __forceinline__ Emitter(const DevIndex& i, const JoinParams& j, uint32_t* h, uint32_t lane)
-      : ix(i), jp(j), s_hist(h), hist_rep(j.hist_rep), lane_rep(lane & (j.hist_rep ? j.hist_rep - 1u : 0u)),
-        exact(j.exact != 0) {}
-
-  __device__ __forceinline__ uint32_t slot_of(uint32_t id) const { return kDense ? id : id_to_slot(ix, id); }
-
-  __device__ __forceinline__ void count(uint32_t slot) {
-#ifdef GJ_EXP_NO_HIST  // timing experiment: results are wrong
-    return;
-#endif
-    if (hist_rep) {
-      atomicAdd(&s_hist[slot * hist_rep + lane_rep], 1u);
-    } else {
-      atomicAdd(&jp.counts[slot], 1ull);
-    }
-  }
-
-  // One inlined payload ((polygon_id << 1) | interior) that emits right here:
-  // a true hit, or a candidate in approximate mode (join.cpp:100-108).
-  __device__ __forceinline__ bool emits_now(uint32_t payload) const { return (payload & 1u) != 0u || !exact; }
-
-  __device__ __forceinline__ uint32_t emit_single(uint32_t payload) {
-    const uint32_t id = payload >> 1;
-    count(slot_of(id));
-    if (kStats) {
-      if (payload & 1u) {
-        ++solely_true;
-      } else {
-        ++refined;
-        ++cand_refs;
-      }
-    }
-    return id;
-  }
-
-  // k-th reference of an entry in the reference's emit order
-  // (act.hpp:169-196): payload = (polygon_id << 1) | interior.
-  __device__ __forceinline__ uint32_t ref_payload(uint64_t entry, uint32_t tag, uint32_t k, uint32_t off,
-                                                  uint32_t t) const {
-    if (tag == 1u) return static_cast<uint32_t>(entry >> 2) & 0x7fffffffu;
-    if (tag == 2u) {
-      return k == 0 ? static_cast<uint32_t>(entry >> 33) & 0x7fffffffu
-                    : static_cast<uint32_t>(entry >> 2) & 0x7fffffffu;
-    }
-    // lookup-table record [t, true ids, c, candidate ids]
-    return k < t ? (__ldg(ix.lut + off + 1 + k) << 1) | 1u : (__ldg(ix.lut + off + 2 + k) << 1);
-  }
-
-  // The per-(point, entry) body of run_join, join.cpp:93-127, for a
-  // non-sentinel entry.  Returns the first-id word of the point.
-  __device__ __forceinline__ uint32_t handle(uint64_t entry, uint32_t local) {
-    if ((static_cast<uint32_t>(entry) & 3u) == 1u) {
-      const uint32_t p = static_cast<uint32_t>(entry >> 2) & 0x7fffffffu;
-      if (emits_now(p)) return emit_single(p);
-    }
-    return handle_general(entry, local);
-  }
-
-  // Everything else: two payloads, lookup-table records, exact-mode
-  // candidates (tasks for K2) and the overflow list.  Cold.
-  __device__ __noinline__ uint32_t handle_general(uint64_t entry, uint32_t local) {
-    const uint32_t tag = static_cast<uint32_t>(entry) & 3u;
-    uint32_t off = 0, t = 0, n_refs, n_cand;
-    if (tag == 1u) {
-      n_refs = 1;
-      n_cand = 1;  // only exact-mode candidates get here with one payload
-    } else if (tag == 2u) {
-      n_refs = 2;
-      n_cand = 2u - ((static_cast<uint32_t>(entry >> 33) & 1u) + (static_cast<uint32_t>(entry >> 2) & 1u));
-    } else {
-      off = static_cast<uint32_t>(entry >> 2) & 0x7fffffffu;
-      t = __ldg(ix.lut + off);
-      n_refs = t + __ldg(ix.lut + off + 1 + t);
-      n_cand = n_refs - t;
-    }
-    if (kStats) {
-      if (n_cand == 0) {
-        ++solely_true;
-      } else {
-        ++refined;
-        cand_refs += n_cand;
-      }
-    }
-    const bool defer = exact && n_cand != 0;                  // some pairs depend on K2
-    const uint32_t n_now = exact ? n_refs - n_cand : n_refs;  // pairs emitted here
-
-    // overflow records: everything after the first pair, or every pair when
-    // the point is deferred
-    uint64_t ovf_base = 0;
-    uint32_t n_ovf = 0;
-    if (kIds) {
-      n_ovf = defer ? n_now : (n_now > 0 ? n_now - 1 : 0);
-      if (n_ovf) {
-        ovf_base = atomicAdd(&jp.status->overflow_count, static_cast<unsigned long long>(n_ovf));
-        if (ovf_base + n_ovf > jp.ovf_cap) {
-          atomicOr(&jp.status->flags, kErrOverflowCap);
-          n_ovf = 0;
-        }
-      }
-    }
-    uint64_t task_base = 0;
-    bool tasks_ok = false;
-    if (defer) {
-      task_base = atomicAdd(&jp.status->task_count, static_cast<unsigned long long>(n_cand));
-      tasks_ok = task_base + n_cand <= jp.task_cap;
-      if (!tasks_ok) atomicOr(&jp.status->flags, kErrTaskCap);
-    }
-
-    uint32_t first = defer ? kDeferred : kNoMatch;
-    uint32_t emitted = 0, tasks = 0;
-    for (uint32_t k = 0; k < n_refs; ++k) {
-      const uint32_t p = ref_payload(entry, tag, k, off, t);
-      const uint32_t id = p >> 1;
-      const uint32_t slot = slot_of(id);
-      if (emits_now(p)) {
-        count(slot);
-        if (kIds) {
-          if (!defer && emitted == 0) {
-            first = id | (n_now > 1 ? kMoreFlag : 0u);
-          } else if (n_ovf) {
-            const uint64_t w = ovf_base + (defer ? emitted : emitted - 1);
-            jp.ovf_point[w] = jp.base_index + local;
-            jp.ovf_id[w] = id;
-            jp.ovf_ord[w] = k;
-          }
-        }
-        ++emitted;
-      } else {
-        if (__ldg(ix.ring_len + slot) == 0u) {  // join.cpp:111-114
-          flag_error(jp.status, kErrUnknownPolygon, jp.base_index + local);
-        }
-        if (tasks_ok) {
-          const uint64_t w = task_base + tasks;
-          jp.task_point[w] = local;
-          jp.task_slot[w] = slot;
-          jp.task_ord[w] = k;
-          atomicAdd(&jp.task_per_slot[slot], 1u);
-        }
-        ++tasks;
-      }
-    }
-    return first;
-  }
+// Where K1 counts: a replicated shared-memory histogram (slot * rep + lane
+// replica) or, for id tables too large for it, global atomics.
+struct HistRef {
+  uint32_t smem;      // shared address of the histogram
+  uint32_t rep;       // replicas per slot (power of two), 0 = global atomics
+  uint32_t lane_rep;  // lane & (rep - 1)
 };
 
-// K1.  Persistent grid (one CTA per SM slot); each CTA stages the first
-// directory tier (and a replicated per-polygon histogram) in shared memory
-// once, then streams tiles of points: 16-byte coalesced loads,
-// kPointsPerThread independent points in flight per thread.  A tile runs in
-// three phases of decreasing population:
-//   1. all points (warp-uniform): cell coordinates, shared-memory directory,
+template <bool kDense>
+__device__ __forceinline__ void count_slot(const DevIndex& ix, const JoinParams& jp, const HistRef& h,
+                                           uint32_t id) {
+  const uint32_t slot = kDense ? id : id_to_slot(ix, id);
+  if (h.rep) {
+    red_inc_shared_if(h.smem + (slot * h.rep + h.lane_rep) * 4u, true);
+  } else {
+    atomicAdd(&jp.counts[slot], 1ull);
+  }
+}
+
+// The per-(point, entry) body of run_join (join.cpp:93-127) for everything
+// the straight-line path does not take: two payloads, lookup-table records,
+// exact-mode candidates (tasks for K2) and the overflow list.  Cold and out
+// of line.  Returns {first-id word, number of candidate references}.
+template <bool kIds, bool kDense>
+__device__ __noinline__ uint2 emit_general(const DevIndex& ix, const JoinParams& jp, HistRef h, uint64_t entry,
+                                           uint32_t local) {
+  const bool exact = jp.exact != 0;
+  const uint32_t tag = static_cast<uint32_t>(entry) & 3u;
+  uint32_t off = 0, t = 0, n_refs, n_cand;
+  if (tag == 1u) {
+    n_refs = 1;
+    n_cand = 1u - (static_cast<uint32_t>(entry >> 2) & 1u);
+  } else if (tag == 2u) {
+    n_refs = 2;
+    n_cand = 2u - ((static_cast<uint32_t>(entry >> 33) & 1u) + (static_cast<uint32_t>(entry >> 2) & 1u));
+  } else {
+    off = static_cast<uint32_t>(entry >> 2) & 0x7fffffffu;
+    t = __ldg(ix.lut + off);
+    n_refs = t + __ldg(ix.lut + off + 1 + t);
+    n_cand = n_refs - t;
+  }
+  const bool defer = exact && n_cand != 0;                  // some pairs depend on K2
+  const uint32_t n_now = exact ? n_refs - n_cand : n_refs;  // pairs emitted here
+
+  // overflow records: everything after the first pair, or every pair when
+  // the point is deferred
+  uint64_t ovf_base = 0;
+  uint32_t n_ovf = 0;
+  if (kIds) {
+    n_ovf = defer ? n_now : (n_now > 0 ? n_now - 1 : 0);
+    if (n_ovf) {
+      ovf_base = atomicAdd(&jp.status->overflow_count, static_cast<unsigned long long>(n_ovf));
+      if (ovf_base + n_ovf > jp.ovf_cap) {
+        atomicOr(&jp.status->flags, kErrOverflowCap);
+        n_ovf = 0;
+      }
+    }
+  }
+  uint64_t task_base = 0;
+  bool tasks_ok = false;
+  if (defer) {
+    task_base = atomicAdd(&jp.status->task_count, static_cast<unsigned long long>(n_cand));
+    tasks_ok = task_base + n_cand <= jp.task_cap;
+    if (!tasks_ok) atomicOr(&jp.status->flags, kErrTaskCap);
+  }
+
+  uint32_t first = defer ? kDeferred : kNoMatch;
+  uint32_t emitted = 0, tasks = 0;
+  for (uint32_t k = 0; k < n_refs; ++k) {
+    // k-th reference in the reference's emit order (act.hpp:169-196)
+    uint32_t p;
+    if (tag == 1u) {
+      p = static_cast<uint32_t>(entry >> 2) & 0x7fffffffu;
+    } else if (tag == 2u) {
+      p = static_cast<uint32_t>(k == 0 ? entry >> 33 : entry >> 2) & 0x7fffffffu;
+    } else {  // record [t, true ids, c, candidate ids]
+      p = k < t ? (__ldg(ix.lut + off + 1 + k) << 1) | 1u : (__ldg(ix.lut + off + 2 + k) << 1);
+    }
+    const uint32_t id = p >> 1;
+    if ((p & 1u) != 0u || !exact) {
+      count_slot<kDense>(ix, jp, h, id);
+      if (kIds) {
+        if (!defer && emitted == 0) {
+          first = id | (n_now > 1 ? kMoreFlag : 0u);
+        } else if (n_ovf) {
+          const uint64_t w = ovf_base + (defer ? emitted : emitted - 1);
+          jp.ovf_point[w] = jp.base_index + local;
+          jp.ovf_id[w] = id;
+          jp.ovf_ord[w] = k;
+        }
+      }
+      ++emitted;
+    } else {
+      const uint32_t slot = kDense ? id : id_to_slot(ix, id);
+      if (__ldg(ix.ring_len + slot) == 0u) {  // join.cpp:111-114
+        flag_error(jp.status, kErrUnknownPolygon, jp.base_index + local);
+      }
+      if (tasks_ok) {
+        const uint64_t w = task_base + tasks;
+        jp.task_point[w] = local;
+        jp.task_slot[w] = slot;
+        jp.task_ord[w] = k;
+        atomicAdd(&jp.task_per_slot[slot], 1u);
+      }
+      ++tasks;
+    }
+  }
+  return make_uint2(first, n_cand);
+}
+
+// K1.  Persistent grid (one CTA per SM); each CTA stages the first directory
+// tier (and a replicated per-polygon histogram) in shared memory once, then
+// streams tiles of points: 16-byte coalesced loads, kPointsPerThread
+// independent points in flight per thread.  A tile runs in three phases of
+// decreasing population:
+//   1. all points, straight-line: cell coordinates, shared-memory directory,
 //      emit when it resolves to one payload;
 //   2. points under a directory link: one independent gather each into the
 //      second, L2-resident directory tier — all gathers of the tile are
 //      issued before any is consumed;
-//   3. the remainder: dependent 8-byte gathers down the arena, dictionary and
-//      lookup-table entries, exact-mode candidates.
+//   3. the remainder (deep boundary nodes, dictionary entries, exact-mode
+//      candidates) is compacted into per-warp queues and drained 32 at a
+//      time: dependent 8-byte gathers down the arena, lookup-table records.
 template <bool kIds, bool kStats, bool kDense>
 __global__ void __launch_bounds__(kJoinThreads, GJ_JOIN_MIN_BLOCKS)
 join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinParams jp) {
   extern __shared__ __align__(16) unsigned char smem[];
-  uint32_t* s_table = reinterpret_cast<uint32_t*>(smem);
-  uint32_t* s_hist = reinterpret_cast<uint32_t*>(smem + jp.smem_hist_off);
   const uint32_t tid = threadIdx.x;
+  const uint32_t lane = tid & 31u;
 
   {  // stage the directory, clear the histogram
     const uint4* src = reinterpret_cast<const uint4*>(ix.dir.table);
-    uint4* dst = reinterpret_cast<uint4*>(s_table);
+    uint4* dst = reinterpret_cast<uint4*>(smem);
     const uint32_t n4 = (ix.dir.n_table + 3) / 4;  // buffers are padded to 16 B
     for (uint32_t i = tid; i < n4; i += kJoinThreads) dst[i] = __ldg(src + i);
+    uint32_t* hist = reinterpret_cast<uint32_t*>(smem + jp.smem_hist_off);
     const uint32_t n_hist = ix.n_ids * jp.hist_rep;
-    for (uint32_t i = tid; i < n_hist; i += kJoinThreads) s_hist[i] = 0;
+    for (uint32_t i = tid; i < n_hist; i += kJoinThreads) hist[i] = 0;
   }
   __syncthreads();
 
-  Emitter<kIds, kStats, kDense> em(ix, jp, s_hist, tid & 31u);
-  uint32_t n_valid = 0;
-
   // loop invariants in registers
-  const uint32_t dir_w = ix.dir.width, dir_h = ix.dir.height, dir_x0 = ix.dir.x0, dir_y0 = ix.dir.y0;
-  const int dir_shift = ix.dir.shift;
+  const uint32_t s_table = smem_addr(smem);
+  const HistRef hist{smem_addr(smem + jp.smem_hist_off), jp.hist_rep, lane & (jp.hist_rep ? jp.hist_rep - 1u : 0u)};
+  const uint32_t s_queue = smem_addr(smem + jp.smem_queue_off) + (tid >> 5) * (kQueueCap * 8u);
+  const uint32_t lane_lt = (1u << lane) - 1u;
+  const uint32_t d1_w = ix.dir.width, d1_h = ix.dir.height, d1_pitch = ix.dir.pitch;
+  const uint32_t d1_x0 = ix.dir.x0, d1_y0 = ix.dir.y0;
+  const int d1_shift = ix.dir.shift;
   const bool has_dir2 = ix.dir2.n_table != 0;
   const uint32_t* __restrict__ table2 = ix.dir2.table;
-  const uint32_t d2_w = ix.dir2.width, d2_h = ix.dir2.height, d2_x0 = ix.dir2.x0, d2_y0 = ix.dir2.y0;
+  const uint32_t d2_w = ix.dir2.width, d2_h = ix.dir2.height, d2_pitch = ix.dir2.pitch;
+  const uint32_t d2_x0 = ix.dir2.x0, d2_y0 = ix.dir2.y0;
   const int d2_shift = ix.dir2.shift;
   const int walk_level = ix.prefix_level0 + 4 * (has_dir2 ? ix.dir2.chunks : ix.dir.chunks);
   const uint32_t leaf_keep = ~((1u << (30 - ix.leaf_level)) - 1u);  // cell_id.cpp:93-94
   const double2* __restrict__ pts = jp.pts;
   uint32_t* __restrict__ first_id = jp.first_id;
-  const uint32_t n = static_cast<uint32_t>(jp.n);  // <= 2^31 per launch
+  const uint32_t n = static_cast<uint32_t>(jp.n);  // 1 <= n <= 2^31 per launch
+  // A code resolves right here when it is one inlined payload that emits: a
+  // true hit, or a candidate in approximate mode (join.cpp:100-108).
+  const uint32_t emit_mask = 0xC0000000u | (jp.exact ? 1u : 0u);
+  const uint32_t emit_bits = kDirInline | (jp.exact ? 1u : 0u);
 
-  // per-warp queue of open points: (point index, directory code)
-  const uint32_t lane = tid & 31u;
-  const uint32_t lane_lt = (1u << lane) - 1u;
-  uint2* s_queue = reinterpret_cast<uint2*>(smem + jp.smem_queue_off) + (tid >> 5) * kQueueCap;
-  uint32_t q_count = 0;  // warp-uniform
+  uint32_t n_valid = 0, false_hits = 0, solely_true = 0, refined = 0, cand_refs = 0;
+  uint32_t q_count = 0;  // open points queued by this warp (warp-uniform)
 
-  // Phase 3 for one open point: arena descent (dependent 8-byte gathers),
-  // dictionary entries, exact-mode candidates.
+  // One resolved directory code of a live point: count, stats, first id.
+  // Returns true when the point is finished (inlined emit or miss).
+  auto settle = [&](uint32_t c, bool active, uint32_t i) -> bool {
+    const bool emit = active && (c & emit_mask) == emit_bits;
+    const bool miss = active && c == 0u;
+    const uint32_t id = (c >> 1) & 0x1FFFFFFFu;
+    if (kDense && hist.rep) {
+      red_inc_shared_if(hist.smem + (id * hist.rep + hist.lane_rep) * 4u, emit);
+    } else if (emit) {
+      count_slot<kDense>(ix, jp, hist, id);
+    }
+    if (kStats) {
+      false_hits += miss;
+      solely_true += emit && (c & 1u);
+      refined += emit && !(c & 1u);
+      cand_refs += emit && !(c & 1u);
+    }
+    if (kIds) stcs32_if(first_id + i, emit ? id : kNoMatch, emit || miss);
+    return emit || miss;
+  };
+
+  // Phase 3 for one open point.
   auto resolve_open = [&](uint32_t i, uint32_t c) {
     uint64_t entry;
     if (c & kDirLink) {
@@ -297,9 +318,25 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
     }
     uint32_t first = kNoMatch;
     if (entry == 0) {
-      if (kStats) ++em.false_hits;
+      if (kStats) ++false_hits;
+    } else if ((static_cast<uint32_t>(entry) & 3u) == 1u &&
+               ((static_cast<uint32_t>(entry >> 2) & 1u) != 0u || !jp.exact)) {
+      first = static_cast<uint32_t>(entry >> 3) & 0x3FFFFFFFu;  // one payload that emits
+      count_slot<kDense>(ix, jp, hist, first);
+      if (kStats) {
+        const bool interior = (entry >> 2) & 1u;
+        solely_true += interior;
+        refined += !interior;
+        cand_refs += !interior;
+      }
     } else {
-      first = em.handle(entry, i);
+      const uint2 r = emit_general<kIds, kDense>(ix, jp, hist, entry, i);
+      first = r.x;
+      if (kStats) {
+        solely_true += r.y == 0;
+        refined += r.y != 0;
+        cand_refs += r.y;
+      }
     }
     if (kIds) __stcs(first_id + i, first);
   };
@@ -308,88 +345,58 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
   const uint32_t n_tiles = (n + kTile - 1) / kTile;
   for (uint32_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
     const uint32_t base = tile * kTile + tid;
-    const bool full = n - tile * kTile >= kTile;
     double2 p[kPointsPerThread];
     uint32_t code[kPointsPerThread], gx[kPointsPerThread], gy[kPointsPerThread];
 #pragma unroll
     for (int j = 0; j < kPointsPerThread; ++j) {
-      const uint32_t i = base + j * kJoinThreads;
-      // streaming read, touched once: evict-first; out-of-range lanes get an invalid point
-      p[j] = (full || i < n) ? __ldcs(pts + i) : make_double2(1e300, 1e300);
+      // streaming read, touched once: evict-first.  Lanes past the end re-read
+      // the last point and are masked below.
+      p[j] = __ldcs(pts + min(base + j * kJoinThreads, n - 1u));
     }
     // ---- phase 1: shared-memory directory ----
 #pragma unroll
     for (int j = 0; j < kPointsPerThread; ++j) {
       const uint32_t i = base + j * kJoinThreads;
-      uint32_t first = kNoMatch;
-      code[j] = 0;
-      if (latlng_valid(p[j].x, p[j].y)) {
-        ++n_valid;
-        uint32_t x, y;
-        grid_xy(p[j].x, p[j].y, &x, &y);
-        const uint32_t cx = (x >> dir_shift) - dir_x0;
-        const uint32_t cy = (y >> dir_shift) - dir_y0;
-        uint32_t c = 0;
-        if (cx < dir_w && cy < dir_h) c = s_table[cy * dir_w + cx];
-        if ((c >> 30) == 1u && em.emits_now(c & 0x3FFFFFFFu)) {
-          first = em.emit_single(c & 0x3FFFFFFFu);
-        } else if (c == 0) {
-          if (kStats) ++em.false_hits;
-        } else {
-          code[j] = c;
-          gx[j] = x;
-          gy[j] = y;
-        }
-      } else if (full || i < n) {
-        flag_error(jp.status, kErrInvalidPoint, jp.base_index + i);  // cell_id.cpp:83-85
-      }
-      if (kIds && code[j] == 0 && (full || i < n)) __stcs(first_id + i, first);
+      const bool live = i < n;
+      const bool valid = latlng_valid(p[j].x, p[j].y);
+      if (live && !valid) flag_error(jp.status, kErrInvalidPoint, jp.base_index + i);  // cell_id.cpp:83-85
+      uint32_t x, y;
+      grid_xy(p[j].x, p[j].y, &x, &y);
+      const uint32_t cx = min((x >> d1_shift) - d1_x0, d1_w);  // clamps into the all-miss padding
+      const uint32_t cy = min((y >> d1_shift) - d1_y0, d1_h);
+      const uint32_t c = lds32(s_table + (cy * d1_pitch + cx) * 4u);
+      const bool active = live && valid;
+      if (kStats) n_valid += active;
+      const bool done = settle(c, active, i);
+      code[j] = (active && !done) ? c : 0u;
+      gx[j] = x;
+      gy[j] = y;
     }
 #ifdef GJ_EXP_PHASE1_ONLY  // timing experiment: results are wrong
     continue;
 #endif
-    // ---- phase 2: second directory tier (one gather per linked point) ----
+    // ---- phase 2: second directory tier, one gather per linked point ----
     if (has_dir2) {
       uint32_t c2[kPointsPerThread];
 #pragma unroll
       for (int j = 0; j < kPointsPerThread; ++j) {
-        c2[j] = code[j];
-        if (code[j] & kDirLink) {
-          const uint32_t cx = (gx[j] >> d2_shift) - d2_x0;
-          const uint32_t cy = (gy[j] >> d2_shift) - d2_y0;
-          c2[j] = (cx < d2_w && cy < d2_h) ? __ldg(table2 + cy * d2_w + cx) : 0u;
-        }
+        const uint32_t cx = min((gx[j] >> d2_shift) - d2_x0, d2_w);
+        const uint32_t cy = min((gy[j] >> d2_shift) - d2_y0, d2_h);
+        c2[j] = ldg32_if(table2 + (cy * d2_pitch + cx), (code[j] & kDirLink) != 0u, code[j]);
       }
 #pragma unroll
       for (int j = 0; j < kPointsPerThread; ++j) {
-        if ((code[j] & kDirLink) == 0) continue;
-        const uint32_t c = c2[j];
-        const uint32_t i = base + j * kJoinThreads;
-        if ((c >> 30) == 1u && em.emits_now(c & 0x3FFFFFFFu)) {
-          const uint32_t first = em.emit_single(c & 0x3FFFFFFFu);
-          if (kIds) __stcs(first_id + i, first);
-          code[j] = 0;
-        } else if (c == 0) {
-          if (kStats) ++em.false_hits;
-          if (kIds) __stcs(first_id + i, kNoMatch);
-          code[j] = 0;
-        } else {
-          code[j] = c;
-        }
+        const bool linked = (code[j] & kDirLink) != 0u;
+        const bool done = settle(c2[j], linked, base + j * kJoinThreads);
+        code[j] = done ? 0u : c2[j];
       }
     }
     // ---- phase 3, deferred: what is still open goes to this warp's queue ----
-    // Few points get here (directory links into deep boundary nodes,
-    // dictionary entries, exact-mode candidates).  Running them where they
-    // occur would drag all 32 lanes through the long path for one or two
-    // active ones, so they are compacted per warp and drained 32 at a time.
 #pragma unroll
     for (int j = 0; j < kPointsPerThread; ++j) {
-      const bool open = code[j] != 0;
+      const bool open = code[j] != 0u;
       const uint32_t mask = __ballot_sync(0xffffffffu, open);
-      if (open) {
-        s_queue[q_count + __popc(mask & lane_lt)] = make_uint2(base + j * kJoinThreads, code[j]);
-      }
+      sts64_if(s_queue + (q_count + __popc(mask & lane_lt)) * 8u, base + j * kJoinThreads, code[j], open);
       q_count += __popc(mask);
     }
 #ifdef GJ_EXP_NO_PHASE3  // timing experiment: results are wrong
@@ -398,31 +405,32 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
     __syncwarp();
     while (q_count >= 32u) {
       q_count -= 32u;
-      const uint2 item = s_queue[q_count + lane];
+      const uint2 item = lds64(s_queue + (q_count + lane) * 8u);
       __syncwarp();
       resolve_open(item.x, item.y);
     }
   }
   if (lane < q_count) {  // the last, partial batch
-    const uint2 item = s_queue[lane];
+    const uint2 item = lds64(s_queue + lane * 8u);
     resolve_open(item.x, item.y);
   }
 
   __syncthreads();
   if (jp.hist_rep) {  // fold the replicas, one global add per non-zero slot
+    const uint32_t* hist_words = reinterpret_cast<const uint32_t*>(smem + jp.smem_hist_off);
     for (uint32_t s = tid; s < ix.n_ids; s += kJoinThreads) {
       uint32_t sum = 0;
-      for (uint32_t r = 0; r < jp.hist_rep; ++r) sum += s_hist[s * jp.hist_rep + r];
+      for (uint32_t r = 0; r < jp.hist_rep; ++r) sum += hist_words[s * jp.hist_rep + r];
       if (sum) atomicAdd(&jp.counts[s], static_cast<unsigned long long>(sum));
     }
   }
   if (kStats && jp.stats) {  // JoinStats, join.hpp:77-84
-    uint32_t v[5] = {n_valid, em.false_hits, em.solely_true, em.refined, em.cand_refs};
+    uint32_t v[5] = {n_valid, false_hits, solely_true, refined, cand_refs};
 #pragma unroll
     for (int k = 0; k < 5; ++k) {
       for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
     }
-    if ((tid & 31u) == 0) {
+    if (lane == 0) {
       atomicAdd(&jp.stats[0], static_cast<unsigned long long>(v[0]));                // probes
       if (jp.exact) atomicAdd(&jp.stats[1], static_cast<unsigned long long>(v[4]));  // pip_tests
       atomicAdd(&jp.stats[2], static_cast<unsigned long long>(v[1]));                // false_hits
