@@ -1,0 +1,214 @@
+// geojoin::gpu — the reference's join API (include/geojoin/join.hpp) served by
+// the B200 library through its C ABI (geojoin_b200.h).
+//
+// This is the binding a maintainer of the reference adds: it includes the
+// reference's own headers, takes the reference's own types, and keeps the
+// signatures of
+//
+//   join_exact / join_approx        include/geojoin/join.hpp:128-138, src/join.cpp:237-247
+//   join_count_per_polygon          include/geojoin/join.hpp:145-146, src/join.cpp:255-285
+//   accumulate_probe_stats          include/geojoin/join.hpp:153-154, src/join.cpp:287-290
+//   collect_metrics                 include/geojoin/join.hpp:148-149, src/join.cpp:309-314
+//
+// so a call site switches by replacing `geojoin::` with `geojoin::gpu::` and
+// handing over a DeviceIndex made once from its IndexBundle.  Errors come back
+// as the reference's exception types.  Header-only; link libgeojoin_b200.so.
+#pragma once
+
+#include <map>
+#include <memory>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "geojoin/join.hpp"
+#include "geojoin_b200.h"
+
+namespace geojoin::gpu {
+
+namespace detail {
+
+[[noreturn]] inline void raise(int status) {
+  const std::string msg = gj_last_error();
+  switch (status) {
+    case GJ_INVALID_POINT:
+    case GJ_INVALID_ARGUMENT:
+      throw std::invalid_argument(msg);  // cell_id.cpp:83-88
+    case GJ_CORRUPT_INDEX:
+    case GJ_UNKNOWN_POLYGON:
+      throw CorruptionError(msg);  // act.hpp:44-46
+    default:
+      throw std::runtime_error(msg);
+  }
+}
+
+inline void check(int status) {
+  if (status != GJ_OK) raise(status);
+}
+
+}  // namespace detail
+
+/// The reference's IndexBundle replicated into one GPU's HBM.  Immutable like
+/// the bundle it came from (join.hpp:86-88); the session inside serialises
+/// callers, so use one DeviceIndex per calling thread or guard it.
+class DeviceIndex {
+ public:
+  /// Copies the bundle's probe view (act.hpp:108-116), lookup table and
+  /// polygons to `device` (-1 = current).  Nothing of `bundle` is retained.
+  explicit DeviceIndex(const IndexBundle& bundle, int device = -1) {
+    const Act& act = bundle.act();
+    const ActProbeView& v = act.view();
+    gj_index_desc d{};
+    d.arena = v.arena;
+    d.node_count = act.node_count();
+    d.lut = act.lookup_table().data();
+    d.lut_len = act.lookup_table().size();
+    for (int f = 0; f < 8; ++f) {
+      d.roots[f] = v.roots[f];
+      d.prefixes[f] = v.prefixes[f];
+      d.prefix_bits[f] = v.prefix_bits[f];
+    }
+    d.k_max = act.config().k_max;
+    d.approx_mode = bundle.report().mode == JoinMode::kApprox;
+    std::vector<uint32_t> ids;
+    std::vector<uint64_t> off{0};
+    std::vector<double> latlng;
+    for (const Polygon& poly : bundle.polygons()) {
+      ids.push_back(poly.id);
+      for (const LatLng& p : poly.vertices) {
+        latlng.push_back(p.lat);
+        latlng.push_back(p.lng);
+      }
+      off.push_back(latlng.size() / 2);
+    }
+    d.n_polygons = ids.size();
+    d.polygon_ids = ids.data();
+    d.vtx_off = off.data();
+    d.vtx_latlng = latlng.data();
+    init(d, device);
+  }
+
+  /// IndexBundle::load without the host-side Act (join.cpp:341-381).
+  explicit DeviceIndex(const std::string& gjx1_path, int device = -1) {
+    gj_index* ix = nullptr;
+    detail::check(gj_index_load_file(gjx1_path.c_str(), device, &ix));
+    adopt(ix);
+  }
+
+  DeviceIndex(const DeviceIndex&) = delete;
+  DeviceIndex& operator=(const DeviceIndex&) = delete;
+
+  gj_session* session() const { return session_.get(); }
+  const gj_index_info& info() const { return info_; }
+  const std::vector<uint32_t>& ids() const { return ids_; }
+  JoinMode mode() const { return info_.approx_mode ? JoinMode::kApprox : JoinMode::kExact; }
+
+ private:
+  void init(const gj_index_desc& d, int device) {
+    gj_index* ix = nullptr;
+    detail::check(gj_index_create(&d, device, &ix));
+    adopt(ix);
+  }
+  void adopt(gj_index* ix) {
+    index_.reset(ix);
+    gj_session* s = nullptr;
+    detail::check(gj_session_create(ix, &s));
+    session_.reset(s);
+    detail::check(gj_index_get_info(ix, &info_));
+    ids_.resize(info_.n_ids);
+    detail::check(gj_index_ids(ix, ids_.data()));
+  }
+
+  struct IndexDeleter {
+    void operator()(gj_index* p) const { gj_index_destroy(p); }
+  };
+  struct SessionDeleter {
+    void operator()(gj_session* p) const { gj_session_destroy(p); }
+  };
+  std::unique_ptr<gj_index, IndexDeleter> index_;
+  std::unique_ptr<gj_session, SessionDeleter> session_;  // destroyed before the index
+  gj_index_info info_{};
+  std::vector<uint32_t> ids_;
+};
+
+namespace detail {
+
+inline const double* as_doubles(std::span<const LatLng> points) {
+  static_assert(sizeof(LatLng) == 2 * sizeof(double), "LatLng is two packed doubles (latlng.hpp:26-29)");
+  return reinterpret_cast<const double*>(points.data());
+}
+
+inline void add_stats(const gj_stats& s, JoinStats* out) {
+  if (!out) return;
+  out->probes += s.probes;
+  out->pip_tests += s.pip_tests;
+  out->false_hits += s.false_hits;
+  out->solely_true_hits += s.solely_true_hits;
+  out->refinement_entered += s.refinement_entered;
+  out->candidate_refs += s.candidate_refs;
+}
+
+inline std::vector<JoinPair> pairs(const DeviceIndex& ix, std::span<const LatLng> points, int mode,
+                                   JoinStats* stats) {
+  uint64_t n_pairs = 0, bad = 0;
+  gj_stats s{};
+  check(gj_join_pairs_host(ix.session(), as_doubles(points), points.size(), mode, &n_pairs,
+                           stats ? &s : nullptr, &bad));
+  std::vector<uint64_t> row_ptr(points.size() + 1);
+  std::vector<uint32_t> ids(n_pairs);
+  check(gj_pairs_copy(ix.session(), row_ptr.data(), ids.data()));
+  std::vector<JoinPair> out;
+  out.reserve(n_pairs);
+  for (size_t i = 0; i < points.size(); ++i) {
+    for (uint64_t k = row_ptr[i]; k < row_ptr[i + 1]; ++k) out.push_back(JoinPair{i, ids[k]});
+  }
+  add_stats(s, stats);
+  return out;
+}
+
+}  // namespace detail
+
+inline std::vector<JoinPair> join_exact(const DeviceIndex& ix, std::span<const LatLng> points,
+                                        JoinStats* stats = nullptr) {
+  return detail::pairs(ix, points, GJ_MODE_EXACT, stats);
+}
+
+inline std::vector<JoinPair> join_approx(const DeviceIndex& ix, std::span<const LatLng> points,
+                                         JoinStats* stats = nullptr) {
+  return detail::pairs(ix, points, GJ_MODE_APPROX, stats);
+}
+
+/// Mode from the bundle (join.cpp:257); zero counts are omitted; `threads` is
+/// accepted for signature parity — the result never depended on it.
+inline std::map<uint32_t, uint64_t> join_count_per_polygon(const DeviceIndex& ix,
+                                                           std::span<const LatLng> points,
+                                                           int /*threads*/ = 1) {
+  std::vector<uint64_t> counts(ix.ids().size() + 1, 0);
+  uint64_t bad = 0;
+  detail::check(gj_join_count_host(ix.session(), detail::as_doubles(points), points.size(), 0,
+                                   GJ_MODE_BUNDLE, counts.data(), nullptr, nullptr, nullptr, &bad));
+  std::map<uint32_t, uint64_t> out;
+  for (size_t s = 0; s < ix.ids().size(); ++s) {
+    if (counts[s]) out.emplace(ix.ids()[s], counts[s]);
+  }
+  return out;
+}
+
+inline void accumulate_probe_stats(const DeviceIndex& ix, std::span<const LatLng> points,
+                                   JoinStats& stats) {
+  std::vector<uint64_t> counts(ix.ids().size() + 1, 0);
+  gj_stats s{};
+  uint64_t bad = 0;
+  detail::check(gj_join_count_host(ix.session(), detail::as_doubles(points), points.size(), 0,
+                                   GJ_MODE_APPROX, counts.data(), &s, nullptr, nullptr, &bad));
+  detail::add_stats(s, &stats);
+}
+
+inline IndexMetrics collect_metrics(const DeviceIndex& ix, std::span<const LatLng> points) {
+  JoinStats stats;
+  accumulate_probe_stats(ix, points, stats);
+  return metrics_from_stats(stats, ix.info().node_count);
+}
+
+}  // namespace geojoin::gpu

@@ -95,7 +95,27 @@ def build_ref(force: bool = False) -> Path | None:
     return REF_LIB
 
 
+def build_dropin_test(force: bool = False) -> Path | None:
+    """tests/cpp/dropin_test: the reference's headers + library and
+    include/geojoin_gpu.hpp + libgeojoin_b200.so in one C++ program."""
+    root = HERE.parent
+    src = root / "tests" / "cpp" / "dropin_test.cpp"
+    out = root / "tests" / "cpp" / "dropin_test"
+    gpu_lib = root / "paper_1802_09488_b200" / "libgeojoin_b200.so"
+    if not reference_available() or not gpu_lib.exists() or build_ref() is None:
+        return out if out.exists() else None
+    deps = [src, root / "include" / "geojoin_gpu.hpp", root / "include" / "geojoin_b200.h", REF_LIB, gpu_lib]
+    if not force and _newer(out, deps):
+        return out
+    _run(["g++", "-std=gnu++20", "-O2", "-ffp-contract=off", "-I", str(REF_ROOT / "include"),
+          "-I", str(root / "include"), str(src), "-o", str(out),
+          "-L", str(REF_DIR), "-lgeojoin_ref", "-L", str(gpu_lib.parent), "-lgeojoin_b200",
+          "-Wl,-rpath,$ORIGIN/../../oracle/_ref:$ORIGIN/../../paper_1802_09488_b200", "-lpthread"])
+    return out
+
+
 if __name__ == "__main__":
     force = "--force" in sys.argv
     print("oracle:", build_oracle(force))
     print("ref   :", build_ref(force))
+    print("dropin:", build_dropin_test(force))

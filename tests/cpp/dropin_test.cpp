@@ -1,0 +1,112 @@
+// Drop-in test: a C++ program written against the REFERENCE's headers that
+// runs the reference's CPU join and geojoin::gpu's join (include/geojoin_gpu.hpp
+// over libgeojoin_b200.so) on the same IndexBundle and compares the results
+// bit for bit.  Mirrors the reference's own join tests (tests/test_join.cpp:
+// 115-134 exact == oracle, :160-189 approx, :200-214 streaming counts) with
+// the reference itself as the oracle.  Built by __graft_entry__.build() where
+// /root/reference exists; run on the GPU box by tests/test_gpu_dropin.py.
+#include <cmath>
+#include <cstdio>
+#include <random>
+#include <vector>
+
+#include "geojoin/join.hpp"
+#include "geojoin_gpu.hpp"
+
+using namespace geojoin;
+
+namespace {
+
+struct Rng {  // same recipe as the reference's test RNG: raw mt19937_64 -> [0,1)
+  std::mt19937_64 gen;
+  explicit Rng(uint64_t seed) : gen(seed) {}
+  double u01() { return static_cast<double>(gen() >> 11) * 0x1.0p-53; }
+  double uniform(double lo, double hi) { return lo + (hi - lo) * u01(); }
+  int uniform_int(int lo, int hi) { return lo + static_cast<int>(gen() % static_cast<uint64_t>(hi - lo + 1)); }
+};
+
+Polygon star(Rng& rng, uint32_t id, LatLng c, double radius, int n) {
+  Polygon poly;
+  poly.id = id;
+  const double pi = std::acos(-1.0);
+  for (int i = 0; i < n; ++i) {
+    const double a = (i + 0.2 + 0.6 * rng.u01()) * 2.0 * pi / n;
+    const double r = radius * rng.uniform(0.55, 1.45);
+    poly.vertices.push_back({c.lat + r * std::sin(a), c.lng + r * std::cos(a)});
+  }
+  return poly;
+}
+
+int failures = 0;
+#define EXPECT(cond)                                                  \
+  do {                                                                \
+    if (!(cond)) {                                                    \
+      std::printf("FAILED %s:%d: %s\n", __FILE__, __LINE__, #cond);   \
+      ++failures;                                                     \
+    }                                                                 \
+  } while (0)
+
+bool same_stats(const JoinStats& a, const JoinStats& b) {
+  return a.probes == b.probes && a.pip_tests == b.pip_tests && a.false_hits == b.false_hits &&
+         a.solely_true_hits == b.solely_true_hits && a.refinement_entered == b.refinement_entered &&
+         a.candidate_refs == b.candidate_refs;
+}
+
+void compare(const IndexBundle& bundle, const std::vector<LatLng>& points) {
+  gpu::DeviceIndex dev(bundle, 0);
+  JoinStats cs, gs;
+  EXPECT(gpu::join_exact(dev, points, &gs) == join_exact(bundle, points, &cs));
+  EXPECT(same_stats(cs, gs));
+  cs = JoinStats{};
+  gs = JoinStats{};
+  EXPECT(gpu::join_approx(dev, points, &gs) == join_approx(bundle, points, &cs));
+  EXPECT(same_stats(cs, gs));
+  for (int threads : {1, 3}) {
+    EXPECT(gpu::join_count_per_polygon(dev, points, threads) == join_count_per_polygon(bundle, points, threads));
+  }
+  cs = JoinStats{};
+  gs = JoinStats{};
+  accumulate_probe_stats(bundle, points, cs);
+  gpu::accumulate_probe_stats(dev, points, gs);
+  EXPECT(same_stats(cs, gs));
+  const IndexMetrics cm = collect_metrics(bundle, points), gm = gpu::collect_metrics(dev, points);
+  EXPECT(cm.tree_nodes == gm.tree_nodes && cm.false_hit_fraction == gm.false_hit_fraction &&
+         cm.solely_true_hit_fraction == gm.solely_true_hit_fraction && cm.avg_candidates == gm.avg_candidates);
+
+  // a single bad coordinate aborts the join with std::invalid_argument on both sides
+  std::vector<LatLng> bad = points;
+  bad[bad.size() / 2].lat = 91.0;
+  bool cpu_threw = false, gpu_threw = false;
+  try { join_exact(bundle, bad); } catch (const std::invalid_argument&) { cpu_threw = true; }
+  try { gpu::join_exact(dev, bad); } catch (const std::invalid_argument&) { gpu_threw = true; }
+  EXPECT(cpu_threw && gpu_threw);
+}
+
+}  // namespace
+
+int main() {
+  Rng rng(0x10e0002);
+  std::vector<Polygon> polygons;
+  for (uint32_t i = 0; i < 8; ++i) {
+    const LatLng c{rng.uniform(-10.0, -6.0), rng.uniform(50.0, 54.0)};
+    const double radius = rng.uniform(0.2, 1.2);
+    polygons.push_back(star(rng, i, c, radius, rng.uniform_int(8, 24)));
+  }
+  std::vector<LatLng> points;
+  for (int i = 0; i < 20000; ++i) points.push_back({rng.uniform(-11.5, -4.5), rng.uniform(48.5, 55.5)});
+  for (int i = 0; i < 16; ++i) points[i] = polygons[3].vertices[i % polygons[3].vertices.size()];  // on vertices
+
+  JoinConfig exact_cfg;
+  exact_cfg.mode = JoinMode::kExact;
+  compare(build_index(polygons, exact_cfg, {}), points);
+
+  JoinConfig approx_cfg;
+  approx_cfg.mode = JoinMode::kApprox;
+  approx_cfg.precision_m = 500.0;
+  const IndexBundle approx_bundle = build_index(polygons, approx_cfg, {});
+  EXPECT(approx_bundle.report().mode == JoinMode::kApprox);
+  compare(approx_bundle, points);
+
+  if (failures == 0) std::printf("DROPIN OK\n");
+  return failures == 0 ? 0 : 1;
+}
