@@ -17,7 +17,7 @@ int load_index_file(const char* path, int device, gj_index** out);
 
 namespace {
 
-constexpr uint64_t kMaxLaunchPoints = 1ull << 31;  // task/point indices are u32
+constexpr uint64_t kMaxLaunchPoints = (1ull << 31) - 1;  // point indices are u32 with a flag bit
 constexpr size_t kScratchBudget = 3ull << 30;      // per-chunk task + overflow scratch
 
 size_t align16(size_t v) { return (v + 15) & ~size_t{15}; }
@@ -30,9 +30,13 @@ struct SmemPlan {
 SmemPlan plan_smem(const gj_index& ix) {
   SmemPlan p{};
   size_t at = align16(std::max<size_t>(ix.dev.dir.n_table * 4, 16));
+#ifdef GJ_SMEM_LIMIT_KB  // tuning: leave room for more than one CTA per SM
+  const size_t limit = static_cast<size_t>(GJ_SMEM_LIMIT_KB) << 10;
+#else
   const size_t limit = ix.smem_optin > 2048 ? ix.smem_optin - 1024 : 0;
+#endif
   p.queue_off = static_cast<uint32_t>(at);
-  at += static_cast<size_t>(kJoinThreads / 32) * kQueueCap * sizeof(uint2);
+  at += static_cast<size_t>(kJoinThreads / 32) * kQueueBytesPerWarp;
   p.hist_off = static_cast<uint32_t>(at);
   const size_t room = std::min<size_t>(limit > at ? limit - at : 0, 64 << 10);
   uint32_t rep = 32;
@@ -412,6 +416,32 @@ int gj_session_create(gj_index* ix, gj_session** out) {
   }
   GJ_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&s->h_status), 4 * sizeof(DevStatus), cudaHostAllocDefault));
   GJ_CUDA(s->d_status.reserve(4 * sizeof(DevStatus)));
+#ifndef GJ_NO_L2_PERSIST
+  // Keep the second directory tier resident in L2: it is small (<= 64 MB),
+  // gathered at random by ~30 % of the points, and would otherwise be churned
+  // out by the point stream that passes through the same cache.
+  if (ix->dev.dir2.n_table) {
+    cudaDeviceProp prop{};
+    GJ_CUDA(cudaGetDeviceProperties(&prop, ix->device));
+    const size_t table_bytes = static_cast<size_t>(ix->dev.dir2.n_table) * 4;
+    const size_t window = std::min<size_t>(table_bytes, static_cast<size_t>(prop.accessPolicyMaxWindowSize));
+    const size_t carve = std::min<size_t>(window, static_cast<size_t>(prop.persistingL2CacheMaxSize));
+    if (carve > 0) {
+      size_t current = 0;
+      cudaDeviceGetLimit(&current, cudaLimitPersistingL2CacheSize);
+      if (current < carve) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, carve);
+      cudaStreamAttrValue attr{};
+      attr.accessPolicyWindow.base_ptr = const_cast<uint32_t*>(ix->dev.dir2.table);
+      attr.accessPolicyWindow.num_bytes = window;
+      attr.accessPolicyWindow.hitRatio = static_cast<float>(std::min(1.0, static_cast<double>(carve) / window));
+      attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+      attr.accessPolicyWindow.missProp = cudaAccessPropertyNormal;
+      if (cudaStreamSetAttribute(s->stream, cudaStreamAttributeAccessPolicyWindow, &attr) != cudaSuccess) {
+        cudaGetLastError();  // persistence is an optimisation, never a requirement
+      }
+    }
+  }
+#endif
   GJ_CUDA(s->d_task_per_slot.reserve(static_cast<size_t>(ix->dev.n_ids + 1) * 4));
   *out = s.release();
   return GJ_OK;

@@ -27,8 +27,14 @@ namespace gj {
 #endif
 constexpr int kJoinThreads = GJ_JOIN_THREADS;
 constexpr int kPointsPerThread = GJ_PPT;
-// open-point queue entries per warp: < 32 left over + up to 32 per point slot of a tile
-constexpr int kQueueCap = 32 * (kPointsPerThread + 1);
+// Per-warp queues of 8-byte items.  Q2 holds the points the shared-memory
+// directory left open (< 32 left over + up to 32 per point slot of a tile);
+// Q3 the few that the second tier leaves open as well (< 32 left over + 32
+// per Q2 drain).
+constexpr int kQueue2Cap = 32 * (kPointsPerThread + 1);
+constexpr int kQueue3Cap = 64;
+constexpr int kQueueBytesPerWarp = (kQueue2Cap + kQueue3Cap) * 8;
+constexpr int kChunkPoints = 32 * kPointsPerThread;  // consecutive points a warp owns in a tile
 constexpr int kRefineThreads = 256;
 constexpr int kRefineTile = 64;  // vertices staged per warp and tile
 
@@ -109,8 +115,8 @@ __device__ __forceinline__ uint32_t ldg32_if(const uint32_t* p, bool pred, uint3
                : "l"(p), "r"(otherwise), "r"(static_cast<uint32_t>(pred)));
   return v;
 }
-__device__ __forceinline__ void stcs32_if(uint32_t* p, uint32_t v, bool pred) {
-  asm volatile("{ .reg .pred p; setp.ne.u32 p, %2, 0; @p st.global.cs.u32 [%0], %1; }" ::"l"(p), "r"(v),
+__device__ __forceinline__ void st32_if(uint32_t* p, uint32_t v, bool pred) {
+  asm volatile("{ .reg .pred p; setp.ne.u32 p, %2, 0; @p st.global.u32 [%0], %1; }" ::"l"(p), "r"(v),
                "r"(static_cast<uint32_t>(pred))
                : "memory");
 }
@@ -227,23 +233,30 @@ __device__ __noinline__ uint2 emit_general(const DevIndex& ix, const JoinParams&
 
 // K1.  Persistent grid (one CTA per SM); each CTA stages the first directory
 // tier (and a replicated per-polygon histogram) in shared memory once, then
-// streams tiles of points: 16-byte coalesced loads, kPointsPerThread
-// independent points in flight per thread.  A tile runs in three phases of
-// decreasing population:
+// streams tiles of points.  A tile is kTile consecutive points; warp w owns
+// the kChunkPoints consecutive points at w*kChunkPoints inside it (lane l,
+// slot j -> point j*32 + l of the chunk), so every load and store of a warp is
+// one contiguous 512 / 128 byte run, and a thread keeps kPointsPerThread
+// independent 16-byte loads in flight.  The work has three populations, and
+// only the first runs where the points are:
 //   1. all points, straight-line: cell coordinates, shared-memory directory,
-//      emit when it resolves to one payload;
-//   2. points under a directory link: one independent gather each into the
-//      second, L2-resident directory tier — all gathers of the tile are
-//      issued before any is consumed;
-//   3. the remainder (deep boundary nodes, dictionary entries, exact-mode
-//      candidates) is compacted into per-warp queues and drained 32 at a
-//      time: dependent 8-byte gathers down the arena, lookup-table records.
+//      emit when it resolves to one payload (71 % on BASELINE config 2);
+//   2. points under a directory link (29 %): compacted into the warp's queue
+//      Q2 and drained 32 at a time — one 4-byte gather each into the second,
+//      L2-resident directory tier, same settle logic;
+//   3. what is still open (2 %: deep boundary nodes, dictionary entries,
+//      exact-mode candidates): compacted again into Q3 and drained 32 at a
+//      time — dependent 8-byte gathers down the arena, lookup-table records,
+//      candidate tasks.
+// Running 2 and 3 in place would drag all 32 lanes through their code for the
+// few active ones; through the queues they always run with full warps.
 template <bool kIds, bool kStats, bool kDense>
 __global__ void __launch_bounds__(kJoinThreads, GJ_JOIN_MIN_BLOCKS)
 join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinParams jp) {
   extern __shared__ __align__(16) unsigned char smem[];
   const uint32_t tid = threadIdx.x;
   const uint32_t lane = tid & 31u;
+  const uint32_t warp = tid >> 5;
 
   {  // stage the directory, clear the histogram
     const uint4* src = reinterpret_cast<const uint4*>(ix.dir.table);
@@ -259,7 +272,8 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
   // loop invariants in registers
   const uint32_t s_table = smem_addr(smem);
   const HistRef hist{smem_addr(smem + jp.smem_hist_off), jp.hist_rep, lane & (jp.hist_rep ? jp.hist_rep - 1u : 0u)};
-  const uint32_t s_queue = smem_addr(smem + jp.smem_queue_off) + (tid >> 5) * (kQueueCap * 8u);
+  const uint32_t s_q2 = smem_addr(smem + jp.smem_queue_off) + warp * kQueueBytesPerWarp;
+  const uint32_t s_q3 = s_q2 + kQueue2Cap * 8u;
   const uint32_t lane_lt = (1u << lane) - 1u;
   const uint32_t d1_w = ix.dir.width, d1_h = ix.dir.height, d1_pitch = ix.dir.pitch;
   const uint32_t d1_x0 = ix.dir.x0, d1_y0 = ix.dir.y0;
@@ -273,18 +287,22 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
   const uint32_t leaf_keep = ~((1u << (30 - ix.leaf_level)) - 1u);  // cell_id.cpp:93-94
   const double2* __restrict__ pts = jp.pts;
   uint32_t* __restrict__ first_id = jp.first_id;
-  const uint32_t n = static_cast<uint32_t>(jp.n);  // 1 <= n <= 2^31 per launch
+  const uint32_t n = static_cast<uint32_t>(jp.n);  // 1 <= n < 2^31 per launch (bit 31 of an index is a queue flag)
   // A code resolves right here when it is one inlined payload that emits: a
   // true hit, or a candidate in approximate mode (join.cpp:100-108).
   const uint32_t emit_mask = 0xC0000000u | (jp.exact ? 1u : 0u);
   const uint32_t emit_bits = kDirInline | (jp.exact ? 1u : 0u);
 
   uint32_t n_valid = 0, false_hits = 0, solely_true = 0, refined = 0, cand_refs = 0;
-  uint32_t q_count = 0;  // open points queued by this warp (warp-uniform)
+  uint32_t q2_count = 0, q3_count = 0;  // warp-uniform
 
   // One resolved directory code of a live point: count, stats, first id.
   // Returns true when the point is finished (inlined emit or miss).
-  auto settle = [&](uint32_t c, bool active, uint32_t i) -> bool {
+  // First ids: population 1 writes the word of EVERY live lane (kNoMatch
+  // unless it emits), i.e. whole 128-byte runs per warp; later populations
+  // only overwrite words that change, and those 4-byte stores then hit a
+  // sector that is still dirty in L2 instead of forcing a 32-byte DRAM fill.
+  auto settle = [&](uint32_t c, bool active, uint32_t i, bool store_all, bool live) -> bool {
     const bool emit = active && (c & emit_mask) == emit_bits;
     const bool miss = active && c == 0u;
     const uint32_t id = (c >> 1) & 0x1FFFFFFFu;
@@ -299,11 +317,11 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
       refined += emit && !(c & 1u);
       cand_refs += emit && !(c & 1u);
     }
-    if (kIds) stcs32_if(first_id + i, emit ? id : kNoMatch, emit || miss);
+    if (kIds) st32_if(first_id + i, emit ? id : kNoMatch, store_all ? live : emit);
     return emit || miss;
   };
 
-  // Phase 3 for one open point.
+  // Population 3, one open point: arena descent / dictionary / candidates.
   auto resolve_open = [&](uint32_t i, uint32_t c) {
     uint64_t entry;
     if (c & kDirLink) {
@@ -338,25 +356,65 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
         cand_refs += r.y;
       }
     }
-    if (kIds) __stcs(first_id + i, first);
+    if (kIds && first != kNoMatch) first_id[i] = first;
+  };
+
+  // Append (a, b) of the lanes with `open` to a warp queue; returns the new count.
+  auto enqueue = [&](uint32_t queue, uint32_t count, bool open, uint32_t a, uint32_t b) -> uint32_t {
+    const uint32_t mask = __ballot_sync(0xffffffffu, open);
+    sts64_if(queue + (count + __popc(mask & lane_lt)) * 8u, a, b, open);
+    return count + __popc(mask);
+  };
+
+  auto drain3 = [&](bool flush) {
+    __syncwarp();
+    while (q3_count >= 32u || (flush && q3_count)) {
+      const uint32_t take = min(q3_count, 32u);
+      q3_count -= take;
+      const uint2 item = lds64(s_q3 + (q3_count + min(lane, take - 1u)) * 8u);
+      __syncwarp();
+      if (lane < take) resolve_open(item.x, item.y);
+    }
+  };
+
+  // Population 2: 32 (or, when flushing, the remaining) Q2 items.  An item is
+  // (point | flag, w): with the flag (bit 31) w indexes the second directory
+  // tier; without it w is a first-tier code that goes straight on to Q3.
+  auto drain2 = [&](bool flush) {
+    __syncwarp();
+    while (q2_count >= 32u || (flush && q2_count)) {
+      const uint32_t take = min(q2_count, 32u);
+      q2_count -= take;
+      const uint2 item = lds64(s_q2 + (q2_count + min(lane, take - 1u)) * 8u);
+      __syncwarp();
+      const bool mine = lane < take;
+      const bool lookup = mine && (item.x & 0x80000000u) != 0u;
+      const uint32_t i = item.x & 0x7FFFFFFFu;
+      const uint32_t c = ldg32_if(table2 + item.y, lookup, item.y);
+      const bool done = settle(c, lookup, i, false, true);
+      q3_count = enqueue(s_q3, q3_count, mine && !done, i, c);
+#ifdef GJ_EXP_NO_PHASE3  // timing experiment: results are wrong
+      q3_count = 0;
+#endif
+      drain3(false);
+    }
   };
 
   constexpr uint32_t kTile = kJoinThreads * kPointsPerThread;
   const uint32_t n_tiles = (n + kTile - 1) / kTile;
   for (uint32_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-    const uint32_t base = tile * kTile + tid;
+    const uint32_t base = tile * kTile + warp * kChunkPoints + lane;  // point of slot j: base + 32 j
     double2 p[kPointsPerThread];
-    uint32_t code[kPointsPerThread], gx[kPointsPerThread], gy[kPointsPerThread];
 #pragma unroll
     for (int j = 0; j < kPointsPerThread; ++j) {
       // streaming read, touched once: evict-first.  Lanes past the end re-read
       // the last point and are masked below.
-      p[j] = __ldcs(pts + min(base + j * kJoinThreads, n - 1u));
+      p[j] = __ldcs(pts + min(base + j * 32u, n - 1u));
     }
-    // ---- phase 1: shared-memory directory ----
+    // ---- population 1: shared-memory directory ----
 #pragma unroll
     for (int j = 0; j < kPointsPerThread; ++j) {
-      const uint32_t i = base + j * kJoinThreads;
+      const uint32_t i = base + j * 32u;
       const bool live = i < n;
       const bool valid = latlng_valid(p[j].x, p[j].y);
       if (live && !valid) flag_error(jp.status, kErrInvalidPoint, jp.base_index + i);  // cell_id.cpp:83-85
@@ -367,53 +425,22 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
       const uint32_t c = lds32(s_table + (cy * d1_pitch + cx) * 4u);
       const bool active = live && valid;
       if (kStats) n_valid += active;
-      const bool done = settle(c, active, i);
-      code[j] = (active && !done) ? c : 0u;
-      gx[j] = x;
-      gy[j] = y;
-    }
+      const bool done = settle(c, active, i, true, live);
 #ifdef GJ_EXP_PHASE1_ONLY  // timing experiment: results are wrong
-    continue;
+      continue;
 #endif
-    // ---- phase 2: second directory tier, one gather per linked point ----
-    if (has_dir2) {
-      uint32_t c2[kPointsPerThread];
-#pragma unroll
-      for (int j = 0; j < kPointsPerThread; ++j) {
-        const uint32_t cx = min((gx[j] >> d2_shift) - d2_x0, d2_w);
-        const uint32_t cy = min((gy[j] >> d2_shift) - d2_y0, d2_h);
-        c2[j] = ldg32_if(table2 + (cy * d2_pitch + cx), (code[j] & kDirLink) != 0u, code[j]);
-      }
-#pragma unroll
-      for (int j = 0; j < kPointsPerThread; ++j) {
-        const bool linked = (code[j] & kDirLink) != 0u;
-        const bool done = settle(c2[j], linked, base + j * kJoinThreads);
-        code[j] = done ? 0u : c2[j];
-      }
+      // what stays open is queued: a link as its cell's index in the second
+      // tier, anything else (or everything, without a second tier) as the code
+      const uint32_t cx2 = min((x >> d2_shift) - d2_x0, d2_w);
+      const uint32_t cy2 = min((y >> d2_shift) - d2_y0, d2_h);
+      const bool via_tier2 = has_dir2 && (c & kDirLink) != 0u;
+      q2_count = enqueue(s_q2, q2_count, active && !done, via_tier2 ? i | 0x80000000u : i,
+                         via_tier2 ? cy2 * d2_pitch + cx2 : c);
     }
-    // ---- phase 3, deferred: what is still open goes to this warp's queue ----
-#pragma unroll
-    for (int j = 0; j < kPointsPerThread; ++j) {
-      const bool open = code[j] != 0u;
-      const uint32_t mask = __ballot_sync(0xffffffffu, open);
-      sts64_if(s_queue + (q_count + __popc(mask & lane_lt)) * 8u, base + j * kJoinThreads, code[j], open);
-      q_count += __popc(mask);
-    }
-#ifdef GJ_EXP_NO_PHASE3  // timing experiment: results are wrong
-    q_count = 0;
-#endif
-    __syncwarp();
-    while (q_count >= 32u) {
-      q_count -= 32u;
-      const uint2 item = lds64(s_queue + (q_count + lane) * 8u);
-      __syncwarp();
-      resolve_open(item.x, item.y);
-    }
+    drain2(false);
   }
-  if (lane < q_count) {  // the last, partial batch
-    const uint2 item = lds64(s_queue + lane * 8u);
-    resolve_open(item.x, item.y);
-  }
+  drain2(true);
+  drain3(true);
 
   __syncthreads();
   if (jp.hist_rep) {  // fold the replicas, one global add per non-zero slot

@@ -22,13 +22,12 @@ from paper_1802_09488_b200 import _build  # noqa: E402
 OUT = ROOT / "tools" / "_variants"
 VARIANTS = {
     "base": [],
-    "t512_b2": ["GJ_JOIN_THREADS=512", "GJ_JOIN_MIN_BLOCKS=2"],
-    "ppt2": ["GJ_PPT=2"],
-    "ppt3": ["GJ_PPT=3"],
+    "t768_b2_ppt2": ["GJ_JOIN_THREADS=768", "GJ_JOIN_MIN_BLOCKS=2", "GJ_PPT=2", "GJ_SMEM_LIMIT_KB=112"],
+    "t768_b2_ppt3": ["GJ_JOIN_THREADS=768", "GJ_JOIN_MIN_BLOCKS=2", "GJ_PPT=3", "GJ_SMEM_LIMIT_KB=112"],
+    "t640_b2_ppt4": ["GJ_JOIN_THREADS=640", "GJ_JOIN_MIN_BLOCKS=2", "GJ_PPT=4", "GJ_SMEM_LIMIT_KB=112"],
     "ppt6": ["GJ_PPT=6"],
     "exp_phase1_only": ["GJ_EXP_PHASE1_ONLY"],
     "exp_no_phase3": ["GJ_EXP_NO_PHASE3"],
-    "exp_no_hist": ["GJ_EXP_NO_HIST"],
 }
 
 
@@ -52,6 +51,12 @@ def run_all(n_points: int):
     d_pts = torch.from_numpy(pts).cuda()
     results = {}
     ref_counts = None
+    # ground truth for a 20 M prefix from the CPU oracle (test infrastructure)
+    from oracle import oracle as _oracle
+    from tests import golden_util
+    n_chk = min(n_points, 20_000_000)
+    ox = golden_util.oracle_index(golden_util.parse_gjx(path.read_bytes()))
+    truth_map, _ = ox.join_count(pts[:n_chk], approx=True, threads=16)
     for name in VARIANTS:
         lib = OUT / f"lib_{name}.so"
         if not lib.exists():
@@ -68,6 +73,17 @@ def run_all(n_points: int):
         def step():
             sess.join_count_device(d_pts.data_ptr(), n_points, d_counts.data_ptr(), capi.GJ_MODE_APPROX,
                                    d_first_id_ptr=d_first.data_ptr())
+        truth = np.zeros(len(bundle.ids), np.int64)
+        for k, v in truth_map.items():
+            truth[np.searchsorted(bundle.ids, k)] = v
+        sess.join_count_device(d_pts.data_ptr(), n_chk, d_counts.data_ptr(), capi.GJ_MODE_APPROX,
+                               d_first_id_ptr=d_first.data_ptr(), sync=True)
+        chk = d_counts.cpu().numpy()
+        truth_ok = bool(np.array_equal(chk, truth))
+        if not truth_ok:
+            print(f"   {name}: prefix counts differ from the oracle: sum {chk.sum()} vs {truth.sum()}, "
+                  f"{(chk != truth).sum()} slots", flush=True)
+        d_counts.zero_()
         for _ in range(3):
             step()
         sess.sync()
@@ -88,8 +104,9 @@ def run_all(n_points: int):
             if ref_counts is None:
                 ref_counts = counts
             ok = bool(np.array_equal(counts, ref_counts))
-        results[name] = {"ms": ms, "gpts": n_points / ms / 1e6, "counts_ok": ok}
-        print(f"{name:28s} {ms:8.4f} ms  {n_points / ms / 1e6:8.1f} Gpts/s  counts_ok={ok}", flush=True)
+        results[name] = {"ms": ms, "gpts": n_points / ms / 1e6, "counts_ok": ok, "oracle_ok": truth_ok}
+        print(f"{name:28s} {ms:8.4f} ms  {n_points / ms / 1e6:8.1f} Gpts/s  counts_ok={ok} oracle_ok={truth_ok}",
+              flush=True)
         sess.close()
         bundle.close()
     (ROOT / "gpurun_out").mkdir(exist_ok=True)
