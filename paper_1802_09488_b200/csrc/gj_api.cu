@@ -117,26 +117,11 @@ int enqueue_join(gj_session* s, const JoinRequest& rq) {
   jp.task_slot = s->d_task_slot.as<uint32_t>();
   jp.task_ord = s->d_task_ord.as<uint32_t>();
   jp.task_cap = rq.exact ? rq.task_cap : 0;
-  jp.task_per_slot = s->d_task_per_slot.as<uint32_t>();
   jp.status = rq.d_status;
   jp.smem_queue_off = sp.queue_off;
   jp.smem_hist_off = sp.hist_off;
   jp.hist_rep = sp.hist_rep;
   jp.exact = rq.exact ? 1 : 0;
-
-  RefinePlan pl{};
-  if (rq.exact) {
-    GJ_CUDA(s->d_task_per_slot.reserve(static_cast<size_t>(n_ids + 1) * 4));
-    GJ_CUDA(s->d_scan_a.reserve(static_cast<size_t>(n_ids + 2) * 4 * 3 + 16));
-    jp.task_per_slot = s->d_task_per_slot.as<uint32_t>();
-    GJ_CUDA(cudaMemsetAsync(jp.task_per_slot, 0, static_cast<size_t>(n_ids + 1) * 4, s->stream));
-    uint32_t* base = s->d_scan_a.as<uint32_t>();
-    pl.task_per_slot = jp.task_per_slot;
-    pl.slot_task_off = base;
-    pl.slot_unit_off = base + (n_ids + 1);
-    pl.slot_cursor = base + 2 * (n_ids + 1);
-    pl.unit_counter = base + 3 * (n_ids + 1);
-  }
 
   const int variant = (rq.d_first_id ? 4 : 0) | (rq.want_stats ? 2 : 0) | (ix.dev.ids_dense ? 1 : 0);
   switch (variant) {
@@ -152,16 +137,13 @@ int enqueue_join(gj_session* s, const JoinRequest& rq) {
   if (rc != GJ_OK) return rc;
 
   if (rq.exact && n_ids) {
-    plan_units_kernel<<<1, 1024, 0, s->stream>>>(pl, n_ids);
-    const unsigned blocks = static_cast<unsigned>(ix.sm_count) * 8u;
-    scatter_tasks_kernel<<<blocks, 256, 0, s->stream>>>(pl, jp.task_slot, rq.d_status, jp.task_cap,
-                                                        s->d_task_sorted.as<uint32_t>());
     RefineParams rp{};
     rp.pts = rq.d_pts;
     rp.base_index = rq.base_index;
     rp.task_point = jp.task_point;
+    rp.task_slot = jp.task_slot;
     rp.task_ord = jp.task_ord;
-    rp.task_sorted = s->d_task_sorted.as<uint32_t>();
+    rp.task_cap = jp.task_cap;
     rp.counts = rq.d_counts;
     rp.ovf_point = jp.ovf_point;
     rp.ovf_id = jp.ovf_id;
@@ -170,8 +152,16 @@ int enqueue_join(gj_session* s, const JoinRequest& rq) {
     rp.task_pass = rq.d_task_pass;
     rp.status = rq.d_status;
     rp.want_ids = rq.d_first_id ? 1 : 0;
-    refine_kernel<<<blocks, kRefineThreads, 0, s->stream>>>(ix.dev, pl, rp);
-    s->launches += 3;
+    const size_t counts_smem = static_cast<size_t>(n_ids) * 4;
+    rp.smem_counts = counts_smem <= (32u << 10) ? 1 : 0;
+    // persistent grid: exactly the blocks that are resident at once (a partial
+    // second wave of a grid-stride kernel only adds a tail)
+    int per_sm = 0;
+    GJ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, refine_kernel, kRefineThreads,
+                                                          rp.smem_counts ? counts_smem : 0));
+    const unsigned blocks = static_cast<unsigned>(ix.sm_count) * static_cast<unsigned>(std::max(per_sm, 1));
+    refine_kernel<<<blocks, kRefineThreads, rp.smem_counts ? counts_smem : 0, s->stream>>>(ix.dev, rp);
+    ++s->launches;
     GJ_CUDA(cudaGetLastError());
   }
   return GJ_OK;
@@ -181,7 +171,6 @@ int reserve_tasks(gj_session* s, uint64_t cap) {
   GJ_CUDA(s->d_task_point.reserve(cap * 4 + 16));
   GJ_CUDA(s->d_task_slot.reserve(cap * 4 + 16));
   GJ_CUDA(s->d_task_ord.reserve(cap * 4 + 16));
-  GJ_CUDA(s->d_task_sorted.reserve(cap * 4 + 16));
   return GJ_OK;
 }
 
@@ -442,7 +431,6 @@ int gj_session_create(gj_index* ix, gj_session** out) {
     }
   }
 #endif
-  GJ_CUDA(s->d_task_per_slot.reserve(static_cast<size_t>(ix->dev.n_ids + 1) * 4));
   *out = s.release();
   return GJ_OK;
 }

@@ -43,6 +43,33 @@ struct DevDirectory {
   int32_t chunks;         // node steps already resolved
 };
 
+// Latitude strips of one polygon: its widened latitude range [y0, y0 + k / inv_h]
+// cut into k equal strips; strip s lists (as 32-byte edge records) every edge
+// whose latitude range, widened by the 1e-9 deg margin of pip_edge, meets it.
+struct StripMeta {
+  double y0;
+  double inv_h;
+  uint32_t k;         // strips (0 = no geometry for this slot)
+  uint32_t ptr_base;  // first entry of this polygon in strip_ptr (k + 1 entries)
+};
+
+struct EdgeRecord {  // x = lng, y = lat (geometry.cpp:35); 64 bytes
+  double ax, ay, bx, by;
+  // the edge's bounding box widened by pip_edge_classify's 1e-9 deg margin:
+  // fmin(ax, bx) - m, fmax(ax, bx) + m, fmin(ay, by) - m, fmax(ay, by) + m
+  double x_lo, x_hi, y_lo, y_hi;
+};
+
+// Strip of latitude y.  The same monotone fp64 expression runs on the host
+// when edges are assigned to strips, so a point inside an edge's widened
+// range always lands in a strip that lists the edge.
+__host__ __device__ inline uint32_t strip_of(double y, double y0, double inv_h, uint32_t k) {
+  const double t = (y - y0) * inv_h;
+  if (!(t > 0.0)) return 0;
+  const double top = static_cast<double>(k - 1);
+  return t >= top ? k - 1 : static_cast<uint32_t>(t);
+}
+
 struct DevIndex {
   const uint64_t* arena;   // payload polygon ids replaced by id-table slots
   const uint32_t* lut;     // records [t, slot*t, c, slot*c]
@@ -52,6 +79,9 @@ struct DevIndex {
   const uint64_t* ring_off;
   const uint32_t* ring_len;
   const double2* ring_xy;
+  const StripMeta* strip_meta;     // [n_ids]
+  const uint32_t* strip_ptr;       // per polygon k + 1 offsets into strip_edges
+  const EdgeRecord* strip_edges;
   uint64_t roots[8];
   uint64_t prefixes[8];
   uint32_t prefix_bits[8];
@@ -269,29 +299,41 @@ __device__ __forceinline__ double point_segment_dist_sq(double px, double py, do
   return __dadd_rn(__dmul_rn(cx, cx), __dmul_rn(cy, cy));
 }
 
-// One edge's contribution to pip_test: bit 0 = on the boundary, bit 1 = the
-// rightward ray crosses it.  The boundary any() and the crossing parity are
-// order-independent, so edges may be evaluated in any order or in parallel;
-// each edge's arithmetic is the reference's.
-__device__ __forceinline__ uint32_t pip_edge(double qx, double qy, double ax, double ay, double bx,
-                                             double by) {
+// One edge's contribution to pip_test, split so that the cheap part can run
+// per lane and the parts with a division can be batched.  The boundary any()
+// and the crossing parity are order-independent, so edges may be evaluated in
+// any order or in parallel; each edge's arithmetic is the reference's.
+//
+// Cheap classification: bit 0 = the boundary test has to be evaluated, bit 1 =
+// the edge straddles the point's latitude and the crossing test has to be.
+//
+// Bit 0 is an exact rejection of the boundary test: a point farther than 1e-9
+// degrees from the edge's bounding box is at distance >= 1e-9 from the
+// segment, and rounding errors of the distance arithmetic (coordinates <= 360,
+// ulp <= 5.7e-14) cannot bring cx^2+cy^2 from >= 1e-18 down to 1e-24, so the
+// reference's comparison is false as well.
+constexpr double kPipBoxMargin = 1e-9;
+
+__device__ __forceinline__ uint32_t pip_edge_classify(double qx, double qy, double ay, double by, double x_lo,
+                                                      double x_hi, double y_lo, double y_hi) {
+  const bool near_box = qx >= x_lo && qx <= x_hi && qy >= y_lo && qy <= y_hi;
+  const bool straddles = (ay > qy) != (by > qy);  // geometry.cpp:197
+  return (near_box ? 1u : 0u) | (straddles ? 2u : 0u);
+}
+
+// geometry.cpp:186-193: on an edge or vertex
+__device__ __forceinline__ bool pip_edge_on_boundary(double qx, double qy, double ax, double ay, double bx,
+                                                     double by) {
   const double eps_sq = __dmul_rn(1e-12, 1e-12);  // the product, not 1e-24
-  uint32_t r = 0;
-  // Cheap exact rejection of the boundary test: a point farther than 1e-9
-  // degrees from the edge's bounding box is at distance >= 1e-9 from the
-  // segment, and rounding errors of the distance arithmetic (coordinates
-  // <= 360, ulp <= 5.7e-14) cannot bring cx^2+cy^2 from >= 1e-18 down to
-  // 1e-24, so the reference's comparison is false as well.
-  const double m = 1e-9;
-  const bool near_box = qx >= fmin(ax, bx) - m && qx <= fmax(ax, bx) + m &&
-                        qy >= fmin(ay, by) - m && qy <= fmax(ay, by) + m;
-  if (near_box && point_segment_dist_sq(qx, qy, ax, ay, bx, by) <= eps_sq) r |= 1u;
-  if ((ay > qy) != (by > qy)) {
-    const double x_cross =
-        __dadd_rn(ax, __dmul_rn(__ddiv_rn(__dsub_rn(qy, ay), __dsub_rn(by, ay)), __dsub_rn(bx, ax)));
-    if (qx < x_cross) r |= 2u;
-  }
-  return r;
+  return point_segment_dist_sq(qx, qy, ax, ay, bx, by) <= eps_sq;
+}
+
+// geometry.cpp:198-199, for an edge that straddles the point's latitude
+__device__ __forceinline__ bool pip_edge_crosses(double qx, double qy, double ax, double ay, double bx,
+                                                 double by) {
+  const double x_cross =
+      __dadd_rn(ax, __dmul_rn(__ddiv_rn(__dsub_rn(qy, ay), __dsub_rn(by, ay)), __dsub_rn(bx, ax)));
+  return qx < x_cross;
 }
 
 }  // namespace gj

@@ -61,7 +61,8 @@ struct gj_index {
   gj::DevIndex dev{};
   gj_index_info info{};
   std::vector<uint32_t> ids;  // slot -> polygon id
-  gj::DeviceBuffer d_arena, d_lut, d_ids, d_ring_off, d_ring_len, d_ring_xy, d_dir_table, d_dir_dict, d_dir2_table;
+  gj::DeviceBuffer d_arena, d_lut, d_ids, d_ring_off, d_ring_len, d_ring_xy, d_dir_table, d_dir_dict, d_dir2_table,
+      d_strip_meta, d_strip_ptr, d_strip_edges;
   int sm_count = 0;
   size_t smem_optin = 0;
   uint64_t max_refs = 0;       // most references behind one reachable entry
@@ -75,11 +76,10 @@ struct gj_session {
   cudaStream_t copy_out = nullptr;     // D2H
   uint64_t launches = 0;
   // scratch
-  gj::DeviceBuffer d_status, d_counts, d_stats, d_task_per_slot;
+  gj::DeviceBuffer d_status, d_counts, d_stats;
   gj::DeviceBuffer d_points[3], d_first_id[3], d_entries;
   gj::DeviceBuffer d_ovf_point, d_ovf_id, d_ovf_ord;
-  gj::DeviceBuffer d_task_point, d_task_slot, d_task_ord, d_task_sorted, d_task_flag;
-  gj::DeviceBuffer d_unit_poly, d_unit_begin, d_scan_a, d_scan_b;
+  gj::DeviceBuffer d_task_point, d_task_slot, d_task_ord;
   cudaEvent_t ev_in[3]{}, ev_done[3]{}, ev_out[3]{};
   gj::DevStatus* h_status = nullptr;   // pinned
   // materialised pairs kept for gj_pairs_copy

@@ -380,6 +380,57 @@ int create_index(const gj_index_desc& d, int device, gj_index** out) {
     }
   }
 
+  // Latitude strips per polygon for the refine kernel (see StripMeta).
+  std::vector<StripMeta> strip_meta(n_ids);
+  std::vector<uint32_t> strip_ptr;
+  std::vector<EdgeRecord> strip_edges;
+  {
+    const double margin = 1e-9;  // pip_edge's rejection margin
+    std::vector<std::vector<uint32_t>> lists;
+    for (size_t s = 0; s < n_ids; ++s) {
+      StripMeta& m = strip_meta[s];
+      m = StripMeta{0.0, 0.0, 0u, static_cast<uint32_t>(strip_ptr.size())};
+      const uint32_t ne = ring_len[s];
+      if (ne == 0) continue;
+      const double2* v = ring_xy.data() + ring_off[s];
+      double y_lo = v[0].y, y_hi = v[0].y;
+      for (uint32_t e = 1; e < ne; ++e) {
+        y_lo = std::min(y_lo, v[e].y);
+        y_hi = std::max(y_hi, v[e].y);
+      }
+      y_lo -= 2 * margin;
+      y_hi += 2 * margin;
+      m.k = std::min<uint32_t>(8192u, std::max<uint32_t>(1u, ne / 2));
+      m.y0 = y_lo;
+      m.inv_h = static_cast<double>(m.k) / (y_hi - y_lo);
+      const double slack = (y_hi - y_lo) / m.k / 64.0;
+      lists.assign(m.k, {});
+      for (uint32_t e = 0; e < ne; ++e) {
+        const double ya = v[e].y, yb = v[e + 1].y;
+        // strip_of is monotone and evaluated identically on the device, so the
+        // strips of [lo - margin, hi + margin] cover every point in that range;
+        // `slack` (1/64 of a strip) is insurance against a host compiler that
+        // rounds the expression differently.
+        const uint32_t first = strip_of(std::min(ya, yb) - margin - slack, m.y0, m.inv_h, m.k);
+        const uint32_t last = strip_of(std::max(ya, yb) + margin + slack, m.y0, m.inv_h, m.k);
+        for (uint32_t st = first; st <= last; ++st) lists[st].push_back(e);
+      }
+      for (uint32_t st = 0; st < m.k; ++st) {
+        strip_ptr.push_back(static_cast<uint32_t>(strip_edges.size()));
+        for (uint32_t e : lists[st]) {
+          const double2 a = v[e], b = v[e + 1];
+          strip_edges.push_back(EdgeRecord{a.x, a.y, b.x, b.y, std::min(a.x, b.x) - margin, std::max(a.x, b.x) + margin,
+                                           std::min(a.y, b.y) - margin, std::max(a.y, b.y) + margin});
+        }
+      }
+      strip_ptr.push_back(static_cast<uint32_t>(strip_edges.size()));
+      if (strip_edges.size() >= (1ull << 32)) {
+        set_error("polygon strip table exceeds 2^32 edge records");
+        return GJ_INVALID_ARGUMENT;
+      }
+    }
+  }
+
   if (an.dir.table.empty()) {  // no tree on face 0: the window is just its all-miss padding
     an.dir = HostDirectory{};
     an.dir.pitch = 1;
@@ -392,6 +443,9 @@ int create_index(const gj_index_desc& d, int device, gj_index** out) {
   if ((rc = upload(ix->d_ring_off, ring_off.data(), ring_off.size(), &bytes)) != GJ_OK) return rc;
   if ((rc = upload(ix->d_ring_len, ring_len.data(), ring_len.size(), &bytes)) != GJ_OK) return rc;
   if ((rc = upload(ix->d_ring_xy, ring_xy.data(), ring_xy.size(), &bytes)) != GJ_OK) return rc;
+  if ((rc = upload(ix->d_strip_meta, strip_meta.data(), strip_meta.size(), &bytes)) != GJ_OK) return rc;
+  if ((rc = upload(ix->d_strip_ptr, strip_ptr.data(), strip_ptr.size(), &bytes)) != GJ_OK) return rc;
+  if ((rc = upload(ix->d_strip_edges, strip_edges.data(), strip_edges.size(), &bytes)) != GJ_OK) return rc;
   if ((rc = upload(ix->d_dir_table, an.dir.table.data(), an.dir.table.size(), &bytes)) != GJ_OK) return rc;
   if ((rc = upload(ix->d_dir_dict, an.dict.data(), an.dict.size(), &bytes)) != GJ_OK) return rc;
   if ((rc = upload(ix->d_dir2_table, an.dir2.table.data(), an.dir2.table.size(), &bytes)) != GJ_OK) return rc;
@@ -403,6 +457,9 @@ int create_index(const gj_index_desc& d, int device, gj_index** out) {
   dv.ring_off = ix->d_ring_off.as<uint64_t>();
   dv.ring_len = ix->d_ring_len.as<uint32_t>();
   dv.ring_xy = ix->d_ring_xy.as<double2>();
+  dv.strip_meta = ix->d_strip_meta.as<StripMeta>();
+  dv.strip_ptr = ix->d_strip_ptr.as<uint32_t>();
+  dv.strip_edges = ix->d_strip_edges.as<EdgeRecord>();
   for (int f = 0; f < 8; ++f) {
     dv.roots[f] = f < 6 ? d.roots[f] : 0;  // refresh_view, act.cpp:373-383
     dv.prefixes[f] = f < 6 ? d.prefixes[f] : 0;

@@ -4,9 +4,9 @@
 //                          (counts, first ids, overflow records, stats) and,
 //                          in exact mode, candidate tasks for K2
 //   K1' probe_points_kernel / probe_cells_kernel   entries only (test hooks)
-//   K2  refine_kernel      ray-crossing PIP over candidate tasks bucketed by
-//                          polygon; edges staged in shared memory per warp
-//   plan_units_kernel / scatter_tasks_kernel        bucket the tasks for K2
+//   K2  refine_kernel      ray-crossing PIP over the candidate tasks: each
+//                          task tests only the edges of its polygon's
+//                          latitude strip (precomputed at index create)
 //
 // All of it is HBM/L2-bound integer and fp64 scalar work; no tensor cores.
 #pragma once
@@ -36,7 +36,6 @@ constexpr int kQueue3Cap = 64;
 constexpr int kQueueBytesPerWarp = (kQueue2Cap + kQueue3Cap) * 8;
 constexpr int kChunkPoints = 32 * kPointsPerThread;  // consecutive points a warp owns in a tile
 constexpr int kRefineThreads = 256;
-constexpr int kRefineTile = 64;  // vertices staged per warp and tile
 
 struct JoinParams {
   const double2* pts;  // (lat, lng) pairs: .x = lat, .y = lng  (latlng.hpp:26-29)
@@ -53,7 +52,6 @@ struct JoinParams {
   uint32_t* task_slot;
   uint32_t* task_ord;
   uint64_t task_cap;
-  uint32_t* task_per_slot;  // [n_ids]
   DevStatus* status;
   uint32_t smem_queue_off;  // bytes: per-warp open-point queues
   uint32_t smem_hist_off;   // bytes
@@ -140,73 +138,98 @@ __device__ __forceinline__ void count_slot(const DevIndex& ix, const JoinParams&
   }
 }
 
+// What one entry needs beyond the straight-line path: how many references
+// it holds, how many of them are candidates, and — for this join mode — how
+// many overflow records and candidate tasks it will write.
+struct EntryPlan {
+  uint32_t tag, off, t;     // lookup-table record [t, true ids, c, candidate ids] at `off`
+  uint32_t n_refs, n_cand;
+  uint32_t n_ovf, n_tasks;  // records to reserve
+  bool defer;               // some pairs depend on K2
+};
+
+template <bool kIds>
+__device__ __forceinline__ EntryPlan plan_entry(const DevIndex& ix, bool exact, uint64_t entry) {
+  EntryPlan e{};
+  e.tag = static_cast<uint32_t>(entry) & 3u;
+  if (e.tag == 1u) {
+    e.n_refs = 1;
+    e.n_cand = 1u - (static_cast<uint32_t>(entry >> 2) & 1u);
+  } else if (e.tag == 2u) {
+    e.n_refs = 2;
+    e.n_cand = 2u - ((static_cast<uint32_t>(entry >> 33) & 1u) + (static_cast<uint32_t>(entry >> 2) & 1u));
+  } else {
+    e.off = static_cast<uint32_t>(entry >> 2) & 0x7fffffffu;
+    e.t = __ldg(ix.lut + e.off);
+    e.n_refs = e.t + __ldg(ix.lut + e.off + 1 + e.t);
+    e.n_cand = e.n_refs - e.t;
+  }
+  e.defer = exact && e.n_cand != 0;
+  const uint32_t n_now = exact ? e.n_refs - e.n_cand : e.n_refs;  // pairs emitted by K1
+  // overflow records: everything after the first pair, or every pair when
+  // the point is deferred
+  e.n_ovf = kIds ? (e.defer ? n_now : (n_now > 0 ? n_now - 1 : 0)) : 0;
+  e.n_tasks = e.defer ? e.n_cand : 0;
+  return e;
+}
+
+// One reservation per warp: every lane asks for `want` consecutive records of
+// a global cursor; lane 0 does a single atomic for the warp's total and the
+// lanes get their bases from a prefix sum.  (Per-lane atomics with return on
+// one address serialise across the whole chip: with 1.8 % of the points
+// entering refinement they made the exact join 4.5x slower than the approx one.)
+__device__ __forceinline__ unsigned long long warp_reserve(unsigned long long* cursor, uint32_t want, uint32_t lane) {
+  uint32_t incl = want;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t up = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= static_cast<uint32_t>(o)) incl += up;
+  }
+  const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+  unsigned long long base = 0;
+  if (total != 0u && lane == 0u) base = atomicAdd(cursor, static_cast<unsigned long long>(total));
+  base = __shfl_sync(0xffffffffu, base, 0);
+  return base + (incl - want);
+}
+
 // The per-(point, entry) body of run_join (join.cpp:93-127) for everything
 // the straight-line path does not take: two payloads, lookup-table records,
 // exact-mode candidates (tasks for K2) and the overflow list.  Cold and out
-// of line.  Returns {first-id word, number of candidate references}.
+// of line.  Returns the first-id word of the point.
 template <bool kIds, bool kDense>
-__device__ __noinline__ uint2 emit_general(const DevIndex& ix, const JoinParams& jp, HistRef h, uint64_t entry,
-                                           uint32_t local) {
+__device__ __noinline__ uint32_t emit_general(const DevIndex& ix, const JoinParams& jp, HistRef h, uint64_t entry,
+                                              uint32_t local, EntryPlan e, unsigned long long ovf_base,
+                                              unsigned long long task_base) {
   const bool exact = jp.exact != 0;
-  const uint32_t tag = static_cast<uint32_t>(entry) & 3u;
-  uint32_t off = 0, t = 0, n_refs, n_cand;
-  if (tag == 1u) {
-    n_refs = 1;
-    n_cand = 1u - (static_cast<uint32_t>(entry >> 2) & 1u);
-  } else if (tag == 2u) {
-    n_refs = 2;
-    n_cand = 2u - ((static_cast<uint32_t>(entry >> 33) & 1u) + (static_cast<uint32_t>(entry >> 2) & 1u));
-  } else {
-    off = static_cast<uint32_t>(entry >> 2) & 0x7fffffffu;
-    t = __ldg(ix.lut + off);
-    n_refs = t + __ldg(ix.lut + off + 1 + t);
-    n_cand = n_refs - t;
+  const uint32_t n_now = exact ? e.n_refs - e.n_cand : e.n_refs;
+  uint32_t n_ovf = e.n_ovf;
+  if (n_ovf && ovf_base + n_ovf > jp.ovf_cap) {
+    atomicOr(&jp.status->flags, kErrOverflowCap);
+    n_ovf = 0;
   }
-  const bool defer = exact && n_cand != 0;                  // some pairs depend on K2
-  const uint32_t n_now = exact ? n_refs - n_cand : n_refs;  // pairs emitted here
+  const bool tasks_ok = e.n_tasks == 0 || task_base + e.n_tasks <= jp.task_cap;
+  if (!tasks_ok) atomicOr(&jp.status->flags, kErrTaskCap);
 
-  // overflow records: everything after the first pair, or every pair when
-  // the point is deferred
-  uint64_t ovf_base = 0;
-  uint32_t n_ovf = 0;
-  if (kIds) {
-    n_ovf = defer ? n_now : (n_now > 0 ? n_now - 1 : 0);
-    if (n_ovf) {
-      ovf_base = atomicAdd(&jp.status->overflow_count, static_cast<unsigned long long>(n_ovf));
-      if (ovf_base + n_ovf > jp.ovf_cap) {
-        atomicOr(&jp.status->flags, kErrOverflowCap);
-        n_ovf = 0;
-      }
-    }
-  }
-  uint64_t task_base = 0;
-  bool tasks_ok = false;
-  if (defer) {
-    task_base = atomicAdd(&jp.status->task_count, static_cast<unsigned long long>(n_cand));
-    tasks_ok = task_base + n_cand <= jp.task_cap;
-    if (!tasks_ok) atomicOr(&jp.status->flags, kErrTaskCap);
-  }
-
-  uint32_t first = defer ? kDeferred : kNoMatch;
+  uint32_t first = e.defer ? kDeferred : kNoMatch;
   uint32_t emitted = 0, tasks = 0;
-  for (uint32_t k = 0; k < n_refs; ++k) {
+  for (uint32_t k = 0; k < e.n_refs; ++k) {
     // k-th reference in the reference's emit order (act.hpp:169-196)
     uint32_t p;
-    if (tag == 1u) {
+    if (e.tag == 1u) {
       p = static_cast<uint32_t>(entry >> 2) & 0x7fffffffu;
-    } else if (tag == 2u) {
+    } else if (e.tag == 2u) {
       p = static_cast<uint32_t>(k == 0 ? entry >> 33 : entry >> 2) & 0x7fffffffu;
-    } else {  // record [t, true ids, c, candidate ids]
-      p = k < t ? (__ldg(ix.lut + off + 1 + k) << 1) | 1u : (__ldg(ix.lut + off + 2 + k) << 1);
+    } else {
+      p = k < e.t ? (__ldg(ix.lut + e.off + 1 + k) << 1) | 1u : (__ldg(ix.lut + e.off + 2 + k) << 1);
     }
     const uint32_t id = p >> 1;
     if ((p & 1u) != 0u || !exact) {
       count_slot<kDense>(ix, jp, h, id);
       if (kIds) {
-        if (!defer && emitted == 0) {
+        if (!e.defer && emitted == 0) {
           first = id | (n_now > 1 ? kMoreFlag : 0u);
         } else if (n_ovf) {
-          const uint64_t w = ovf_base + (defer ? emitted : emitted - 1);
+          const uint64_t w = ovf_base + (e.defer ? emitted : emitted - 1);
           jp.ovf_point[w] = jp.base_index + local;
           jp.ovf_id[w] = id;
           jp.ovf_ord[w] = k;
@@ -223,12 +246,11 @@ __device__ __noinline__ uint2 emit_general(const DevIndex& ix, const JoinParams&
         jp.task_point[w] = local;
         jp.task_slot[w] = slot;
         jp.task_ord[w] = k;
-        atomicAdd(&jp.task_per_slot[slot], 1u);
       }
       ++tasks;
     }
   }
-  return make_uint2(first, n_cand);
+  return first;
 }
 
 // K1.  Persistent grid (one CTA per SM); each CTA stages the first directory
@@ -321,25 +343,39 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
     return emit || miss;
   };
 
-  // Population 3, one open point: arena descent / dictionary / candidates.
-  auto resolve_open = [&](uint32_t i, uint32_t c) {
-    uint64_t entry;
-    if (c & kDirLink) {
-      const double2 q = __ldg(pts + i);  // cheaper to re-read than to queue the coordinates
-      uint32_t x, y;
-      grid_xy(q.x, q.y, &x, &y);
-      entry = walk_from(ix, c & ~kDirLink, walk_level, (x & leaf_keep) << 2, (y & leaf_keep) << 2);
-    } else if (c & kDirInline) {
-      entry = (static_cast<uint64_t>(c & 0x3FFFFFFFu) << 2) | 1u;  // exact-mode candidate
-    } else {
-      entry = __ldg(ix.dict + c);
+  // Population 3, one batch of open points (one per lane, `mine` = the lane
+  // holds one): arena descent / dictionary / candidates.  All 32 lanes go
+  // through it together because the record reservations are per warp.
+  auto resolve_open = [&](bool mine, uint32_t i, uint32_t c) {
+    uint64_t entry = 0;
+    if (mine) {
+      if (c & kDirLink) {
+        const double2 q = __ldg(pts + i);  // cheaper to re-read than to queue the coordinates
+        uint32_t x, y;
+        grid_xy(q.x, q.y, &x, &y);
+        entry = walk_from(ix, c & ~kDirLink, walk_level, (x & leaf_keep) << 2, (y & leaf_keep) << 2);
+      } else if (c & kDirInline) {
+        entry = (static_cast<uint64_t>(c & 0x3FFFFFFFu) << 2) | 1u;  // exact-mode candidate
+      } else {
+        entry = __ldg(ix.dict + c);
+      }
     }
+    const bool single = (static_cast<uint32_t>(entry) & 3u) == 1u &&
+                        ((static_cast<uint32_t>(entry >> 2) & 1u) != 0u || !jp.exact);  // one payload that emits
+    const bool general = mine && entry != 0 && !single;
+    EntryPlan plan{};
+    if (general) plan = plan_entry<kIds>(ix, jp.exact != 0, entry);
+    unsigned long long ovf_base = 0, task_base = 0;
+    if (__any_sync(0xffffffffu, general)) {
+      if (kIds) ovf_base = warp_reserve(&jp.status->overflow_count, plan.n_ovf, lane);
+      if (jp.exact) task_base = warp_reserve(&jp.status->task_count, plan.n_tasks, lane);
+    }
+    if (!mine) return;
     uint32_t first = kNoMatch;
     if (entry == 0) {
       if (kStats) ++false_hits;
-    } else if ((static_cast<uint32_t>(entry) & 3u) == 1u &&
-               ((static_cast<uint32_t>(entry >> 2) & 1u) != 0u || !jp.exact)) {
-      first = static_cast<uint32_t>(entry >> 3) & 0x3FFFFFFFu;  // one payload that emits
+    } else if (single) {
+      first = static_cast<uint32_t>(entry >> 3) & 0x3FFFFFFFu;
       count_slot<kDense>(ix, jp, hist, first);
       if (kStats) {
         const bool interior = (entry >> 2) & 1u;
@@ -348,12 +384,11 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
         cand_refs += !interior;
       }
     } else {
-      const uint2 r = emit_general<kIds, kDense>(ix, jp, hist, entry, i);
-      first = r.x;
+      first = emit_general<kIds, kDense>(ix, jp, hist, entry, i, plan, ovf_base, task_base);
       if (kStats) {
-        solely_true += r.y == 0;
-        refined += r.y != 0;
-        cand_refs += r.y;
+        solely_true += plan.n_cand == 0;
+        refined += plan.n_cand != 0;
+        cand_refs += plan.n_cand;
       }
     }
     if (kIds && first != kNoMatch) first_id[i] = first;
@@ -373,7 +408,7 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
       q3_count -= take;
       const uint2 item = lds64(s_q3 + (q3_count + min(lane, take - 1u)) * 8u);
       __syncwarp();
-      if (lane < take) resolve_open(item.x, item.y);
+      resolve_open(lane < take, item.x, item.y);
     }
   };
 
@@ -518,77 +553,31 @@ probe_cells_kernel(const __grid_constant__ DevIndex ix, const uint64_t* __restri
 }
 
 // ---------------------------------------------------------------------------
-// Task bucketing for K2: tasks grouped by polygon slot, cut into units of
-// <= 32 tasks (one warp each).  Single-CTA scan over the id table.
+// K2.  PIP refine of the candidate tasks K1 queued (exact mode).
+//
+// One thread per (point, polygon) task, tasks in arrival order.  The polygon's
+// edges are not scanned: the host cut every polygon into latitude strips at
+// index-create time (StripMeta), so a task reads its strip's handful of
+// 32-byte edge records (L1/L2-resident: a few MB for all polygons) and runs
+// the reference's exact fp64 edge arithmetic (pip_edge) on those only.  An
+// edge outside the point's strip has a latitude range — widened by pip_edge's
+// own 1e-9 deg rejection margin — that does not contain the point, so it can
+// neither be within the boundary tolerance nor cross the point's ray; the
+// boundary any() and the crossing parity over the remaining edges are the
+// reference's result bit for bit (geometry.cpp:184-204).  Work per task is a
+// few edges whatever the polygon's size, so a grid-stride loop balances.
+//
+// (Two earlier designs, kept in git history: thread-per-task over all edges
+// staged in shared memory per polygon bucket — 1.36 ms per 3.5 M tasks, fp64
+// pipe bound; the same with an fp32 filter-then-compact pass — 0.65 ms.)
 // ---------------------------------------------------------------------------
-struct RefinePlan {
-  const uint32_t* task_per_slot;  // [n_ids]
-  uint32_t* slot_task_off;        // [n_ids + 1]
-  uint32_t* slot_unit_off;        // [n_ids + 1]
-  uint32_t* slot_cursor;          // [n_ids]
-  uint32_t* unit_counter;         // [1] dynamic unit queue head
-};
-
-__global__ void __launch_bounds__(1024) plan_units_kernel(RefinePlan pl, uint32_t n_ids) {
-  __shared__ uint32_t s_a[1024], s_b[1024];
-  __shared__ uint32_t carry_a, carry_b;
-  const uint32_t tid = threadIdx.x;
-  if (tid == 0) {
-    carry_a = 0;
-    carry_b = 0;
-    *pl.unit_counter = 0;
-  }
-  __syncthreads();
-  for (uint32_t base = 0; base < n_ids; base += 1024) {
-    const uint32_t i = base + tid;
-    const uint32_t c = i < n_ids ? pl.task_per_slot[i] : 0u;
-    const uint32_t u = (c + 31u) / 32u;
-    s_a[tid] = c;
-    s_b[tid] = u;
-    __syncthreads();
-    for (uint32_t o = 1; o < 1024; o <<= 1) {  // Hillis-Steele inclusive scan
-      const uint32_t va = tid >= o ? s_a[tid - o] : 0u;
-      const uint32_t vb = tid >= o ? s_b[tid - o] : 0u;
-      __syncthreads();
-      s_a[tid] += va;
-      s_b[tid] += vb;
-      __syncthreads();
-    }
-    if (i < n_ids) {
-      pl.slot_task_off[i] = carry_a + s_a[tid] - c;
-      pl.slot_unit_off[i] = carry_b + s_b[tid] - u;
-      pl.slot_cursor[i] = 0;
-    }
-    __syncthreads();
-    if (tid == 1023) {
-      carry_a += s_a[1023];
-      carry_b += s_b[1023];
-    }
-    __syncthreads();
-  }
-  if (tid == 0) {
-    pl.slot_task_off[n_ids] = carry_a;
-    pl.slot_unit_off[n_ids] = carry_b;
-  }
-}
-
-__global__ void __launch_bounds__(256)
-scatter_tasks_kernel(RefinePlan pl, const uint32_t* __restrict__ task_slot, const DevStatus* status,
-                     uint64_t task_cap, uint32_t* __restrict__ task_sorted) {
-  const uint64_t n = min(static_cast<uint64_t>(status->task_count), task_cap);
-  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
-  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
-    const uint32_t slot = task_slot[i];
-    task_sorted[pl.slot_task_off[slot] + atomicAdd(&pl.slot_cursor[slot], 1u)] = static_cast<uint32_t>(i);
-  }
-}
-
 struct RefineParams {
   const double2* pts;
   uint64_t base_index;
   const uint32_t* task_point;
+  const uint32_t* task_slot;
   const uint32_t* task_ord;
-  const uint32_t* task_sorted;
+  uint64_t task_cap;
   unsigned long long* counts;
   // ids mode: accepted candidates become overflow records
   uint64_t* ovf_point;
@@ -599,88 +588,149 @@ struct RefineParams {
   uint8_t* task_pass;
   DevStatus* status;
   int32_t want_ids;
+  int32_t smem_counts;  // the launch carries n_ids * 4 bytes of dynamic shared memory
 };
 
-// K2.  One warp per unit (<= 32 candidate points of ONE polygon): the
-// polygon's closed ring is staged tile by tile into the warp's slice of
-// shared memory with coalesced 16-byte loads; every lane then runs its point
-// over the staged edges (broadcast reads, conflict-free).  Units are handed
-// out through an atomic queue, so warps balance by edge count on their own.
-__global__ void __launch_bounds__(kRefineThreads)
-refine_kernel(const __grid_constant__ DevIndex ix, RefinePlan pl, RefineParams rp) {
-  __shared__ double2 s_ring[kRefineThreads / 32][kRefineTile + 1];
+__global__ void __launch_bounds__(kRefineThreads, 4)
+refine_kernel(const __grid_constant__ DevIndex ix, RefineParams rp) {
+  constexpr int kWarps = kRefineThreads / 32;
+  constexpr uint32_t kListCap = 64;  // < 32 left over + up to 32 appended per loop step
+  // (edge record, lane << 2 | kinds) of the edge evaluations that need a
+  // division: the distance to the edge (kind bit 0) and/or the crossing
+  // abscissa (bit 1).  They are rare per task but would each run at 1/32
+  // utilisation inside the per-lane loop, so they are compacted and batched.
+  __shared__ uint2 s_list[kWarps][kListCap];
+  __shared__ uint32_t s_result[kWarps][32];  // bit 0: on the boundary, bit 1: crossing parity
+  // per-polygon counts of this CTA (when the id table fits): global atomics
+  // on a few hundred hot words serialise at L2
+  extern __shared__ uint32_t s_counts[];
+  const bool local_counts = rp.smem_counts != 0;
+  if (local_counts) {
+    for (uint32_t s = threadIdx.x; s < ix.n_ids; s += kRefineThreads) s_counts[s] = 0;
+  }
+  __syncthreads();
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t warp = threadIdx.x >> 5;
-  const uint32_t n_units = pl.slot_unit_off[ix.n_ids];
-  for (;;) {
-    uint32_t unit = 0;
-    if (lane == 0) unit = atomicAdd(pl.unit_counter, 1u);
-    unit = __shfl_sync(0xffffffffu, unit, 0);
-    if (unit >= n_units) break;
-    // slot owning this unit: last slot with unit_off <= unit
-    uint32_t lo = 0, hi = ix.n_ids;
-    while (hi - lo > 1) {
-      const uint32_t mid = (lo + hi) >> 1;
-      if (__ldg(pl.slot_unit_off + mid) <= unit) {
-        lo = mid;
-      } else {
-        hi = mid;
-      }
-    }
-    const uint32_t slot = lo;
-    const uint32_t t_begin = pl.slot_task_off[slot] + (unit - pl.slot_unit_off[slot]) * 32u;
-    const uint32_t t_end = min(t_begin + 32u, pl.slot_task_off[slot + 1]);
-    const bool active = t_begin + lane < t_end;
-    uint32_t task = 0, point = 0;
+  const uint32_t lane_lt = (1u << lane) - 1u;
+  const uint64_t n_tasks = min(static_cast<uint64_t>(rp.status->task_count), rp.task_cap);
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  // whole warps stay in the loop together
+  for (uint64_t t0 = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) & ~31ull; t0 < n_tasks;
+       t0 += stride) {
+    const uint64_t task = t0 + lane;
+    const bool active = task < n_tasks;
+    uint32_t point = 0, slot = 0, e_begin = 0, len = 0;
     double qx = 0.0, qy = 0.0;
     if (active) {
-      task = rp.task_sorted[t_begin + lane];
       point = rp.task_point[task];
+      slot = rp.task_slot[task];
       const double2 p = __ldg(rp.pts + point);
-      qx = p.y;  // x = lng
-      qy = p.x;  // y = lat
-    }
-    const uint64_t ring = __ldg(ix.ring_off + slot);
-    const uint32_t n_edges = __ldg(ix.ring_len + slot);
-    uint32_t boundary = 0, crossings = 0;
-    for (uint32_t e0 = 0; e0 < n_edges; e0 += kRefineTile) {
-      const uint32_t n_tile = min(static_cast<uint32_t>(kRefineTile), n_edges - e0);
-      __syncwarp();
-      for (uint32_t v = lane; v <= n_tile; v += 32u) s_ring[warp][v] = __ldg(ix.ring_xy + ring + e0 + v);
-      __syncwarp();
-      if (active) {
-        for (uint32_t e = 0; e < n_tile; ++e) {
-          const double2 a = s_ring[warp][e];
-          const double2 b = s_ring[warp][e + 1];
-          const uint32_t r = pip_edge(qx, qy, a.x, a.y, b.x, b.y);
-          boundary |= r & 1u;
-          crossings ^= r >> 1;
-        }
+      qx = p.y;  // x = lng, y = lat (geometry.cpp:35)
+      qy = p.x;
+      const StripMeta m = ix.strip_meta[slot];
+      if (m.k != 0u) {
+        const uint32_t st = strip_of(qy, m.y0, m.inv_h, m.k);
+        e_begin = __ldg(ix.strip_ptr + m.ptr_base + st);
+        len = __ldg(ix.strip_ptr + m.ptr_base + st + 1) - e_begin;
       }
     }
-    const bool pass = active && n_edges != 0 && (boundary | crossings) != 0u;
-    const uint32_t pass_mask = __ballot_sync(0xffffffffu, pass);
+    __syncwarp();
+    s_result[warp][lane] = 0;
+    __syncwarp();
+
+    // Evaluate up to 32 listed (task, edge) pairs with all lanes.
+    auto drain = [&](uint32_t first, uint32_t take) {
+      const uint2 item = s_list[warp][first + min(lane, take - 1u)];
+      const uint32_t owner = item.y >> 2;  // lane that holds the point
+      const double ox = __shfl_sync(0xffffffffu, qx, owner);
+      const double oy = __shfl_sync(0xffffffffu, qy, owner);
+      if (lane < take) {
+        const double2 a = __ldg(reinterpret_cast<const double2*>(ix.strip_edges + item.x));
+        const double2 b = __ldg(reinterpret_cast<const double2*>(ix.strip_edges + item.x) + 1);
+        if ((item.y & 1u) && pip_edge_on_boundary(ox, oy, a.x, a.y, b.x, b.y)) atomicOr(&s_result[warp][owner], 1u);
+        if ((item.y & 2u) && pip_edge_crosses(ox, oy, a.x, a.y, b.x, b.y)) atomicXor(&s_result[warp][owner], 2u);
+      }
+    };
+
+    // The batch's (task, edge) pairs, flattened: pair g belongs to the first
+    // lane whose inclusive prefix of list lengths exceeds g.  Every loop step
+    // classifies 32 real pairs whatever the individual list lengths are.
+    uint32_t incl = len;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t up = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= static_cast<uint32_t>(o)) incl += up;
+    }
+    const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+    const uint32_t excl = incl - len;
+    uint32_t n_list = 0;
+    for (uint32_t k = 0; k < total; k += 32u) {
+      const uint32_t g = k + lane;
+      uint32_t owner = 0;  // number of lanes with incl <= g
+#pragma unroll
+      for (int step = 16; step >= 1; step >>= 1) {
+        const uint32_t v = __shfl_sync(0xffffffffu, incl, min(owner + step - 1u, 31u));
+        if (v <= g) owner += step;
+      }
+      const bool real = g < total;
+      const uint32_t src = min(owner, 31u);
+      const uint32_t e = __shfl_sync(0xffffffffu, e_begin, src) + (g - __shfl_sync(0xffffffffu, excl, src));
+      const double ox = __shfl_sync(0xffffffffu, qx, src);
+      const double oy = __shfl_sync(0xffffffffu, qy, src);
+      uint32_t kinds = 0;
+      if (real) {
+        const double2* rec = reinterpret_cast<const double2*>(ix.strip_edges + e);
+        const double ay = __ldg(reinterpret_cast<const double*>(rec) + 1);
+        const double by = __ldg(reinterpret_cast<const double*>(rec) + 3);
+        const double2 bx = __ldg(rec + 2), byr = __ldg(rec + 3);
+        kinds = pip_edge_classify(ox, oy, ay, by, bx.x, bx.y, byr.x, byr.y);
+      }
+      const uint32_t mask = __ballot_sync(0xffffffffu, kinds != 0u);
+      if (kinds) s_list[warp][n_list + __popc(mask & lane_lt)] = make_uint2(e, (src << 2) | kinds);
+      n_list += __popc(mask);
+      if (n_list >= 32u) {
+        __syncwarp();
+        n_list -= 32u;
+        drain(n_list, 32u);
+        __syncwarp();
+      }
+    }
+    __syncwarp();
+    if (n_list) drain(0, n_list);
+    __syncwarp();
+    const bool pass = active && s_result[warp][lane] != 0u;
+
     if (rp.task_pass) {
       if (active) rp.task_pass[task] = pass ? 1 : 0;
-    } else {
-      if (lane == 0 && pass_mask) {
-        atomicAdd(&rp.counts[slot], static_cast<unsigned long long>(__popc(pass_mask)));
+      continue;
+    }
+    if (pass) {
+      if (local_counts) {
+        atomicAdd(&s_counts[slot], 1u);
+      } else {
+        atomicAdd(&rp.counts[slot], 1ull);
       }
-      if (rp.want_ids && pass_mask) {
-        unsigned long long base = 0;
-        if (lane == 0) {
-          base = atomicAdd(&rp.status->overflow_count, static_cast<unsigned long long>(__popc(pass_mask)));
-        }
-        base = __shfl_sync(0xffffffffu, base, 0);
-        if (base + __popc(pass_mask) > rp.ovf_cap) {
-          if (lane == 0) atomicOr(&rp.status->flags, kErrOverflowCap);
-        } else if (pass) {
-          const uint64_t w = base + __popc(pass_mask & ((1u << lane) - 1u));
-          rp.ovf_point[w] = rp.base_index + point;
-          rp.ovf_id[w] = __ldg(ix.ids + slot);
-          rp.ovf_ord[w] = rp.task_ord[task];
-        }
+    }
+    if (rp.want_ids) {
+      const uint32_t pass_mask = __ballot_sync(0xffffffffu, pass);
+      if (pass_mask == 0u) continue;
+      unsigned long long base = 0;
+      if (lane == 0) base = atomicAdd(&rp.status->overflow_count, static_cast<unsigned long long>(__popc(pass_mask)));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (base + __popc(pass_mask) > rp.ovf_cap) {
+        if (lane == 0) atomicOr(&rp.status->flags, kErrOverflowCap);
+      } else if (pass) {
+        const uint64_t w = base + __popc(pass_mask & lane_lt);
+        rp.ovf_point[w] = rp.base_index + point;
+        rp.ovf_id[w] = __ldg(ix.ids + slot);
+        rp.ovf_ord[w] = rp.task_ord[task];
       }
+    }
+  }
+  __syncthreads();
+  if (local_counts) {
+    for (uint32_t sl = threadIdx.x; sl < ix.n_ids; sl += kRefineThreads) {
+      if (s_counts[sl]) atomicAdd(&rp.counts[sl], static_cast<unsigned long long>(s_counts[sl]));
     }
   }
 }

@@ -1,0 +1,122 @@
+"""Secondary measurements: the device-resident join on the other BASELINE
+configs (bench.py is the headline, config 2).  For each config: load the
+cached reference-built index, generate the seeded points, time the join in the
+config's mode (first id per point + per-polygon counts + JoinStats) with CUDA
+events, and check a prefix against the CPU oracle (test infrastructure).
+
+    python tools/bench_configs.py [configs...] [--points N]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent.parent
+sys.path.insert(0, str(ROOT))
+
+from paper_1802_09488_b200 import capi, join, synth  # noqa: E402
+from tools import build_bundles  # noqa: E402
+
+
+def run_config(config: int, n_points: int, scale: float, reps: int, check: int, want_ids: bool = True):
+    import torch
+
+    spec = synth.SPECS[config]
+    name = build_bundles.workload_name(config, scale)
+    path = build_bundles.ensure_workload_bundle(config, scale, log=lambda *a: print(*a, file=sys.stderr))
+    bundle = join.IndexBundle.load(path, device=0)
+    sess = bundle.session()
+    info = bundle.info
+    polys = synth.polygons_for(config, scale) if spec.boundary_fraction > 0 else None
+    n = min(n_points, spec.n_points)
+    t0 = time.time()
+    pts = synth.points_for(config, n, polys)
+    gen_s = time.time() - t0
+    mode = capi.GJ_MODE_EXACT if spec.exact else capi.GJ_MODE_APPROX
+
+    d_pts = torch.from_numpy(pts).cuda()
+    n_ids = len(bundle.ids)
+    d_counts = torch.zeros(max(1, n_ids), dtype=torch.int64, device="cuda")
+    d_stats = torch.zeros(6, dtype=torch.int64, device="cuda")
+    d_first = torch.empty(n, dtype=torch.int32, device="cuda")
+    stream = torch.cuda.ExternalStream(sess.stream)
+
+    def step():
+        sess.join_count_device(d_pts.data_ptr(), n, d_counts.data_ptr(), mode, d_stats_ptr=d_stats.data_ptr(),
+                               d_first_id_ptr=d_first.data_ptr() if want_ids else 0)
+
+    for _ in range(3):
+        step()
+    sess.sync()
+    d_counts.zero_()
+    d_stats.zero_()
+    torch.cuda.synchronize()
+    launches0 = sess.launches
+    launches1 = None
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        e0.record()
+        for _ in range(reps):
+            step()
+        e1.record()
+    sess.sync()
+    launches1 = sess.launches
+    ms = e0.elapsed_time(e1) / reps
+    stats = (d_stats.cpu().numpy() // reps).tolist()
+    counts = d_counts.cpu().numpy() // reps
+
+    # parity on a prefix against the CPU oracle
+    from tests import golden_util
+    m = min(check, n)
+    ox = golden_util.oracle_index(golden_util.parse_gjx(Path(path).read_bytes()))
+    t0 = time.time()
+    want, total = ox.join_count(pts[:m], approx=not spec.exact, threads=16)
+    cpu_s = time.time() - t0
+    got, _, _ = sess.join_count(pts[:m], mode)
+    got_map = {int(bundle.ids[k]): int(got[k]) for k in np.nonzero(got)[0]}
+    ok = got_map == want
+    # ordered pairs on a smaller prefix
+    mp = min(200_000, n)
+    row_ptr, ids = sess.join_pairs(pts[:mp], mode)
+    pi, pid, ost, _ = ox.join(pts[:mp], approx=not spec.exact)
+    gpi = np.repeat(np.arange(mp, dtype=np.uint64), np.diff(row_ptr.astype(np.int64)))
+    ok_pairs = bool(np.array_equal(gpi, pi) and np.array_equal(ids, pid))
+
+    res = {
+        "config": config, "name": name, "mode": "exact" if spec.exact else "approx", "points": n,
+        "ms": ms, "gpoints_per_s": n / ms / 1e6, "launches_per_step": (launches1 - launches0) // reps, "ids": want_ids,
+        "index_nodes": int(info.node_count), "index_mb": info.device_bytes / 1e6, "n_polygons": int(info.n_polygons),
+        "dir1_level": info.dir_level, "dir2_level": info.dir2_level,
+        "stats": dict(zip(["probes", "pip_tests", "false_hits", "solely_true_hits", "refinement_entered",
+                           "candidate_refs"], stats)),
+        "pairs_per_point": float(counts.sum()) / n,
+        "oracle_counts_equal": bool(ok), "oracle_pairs_equal": ok_pairs, "oracle_prefix": m,
+        "cpu_oracle_prefix_mpts_per_s_16thr": m / cpu_s / 1e6, "gen_s": gen_s,
+    }
+    print(json.dumps(res), flush=True)
+    sess.close()
+    bundle.close()
+    return res
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("configs", nargs="*", type=int, default=[1, 2, 3])
+    ap.add_argument("--points", type=int, default=100_000_000)
+    ap.add_argument("--scale", type=float, default=1.0)
+    ap.add_argument("--reps", type=int, default=10)
+    ap.add_argument("--check", type=int, default=5_000_000)
+    ap.add_argument("--no-ids", action="store_true", help="counts + stats only (no first id per point)")
+    args = ap.parse_args()
+    out = [run_config(c, args.points, args.scale, args.reps, args.check, not args.no_ids) for c in args.configs]
+    (ROOT / "gpurun_out").mkdir(exist_ok=True)
+    (ROOT / "gpurun_out" / "bench_configs.json").write_text(json.dumps(out, indent=1))
+
+
+if __name__ == "__main__":
+    main()
