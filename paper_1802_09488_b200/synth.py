@@ -384,9 +384,22 @@ SPECS = {
 }
 
 
+def box_for(config: int, scale: float = 1.0):
+    """Configs 4 and 5 scale down DENSITY-MATCHED: ``scale`` of the polygons in
+    ``scale`` of the area (a centred sub-box), so polygon size, overlap and the
+    index depth per point stay those of the full config."""
+    if scale >= 1.0 or config not in (4, 5):
+        return BOX
+    lat_lo, lat_hi, lng_lo, lng_hi = BOX
+    f = float(np.sqrt(scale))
+    clat, clng = (lat_lo + lat_hi) / 2, (lng_lo + lng_hi) / 2
+    hlat, hlng = (lat_hi - lat_lo) / 2 * f, (lng_hi - lng_lo) / 2 * f
+    return (clat - hlat, clat + hlat, clng - hlng, clng + hlng)
+
+
 def polygons_for(config: int, scale: float = 1.0) -> PolygonSet:
     """Polygons of a BASELINE config; ``scale`` < 1 shrinks the polygon COUNT
-    (parity tests use scaled-down configs 4 and 5 the oracle finishes in seconds)."""
+    (for configs 4 and 5 together with the box, see box_for)."""
     s = seed_for(config, 0)
     if config == 1:
         return voronoi_tessellation(5, s, mean_vertices=1100.0, max_depth=9)
@@ -397,20 +410,23 @@ def polygons_for(config: int, scale: float = 1.0) -> PolygonSet:
     if config == 4:
         n = max(16, int(round(40_000 * scale)))
         g = int(round(np.sqrt(n)))
-        return voronoi_tessellation(g * g, s, mean_vertices=15.0, max_depth=3)
+        return voronoi_tessellation(g * g, s, mean_vertices=15.0, max_depth=3, box=box_for(4, scale))
     if config == 5:
-        return star_polygons(max(4, int(round(10_000 * scale))), s)
+        return star_polygons(max(4, int(round(10_000 * scale))), s, box=box_for(5, scale))
     raise ValueError(config)
 
 
 def points_for(config: int, n: int, polys: PolygonSet | None = None, stream: int = 2,
-               out: np.ndarray | None = None) -> np.ndarray:
+               out: np.ndarray | None = None, scale: float = 1.0) -> np.ndarray:
     spec = SPECS[config]
     s = seed_for(config, stream)
+    box = box_for(config, scale)
     if spec.distribution == "uniform":
-        pts = uniform_points(n, s, out=out)
+        pts = uniform_points(n, s, box=box, out=out)
     else:
-        pts = mixture_points(n, s, gaussian_mixture(seed_for(3, 1)), out=out)
+        f = float(np.sqrt(scale)) if box is not BOX else 1.0
+        mix = gaussian_mixture(seed_for(3, 1), sigma=(0.002 * f, 0.02 * f), box=box)
+        pts = mixture_points(n, s, mix, box=box, out=out)
     if spec.boundary_fraction > 0 and polys is not None and stream == 2:
         plant_boundary_points(pts, polys, s, spec.boundary_fraction)
     return pts

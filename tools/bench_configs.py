@@ -35,7 +35,7 @@ def run_config(config: int, n_points: int, scale: float, reps: int, check: int, 
     polys = synth.polygons_for(config, scale) if spec.boundary_fraction > 0 else None
     n = min(n_points, spec.n_points)
     t0 = time.time()
-    pts = synth.points_for(config, n, polys)
+    pts = synth.points_for(config, n, polys, scale=scale)
     gen_s = time.time() - t0
     mode = capi.GJ_MODE_EXACT if spec.exact else capi.GJ_MODE_APPROX
 

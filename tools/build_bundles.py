@@ -89,7 +89,7 @@ def ensure_workload_bundle(config: int, scale: float = 1.0, log=print) -> Path:
     polys = synth.polygons_for(config, scale)
     training = None
     if spec.training_points:
-        training = synth.points_for(config, int(spec.training_points * min(1.0, scale * 4)), stream=1)
+        training = synth.points_for(config, int(spec.training_points * min(1.0, scale * 4)), stream=1, scale=scale)
     return build_bundle(name, polys, spec, training, log)
 
 
