@@ -348,6 +348,131 @@ int run_host_join(gj_session* s, const double* latlng, uint64_t n, uint64_t base
   return GJ_OK;
 }
 
+// join_exact / join_approx materialised as CSR, entirely on the device (see
+// the pipeline comment in gj_kernels.cuh).  Chunks are processed one after
+// the other; a chunk's pair count is only known after its scan, so the id
+// buffer is sized then.
+int run_host_pairs(gj_session* s, const double* latlng, uint64_t n, bool exact, gj_stats* stats,
+                   uint64_t* bad_index) {
+  gj_index& ix = *s->ix;
+  GJ_CUDA(cudaSetDevice(ix.device));
+  s->pairs_row_ptr.assign(n + 1, 0);
+  s->pairs_id.clear();
+  const uint64_t max_cand = std::max<uint64_t>(1, ix.max_cand_refs);
+  const uint64_t per_point = 48 + (exact ? max_cand * 13 : 0);
+  uint64_t chunk = std::min<uint64_t>(4ull << 20, std::max<uint64_t>(4096, kScratchBudget / per_point));
+  chunk = std::min<uint64_t>(chunk, std::max<uint64_t>(n, 1));
+  const uint64_t task_cap = exact ? chunk * max_cand : 0;
+  if (task_cap >= (1ull << 32)) {
+    set_error("candidate task capacity exceeds 2^32");
+    return GJ_INVALID_ARGUMENT;
+  }
+  int rc;
+  if (exact) {
+    if ((rc = reserve_tasks(s, task_cap)) != GJ_OK) return rc;
+    GJ_CUDA(s->d_task_pass.reserve(task_cap + 16));
+  }
+  const uint32_t n_blocks_max = static_cast<uint32_t>((chunk + kScanTile - 1) / kScanTile);
+  GJ_CUDA(s->d_points[0].reserve(chunk * 16));
+  GJ_CUDA(s->d_entries.reserve(chunk * 8));
+  GJ_CUDA(s->d_nrefs.reserve(chunk * 4));
+  GJ_CUDA(s->d_task_base.reserve(chunk * 4));
+  GJ_CUDA(s->d_pair_count.reserve(chunk * 4));
+  GJ_CUDA(s->d_row_ptr.reserve((chunk + 1) * 8));
+  GJ_CUDA(s->d_block_sums.reserve((static_cast<size_t>(n_blocks_max) + 2) * 8));
+  GJ_CUDA(s->d_stats.reserve(6 * 8));
+  GJ_CUDA(cudaMemsetAsync(s->d_stats.ptr, 0, 6 * 8, s->stream));
+  DevStatus* d_status = s->d_status.as<DevStatus>() + 3;
+  const size_t probe_smem = align16(std::max<size_t>(ix.dev.dir.n_table * 4, 16));
+  GJ_CUDA(cudaFuncSetAttribute(probe_points_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(probe_smem)));
+  const unsigned wide = static_cast<unsigned>(ix.sm_count) * 8u;
+
+  for (uint64_t begin = 0; begin < n; begin += chunk) {
+    const uint64_t len = std::min(chunk, n - begin);
+    const uint32_t n_blocks = static_cast<uint32_t>((len + kScanTile - 1) / kScanTile);
+    GJ_CUDA(cudaMemcpyAsync(s->d_points[0].ptr, latlng + 2 * begin, len * 16, cudaMemcpyHostToDevice, s->stream));
+    if ((rc = reset_status(s, d_status)) != GJ_OK) return rc;
+    probe_points_kernel<<<static_cast<unsigned>(std::min<uint64_t>((len + 255) / 256, ix.sm_count * 4ull)), 256,
+                          probe_smem, s->stream>>>(ix.dev, s->d_points[0].as<double2>(), len, begin,
+                                                   s->d_entries.as<uint64_t>(), d_status);
+    PairsParams pp{};
+    pp.entries = s->d_entries.as<uint64_t>();
+    pp.n = len;
+    pp.base_index = begin;
+    pp.n_refs = s->d_nrefs.as<uint32_t>();
+    pp.task_base = s->d_task_base.as<uint32_t>();
+    pp.task_point = s->d_task_point.as<uint32_t>();
+    pp.task_slot = s->d_task_slot.as<uint32_t>();
+    pp.task_ord = s->d_task_ord.as<uint32_t>();
+    pp.task_cap = task_cap;
+    pp.task_pass = s->d_task_pass.as<uint8_t>();
+    pp.count = s->d_pair_count.as<uint32_t>();
+    pp.row_ptr = s->d_row_ptr.as<uint64_t>();
+    pp.stats = stats ? s->d_stats.as<unsigned long long>() : nullptr;
+    pp.status = d_status;
+    pp.exact = exact ? 1 : 0;
+    pairs_plan_kernel<<<wide, 256, 0, s->stream>>>(ix.dev, pp);
+    s->launches += 2;
+    if (exact) {
+      RefineParams rp{};
+      rp.pts = s->d_points[0].as<double2>();
+      rp.base_index = begin;
+      rp.task_point = pp.task_point;
+      rp.task_slot = pp.task_slot;
+      rp.task_ord = pp.task_ord;
+      rp.task_cap = task_cap;
+      rp.task_pass = s->d_task_pass.as<uint8_t>();
+      rp.status = d_status;
+      int per_sm = 0;
+      GJ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, refine_kernel, kRefineThreads, 0));
+      refine_kernel<<<static_cast<unsigned>(ix.sm_count) * static_cast<unsigned>(std::max(per_sm, 1)), kRefineThreads, 0,
+                      s->stream>>>(ix.dev, rp);
+      ++s->launches;
+    }
+    pairs_emit_kernel<false><<<wide, 256, 0, s->stream>>>(ix.dev, pp);
+    scan_block_sums_kernel<<<n_blocks, kScanThreads, 0, s->stream>>>(pp.count, len, s->d_block_sums.as<uint64_t>());
+    uint64_t* d_total = s->d_block_sums.as<uint64_t>() + n_blocks_max + 1;
+    scan_sums_kernel<<<1, kScanThreads, 0, s->stream>>>(s->d_block_sums.as<uint64_t>(), n_blocks, d_total);
+    scan_apply_kernel<<<n_blocks, kScanThreads, 0, s->stream>>>(pp.count, len, s->d_block_sums.as<uint64_t>(),
+                                                                s->d_row_ptr.as<uint64_t>());
+    s->launches += 4;
+    GJ_CUDA(cudaGetLastError());
+    uint64_t total = 0;
+    GJ_CUDA(cudaMemcpyAsync(&total, d_total, 8, cudaMemcpyDeviceToHost, s->stream));
+    GJ_CUDA(cudaMemcpyAsync(&s->h_status[3], d_status, sizeof(DevStatus), cudaMemcpyDeviceToHost, s->stream));
+    GJ_CUDA(cudaStreamSynchronize(s->stream));
+    if ((rc = status_to_code(s->h_status[3], bad_index)) != GJ_OK) return rc;
+    GJ_CUDA(s->d_pair_ids.reserve(std::max<uint64_t>(total, 1) * 4));
+    pp.out_id = s->d_pair_ids.as<uint32_t>();
+    pairs_emit_kernel<true><<<wide, 256, 0, s->stream>>>(ix.dev, pp);
+    ++s->launches;
+    GJ_CUDA(cudaGetLastError());
+    const uint64_t id_base = s->pairs_id.size();
+    s->pairs_id.resize(id_base + total);
+    GJ_CUDA(cudaMemcpyAsync(s->pairs_row_ptr.data() + begin, s->d_row_ptr.ptr, len * 8, cudaMemcpyDeviceToHost, s->stream));
+    if (total) {
+      GJ_CUDA(cudaMemcpyAsync(s->pairs_id.data() + id_base, s->d_pair_ids.ptr, total * 4, cudaMemcpyDeviceToHost, s->stream));
+    }
+    GJ_CUDA(cudaStreamSynchronize(s->stream));
+    if (id_base) {
+      for (uint64_t i = begin; i < begin + len; ++i) s->pairs_row_ptr[i] += id_base;
+    }
+  }
+  s->pairs_row_ptr[n] = s->pairs_id.size();
+  if (stats) {
+    unsigned long long h_stats[6];
+    GJ_CUDA(cudaMemcpy(h_stats, s->d_stats.ptr, sizeof h_stats, cudaMemcpyDeviceToHost));
+    stats->probes += h_stats[0];
+    stats->pip_tests += h_stats[1];
+    stats->false_hits += h_stats[2];
+    stats->solely_true_hits += h_stats[3];
+    stats->refinement_entered += h_stats[4];
+    stats->candidate_refs += h_stats[5];
+  }
+  return GJ_OK;
+}
+
 }  // namespace
 }  // namespace gj
 
@@ -631,31 +756,12 @@ int gj_join_pairs_host(gj_session* s, const double* latlng, uint64_t n, int mode
   if (!s || (n && !latlng)) return GJ_INVALID_ARGUMENT;
   bool exact = false;
   if (!resolve_exact(*s->ix, mode, &exact)) return GJ_INVALID_ARGUMENT;
-  std::vector<uint32_t> first(n);
-  OverflowSink sink;
-  s->pairs_row_ptr.clear();
-  s->pairs_id.clear();
-  const int rc = run_host_join(s, latlng, n, 0, exact, nullptr, stats, first.data(), &sink, bad_index);
-  if (rc != GJ_OK) return rc;
-  // Assemble CSR in the reference's order (join.hpp:125-127): per point the
-  // inline first id (ordinal 0 of a non-deferred point) and then its
-  // overflow records by ordinal.
-  const size_t m = sink.point.size();
-  std::vector<uint64_t> order(m);
-  std::iota(order.begin(), order.end(), 0);
-  std::sort(order.begin(), order.end(), [&](uint64_t a, uint64_t b) {
-    return sink.point[a] != sink.point[b] ? sink.point[a] < sink.point[b] : sink.ord[a] < sink.ord[b];
-  });
-  s->pairs_row_ptr.assign(n + 1, 0);
-  s->pairs_id.reserve(n + m);
-  size_t k = 0;
-  for (uint64_t i = 0; i < n; ++i) {
-    s->pairs_row_ptr[i] = s->pairs_id.size();
-    const uint32_t f = first[i];
-    if (f != kNoMatch && f != kDeferred) s->pairs_id.push_back(f & ~kMoreFlag);
-    while (k < m && sink.point[order[k]] == i) s->pairs_id.push_back(sink.id[order[k++]]);
+  const int rc = run_host_pairs(s, latlng, n, exact, stats, bad_index);
+  if (rc != GJ_OK) {
+    s->pairs_row_ptr.clear();
+    s->pairs_id.clear();
+    return rc;
   }
-  s->pairs_row_ptr[n] = s->pairs_id.size();
   if (n_pairs) *n_pairs = s->pairs_id.size();
   return GJ_OK;
 }

@@ -79,7 +79,9 @@ struct gj_session {
   gj::DeviceBuffer d_status, d_counts, d_stats;
   gj::DeviceBuffer d_points[3], d_first_id[3], d_entries;
   gj::DeviceBuffer d_ovf_point, d_ovf_id, d_ovf_ord;
-  gj::DeviceBuffer d_task_point, d_task_slot, d_task_ord;
+  gj::DeviceBuffer d_task_point, d_task_slot, d_task_ord, d_task_pass;
+  // CSR pairs pipeline
+  gj::DeviceBuffer d_nrefs, d_task_base, d_pair_count, d_row_ptr, d_block_sums, d_pair_ids;
   cudaEvent_t ev_in[3]{}, ev_done[3]{}, ev_out[3]{};
   gj::DevStatus* h_status = nullptr;   // pinned
   // materialised pairs kept for gj_pairs_copy

@@ -735,4 +735,220 @@ refine_kernel(const __grid_constant__ DevIndex ix, RefineParams rp) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Materialised pairs in CSR form (join_exact / join_approx, join.cpp:131-140,
+// 237-247): row_ptr[n + 1] and polygon_id[] in the reference's emit order
+// (ascending point index, references in index order, join.hpp:125-127).
+//
+//   probe_points_kernel   entries[i]                       (above)
+//   pairs_plan_kernel     per point: reference count; exact mode: candidate
+//                         tasks (contiguous per point, in reference order)
+//                         and the point's first task
+//   refine_kernel         pass flag per task               (K2, exact mode)
+//   pairs_count_kernel    pairs the point really emits
+//   scan_* kernels        exclusive scan -> row_ptr
+//   pairs_fill_kernel     polygon ids
+// ---------------------------------------------------------------------------
+struct PairsParams {
+  const uint64_t* entries;  // [n]
+  uint64_t n;
+  uint64_t base_index;
+  uint32_t* n_refs;         // [n] out (plan): references behind the entry
+  uint32_t* task_base;      // [n] out (plan, exact): first task of the point
+  uint32_t* task_point;
+  uint32_t* task_slot;
+  uint32_t* task_ord;
+  uint64_t task_cap;
+  const uint8_t* task_pass; // K2's verdicts (count / fill)
+  uint32_t* count;          // [n] out (count): pairs of the point
+  const uint64_t* row_ptr;  // [n + 1] (fill)
+  uint32_t* out_id;         // (fill)
+  unsigned long long* stats;  // [6] or null
+  DevStatus* status;
+  int32_t exact;
+};
+
+// k-th reference of an entry: (polygon_id << 1) | interior (act.hpp:169-196)
+__device__ __forceinline__ uint32_t entry_ref(const DevIndex& ix, uint64_t entry, uint32_t tag, uint32_t off,
+                                              uint32_t t, uint32_t k) {
+  if (tag == 1u) return static_cast<uint32_t>(entry >> 2) & 0x7fffffffu;
+  if (tag == 2u) return static_cast<uint32_t>(k == 0 ? entry >> 33 : entry >> 2) & 0x7fffffffu;
+  return k < t ? (__ldg(ix.lut + off + 1 + k) << 1) | 1u : (__ldg(ix.lut + off + 2 + k) << 1);
+}
+
+__global__ void __launch_bounds__(256)
+pairs_plan_kernel(const __grid_constant__ DevIndex ix, PairsParams pp) {
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  uint32_t probes = 0, false_hits = 0, solely_true = 0, refined = 0, cand_refs = 0;
+  for (uint64_t i0 = (static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x) & ~31ull; i0 < pp.n; i0 += stride) {
+    const uint64_t i = i0 + lane;
+    const bool live = i < pp.n;
+    const uint64_t entry = live ? pp.entries[i] : 0;
+    EntryPlan e{};
+    if (entry != 0) e = plan_entry<false>(ix, pp.exact != 0, entry);
+    if (live) {
+      ++probes;
+      if (entry == 0) {
+        ++false_hits;
+      } else if (e.n_cand == 0) {
+        ++solely_true;
+      } else {
+        ++refined;
+        cand_refs += e.n_cand;
+      }
+    }
+    unsigned long long task_base = 0;
+    if (pp.exact && __any_sync(0xffffffffu, e.n_tasks != 0u)) {
+      task_base = warp_reserve(&pp.status->task_count, e.n_tasks, lane);
+    }
+    if (!live) continue;
+    pp.n_refs[i] = e.n_refs;
+    if (e.n_tasks) {
+      const bool ok = task_base + e.n_tasks <= pp.task_cap;
+      if (!ok) atomicOr(&pp.status->flags, kErrTaskCap);
+      pp.task_base[i] = static_cast<uint32_t>(task_base);
+      uint32_t w = 0;
+      for (uint32_t k = 0; k < e.n_refs && ok; ++k) {
+        const uint32_t p = entry_ref(ix, entry, e.tag, e.off, e.t, k);
+        if (p & 1u) continue;
+        const uint32_t slot = id_to_slot(ix, p >> 1);
+        if (__ldg(ix.ring_len + slot) == 0u) flag_error(pp.status, kErrUnknownPolygon, pp.base_index + i);
+        pp.task_point[task_base + w] = static_cast<uint32_t>(i);
+        pp.task_slot[task_base + w] = slot;
+        pp.task_ord[task_base + w] = k;
+        ++w;
+      }
+    }
+  }
+  if (pp.stats) {  // JoinStats, join.hpp:77-84
+    uint32_t v[5] = {probes, false_hits, solely_true, refined, cand_refs};
+#pragma unroll
+    for (int k = 0; k < 5; ++k) {
+      for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
+    }
+    if (lane == 0) {
+      atomicAdd(&pp.stats[0], static_cast<unsigned long long>(v[0]));
+      if (pp.exact) atomicAdd(&pp.stats[1], static_cast<unsigned long long>(v[4]));
+      atomicAdd(&pp.stats[2], static_cast<unsigned long long>(v[1]));
+      atomicAdd(&pp.stats[3], static_cast<unsigned long long>(v[2]));
+      atomicAdd(&pp.stats[4], static_cast<unsigned long long>(v[3]));
+      atomicAdd(&pp.stats[5], static_cast<unsigned long long>(v[4]));
+    }
+  }
+}
+
+// count (kFill = false) or write (kFill = true) the pairs of every point
+template <bool kFill>
+__global__ void __launch_bounds__(256)
+pairs_emit_kernel(const __grid_constant__ DevIndex ix, PairsParams pp) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < pp.n; i += stride) {
+    const uint32_t n_refs = pp.n_refs[i];
+    uint32_t emitted = 0;
+    if (n_refs) {
+      const uint64_t entry = pp.entries[i];
+      const uint32_t tag = static_cast<uint32_t>(entry) & 3u;
+      uint32_t off = 0, t = 0;
+      if (tag == 3u) {
+        off = static_cast<uint32_t>(entry >> 2) & 0x7fffffffu;
+        t = __ldg(ix.lut + off);
+      }
+      const uint64_t out = kFill ? pp.row_ptr[i] : 0;
+      uint32_t cand = 0;
+      const uint32_t task_base = pp.exact ? pp.task_base[i] : 0u;
+      for (uint32_t k = 0; k < n_refs; ++k) {
+        const uint32_t p = entry_ref(ix, entry, tag, off, t, k);
+        bool emit = true;
+        if (pp.exact && !(p & 1u)) emit = pp.task_pass[task_base + cand++] != 0;
+        if (emit) {
+          if (kFill) pp.out_id[out + emitted] = p >> 1;
+          ++emitted;
+        }
+      }
+    }
+    if (!kFill) pp.count[i] = emitted;
+  }
+}
+
+// Exclusive scan of u32 counts into u64 offsets: block sums, a single-CTA
+// scan of the block sums, then the per-block scan with its prefix.
+constexpr int kScanThreads = 1024;
+constexpr int kScanItems = 4;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+__device__ __forceinline__ uint64_t block_exclusive_scan(uint64_t v, uint64_t* total) {
+  __shared__ uint64_t s_warp[kScanThreads / 32];
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  uint64_t incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint64_t up = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= static_cast<uint32_t>(o)) incl += up;
+  }
+  if (lane == 31) s_warp[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    uint64_t w = lane < kScanThreads / 32 ? s_warp[lane] : 0;
+    uint64_t wi = w;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint64_t up = __shfl_up_sync(0xffffffffu, wi, o);
+      if (lane >= static_cast<uint32_t>(o)) wi += up;
+    }
+    if (lane < kScanThreads / 32) s_warp[lane] = wi - w;  // exclusive warp prefix
+    if (lane == 31) *total = wi;
+  }
+  __syncthreads();
+  const uint64_t res = s_warp[warp] + incl - v;
+  __syncthreads();
+  return res;
+}
+
+__global__ void __launch_bounds__(kScanThreads)
+scan_block_sums_kernel(const uint32_t* __restrict__ in, uint64_t n, uint64_t* __restrict__ block_sums) {
+  __shared__ uint64_t s_total;
+  const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kScanTile + threadIdx.x * kScanItems;
+  uint64_t v = 0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) v += base + k < n ? in[base + k] : 0u;
+  block_exclusive_scan(v, &s_total);
+  if (threadIdx.x == 0) block_sums[blockIdx.x] = s_total;
+}
+
+__global__ void __launch_bounds__(kScanThreads)
+scan_sums_kernel(uint64_t* __restrict__ block_sums, uint32_t n_blocks, uint64_t* __restrict__ grand_total) {
+  __shared__ uint64_t s_total;
+  uint64_t carry = 0;
+  for (uint32_t b0 = 0; b0 < n_blocks; b0 += kScanThreads) {
+    const uint32_t b = b0 + threadIdx.x;
+    const uint64_t v = b < n_blocks ? block_sums[b] : 0;
+    const uint64_t ex = block_exclusive_scan(v, &s_total);
+    if (b < n_blocks) block_sums[b] = carry + ex;
+    carry += s_total;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *grand_total = carry;
+}
+
+__global__ void __launch_bounds__(kScanThreads)
+scan_apply_kernel(const uint32_t* __restrict__ in, uint64_t n, const uint64_t* __restrict__ block_sums,
+                  uint64_t* __restrict__ out) {
+  __shared__ uint64_t s_total;
+  const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kScanTile + threadIdx.x * kScanItems;
+  uint32_t item[kScanItems];
+  uint64_t v = 0;
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    item[k] = base + k < n ? in[base + k] : 0u;
+    v += item[k];
+  }
+  uint64_t run = block_sums[blockIdx.x] + block_exclusive_scan(v, &s_total);
+#pragma unroll
+  for (int k = 0; k < kScanItems; ++k) {
+    if (base + k < n) out[base + k] = run;
+    run += item[k];
+  }
+}
+
 }  // namespace gj

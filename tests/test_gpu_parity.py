@@ -193,3 +193,24 @@ def test_cell_ids_adversarial_grid_lines_vs_oracle():
     pts.append(np.stack([rng.uniform(40.5, 40.95, 2_000_000), rng.uniform(-74.25, -73.70, 2_000_000)], axis=1))
     pts = np.concatenate(pts)
     assert np.array_equal(s.cells_from_points(pts, 30), oracle.cell_from_point(pts, 30))
+
+
+def test_multi_chunk_inputs_match_oracle():
+    """Inputs larger than the internal chunk sizes (4 M points for pairs, 8 M
+    for counts): chunk seams must not show in pairs, row offsets or counts."""
+    fx, bundle = setup("join_small_exact")
+    ox = golden_util.oracle_index(fx)
+    rng = np.random.default_rng(0xC4A2)
+    n = 9_000_000
+    pts = np.stack([rng.uniform(-11.5, -4.5, n), rng.uniform(48.5, 55.5, n)], axis=1)
+    s = bundle.session()
+    want, total = ox.join_count(pts, approx=False, threads=16)
+    assert join.join_count_per_polygon(bundle, pts) == want
+    m = 4_500_000  # two pairs chunks
+    st = join.JoinStats()
+    row_ptr, ids = s.join_pairs(pts[:m], capi.GJ_MODE_EXACT, st)
+    pi, pid, ost, _ = ox.join(pts[:m], approx=False)
+    assert np.array_equal(np.repeat(np.arange(m, dtype=np.uint64), np.diff(row_ptr.astype(np.int64))), pi)
+    assert np.array_equal(ids, pid)
+    assert st.as_tuple() == tuple(int(v) for v in ost)
+    assert int(row_ptr[-1]) == len(pid) and int(row_ptr[0]) == 0
