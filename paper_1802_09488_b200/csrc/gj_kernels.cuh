@@ -412,26 +412,46 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
     }
   };
 
-  // Population 2: 32 (or, when flushing, the remaining) Q2 items.  An item is
-  // (point | flag, w): with the flag (bit 31) w indexes the second directory
-  // tier; without it w is a first-tier code that goes straight on to Q3.
+  // Population 2: Q2 items 32 at a time.  An item is (point | flag, w): with
+  // the flag (bit 31) w indexes the second directory tier; without it w is a
+  // first-tier code that goes straight on to Q3.  The batch is software-
+  // pipelined across tiles: its tier-2 gathers are ISSUED when the batch is
+  // taken off the queue and SETTLED one tile later, so their L2 latency hides
+  // behind the next tile's streaming work instead of stalling the warp.
+  bool batch_open = false;      // a batch is in flight (warp-uniform)
+  uint32_t batch_take = 0;      // its size
+  uint2 batch_item = make_uint2(0u, 0u);
+  uint32_t batch_code = 0;      // the gather in flight (or the forwarded code)
+
+  auto settle_batch = [&]() {
+    if (!batch_open) return;
+    batch_open = false;
+    const bool mine = lane < batch_take;
+    const bool lookup = mine && (batch_item.x & 0x80000000u) != 0u;
+    const uint32_t i = batch_item.x & 0x7FFFFFFFu;
+    const bool done = settle(batch_code, lookup, i, false, true);
+    q3_count = enqueue(s_q3, q3_count, mine && !done, i, batch_code);
+#ifdef GJ_EXP_NO_PHASE3  // timing experiment: results are wrong
+    q3_count = 0;
+#endif
+    drain3(false);
+  };
+
+  auto issue_batch = [&](uint32_t take) {  // requires !batch_open
+    q2_count -= take;
+    batch_item = lds64(s_q2 + (q2_count + min(lane, take - 1u)) * 8u);
+    __syncwarp();
+    batch_take = take;
+    batch_code = ldg32_if(table2 + batch_item.y, lane < take && (batch_item.x & 0x80000000u) != 0u, batch_item.y);
+    batch_open = true;
+  };
+
   auto drain2 = [&](bool flush) {
     __syncwarp();
+    settle_batch();  // the batch issued one tile ago
     while (q2_count >= 32u || (flush && q2_count)) {
-      const uint32_t take = min(q2_count, 32u);
-      q2_count -= take;
-      const uint2 item = lds64(s_q2 + (q2_count + min(lane, take - 1u)) * 8u);
-      __syncwarp();
-      const bool mine = lane < take;
-      const bool lookup = mine && (item.x & 0x80000000u) != 0u;
-      const uint32_t i = item.x & 0x7FFFFFFFu;
-      const uint32_t c = ldg32_if(table2 + item.y, lookup, item.y);
-      const bool done = settle(c, lookup, i, false, true);
-      q3_count = enqueue(s_q3, q3_count, mine && !done, i, c);
-#ifdef GJ_EXP_NO_PHASE3  // timing experiment: results are wrong
-      q3_count = 0;
-#endif
-      drain3(false);
+      issue_batch(min(q2_count, 32u));
+      if (q2_count >= 32u || flush) settle_batch();  // more to take: no point in deferring
     }
   };
 
@@ -475,6 +495,7 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
     drain2(false);
   }
   drain2(true);
+  settle_batch();
   drain3(true);
 
   __syncthreads();
