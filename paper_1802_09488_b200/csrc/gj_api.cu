@@ -215,9 +215,18 @@ bool resolve_exact(const gj_index& ix, int mode, bool* exact) {
   }
 }
 
+// Overflow records brought back chunk by chunk.  Chunks arrive in point
+// order, so sorting each chunk's records by (point, ordinal) right after its
+// copy — while the copy engine is busy with later chunks — leaves the whole
+// list sorted without a pass at the end.
+struct OverflowRecord {
+  uint64_t point;
+  uint32_t id, ord;
+};
 struct OverflowSink {
-  std::vector<uint64_t> point;
-  std::vector<uint32_t> id, ord;
+  std::vector<OverflowRecord> records;
+  std::vector<uint64_t> tmp_point;
+  std::vector<uint32_t> tmp_id, tmp_ord;
 };
 
 // The chunked host pipeline shared by gj_join_count_host and
@@ -270,15 +279,22 @@ int run_host_join(gj_session* s, const double* latlng, uint64_t n, uint64_t base
     worst.flags |= st.flags;
     worst.bad_index = std::min(worst.bad_index, st.bad_index);
     if (sink && st.overflow_count && !(st.flags & kErrOverflowCap)) {
-      const size_t at = sink->point.size();
       const size_t m = st.overflow_count;
-      sink->point.resize(at + m);
-      sink->id.resize(at + m);
-      sink->ord.resize(at + m);
-      GJ_CUDA(cudaMemcpyAsync(sink->point.data() + at, s->d_ovf_point.ptr, m * 8, cudaMemcpyDeviceToHost, s->stream));
-      GJ_CUDA(cudaMemcpyAsync(sink->id.data() + at, s->d_ovf_id.ptr, m * 4, cudaMemcpyDeviceToHost, s->stream));
-      GJ_CUDA(cudaMemcpyAsync(sink->ord.data() + at, s->d_ovf_ord.ptr, m * 4, cudaMemcpyDeviceToHost, s->stream));
+      sink->tmp_point.resize(m);
+      sink->tmp_id.resize(m);
+      sink->tmp_ord.resize(m);
+      GJ_CUDA(cudaMemcpyAsync(sink->tmp_point.data(), s->d_ovf_point.ptr, m * 8, cudaMemcpyDeviceToHost, s->stream));
+      GJ_CUDA(cudaMemcpyAsync(sink->tmp_id.data(), s->d_ovf_id.ptr, m * 4, cudaMemcpyDeviceToHost, s->stream));
+      GJ_CUDA(cudaMemcpyAsync(sink->tmp_ord.data(), s->d_ovf_ord.ptr, m * 4, cudaMemcpyDeviceToHost, s->stream));
       GJ_CUDA(cudaStreamSynchronize(s->stream));
+      const size_t at = sink->records.size();
+      sink->records.resize(at + m);
+      for (size_t k = 0; k < m; ++k) {
+        sink->records[at + k] = OverflowRecord{sink->tmp_point[k], sink->tmp_id[k], sink->tmp_ord[k]};
+      }
+      std::sort(sink->records.begin() + at, sink->records.end(), [](const OverflowRecord& x, const OverflowRecord& y) {
+        return x.point != y.point ? x.point < y.point : x.ord < y.ord;
+      });
     }
     return GJ_OK;
   };
@@ -691,20 +707,15 @@ int gj_join_count_host(gj_session* s, const double* latlng, uint64_t n, uint64_t
                                out_first_id ? &sink : nullptr, bad_index);
   if (rc != GJ_OK) return rc;
   if (overflow) {
-    const size_t m = sink.point.size();
+    const size_t m = sink.records.size();
     overflow->count = m;
     if (m > overflow->capacity) {
       set_error("overflow list larger than the caller's capacity");
       return GJ_CAPACITY;
     }
-    std::vector<uint64_t> order(m);
-    std::iota(order.begin(), order.end(), 0);
-    std::sort(order.begin(), order.end(), [&](uint64_t a, uint64_t b) {
-      return sink.point[a] != sink.point[b] ? sink.point[a] < sink.point[b] : sink.ord[a] < sink.ord[b];
-    });
     for (size_t k = 0; k < m; ++k) {
-      overflow->point_index[k] = sink.point[order[k]];
-      overflow->polygon_id[k] = sink.id[order[k]];
+      overflow->point_index[k] = sink.records[k].point;
+      overflow->polygon_id[k] = sink.records[k].id;
     }
   }
   return GJ_OK;
