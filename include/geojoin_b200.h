@@ -92,14 +92,18 @@ typedef struct {
   int32_t k_max;
   int32_t approx_mode;
   int32_t device;
-  int32_t dir_level;          /* grid level resolved by the shared-memory directory */
-  int32_t dir_width;          /* directory window, cells */
+  int32_t dir_level;          /* first 32-bit directory tier (trie-node boundary): grid level */
+  int32_t dir_width;          /* its window, cells */
   int32_t dir_height;
   int32_t dir_dict_len;       /* terminal entries that do not fit a directory code */
   int32_t dir2_level;         /* second, L2-resident directory tier (0 = absent) */
   int32_t dir2_width;
   int32_t dir2_height;
   int32_t ids_dense;          /* 1 when id == slot for every polygon */
+  int32_t dir16_level;        /* the join kernel's shared-memory tier (16-bit codes) */
+  int32_t dir16_width;
+  int32_t dir16_height;
+  int32_t reserved0;
 } gj_index_info;
 
 /* JoinStats (include/geojoin/join.hpp:77-84), in this order. */

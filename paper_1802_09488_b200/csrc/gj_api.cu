@@ -2,6 +2,8 @@
 // plumbing and the host-buffer pipelines (H2D / kernels / D2H overlapped on
 // three streams).
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <numeric>
@@ -27,23 +29,46 @@ struct SmemPlan {
   size_t total;
 };
 
+// Shared memory of K1: [16-bit tier | per-warp queues | histogram].  The SM's
+// L1 is what shared memory leaves of 256 KB, in carve-out steps, and K1 needs
+// L1 for its loads in flight (measured on config 2: 0.53 ms per 100 M points
+// up to the 164 KB step, 0.545 at 196 KB, 0.81 at 228 KB).  The histogram's
+// replication hardly matters (ATOMS.POPC.INC aggregates equal addresses), so
+// it only takes what is left inside the carve-out step the rest already needs.
 SmemPlan plan_smem(const gj_index& ix) {
   SmemPlan p{};
-  size_t at = align16(std::max<size_t>(ix.dev.dir.n_table * 4, 16));
+  const size_t table_bytes = static_cast<size_t>(ix.dev.dir16.n_table) * 2;
+  size_t at = align16(std::max<size_t>(table_bytes, 16));
+  p.queue_off = static_cast<uint32_t>(at);
+  at += static_cast<size_t>(kJoinThreads / 32) * kQueueBytesPerWarp;
+  p.hist_off = static_cast<uint32_t>(at);
 #ifdef GJ_SMEM_LIMIT_KB  // tuning: leave room for more than one CTA per SM
   const size_t limit = static_cast<size_t>(GJ_SMEM_LIMIT_KB) << 10;
 #else
   const size_t limit = ix.smem_optin > 2048 ? ix.smem_optin - 1024 : 0;
 #endif
-  p.queue_off = static_cast<uint32_t>(at);
-  at += static_cast<size_t>(kJoinThreads / 32) * kQueueBytesPerWarp;
-  p.hist_off = static_cast<uint32_t>(at);
-  const size_t room = std::min<size_t>(limit > at ? limit - at : 0, 64 << 10);
-  uint32_t rep = 32;
-  while (rep && static_cast<size_t>(ix.dev.n_ids) * rep * 4 > room) rep >>= 1;
-  p.hist_rep = ix.dev.n_ids ? rep : 0;
-  at += static_cast<size_t>(ix.dev.n_ids) * p.hist_rep * 4;
+  const size_t one = static_cast<size_t>(ix.dev.n_ids) * 4;
+  uint32_t rep = 0;
+  if (one && at + one <= limit) {
+    size_t step = limit;  // carve-out steps hold 1 KB of system shared memory per CTA
+    for (size_t kb : {64, 100, 132, 164, 196}) {
+      if (at + one <= (kb - 1) << 10) {
+        step = std::min(limit, (kb - 1) << 10);
+        break;
+      }
+    }
+    rep = 1;
+    while (rep < 32 && at + one * rep * 2 <= step) rep <<= 1;
+  }
+  if (const char* e = std::getenv("GJ_HIST_REP")) rep = std::min<uint32_t>(rep, static_cast<uint32_t>(std::atoi(e)));
+  p.hist_rep = rep;
+  at += one * rep;
+  if (const char* e = std::getenv("GJ_SMEM_PAD")) at += static_cast<size_t>(std::atoi(e));  // tuning knob
   p.total = at;
+  if (std::getenv("GJ_DEBUG_PLAN")) {
+    std::fprintf(stderr, "[gj] K1 smem: 16-bit tier level %d, %zu B; queues at %u; histogram at %u x%u; total %zu\n",
+                 30 - ix.dev.dir16.shift, table_bytes, p.queue_off, p.hist_off, p.hist_rep, p.total);
+  }
   return p;
 }
 
@@ -123,7 +148,7 @@ int enqueue_join(gj_session* s, const JoinRequest& rq) {
   jp.hist_rep = sp.hist_rep;
   jp.exact = rq.exact ? 1 : 0;
 
-  const int variant = (rq.d_first_id ? 4 : 0) | (rq.want_stats ? 2 : 0) | (ix.dev.ids_dense ? 1 : 0);
+  const int variant = (rq.d_first_id ? 4 : 0) | (rq.want_stats ? 2 : 0) | (ix.dev.ids_dense && sp.hist_rep ? 1 : 0);
   switch (variant) {
     case 0: rc = launch_join_variant<false, false, false>(s, jp, sp); break;
     case 1: rc = launch_join_variant<false, false, true>(s, jp, sp); break;

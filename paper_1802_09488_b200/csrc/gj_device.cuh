@@ -96,6 +96,11 @@ struct DevIndex {
   // not fit a 32-bit code (two payloads, lookup-table offsets).
   DevDirectory dir;
   DevDirectory dir2;
+  // Optional finer first tier with 16-bit codes, derived from `dir2` by
+  // downsampling (any level between the two): 0 = miss, 0xFFFF = look in
+  // dir2, otherwise 1 + ((polygon_id << 1) | interior).  K1 stages it instead
+  // of `dir` when present; `table` then points at uint16 data.
+  DevDirectory dir16;
   const uint64_t* dict;  // [n_dict], dict[0] == 0
   uint32_t n_dict;
 };
@@ -156,6 +161,31 @@ __device__ __forceinline__ void grid_xy(double lat, double lng, uint32_t* x, uin
     *x = grid_coord(lng, -180.0, 360.0);
     *y = grid_coord(lat, -90.0, 180.0);
   }
+}
+
+// grid_xy_fast for ANY pair of doubles, branch-free: true means the point is
+// valid (latlng.hpp:31-34) AND (*x, *y) are its exact grid coordinates; false
+// means "decide on the slow path" (invalid, NaN/inf, on or next to a grid line,
+// on the +90/+180 edge).  On top of the fraction guard above it checks that
+// tx, ty landed in [2^31, 2^31 + 2^30): exponent 0x41E and top mantissa bit 0,
+// i.e. hi >> 19 == 0x41E00000 >> 19.  Why that is enough for validity:
+//  * v > hi: d = RN(v - lo) >= span, p = RN(d R) >= 2^30 - 2^-23, so
+//    t = RN(p + 2^31) >= 2^31 + 2^30 (ulp there is 2^-21): top mantissa bit set;
+//  * v < lo: p < 0, so t < 2^31 (exponent differs) or t rounds to 2^31 exactly
+//    (fraction field 0, the guard rejects);
+//  * NaN / inf / huge: the exponent differs.
+__device__ __forceinline__ bool grid_xy_try(double lat, double lng, uint32_t* x, uint32_t* y) {
+  const double rx = 1073741824.0 / 360.0;
+  const double ry = 1073741824.0 / 180.0;
+  const double tx = __dadd_rn(__dmul_rn(__dsub_rn(lng, -180.0), rx), 2147483648.0);
+  const double ty = __dadd_rn(__dmul_rn(__dsub_rn(lat, -90.0), ry), 2147483648.0);
+  const uint32_t xl = static_cast<uint32_t>(__double2loint(tx)), xh = static_cast<uint32_t>(__double2hiint(tx));
+  const uint32_t yl = static_cast<uint32_t>(__double2loint(ty)), yh = static_cast<uint32_t>(__double2hiint(ty));
+  *x = __funnelshift_l(xl, xh, 11);
+  *y = __funnelshift_l(yl, yh, 11);
+  const uint32_t fx = ((xl & 0x1FFFFFu) - 2u), fy = ((yl & 0x1FFFFFu) - 2u);
+  const uint32_t range = (xh ^ 0x41E00000u) | (yh ^ 0x41E00000u);
+  return (range < (1u << 19)) & (max(fx, fy) <= 0x1FFFFFu - 4u);
 }
 
 // spread_bits (cell_id.cpp:30-37): bit i of the low 30 bits moves to bit 2i.

@@ -52,6 +52,7 @@ struct HostDirectory {
   int chunks = 0;  // node steps folded in
   uint32_t x0 = 0, y0 = 0, width = 0, height = 0, pitch = 0;
   std::vector<uint32_t> table;
+  std::vector<uint16_t> table16;  // the 16-bit first tier uses this instead
 };
 
 }  // namespace gj
@@ -61,7 +62,7 @@ struct gj_index {
   gj::DevIndex dev{};
   gj_index_info info{};
   std::vector<uint32_t> ids;  // slot -> polygon id
-  gj::DeviceBuffer d_arena, d_lut, d_ids, d_ring_off, d_ring_len, d_ring_xy, d_dir_table, d_dir_dict, d_dir2_table,
+  gj::DeviceBuffer d_arena, d_lut, d_ids, d_ring_off, d_ring_len, d_ring_xy, d_dir_table, d_dir_dict, d_dir2_table, d_dir16_table,
       d_strip_meta, d_strip_ptr, d_strip_edges;
   int sm_count = 0;
   size_t smem_optin = 0;

@@ -9,6 +9,7 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <unordered_map>
@@ -23,6 +24,10 @@ thread_local std::string g_error;
 
 constexpr uint64_t kMaxDirEntries = 32768;         // 128 KB of u32 codes (shared memory)
 constexpr uint64_t kMaxDir2Entries = 16ull << 20;  // 64 MB of u32 codes (stays in the 126 MB L2)
+// 68 KB of u16 codes: with K1's queues and histogram that stays inside the
+// 132 KB shared-memory carve-out step, which leaves the SM 124 KB of L1 for loads
+// in flight (a finer tier at 196 KB measured slower, see plan_smem in gj_api.cu)
+constexpr uint64_t kMaxDir16Entries = 34816;
 constexpr uint64_t kMaxPolygonId = (1u << 30) - 1;
 
 struct Bitmap {
@@ -84,10 +89,73 @@ struct Analysis {
   std::vector<uint32_t> ids;
   HostDirectory dir;           // shared-memory tier
   HostDirectory dir2;          // global-memory (L2-resident) tier, deeper; may be empty
+  HostDirectory dir16;         // K1's shared-memory tier (16-bit codes), see build_dir16
   std::vector<uint64_t> dict;  // terminal entries that do not fit a directory code
   uint64_t max_refs = 0;       // most references behind one entry
   uint64_t max_cand_refs = 0;  // most candidate references behind one entry
 };
+
+// The first directory tier K1 keeps in shared memory: 16-bit codes over a
+// window at `level`, derived from a 32-bit tier `tb` (the second tier when
+// there is one, else the first) by downsampling.  A cell resolves here when
+// every `tb` cell below it holds the same miss or the same inlined payload
+// below 0xFFFE; anything else says "look in tb".  Codes: 0 = miss, 0xFFFF =
+// look in tb, otherwise 1 + ((polygon_id << 1) | interior).  Any level up to
+// tb's works (not only trie-node boundaries); the deepest whose padded window
+// has at most `max_entries` cells is taken.
+void build_dir16(const HostDirectory& tb, uint64_t max_entries, HostDirectory* d16) {
+  *d16 = HostDirectory{};
+  d16->pitch = 1;
+  d16->table16.assign(1, 0);  // an empty window is just its all-miss padding
+  if (tb.width == 0 || tb.height == 0) return;
+  for (int level = tb.level; level >= 0; --level) {
+    const int down = tb.level - level;
+    const uint32_t x0 = tb.x0 >> down, y0 = tb.y0 >> down;
+    const uint32_t w = ((tb.x0 + tb.width - 1) >> down) - x0 + 1;
+    const uint32_t h = ((tb.y0 + tb.height - 1) >> down) - y0 + 1;
+    if (static_cast<uint64_t>(w + 1) * (h + 1) > max_entries && level > 0) continue;
+    d16->level = level;
+    d16->x0 = x0;
+    d16->y0 = y0;
+    d16->width = w;
+    d16->height = h;
+    d16->pitch = w + 1;
+    d16->table16.assign(static_cast<size_t>(d16->pitch) * (h + 1), 0);
+    const uint64_t side = 1ull << down;
+    for (uint32_t cy = 0; cy < h; ++cy) {
+      const uint64_t ty0 = static_cast<uint64_t>(y0 + cy) << down;
+      for (uint32_t cx = 0; cx < w; ++cx) {
+        const uint64_t tx0 = static_cast<uint64_t>(x0 + cx) << down;
+        bool first = true, uniform = true;
+        uint32_t code = 0;
+        for (uint64_t ty = ty0; ty < ty0 + side && uniform; ++ty) {
+          const bool row_in = ty >= tb.y0 && ty < static_cast<uint64_t>(tb.y0) + tb.height;
+          for (uint64_t tx = tx0; tx < tx0 + side; ++tx) {
+            uint32_t c = 0;  // outside tb's window: a miss
+            if (row_in && tx >= tb.x0 && tx < static_cast<uint64_t>(tb.x0) + tb.width) {
+              c = tb.table[(ty - tb.y0) * tb.pitch + (tx - tb.x0)];
+            }
+            if (first) {
+              code = c;
+              first = false;
+            } else if (c != code) {
+              uniform = false;
+              break;
+            }
+          }
+        }
+        uint16_t c16 = 0xFFFF;
+        if (uniform && code == 0) {
+          c16 = 0;
+        } else if (uniform && (code >> 30) == 1u && (code & 0x3FFFFFFFu) < 0xFFFEu) {
+          c16 = static_cast<uint16_t>((code & 0x3FFFFFFFu) + 1u);
+        }
+        d16->table16[static_cast<size_t>(cy) * d16->pitch + cx] = c16;
+      }
+    }
+    return;
+  }
+}
 
 // One breadth-first pass per face: forest check, depth bound, record bounds,
 // id collection; for face 0 the first levels also feed the directory.
@@ -299,7 +367,7 @@ int analyse(const gj_index_desc& d, Analysis* out) {
 
 template <typename T>
 int upload(DeviceBuffer& buf, const T* src, size_t count, size_t* total) {
-  const size_t bytes = std::max<size_t>(count * sizeof(T), 16);
+  const size_t bytes = std::max<size_t>((count * sizeof(T) + 15) & ~size_t{15}, 16);  // K1 stages tables as uint4
   GJ_CUDA(buf.reserve(bytes));
   if (count) GJ_CUDA(cudaMemcpy(buf.ptr, src, count * sizeof(T), cudaMemcpyHostToDevice));
   *total += bytes;
@@ -436,6 +504,11 @@ int create_index(const gj_index_desc& d, int device, gj_index** out) {
     an.dir.pitch = 1;
     an.dir.table.assign(1, 0u);
   }
+  {
+    uint64_t max16 = kMaxDir16Entries;
+    if (const char* e = std::getenv("GJ_DIR16_MAX")) max16 = std::strtoull(e, nullptr, 10);  // tuning knob
+    build_dir16(an.dir2.table.empty() ? an.dir : an.dir2, max16, &an.dir16);
+  }
   size_t bytes = 0;
   if ((rc = upload(ix->d_arena, d.arena, d.node_count * kNodeSlots, &bytes)) != GJ_OK) return rc;
   if ((rc = upload(ix->d_lut, d.lut, d.lut_len, &bytes)) != GJ_OK) return rc;
@@ -449,6 +522,7 @@ int create_index(const gj_index_desc& d, int device, gj_index** out) {
   if ((rc = upload(ix->d_dir_table, an.dir.table.data(), an.dir.table.size(), &bytes)) != GJ_OK) return rc;
   if ((rc = upload(ix->d_dir_dict, an.dict.data(), an.dict.size(), &bytes)) != GJ_OK) return rc;
   if ((rc = upload(ix->d_dir2_table, an.dir2.table.data(), an.dir2.table.size(), &bytes)) != GJ_OK) return rc;
+  if ((rc = upload(ix->d_dir16_table, an.dir16.table16.data(), an.dir16.table16.size(), &bytes)) != GJ_OK) return rc;
 
   DevIndex& dv = ix->dev;
   dv.arena = ix->d_arena.as<uint64_t>();
@@ -483,6 +557,8 @@ int create_index(const gj_index_desc& d, int device, gj_index** out) {
   };
   set_dir(dv.dir, an.dir, ix->d_dir_table.as<uint32_t>());
   set_dir(dv.dir2, an.dir2, ix->d_dir2_table.as<uint32_t>());
+  set_dir(dv.dir16, an.dir16, ix->d_dir16_table.as<uint32_t>());
+  dv.dir16.n_table = static_cast<uint32_t>(an.dir16.table16.size());
   dv.dict = ix->d_dir_dict.as<uint64_t>();
   dv.n_dict = static_cast<uint32_t>(an.dict.size());
 
@@ -504,6 +580,9 @@ int create_index(const gj_index_desc& d, int device, gj_index** out) {
   info.dir_width = static_cast<int32_t>(an.dir.width);
   info.dir_height = static_cast<int32_t>(an.dir.height);
   info.dir_dict_len = static_cast<int32_t>(an.dict.size());
+  info.dir16_level = an.dir16.level;
+  info.dir16_width = static_cast<int32_t>(an.dir16.width);
+  info.dir16_height = static_cast<int32_t>(an.dir16.height);
   info.dir2_level = an.dir2.table.empty() ? 0 : an.dir2.level;
   info.dir2_width = static_cast<int32_t>(an.dir2.width);
   info.dir2_height = static_cast<int32_t>(an.dir2.height);

@@ -91,6 +91,11 @@ __device__ __forceinline__ uint32_t lds32(uint32_t addr) {
   asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
   return v;
 }
+__device__ __forceinline__ uint32_t lds16(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
 __device__ __forceinline__ uint2 lds64(uint32_t addr) {
   uint2 v;
   asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr) : "memory");
@@ -253,25 +258,30 @@ __device__ __noinline__ uint32_t emit_general(const DevIndex& ix, const JoinPara
   return first;
 }
 
-// K1.  Persistent grid (one CTA per SM); each CTA stages the first directory
-// tier (and a replicated per-polygon histogram) in shared memory once, then
-// streams tiles of points.  A tile is kTile consecutive points; warp w owns
-// the kChunkPoints consecutive points at w*kChunkPoints inside it (lane l,
-// slot j -> point j*32 + l of the chunk), so every load and store of a warp is
-// one contiguous 512 / 128 byte run, and a thread keeps kPointsPerThread
-// independent 16-byte loads in flight.  The work has three populations, and
-// only the first runs where the points are:
-//   1. all points, straight-line: cell coordinates, shared-memory directory,
-//      emit when it resolves to one payload (71 % on BASELINE config 2);
-//   2. points under a directory link (29 %): compacted into the warp's queue
-//      Q2 and drained 32 at a time — one 4-byte gather each into the second,
-//      L2-resident directory tier, same settle logic;
+// K1.  Persistent grid (one CTA per SM); each CTA stages the 16-bit first
+// directory tier (and a replicated per-polygon histogram) in shared memory
+// once, then streams tiles of points.  A tile is kTile consecutive points;
+// warp w owns the kChunkPoints consecutive points at w*kChunkPoints inside it
+// (lane l, slot j -> point j*32 + l of the chunk), so every load and store of
+// a warp is one contiguous 512 / 128 byte run, and a thread keeps
+// kPointsPerThread independent 16-byte loads in flight.  The work has three
+// populations, and only the first runs where the points are:
+//   1. all points, straight-line and call-free: branch-free grid coordinates
+//      (grid_xy_try), shared-memory tier, emit when the 16-bit code is one
+//      payload that emits (85 % on BASELINE config 2);
+//   2. points the first tier cannot resolve: compacted into the warp's queue
+//      Q2 and drained 32 at a time — one 4-byte gather each into the 32-bit
+//      tier `tb` (the L2-resident second tier, or the small first one when
+//      the index has no second), settled the same way;
 //   3. what is still open (2 %: deep boundary nodes, dictionary entries,
-//      exact-mode candidates): compacted again into Q3 and drained 32 at a
+//      exact-mode candidates) and the points population 1 would not decide
+//      (invalid, on a grid line): compacted again into Q3 and drained 32 at a
 //      time — dependent 8-byte gathers down the arena, lookup-table records,
-//      candidate tasks.
+//      candidate tasks; slow points redo everything with the IEEE division.
 // Running 2 and 3 in place would drag all 32 lanes through their code for the
 // few active ones; through the queues they always run with full warps.
+// kDense: id == count slot for every polygon AND the histogram is in shared
+// memory (jp.hist_rep != 0), the common case; otherwise the general counting path.
 template <bool kIds, bool kStats, bool kDense>
 __global__ void __launch_bounds__(kJoinThreads, GJ_JOIN_MIN_BLOCKS)
 join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinParams jp) {
@@ -280,10 +290,10 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
   const uint32_t lane = tid & 31u;
   const uint32_t warp = tid >> 5;
 
-  {  // stage the directory, clear the histogram
-    const uint4* src = reinterpret_cast<const uint4*>(ix.dir.table);
+  {  // stage the first directory tier, clear the histogram
+    const uint4* src = reinterpret_cast<const uint4*>(ix.dir16.table);
     uint4* dst = reinterpret_cast<uint4*>(smem);
-    const uint32_t n4 = (ix.dir.n_table + 3) / 4;  // buffers are padded to 16 B
+    const uint32_t n4 = (ix.dir16.n_table * 2u + 15u) / 16u;  // buffers are padded to 16 B
     for (uint32_t i = tid; i < n4; i += kJoinThreads) dst[i] = __ldg(src + i);
     uint32_t* hist = reinterpret_cast<uint32_t*>(smem + jp.smem_hist_off);
     const uint32_t n_hist = ix.n_ids * jp.hist_rep;
@@ -297,38 +307,35 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
   const uint32_t s_q2 = smem_addr(smem + jp.smem_queue_off) + warp * kQueueBytesPerWarp;
   const uint32_t s_q3 = s_q2 + kQueue2Cap * 8u;
   const uint32_t lane_lt = (1u << lane) - 1u;
-  const uint32_t d1_w = ix.dir.width, d1_h = ix.dir.height, d1_pitch = ix.dir.pitch;
-  const uint32_t d1_x0 = ix.dir.x0, d1_y0 = ix.dir.y0;
-  const int d1_shift = ix.dir.shift;
-  const bool has_dir2 = ix.dir2.n_table != 0;
-  const uint32_t* __restrict__ table2 = ix.dir2.table;
-  const uint32_t d2_w = ix.dir2.width, d2_h = ix.dir2.height, d2_pitch = ix.dir2.pitch;
-  const uint32_t d2_x0 = ix.dir2.x0, d2_y0 = ix.dir2.y0;
-  const int d2_shift = ix.dir2.shift;
-  const int walk_level = ix.prefix_level0 + 4 * (has_dir2 ? ix.dir2.chunks : ix.dir.chunks);
-  const uint32_t leaf_keep = ~((1u << (30 - ix.leaf_level)) - 1u);  // cell_id.cpp:93-94
+  const uint32_t d1_w = ix.dir16.width, d1_h = ix.dir16.height, d1_pitch = ix.dir16.pitch;
+  const uint32_t d1_x0 = ix.dir16.x0, d1_y0 = ix.dir16.y0;
+  const int d1_shift = ix.dir16.shift;
+  const DevDirectory& tb = ix.dir2.n_table ? ix.dir2 : ix.dir;  // the 32-bit tier behind it
+  const uint32_t* __restrict__ table2 = tb.table;
+  const uint32_t d2_w = tb.width, d2_h = tb.height, d2_pitch = tb.pitch;
+  const uint32_t d2_x0 = tb.x0, d2_y0 = tb.y0;
+  const int d2_shift = tb.shift;
   const double2* __restrict__ pts = jp.pts;
   uint32_t* __restrict__ first_id = jp.first_id;
   const uint32_t n = static_cast<uint32_t>(jp.n);  // 1 <= n < 2^31 per launch (bit 31 of an index is a queue flag)
-  // A code resolves right here when it is one inlined payload that emits: a
-  // true hit, or a candidate in approximate mode (join.cpp:100-108).
-  const uint32_t emit_mask = 0xC0000000u | (jp.exact ? 1u : 0u);
-  const uint32_t emit_bits = kDirInline | (jp.exact ? 1u : 0u);
+  // A code resolves where it is read when it is one inlined payload that
+  // emits: a true hit, or a candidate in approximate mode (join.cpp:100-108).
+  const uint32_t need_interior = jp.exact ? 1u : 0u;
+  const uint32_t emit_mask = 0xC0000000u | need_interior;
+  const uint32_t emit_bits = kDirInline | need_interior;
 
   uint32_t n_valid = 0, false_hits = 0, solely_true = 0, refined = 0, cand_refs = 0;
   uint32_t q2_count = 0, q3_count = 0;  // warp-uniform
 
-  // One resolved directory code of a live point: count, stats, first id.
-  // Returns true when the point is finished (inlined emit or miss).
-  // First ids: population 1 writes the word of EVERY live lane (kNoMatch
-  // unless it emits), i.e. whole 128-byte runs per warp; later populations
-  // only overwrite words that change, and those 4-byte stores then hit a
-  // sector that is still dirty in L2 instead of forcing a 32-byte DRAM fill.
-  auto settle = [&](uint32_t c, bool active, uint32_t i, bool store_all, bool live) -> bool {
+  // One resolved 32-bit directory code of a point of population 2: count,
+  // stats, first id.  Returns true when the point is finished (inlined emit or
+  // miss).  Population 1 has already written kNoMatch for it (see below), so
+  // only an emit stores.
+  auto settle = [&](uint32_t c, bool active, uint32_t i) -> bool {
     const bool emit = active && (c & emit_mask) == emit_bits;
     const bool miss = active && c == 0u;
     const uint32_t id = (c >> 1) & 0x1FFFFFFFu;
-    if (kDense && hist.rep) {
+    if (kDense) {
       red_inc_shared_if(hist.smem + (id * hist.rep + hist.lane_rep) * 4u, emit);
     } else if (emit) {
       count_slot<kDense>(ix, jp, hist, id);
@@ -339,21 +346,34 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
       refined += emit && !(c & 1u);
       cand_refs += emit && !(c & 1u);
     }
-    if (kIds) st32_if(first_id + i, emit ? id : kNoMatch, store_all ? live : emit);
+    if (kIds) st32_if(first_id + i, id, emit);
     return emit || miss;
   };
 
   // Population 3, one batch of open points (one per lane, `mine` = the lane
-  // holds one): arena descent / dictionary / candidates.  All 32 lanes go
-  // through it together because the record reservations are per warp.
-  auto resolve_open = [&](bool mine, uint32_t i, uint32_t c) {
+  // holds one; bit 31 of `iw` marks a slow point): arena descent / dictionary
+  // / candidates.  All 32 lanes go through it together because the record
+  // reservations are per warp.
+  auto resolve_open = [&](bool mine, uint32_t iw, uint32_t c) {
+    const uint32_t i = iw & 0x7FFFFFFFu;
     uint64_t entry = 0;
     if (mine) {
-      if (c & kDirLink) {
+      if (iw & 0x80000000u) {  // nothing decided yet: the reference's own sequence
+        const double2 q = __ldg(pts + i);
+        if (!latlng_valid(q.x, q.y)) {
+          flag_error(jp.status, kErrInvalidPoint, jp.base_index + i);  // cell_id.cpp:83-85
+          mine = false;
+        } else {
+          if (kStats) ++n_valid;
+          entry = probe_raw(ix, cell_from_point(q.x, q.y, ix.leaf_level));
+        }
+      } else if (c & kDirLink) {
         const double2 q = __ldg(pts + i);  // cheaper to re-read than to queue the coordinates
         uint32_t x, y;
         grid_xy(q.x, q.y, &x, &y);
-        entry = walk_from(ix, c & ~kDirLink, walk_level, (x & leaf_keep) << 2, (y & leaf_keep) << 2);
+        const uint32_t leaf_keep = ~((1u << (30 - ix.leaf_level)) - 1u);  // cell_id.cpp:93-94
+        entry = walk_from(ix, c & ~kDirLink, ix.prefix_level0 + 4 * tb.chunks, (x & leaf_keep) << 2,
+                          (y & leaf_keep) << 2);
       } else if (c & kDirInline) {
         entry = (static_cast<uint64_t>(c & 0x3FFFFFFFu) << 2) | 1u;  // exact-mode candidate
       } else {
@@ -412,25 +432,24 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
     }
   };
 
-  // Population 2: Q2 items 32 at a time.  An item is (point | flag, w): with
-  // the flag (bit 31) w indexes the second directory tier; without it w is a
-  // first-tier code that goes straight on to Q3.  The batch is software-
-  // pipelined across tiles: its tier-2 gathers are ISSUED when the batch is
-  // taken off the queue and SETTLED one tile later, so their L2 latency hides
-  // behind the next tile's streaming work instead of stalling the warp.
+  // Population 2: Q2 items 32 at a time.  An item is (point | slow, w): w
+  // indexes the 32-bit tier; a slow point (bit 31) skips the lookup and goes
+  // straight on to Q3.  The batch is software-pipelined across tiles: its
+  // gathers are ISSUED when the batch is taken off the queue and SETTLED one
+  // tile later, so their L2 latency hides behind the next tile's streaming
+  // work instead of stalling the warp.
   bool batch_open = false;      // a batch is in flight (warp-uniform)
   uint32_t batch_take = 0;      // its size
-  uint2 batch_item = make_uint2(0u, 0u);
-  uint32_t batch_code = 0;      // the gather in flight (or the forwarded code)
+  uint32_t batch_point = 0;     // point | slow of this lane's item
+  uint32_t batch_code = 0;      // the gather in flight
 
   auto settle_batch = [&]() {
     if (!batch_open) return;
     batch_open = false;
     const bool mine = lane < batch_take;
-    const bool lookup = mine && (batch_item.x & 0x80000000u) != 0u;
-    const uint32_t i = batch_item.x & 0x7FFFFFFFu;
-    const bool done = settle(batch_code, lookup, i, false, true);
-    q3_count = enqueue(s_q3, q3_count, mine && !done, i, batch_code);
+    const bool lookup = mine && (batch_point & 0x80000000u) == 0u;
+    const bool done = settle(batch_code, lookup, batch_point);
+    q3_count = enqueue(s_q3, q3_count, mine && !done, batch_point, batch_code);
 #ifdef GJ_EXP_NO_PHASE3  // timing experiment: results are wrong
     q3_count = 0;
 #endif
@@ -439,10 +458,11 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
 
   auto issue_batch = [&](uint32_t take) {  // requires !batch_open
     q2_count -= take;
-    batch_item = lds64(s_q2 + (q2_count + min(lane, take - 1u)) * 8u);
+    const uint2 item = lds64(s_q2 + (q2_count + min(lane, take - 1u)) * 8u);
     __syncwarp();
     batch_take = take;
-    batch_code = ldg32_if(table2 + batch_item.y, lane < take && (batch_item.x & 0x80000000u) != 0u, batch_item.y);
+    batch_point = item.x;
+    batch_code = ldg32_if(table2 + item.y, lane < take && (item.x & 0x80000000u) == 0u, 0u);
     batch_open = true;
   };
 
@@ -466,31 +486,44 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
       // the last point and are masked below.
       p[j] = __ldcs(pts + min(base + j * 32u, n - 1u));
     }
-    // ---- population 1: shared-memory directory ----
+    // ---- population 1: shared-memory tier, no branches, no calls ----
 #pragma unroll
     for (int j = 0; j < kPointsPerThread; ++j) {
       const uint32_t i = base + j * 32u;
       const bool live = i < n;
-      const bool valid = latlng_valid(p[j].x, p[j].y);
-      if (live && !valid) flag_error(jp.status, kErrInvalidPoint, jp.base_index + i);  // cell_id.cpp:83-85
       uint32_t x, y;
-      grid_xy(p[j].x, p[j].y, &x, &y);
+      const bool ok = grid_xy_try(p[j].x, p[j].y, &x, &y) && live;  // valid, coordinates exact
       const uint32_t cx = min((x >> d1_shift) - d1_x0, d1_w);  // clamps into the all-miss padding
       const uint32_t cy = min((y >> d1_shift) - d1_y0, d1_h);
-      const uint32_t c = lds32(s_table + (cy * d1_pitch + cx) * 4u);
-      const bool active = live && valid;
-      if (kStats) n_valid += active;
-      const bool done = settle(c, active, i, true, live);
+      // 0 = miss, 0xFFFF = look in the 32-bit tier, else 1 + payload
+      const uint32_t e = lds16(s_table + (cy * d1_pitch + cx) * 2u) - 1u;
+      const bool emit = ok && e < 0xFFFEu && (e & need_interior) == need_interior;
+      const uint32_t id = e >> 1;
+      if (kDense) {
+        red_inc_shared_if(hist.smem + (id * hist.rep + hist.lane_rep) * 4u, emit);
+      } else if (emit) {
+        count_slot<kDense>(ix, jp, hist, id);
+      }
+      if (kStats) {
+        n_valid += ok;
+        false_hits += ok && e == 0xFFFFFFFFu;
+        solely_true += emit && (e & 1u);
+        refined += emit && !(e & 1u);
+        cand_refs += emit && !(e & 1u);
+      }
+      // First ids: every live lane writes its word here (kNoMatch unless it
+      // emits), i.e. whole 128-byte runs per warp; later populations only
+      // overwrite words that change, and those 4-byte stores then hit a
+      // sector that is still dirty in L2 instead of forcing a 32-byte DRAM fill.
+      if (kIds) st32_if(first_id + i, emit ? id : kNoMatch, live);
 #ifdef GJ_EXP_PHASE1_ONLY  // timing experiment: results are wrong
       continue;
 #endif
-      // what stays open is queued: a link as its cell's index in the second
-      // tier, anything else (or everything, without a second tier) as the code
+      // what stays open is queued with its cell's index in the 32-bit tier
       const uint32_t cx2 = min((x >> d2_shift) - d2_x0, d2_w);
       const uint32_t cy2 = min((y >> d2_shift) - d2_y0, d2_h);
-      const bool via_tier2 = has_dir2 && (c & kDirLink) != 0u;
-      q2_count = enqueue(s_q2, q2_count, active && !done, via_tier2 ? i | 0x80000000u : i,
-                         via_tier2 ? cy2 * d2_pitch + cx2 : c);
+      const bool open = live && !emit && !(ok && e == 0xFFFFFFFFu);
+      q2_count = enqueue(s_q2, q2_count, open, ok ? i : i | 0x80000000u, cy2 * d2_pitch + cx2);
     }
     drain2(false);
   }
