@@ -47,9 +47,9 @@ SmemPlan plan_smem(const gj_index& ix) {
 #else
   const size_t limit = ix.smem_optin > 2048 ? ix.smem_optin - 1024 : 0;
 #endif
-  const size_t one = static_cast<size_t>(ix.dev.n_ids) * 4;
+  const size_t one = (static_cast<size_t>(ix.dev.n_ids) + 1) * 4;  // + the spare row non-emitting lanes count into
   uint32_t rep = 0;
-  if (one && at + one <= limit) {
+  if (ix.dev.n_ids && at + one <= limit) {
     size_t step = limit;  // carve-out steps hold 1 KB of system shared memory per CTA
     for (size_t kb : {64, 100, 132, 164, 196}) {
       if (at + one <= (kb - 1) << 10) {
@@ -571,6 +571,9 @@ int gj_session_create(gj_index* ix, gj_session** out) {
   }
   GJ_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&s->h_status), 4 * sizeof(DevStatus), cudaHostAllocDefault));
   GJ_CUDA(s->d_status.reserve(4 * sizeof(DevStatus)));
+  if (const char* e = std::getenv("GJ_L2_FETCH")) {  // tuning knob: 32 / 64 / 128
+    if (cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, static_cast<size_t>(std::atoi(e))) != cudaSuccess) cudaGetLastError();
+  }
 #ifndef GJ_NO_L2_PERSIST
   // Keep the second directory tier resident in L2: it is small (<= 64 MB),
   // gathered at random by ~30 % of the points, and would otherwise be churned

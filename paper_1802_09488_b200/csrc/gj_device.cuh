@@ -43,6 +43,26 @@ struct DevDirectory {
   int32_t chunks;         // node steps already resolved
 };
 
+// How K1 codes a point's position in the 32-bit tier `tb` into one queue
+// word.  Packed (the usual case): the word holds the point's cell at level
+// tb.level + 4 relative to the window, (Y << xbits) | X, so the drain gets both
+// the tier index ((Y >> 4) * pitch + (X >> 4)) and the 4 + 4 sub-cell bits that
+// select the slot in the trie node under a link — population 3 then reads the
+// arena without re-reading the point (a random 16-byte read costs a 128-byte
+// DRAM burst).  Unpacked (window too wide for 32 bits, arena above 2^23 nodes,
+// tier deeper than level 28): the word is the tier index and population 3
+// re-reads the point.  Both forms are  min((v32 >> shift) - origin, clamp)  per
+// axis, word = qy * mul + qx, where v32 is the grid coordinate left-aligned to 32 bits.
+struct DevQueueCoding {
+  uint32_t packed;
+  uint32_t shift;           // applied to the 32-bit-aligned coordinate
+  uint32_t x0, y0;          // window origin at the coded level
+  uint32_t x_clamp, y_clamp;
+  uint32_t mul;             // packed: 1 << xbits, unpacked: tb.pitch
+  uint32_t xbits;           // packed only
+  uint32_t sub_mask;        // packed only: the sub-cell bits at or above the leaf level (cell_id.cpp:93-94)
+};
+
 // Latitude strips of one polygon: its widened latitude range [y0, y0 + k / inv_h]
 // cut into k equal strips; strip s lists (as 32-byte edge records) every edge
 // whose latitude range, widened by the 1e-9 deg margin of pip_edge, meets it.
@@ -101,6 +121,7 @@ struct DevIndex {
   // dir2, otherwise 1 + ((polygon_id << 1) | interior).  K1 stages it instead
   // of `dir` when present; `table` then points at uint16 data.
   DevDirectory dir16;
+  DevQueueCoding qc;  // for the 32-bit tier behind dir16 (dir2 when present, else dir)
   const uint64_t* dict;  // [n_dict], dict[0] == 0
   uint32_t n_dict;
 };
@@ -163,26 +184,38 @@ __device__ __forceinline__ void grid_xy(double lat, double lng, uint32_t* x, uin
   }
 }
 
-// grid_xy_fast for ANY pair of doubles, branch-free: true means the point is
-// valid (latlng.hpp:31-34) AND (*x, *y) are its exact grid coordinates; false
-// means "decide on the slow path" (invalid, NaN/inf, on or next to a grid line,
-// on the +90/+180 edge).  On top of the fraction guard above it checks that
-// tx, ty landed in [2^31, 2^31 + 2^30): exponent 0x41E and top mantissa bit 0,
-// i.e. hi >> 19 == 0x41E00000 >> 19.  Why that is enough for validity:
-//  * v > hi: d = RN(v - lo) >= span, p = RN(d R) >= 2^30 - 2^-23, so
-//    t = RN(p + 2^31) >= 2^31 + 2^30 (ulp there is 2^-21): top mantissa bit set;
-//  * v < lo: p < 0, so t < 2^31 (exponent differs) or t rounds to 2^31 exactly
-//    (fraction field 0, the guard rejects);
+// Grid coordinates of ANY pair of doubles, branch-free, two DFMAs: true means
+// the point is valid (latlng.hpp:31-34) AND (*x32, *y32) are its exact grid
+// coordinates, left-aligned to 32 bits ((x << 2) | two fraction bits, so
+// x32 >> (32 - L) is the level-L cell for any L <= 30); false means "decide on
+// the slow path" (invalid, NaN/inf, on or next to a grid line, on the +90/+180
+// edge).
+//
+// t = fma(v, R, C), R = RN(2^30 / span), C = 2^31 + 2^29 (= 2^31 - lo R up to
+// 2^-24).  For t in [2^31, 2^32) the 52 mantissa bits are the fixed-point value
+// t - 2^31 with 21 fraction bits (unit u = 2^-21).  Against the reference's
+// s = RN(RN(RN(v - lo) / span) 2^30):
+//   ours:  fma rounding <= 0.5 u, R's rounding <= |v| R 2^-53 <= 0.125 u, C <= 0.125 u
+//   theirs: RN(v - lo) <= 2^-45 (2^30 / span) <= 0.18 u, the division <= 2^-23 = 0.25 u
+// so |t - 2^31 - s| < 1.2 u, and whenever the fraction field f satisfies
+// 2 <= f <= 2^21 - 3 the integer part equals trunc(s) exactly (and is < 2^30,
+// so the upper clamp cannot bind).  Validity comes from the same word: t must
+// land in [2^31, 2^31 + 2^30), i.e. exponent 0x41E and top mantissa bit 0
+// (hi >> 19 == 0x41E00000 >> 19):
+//  * v > hi: v R + C >= 2^31 + 2^30 + 8e-8, which rounds to >= 2^31 + 2^30;
+//  * v < lo: t < 2^31 (exponent differs) or t rounds to 2^31 exactly (f = 0);
 //  * NaN / inf / huge: the exponent differs.
-__device__ __forceinline__ bool grid_xy_try(double lat, double lng, uint32_t* x, uint32_t* y) {
-  const double rx = 1073741824.0 / 360.0;
+// The explicit fma is deliberate (the build is -fmad=false everywhere else).
+__device__ __forceinline__ bool grid_xy_try(double lat, double lng, uint32_t* x32, uint32_t* y32) {
+  const double rx = 1073741824.0 / 360.0;  // RN(2^30 / 360), folded at compile time
   const double ry = 1073741824.0 / 180.0;
-  const double tx = __dadd_rn(__dmul_rn(__dsub_rn(lng, -180.0), rx), 2147483648.0);
-  const double ty = __dadd_rn(__dmul_rn(__dsub_rn(lat, -90.0), ry), 2147483648.0);
+  const double c = 2147483648.0 + 536870912.0;
+  const double tx = __fma_rn(lng, rx, c);
+  const double ty = __fma_rn(lat, ry, c);
   const uint32_t xl = static_cast<uint32_t>(__double2loint(tx)), xh = static_cast<uint32_t>(__double2hiint(tx));
   const uint32_t yl = static_cast<uint32_t>(__double2loint(ty)), yh = static_cast<uint32_t>(__double2hiint(ty));
-  *x = __funnelshift_l(xl, xh, 11);
-  *y = __funnelshift_l(yl, yh, 11);
+  *x32 = __funnelshift_l(xl, xh, 13);  // exponent and the (zero) top mantissa bit fall off
+  *y32 = __funnelshift_l(yl, yh, 13);
   const uint32_t fx = ((xl & 0x1FFFFFu) - 2u), fy = ((yl & 0x1FFFFFu) - 2u);
   const uint32_t range = (xh ^ 0x41E00000u) | (yh ^ 0x41E00000u);
   return (range < (1u << 19)) & (max(fx, fy) <= 0x1FFFFFu - 4u);

@@ -559,6 +559,38 @@ int create_index(const gj_index_desc& d, int device, gj_index** out) {
   set_dir(dv.dir2, an.dir2, ix->d_dir2_table.as<uint32_t>());
   set_dir(dv.dir16, an.dir16, ix->d_dir16_table.as<uint32_t>());
   dv.dir16.n_table = static_cast<uint32_t>(an.dir16.table16.size());
+  {  // queue coding for the 32-bit tier K1 gathers from
+    const HostDirectory& tb = an.dir2.table.empty() ? an.dir : an.dir2;
+    const int tb_shift = 30 - tb.level;
+    auto bits_for = [](uint64_t v) {  // smallest b with v <= 2^b
+      uint32_t b = 0;
+      while ((1ull << b) < v) ++b;
+      return b;
+    };
+    const uint32_t xbits = bits_for((static_cast<uint64_t>(tb.width) + 1) * 16);
+    const uint32_t ybits = bits_for((static_cast<uint64_t>(tb.height) + 1) * 16);
+    DevQueueCoding& qc = dv.qc;
+    qc = DevQueueCoding{};
+    if (tb_shift >= 2 && xbits + ybits <= 32 && d.node_count <= (1ull << 23)) {
+      qc.packed = 1;
+      qc.shift = static_cast<uint32_t>(tb_shift + 2 - 4);
+      qc.x0 = tb.x0 * 16;
+      qc.y0 = tb.y0 * 16;
+      qc.x_clamp = tb.width * 16;
+      qc.y_clamp = tb.height * 16;
+      qc.mul = 1u << xbits;
+      qc.xbits = xbits;
+      const int below_leaf = tb.level + 4 - d.k_max / 2;  // sub-cell levels finer than the leaf level
+      qc.sub_mask = below_leaf > 0 ? (0xFu & ~((1u << std::min(below_leaf, 4)) - 1u)) : 0xFu;
+    } else {
+      qc.shift = static_cast<uint32_t>(tb_shift + 2);
+      qc.x0 = tb.x0;
+      qc.y0 = tb.y0;
+      qc.x_clamp = tb.width;
+      qc.y_clamp = tb.height;
+      qc.mul = tb.pitch;
+    }
+  }
   dv.dict = ix->d_dir_dict.as<uint64_t>();
   dv.n_dict = static_cast<uint32_t>(an.dict.size());
 

@@ -31,6 +31,10 @@ constexpr int kPointsPerThread = GJ_PPT;
 // directory left open (< 32 left over + up to 32 per point slot of a tile);
 // Q3 the few that the second tier leaves open as well (< 32 left over + 32
 // per Q2 drain).
+#ifndef GJ_PF_DIST
+#define GJ_PF_DIST 1
+#endif
+constexpr uint32_t kPrefetchTiles = GJ_PF_DIST;  // K1: L2 prefetch distance in tiles, 0 = off
 constexpr int kQueue2Cap = 32 * (kPointsPerThread + 1);
 constexpr int kQueue3Cap = 64;
 constexpr int kQueueBytesPerWarp = (kQueue2Cap + kQueue3Cap) * 8;
@@ -296,7 +300,7 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
     const uint32_t n4 = (ix.dir16.n_table * 2u + 15u) / 16u;  // buffers are padded to 16 B
     for (uint32_t i = tid; i < n4; i += kJoinThreads) dst[i] = __ldg(src + i);
     uint32_t* hist = reinterpret_cast<uint32_t*>(smem + jp.smem_hist_off);
-    const uint32_t n_hist = ix.n_ids * jp.hist_rep;
+    const uint32_t n_hist = (ix.n_ids + 1u) * jp.hist_rep;
     for (uint32_t i = tid; i < n_hist; i += kJoinThreads) hist[i] = 0;
   }
   __syncthreads();
@@ -306,15 +310,15 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
   const HistRef hist{smem_addr(smem + jp.smem_hist_off), jp.hist_rep, lane & (jp.hist_rep ? jp.hist_rep - 1u : 0u)};
   const uint32_t s_q2 = smem_addr(smem + jp.smem_queue_off) + warp * kQueueBytesPerWarp;
   const uint32_t s_q3 = s_q2 + kQueue2Cap * 8u;
+  const uint32_t hist_spare = ix.n_ids;  // the histogram has n_ids + 1 rows
   const uint32_t lane_lt = (1u << lane) - 1u;
   const uint32_t d1_w = ix.dir16.width, d1_h = ix.dir16.height, d1_pitch = ix.dir16.pitch;
   const uint32_t d1_x0 = ix.dir16.x0, d1_y0 = ix.dir16.y0;
-  const int d1_shift = ix.dir16.shift;
+  const uint32_t d1_shift = min(static_cast<uint32_t>(ix.dir16.shift) + 2u, 31u);  // on 32-bit-aligned coordinates
   const DevDirectory& tb = ix.dir2.n_table ? ix.dir2 : ix.dir;  // the 32-bit tier behind it
   const uint32_t* __restrict__ table2 = tb.table;
-  const uint32_t d2_w = tb.width, d2_h = tb.height, d2_pitch = tb.pitch;
-  const uint32_t d2_x0 = tb.x0, d2_y0 = tb.y0;
-  const int d2_shift = tb.shift;
+  const uint32_t qc_shift = ix.qc.shift, qc_mul = ix.qc.mul;
+  const uint32_t qc_x0 = ix.qc.x0, qc_y0 = ix.qc.y0, qc_xc = ix.qc.x_clamp, qc_yc = ix.qc.y_clamp;
   const double2* __restrict__ pts = jp.pts;
   uint32_t* __restrict__ first_id = jp.first_id;
   const uint32_t n = static_cast<uint32_t>(jp.n);  // 1 <= n < 2^31 per launch (bit 31 of an index is a queue flag)
@@ -368,12 +372,23 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
           entry = probe_raw(ix, cell_from_point(q.x, q.y, ix.leaf_level));
         }
       } else if (c & kDirLink) {
-        const double2 q = __ldg(pts + i);  // cheaper to re-read than to queue the coordinates
-        uint32_t x, y;
-        grid_xy(q.x, q.y, &x, &y);
-        const uint32_t leaf_keep = ~((1u << (30 - ix.leaf_level)) - 1u);  // cell_id.cpp:93-94
-        entry = walk_from(ix, c & ~kDirLink, ix.prefix_level0 + 4 * tb.chunks, (x & leaf_keep) << 2,
-                          (y & leaf_keep) << 2);
+        const int walk_level = ix.prefix_level0 + 4 * tb.chunks;
+        uint64_t node = c & ~kDirLink;
+        int level = walk_level;
+        bool walk = true;
+        if (ix.qc.packed) {  // the word is the arena slot under the link: (node - 1) * 256 + slot
+          entry = ld_arena(ix.arena + node);
+          walk = (entry & 3u) == 0u && entry != 0u;  // a link again: deeper than the queued bits reach
+          node = entry >> 2;
+          level += 4;
+        }
+        if (walk) {
+          const double2 q = __ldg(pts + i);
+          uint32_t x, y;
+          grid_xy(q.x, q.y, &x, &y);
+          const uint32_t leaf_keep = ~((1u << (30 - ix.leaf_level)) - 1u);  // cell_id.cpp:93-94
+          entry = walk_from(ix, node, level, (x & leaf_keep) << 2, (y & leaf_keep) << 2);
+        }
       } else if (c & kDirInline) {
         entry = (static_cast<uint64_t>(c & 0x3FFFFFFFu) << 2) | 1u;  // exact-mode candidate
       } else {
@@ -442,6 +457,7 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
   uint32_t batch_take = 0;      // its size
   uint32_t batch_point = 0;     // point | slow of this lane's item
   uint32_t batch_code = 0;      // the gather in flight
+  uint32_t batch_slot = 0;      // packed coding: the node slot under a link
 
   auto settle_batch = [&]() {
     if (!batch_open) return;
@@ -449,7 +465,9 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
     const bool mine = lane < batch_take;
     const bool lookup = mine && (batch_point & 0x80000000u) == 0u;
     const bool done = settle(batch_code, lookup, batch_point);
-    q3_count = enqueue(s_q3, q3_count, mine && !done, batch_point, batch_code);
+    uint32_t fwd = batch_code;
+    if (ix.qc.packed && (fwd & kDirLink)) fwd = kDirLink | (((fwd & ~kDirLink) - 1u) * kNodeSlots + batch_slot);
+    q3_count = enqueue(s_q3, q3_count, mine && !done, batch_point, fwd);
 #ifdef GJ_EXP_NO_PHASE3  // timing experiment: results are wrong
     q3_count = 0;
 #endif
@@ -462,7 +480,13 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
     __syncwarp();
     batch_take = take;
     batch_point = item.x;
-    batch_code = ldg32_if(table2 + item.y, lane < take && (item.x & 0x80000000u) == 0u, 0u);
+    uint32_t idx = item.y;
+    if (ix.qc.packed) {  // (Y << xbits) | X at level tb.level + 4, see DevQueueCoding
+      const uint32_t X = item.y & (qc_mul - 1u), Y = item.y >> ix.qc.xbits;
+      idx = (Y >> 4) * tb.pitch + (X >> 4);
+      batch_slot = (spread4(Y & ix.qc.sub_mask) << 1) | spread4(X & ix.qc.sub_mask);  // chunk_slot
+    }
+    batch_code = ldg32_if(table2 + idx, lane < take && (item.x & 0x80000000u) == 0u, 0u);
     batch_open = true;
   };
 
@@ -477,8 +501,21 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
 
   constexpr uint32_t kTile = kJoinThreads * kPointsPerThread;
   const uint32_t n_tiles = (n + kTile - 1) / kTile;
+  // Pull this warp's chunk of a tile the CTA will reach kPrefetchTiles tile
+  // periods from now into L2 (one bulk prefetch per warp): its loads then pay
+  // L2 latency instead of DRAM latency.
+  auto prefetch_chunk = [&](uint32_t t) {  // t * kTile < 2^32: n < 2^31 and t stays within a few grids of n_tiles
+    const uint32_t first = t * kTile + warp * kChunkPoints;
+    if (kPrefetchTiles != 0 && lane == 0 && first < n) {
+      const uint32_t bytes = min(static_cast<uint32_t>(kChunkPoints), n - first) * 16u;
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pts + first), "r"(bytes) : "memory");
+    }
+  };
+#pragma unroll 1
+  for (uint32_t k = 0; k < kPrefetchTiles; ++k) prefetch_chunk(blockIdx.x + k * gridDim.x);
   for (uint32_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
     const uint32_t base = tile * kTile + warp * kChunkPoints + lane;  // point of slot j: base + 32 j
+    prefetch_chunk(tile + kPrefetchTiles * gridDim.x);
     double2 p[kPointsPerThread];
 #pragma unroll
     for (int j = 0; j < kPointsPerThread; ++j) {
@@ -491,7 +528,7 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
     for (int j = 0; j < kPointsPerThread; ++j) {
       const uint32_t i = base + j * 32u;
       const bool live = i < n;
-      uint32_t x, y;
+      uint32_t x, y;  // left-aligned to 32 bits
       const bool ok = grid_xy_try(p[j].x, p[j].y, &x, &y) && live;  // valid, coordinates exact
       const uint32_t cx = min((x >> d1_shift) - d1_x0, d1_w);  // clamps into the all-miss padding
       const uint32_t cy = min((y >> d1_shift) - d1_y0, d1_h);
@@ -499,8 +536,8 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
       const uint32_t e = lds16(s_table + (cy * d1_pitch + cx) * 2u) - 1u;
       const bool emit = ok && e < 0xFFFEu && (e & need_interior) == need_interior;
       const uint32_t id = e >> 1;
-      if (kDense) {
-        red_inc_shared_if(hist.smem + (id * hist.rep + hist.lane_rep) * 4u, emit);
+      if (kDense) {  // unconditional: lanes that do not emit count into a spare row past the last slot
+        red_inc_shared_if(hist.smem + ((emit ? id : hist_spare) * hist.rep + hist.lane_rep) * 4u, true);
       } else if (emit) {
         count_slot<kDense>(ix, jp, hist, id);
       }
@@ -519,11 +556,11 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
 #ifdef GJ_EXP_PHASE1_ONLY  // timing experiment: results are wrong
       continue;
 #endif
-      // what stays open is queued with its cell's index in the 32-bit tier
-      const uint32_t cx2 = min((x >> d2_shift) - d2_x0, d2_w);
-      const uint32_t cy2 = min((y >> d2_shift) - d2_y0, d2_h);
+      // what stays open is queued with its position in the 32-bit tier (DevQueueCoding)
+      const uint32_t qx = min((x >> qc_shift) - qc_x0, qc_xc);
+      const uint32_t qy = min((y >> qc_shift) - qc_y0, qc_yc);
       const bool open = live && !emit && !(ok && e == 0xFFFFFFFFu);
-      q2_count = enqueue(s_q2, q2_count, open, ok ? i : i | 0x80000000u, cy2 * d2_pitch + cx2);
+      q2_count = enqueue(s_q2, q2_count, open, ok ? i : i | 0x80000000u, qy * qc_mul + qx);
     }
     drain2(false);
   }
