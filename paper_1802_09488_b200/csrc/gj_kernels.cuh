@@ -376,8 +376,9 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
         uint64_t node = c & ~kDirLink;
         int level = walk_level;
         bool walk = true;
-        if (ix.qc.packed) {  // the word is the arena slot under the link: (node - 1) * 256 + slot
-          entry = ld_arena(ix.arena + node);
+        if (ix.qc.packed) {  // the word is (node - 1) * 256 + (y sub-cell bits << 4 | x sub-cell bits)
+          const uint32_t slot = (spread4((c >> 4) & 0xFu) << 1) | spread4(c & 0xFu);  // chunk_slot
+          entry = ld_arena(ix.arena + ((node & ~0xFFull) | slot));
           walk = (entry & 3u) == 0u && entry != 0u;  // a link again: deeper than the queued bits reach
           node = entry >> 2;
           level += 4;
@@ -484,7 +485,7 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
     if (ix.qc.packed) {  // (Y << xbits) | X at level tb.level + 4, see DevQueueCoding
       const uint32_t X = item.y & (qc_mul - 1u), Y = item.y >> ix.qc.xbits;
       idx = (Y >> 4) * tb.pitch + (X >> 4);
-      batch_slot = (spread4(Y & ix.qc.sub_mask) << 1) | spread4(X & ix.qc.sub_mask);  // chunk_slot
+      batch_slot = ((Y & ix.qc.sub_mask) << 4) | (X & ix.qc.sub_mask);  // spread into a node slot in population 3
     }
     batch_code = ldg32_if(table2 + idx, lane < take && (item.x & 0x80000000u) == 0u, 0u);
     batch_open = true;
@@ -505,10 +506,10 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
   // periods from now into L2 (one bulk prefetch per warp): its loads then pay
   // L2 latency instead of DRAM latency.
   auto prefetch_chunk = [&](uint32_t t) {  // t * kTile < 2^32: n < 2^31 and t stays within a few grids of n_tiles
-    const uint32_t first = t * kTile + warp * kChunkPoints;
-    if (kPrefetchTiles != 0 && lane == 0 && first < n) {
-      const uint32_t bytes = min(static_cast<uint32_t>(kChunkPoints), n - first) * 16u;
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(pts + first), "r"(bytes) : "memory");
+    // per-lane line prefetches (the bulk form wants warp-uniform operands, which costs a uniformity loop)
+    const uint32_t at = t * kTile + warp * kChunkPoints + lane * 8u;  // 8 points = one 128-byte line
+    if (kPrefetchTiles != 0 && lane < kChunkPoints / 8u && at < n) {
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(pts + at) : "memory");
     }
   };
 #pragma unroll 1
