@@ -151,39 +151,6 @@ __device__ __forceinline__ uint32_t grid_coord(double value, double lo, double s
   return cell >= (1u << 30) ? (1u << 30) - 1u : cell;
 }
 
-// grid_coord for both axes without the division in the common case.
-//
-// Reference value: cell = trunc(s), s = RN(d / span) * 2^30, d = RN(v - lo).
-// Here p = RN(d * R) with R = RN(2^30 / span), so |p - s| <= 3.01 * 2^-53 * 2^30
-// < 3.6e-7.  Adding 2^31 puts p in [2^31, 2^32), where the double's 52
-// mantissa bits ARE the fixed-point number k = RN(p * 2^21) (|k 2^-21 - p| <=
-// 2^-22): integer part k >> 21, 21 fraction bits below.  Hence
-// |k 2^-21 - s| < 6.0e-7 = 1.26 * 2^-21, and whenever the fraction field f
-// satisfies 2 <= f <= 2^21 - 3 the integer part equals trunc(s) exactly
-// (and is < 2^30, so the upper clamp cannot bind).
-// Otherwise (probability 5 * 2^-21 per axis, and always for points on a grid
-// line or on the +90/+180 edge) the caller falls back to grid_coord().
-__device__ __forceinline__ bool grid_xy_fast(double lat, double lng, uint32_t* x, uint32_t* y) {
-  const double rx = 1073741824.0 / 360.0;  // RN(2^30 / 360), folded at compile time
-  const double ry = 1073741824.0 / 180.0;
-  const double tx = __dadd_rn(__dmul_rn(__dsub_rn(lng, -180.0), rx), 2147483648.0);
-  const double ty = __dadd_rn(__dmul_rn(__dsub_rn(lat, -90.0), ry), 2147483648.0);
-  const uint32_t xl = static_cast<uint32_t>(__double2loint(tx)), xh = static_cast<uint32_t>(__double2hiint(tx));
-  const uint32_t yl = static_cast<uint32_t>(__double2loint(ty)), yh = static_cast<uint32_t>(__double2hiint(ty));
-  *x = __funnelshift_l(xl, xh, 11);  // (hi << 11) | (lo >> 21): exponent bits fall off, bit 31 stays 0
-  *y = __funnelshift_l(yl, yh, 11);
-  const uint32_t fx = ((xl & 0x1FFFFFu) - 2u), fy = ((yl & 0x1FFFFFu) - 2u);
-  return max(fx, fy) <= 0x1FFFFFu - 4u;  // both fractions inside [2, 2^21 - 3]
-}
-
-// Both grid coordinates of a valid point, bit-exact (fast path + fallback).
-__device__ __forceinline__ void grid_xy(double lat, double lng, uint32_t* x, uint32_t* y) {
-  if (!grid_xy_fast(lat, lng, x, y)) {  // within 2^-20 of a cell boundary: do the division
-    *x = grid_coord(lng, -180.0, 360.0);
-    *y = grid_coord(lat, -90.0, 180.0);
-  }
-}
-
 // Grid coordinates of ANY pair of doubles, branch-free, two DFMAs: true means
 // the point is valid (latlng.hpp:31-34) AND (*x32, *y32) are its exact grid
 // coordinates, left-aligned to 32 bits ((x << 2) | two fraction bits, so
@@ -219,6 +186,19 @@ __device__ __forceinline__ bool grid_xy_try(double lat, double lng, uint32_t* x3
   const uint32_t fx = ((xl & 0x1FFFFFu) - 2u), fy = ((yl & 0x1FFFFFu) - 2u);
   const uint32_t range = (xh ^ 0x41E00000u) | (yh ^ 0x41E00000u);
   return (range < (1u << 19)) & (max(fx, fy) <= 0x1FFFFFu - 4u);
+}
+
+// Both grid coordinates (30 bits each) of a valid point, bit-exact: the fast
+// path above, else the reference's own arithmetic.
+__device__ __forceinline__ void grid_xy(double lat, double lng, uint32_t* x, uint32_t* y) {
+  uint32_t x32, y32;
+  if (grid_xy_try(lat, lng, &x32, &y32)) {
+    *x = x32 >> 2;
+    *y = y32 >> 2;
+  } else {  // within 2^-20 of a cell boundary (or on the +90 / +180 edge): do the division
+    *x = grid_coord(lng, -180.0, 360.0);
+    *y = grid_coord(lat, -90.0, 180.0);
+  }
 }
 
 // spread_bits (cell_id.cpp:30-37): bit i of the low 30 bits moves to bit 2i.

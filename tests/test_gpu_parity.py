@@ -183,12 +183,18 @@ def test_cell_ids_adversarial_grid_lines_vs_oracle():
         k = rng.integers(0, (1 << level) + 1, 40000)
         lat = k / float(1 << level) * 180.0 - 90.0
         lng = k[::-1] / float(1 << level) * 360.0 - 180.0
-        for ulps in (0, 1, 2, 3, -1, -2, -3):
+        for ulps in (0, 1, 2, 3, 4, 7, -1, -2, -3, -4, -7):
             a, o = lat.copy(), lng.copy()
             for _ in range(abs(ulps)):
                 a = np.nextafter(a, np.inf if ulps > 0 else -np.inf)
                 o = np.nextafter(o, np.inf if ulps > 0 else -np.inf)
             pts.append(np.stack([np.clip(a, -90.0, 90.0), np.clip(o, -180.0, 180.0)], axis=1))
+    edge_lat = np.array([90.0, -90.0, 0.0, -0.0, 5e-324, -5e-324, 1e-300, np.nextafter(90.0, 0.0),
+                         np.nextafter(-90.0, 0.0), 89.99999999999999, 45.0, 1e-17])
+    edge_lng = np.array([180.0, -180.0, -0.0, 0.0, -5e-324, 5e-324, -1e-300, np.nextafter(180.0, 0.0),
+                         np.nextafter(-180.0, 0.0), 179.99999999999997, -135.0, -1e-17])
+    pts.append(np.stack([np.repeat(edge_lat, len(edge_lng)), np.tile(edge_lng, len(edge_lat))], axis=1))
+    pts.append(np.stack([rng.uniform(-1e-7, 1e-7, 200_000), rng.uniform(-1e-7, 1e-7, 200_000)], axis=1))
     pts.append(np.stack([rng.uniform(-90, 90, 2_000_000), rng.uniform(-180, 180, 2_000_000)], axis=1))
     pts.append(np.stack([rng.uniform(40.5, 40.95, 2_000_000), rng.uniform(-74.25, -73.70, 2_000_000)], axis=1))
     pts = np.concatenate(pts)

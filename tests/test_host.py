@@ -123,3 +123,57 @@ def test_ring_is_simple_rejects_bowtie():
     bow = np.array([[0.0, 0.0], [1.0, 1.0], [0.0, 1.0], [1.0, 0.0]])
     assert not synth.ring_is_simple(bow)
     assert synth.ring_is_simple(np.array([[0.0, 0.0], [0.0, 1.0], [1.0, 1.0], [1.0, 0.0]]))
+
+
+def _fma_exact(v: float, r: float, c: float) -> float:
+    """RN(v*r + c) with one rounding, like the device fma: exact rational
+    arithmetic, then Fraction -> float (correctly rounded int true division)."""
+    from fractions import Fraction
+    return float(Fraction(v) * Fraction(r) + Fraction(c))
+
+
+def test_fast_grid_coordinates_claim():
+    """The arithmetic claim behind csrc/gj_device.cuh::grid_xy_try, checked on
+    the CPU without any CUDA: t = fma(v, RN(2^30/span), 2^31 + 2^29); whenever t
+    has exponent 0x41E with a clear top mantissa bit and its 21-bit fraction
+    field lies in [2, 2^21 - 3], v is inside [lo, hi] and the 30 bits above the
+    fraction are exactly trunc(((v - lo) / span) * 2^30) as the reference
+    computes it (cell_id.cpp:50-56); otherwise the fast path must refuse."""
+    import struct
+    rng = np.random.default_rng(0xF4A)
+    accepted = refused = 0
+    for lo, span in ((-90.0, 180.0), (-180.0, 360.0)):
+        hi = lo + span
+        r = 1073741824.0 / span
+        vals = []
+        for level in (30, 27, 24, 16, 3):
+            k = rng.integers(0, (1 << level) + 1, 300)
+            base = k / float(1 << level) * span + lo
+            for ulps in range(-4, 5):
+                v = base.copy()
+                for _ in range(abs(ulps)):
+                    v = np.nextafter(v, np.inf if ulps > 0 else -np.inf)
+                vals.append(v)
+        vals.append(rng.uniform(lo, hi, 4000))
+        vals.append(rng.uniform(-1e-9, 1e-9, 200))
+        vals.append(np.array([lo, hi, 0.0, -0.0, 5e-324, -5e-324, np.nextafter(hi, np.inf), np.nextafter(lo, -np.inf),
+                              hi + 1.0, lo - 1.0, 1e300, -1e300, np.inf, -np.inf, np.nan]))
+        for v in np.concatenate(vals):
+            v = float(v)
+            valid = lo <= v <= hi  # False for NaN
+            if np.isfinite(v):
+                t = _fma_exact(v, r, 2147483648.0 + 536870912.0)
+            else:
+                t = v * r  # inf / nan propagate
+            bits = struct.unpack("<Q", struct.pack("<d", t))[0]
+            hi_word, frac = bits >> 32, bits & 0x1FFFFF
+            ok = ((hi_word ^ 0x41E00000) >> 19) == 0 and 2 <= frac <= (1 << 21) - 3
+            if not ok:
+                refused += 1
+                continue
+            accepted += 1
+            assert valid, v
+            cell = (bits >> 21) & 0x3FFFFFFF
+            want = int(np.float64(v - lo) / np.float64(span) * np.float64(1073741824.0))  # the reference's order
+            assert cell == min(want, (1 << 30) - 1), (v, cell, want)
+    assert accepted > 5000 and refused > 2000
