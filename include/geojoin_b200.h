@@ -167,6 +167,20 @@ GJ_API int gj_probe_points_host(gj_session* s, const double* latlng, uint64_t n,
 GJ_API int gj_probe_cells_host(gj_session* s, const uint64_t* raw_ids, uint64_t n,
                                uint64_t* out_entries);
 
+/* ---- training pre-pass: the probe half of Act::train (act.cpp:414-440) ----
+ * Finds the points whose probe lands in a candidate-bearing cell, i.e. for
+ * which the reference's `any_candidate` is true: the only points Act::train
+ * does split work for, and the numerator of TrainingStats::expensive_fraction_*.
+ * Writes their global indices (base_index + i), ascending, into
+ * out_indices[0 .. min(cap, *n_candidates)); *n_candidates is always the total
+ * (so expensive_fraction = *n_candidates / n; call with cap = 0 to size).
+ * A point that hits no candidate cell now never does after further training
+ * (splits only refine candidate cells), so the list is a valid work list for
+ * the whole training pass.  An invalid point returns GJ_INVALID_POINT. */
+GJ_API int gj_training_candidates_host(gj_session* s, const double* latlng, uint64_t n,
+                                       uint64_t base_index, uint64_t* out_indices, uint64_t cap,
+                                       uint64_t* n_candidates, uint64_t* bad_index);
+
 /* ---- streaming join: per-polygon counts (+ first id per point) ----------
  * ≙ join_count_per_polygon / run_join with a counting emit.
  *   counts[n_ids]   ADDED to (caller zeroes); slot order = gj_index_ids.

@@ -10,6 +10,9 @@
 //   accumulate_probe_stats          include/geojoin/join.hpp:153-154, src/join.cpp:287-290
 //   collect_metrics                 include/geojoin/join.hpp:148-149, src/join.cpp:309-314
 //
+// plus the probe half of Act::train (src/act.cpp:414-440) as a pre-pass:
+// training_candidates / expensive_fraction.
+//
 // so a call site switches by replacing `geojoin::` with `geojoin::gpu::` and
 // handing over a DeviceIndex made once from its IndexBundle.  Errors come back
 // as the reference's exception types.  Header-only; link libgeojoin_b200.so.
@@ -209,6 +212,28 @@ inline IndexMetrics collect_metrics(const DeviceIndex& ix, std::span<const LatLn
   JoinStats stats;
   accumulate_probe_stats(ix, points, stats);
   return metrics_from_stats(stats, ix.info().node_count);
+}
+
+// The training points Act::train has split work for (src/act.cpp:428-440):
+// those whose probe meets at least one candidate reference, ascending.  A point
+// that meets none now meets none after any amount of training (splits only
+// refine candidate cells), so train() may iterate over this list instead of
+// probing every point.
+inline std::vector<size_t> training_candidates(const DeviceIndex& ix, std::span<const LatLng> points) {
+  std::vector<uint64_t> idx(points.size());
+  uint64_t found = 0, bad = 0;
+  detail::check(gj_training_candidates_host(ix.session(), detail::as_doubles(points), points.size(), 0, idx.data(),
+                                            idx.size(), &found, &bad));
+  return std::vector<size_t>(idx.begin(), idx.begin() + static_cast<std::ptrdiff_t>(found));
+}
+
+// TrainingStats::expensive_fraction_{before,after} (src/act.cpp:414-426).
+inline double expensive_fraction(const DeviceIndex& ix, std::span<const LatLng> points) {
+  if (points.empty()) return 0.0;
+  uint64_t found = 0, bad = 0;
+  detail::check(gj_training_candidates_host(ix.session(), detail::as_doubles(points), points.size(), 0, nullptr, 0,
+                                            &found, &bad));
+  return static_cast<double>(found) / static_cast<double>(points.size());
 }
 
 }  // namespace geojoin::gpu

@@ -208,6 +208,50 @@ int gjo_decode(const gjo_index* ix, uint64_t entry, uint32_t* ids,
   return n > cap ? GJO_CAPACITY : GJO_OK;
 }
 
+/* The probe half of Act::train (act.cpp:414-440): per point, probe at the
+ * maximum indexed level and ask whether any reference of the entry is a
+ * candidate (for_each_reference with !interior).  flags[i] = 0 / 1;
+ * *n_flagged counts the ones (expensive_fraction = n_flagged / n). */
+int gjo_training_candidates(const gjo_index* ix, const double* latlng,
+                            uint64_t n, uint8_t* flags, uint64_t* n_flagged,
+                            uint64_t* bad_index) {
+  const int level = ix->k_max / 2; /* max_indexed_level, act.hpp:148 */
+  uint64_t count = 0;
+  for (uint64_t i = 0; i < n; ++i) {
+    uint64_t raw, e = 0;
+    int rc = gjo_cell_from_point(latlng[2 * i], latlng[2 * i + 1], level, &raw);
+    if (rc == GJO_OK) rc = gjo_probe(ix, raw, &e, NULL);
+    if (rc != GJO_OK) {
+      if (bad_index) *bad_index = i;
+      return rc;
+    }
+    int any_candidate = 0;
+    switch (e & 3) {
+      case 0:
+        break;
+      case 1:
+        any_candidate = ((e >> 2) & 1) == 0;
+        break;
+      case 2:
+        any_candidate = ((e >> 33) & 1) == 0 || ((e >> 2) & 1) == 0;
+        break;
+      default: {
+        const uint64_t off = (e >> 2) & 0x7fffffffu;
+        if (!record_in_bounds(ix, off)) {
+          if (bad_index) *bad_index = i;
+          return GJO_CORRUPT_INDEX;
+        }
+        any_candidate = ix->lut[off + 1 + ix->lut[off]] != 0;
+        break;
+      }
+    }
+    if (flags) flags[i] = (uint8_t)any_candidate;
+    count += (uint64_t)any_candidate;
+  }
+  if (n_flagged) *n_flagged = count;
+  return GJO_OK;
+}
+
 /* geometry.cpp:63-75; x = lng, y = lat (geometry.cpp:35). */
 double gjo_point_segment_dist_sq(double px, double py, double ax, double ay,
                                  double bx, double by) {

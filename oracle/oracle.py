@@ -190,6 +190,19 @@ class OracleIndex:
             raise OracleError(rc, bad.value)
         return out
 
+    def training_candidates(self, points) -> np.ndarray:
+        """Ascending indices of the points Act::train would do split work for."""
+        p = _pts(points)
+        flags = np.zeros(len(p), np.uint8)
+        bad, cnt = C.c_uint64(0), C.c_uint64(0)
+        rc = lib().gjo_training_candidates(C.byref(self._s), _p(p), C.c_uint64(len(p)), _p(flags), C.byref(cnt),
+                                           C.byref(bad))
+        if rc:
+            raise OracleError(rc, bad.value)
+        idx = np.flatnonzero(flags).astype(np.uint64)
+        assert len(idx) == cnt.value
+        return idx
+
     def decode(self, entry: int):
         ids = np.empty(4096, np.uint32)
         inter = np.empty(4096, np.uint8)

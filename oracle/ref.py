@@ -331,6 +331,13 @@ class RefBundle:
             _check(int(m))
         return {int(ids[k]): int(cnt[k]) for k in range(min(m, cap))}
 
+    def training_candidates(self, points) -> np.ndarray:
+        """Indices of the points for which Act::train's any_candidate is true."""
+        p = _pts(points)
+        flags = np.zeros(len(p), np.uint8)
+        _check(lib().ref_training_candidates(self._h, _p(p), C.c_uint64(len(p)), _p(flags)))
+        return np.flatnonzero(flags).astype(np.uint64)
+
     def accumulate_probe_stats(self, points, stats=None) -> np.ndarray:
         p = _pts(points)
         s = np.zeros(6, np.uint64) if stats is None else np.ascontiguousarray(stats, np.uint64)

@@ -463,6 +463,25 @@ int64_t ref_join_exact_count_threads(const void* h, const double* latlng,
   return rc == kOk ? m : rc;
 }
 
+// The `any_candidate` test Act::train applies to every training point
+// (act.cpp:414-440), through the reference's own probe / for_each_reference.
+int ref_training_candidates(const void* h, const double* latlng, uint64_t n,
+                            uint8_t* out_flags) {
+  return guarded([&] {
+    const Act& act = static_cast<const IndexBundle*>(h)->act();
+    const auto pts = as_points(latlng, n);
+    const int level = act.max_indexed_level();
+    for (uint64_t i = 0; i < n; ++i) {
+      const uint64_t e = act.probe(cell_from_point(pts[i], level));
+      bool any_candidate = false;
+      act.for_each_reference(e, [&](uint32_t, bool interior) {
+        if (!interior) any_candidate = true;
+      });
+      out_flags[i] = any_candidate ? 1 : 0;
+    }
+  });
+}
+
 int ref_accumulate_probe_stats(const void* h, const double* latlng, uint64_t n,
                                uint64_t stats[6]) {
   return guarded([&] {

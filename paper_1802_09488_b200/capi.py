@@ -24,7 +24,7 @@ EXPORTS = [
     "gj_index_get_info", "gj_index_ids", "gj_session_create", "gj_session_destroy", "gj_session_stream",
     "gj_host_alloc", "gj_host_free", "gj_cells_from_points_host", "gj_probe_points_host", "gj_probe_cells_host",
     "gj_join_count_host", "gj_join_count_device", "gj_session_sync", "gj_session_launches",
-    "gj_join_pairs_host", "gj_pairs_copy",
+    "gj_join_pairs_host", "gj_pairs_copy", "gj_training_candidates_host",
 ]
 
 
@@ -110,5 +110,7 @@ def lib():
         L.gj_join_pairs_host.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_int, C.POINTER(C.c_uint64),
                                          C.POINTER(Stats), C.POINTER(C.c_uint64)]
         L.gj_pairs_copy.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+        L.gj_training_candidates_host.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p,
+                                                  C.c_uint64, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
         _LIB = L
     return _LIB

@@ -668,6 +668,60 @@ int gj_probe_points_host(gj_session* s, const double* latlng, uint64_t n, uint64
   return status_to_code(s->h_status[3], bad_index);
 }
 
+int gj_training_candidates_host(gj_session* s, const double* latlng, uint64_t n, uint64_t base_index,
+                                uint64_t* out_indices, uint64_t cap, uint64_t* n_candidates, uint64_t* bad_index) {
+  if (!s || !n_candidates || (n && !latlng) || (cap && !out_indices)) return GJ_INVALID_ARGUMENT;
+  *n_candidates = 0;
+  gj_index& ix = *s->ix;
+  GJ_CUDA(cudaSetDevice(ix.device));
+  const uint64_t chunk = std::min<uint64_t>(4ull << 20, std::max<uint64_t>(n, 1));
+  const uint32_t n_blocks_max = static_cast<uint32_t>((chunk + kScanTile - 1) / kScanTile);
+  GJ_CUDA(s->d_points[0].reserve(chunk * 16));
+  GJ_CUDA(s->d_pair_count.reserve(chunk * 4));
+  GJ_CUDA(s->d_row_ptr.reserve((chunk + 1) * 8));
+  GJ_CUDA(s->d_entries.reserve(chunk * 8));  // the ordered indices of one chunk
+  GJ_CUDA(s->d_block_sums.reserve((static_cast<size_t>(n_blocks_max) + 2) * 8));
+  DevStatus* d_status = s->d_status.as<DevStatus>() + 3;
+  int rc = reset_status(s, d_status);
+  if (rc != GJ_OK) return rc;
+  const size_t smem = align16(std::max<size_t>(ix.dev.dir.n_table * 4, 16));
+  GJ_CUDA(cudaFuncSetAttribute(candidate_flags_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(smem)));
+  uint64_t found = 0;
+  for (uint64_t begin = 0; begin < n; begin += chunk) {
+    const uint64_t len = std::min(chunk, n - begin);
+    const uint32_t n_blocks = static_cast<uint32_t>((len + kScanTile - 1) / kScanTile);
+    const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((len + 255) / 256, ix.sm_count * 4ull));
+    uint32_t* d_flags = s->d_pair_count.as<uint32_t>();
+    uint64_t* d_sums = s->d_block_sums.as<uint64_t>();
+    uint64_t* d_total = d_sums + n_blocks_max + 1;
+    GJ_CUDA(cudaMemcpyAsync(s->d_points[0].ptr, latlng + 2 * begin, len * 16, cudaMemcpyHostToDevice, s->stream));
+    candidate_flags_kernel<<<grid, 256, smem, s->stream>>>(ix.dev, s->d_points[0].as<double2>(), len,
+                                                           base_index + begin, d_flags, d_status);
+    scan_block_sums_kernel<<<n_blocks, kScanThreads, 0, s->stream>>>(d_flags, len, d_sums);
+    scan_sums_kernel<<<1, kScanThreads, 0, s->stream>>>(d_sums, n_blocks, d_total);
+    scan_apply_kernel<<<n_blocks, kScanThreads, 0, s->stream>>>(d_flags, len, d_sums, s->d_row_ptr.as<uint64_t>());
+    candidate_scatter_kernel<<<grid, 256, 0, s->stream>>>(d_flags, s->d_row_ptr.as<uint64_t>(), len,
+                                                          base_index + begin, s->d_entries.as<uint64_t>());
+    s->launches += 5;
+    GJ_CUDA(cudaGetLastError());
+    uint64_t total = 0;
+    GJ_CUDA(cudaMemcpyAsync(&total, d_total, 8, cudaMemcpyDeviceToHost, s->stream));
+    GJ_CUDA(cudaStreamSynchronize(s->stream));
+    const uint64_t room = cap > found ? cap - found : 0;
+    const uint64_t take = std::min(total, room);
+    if (take) {
+      GJ_CUDA(cudaMemcpyAsync(out_indices + found, s->d_entries.ptr, take * 8, cudaMemcpyDeviceToHost, s->stream));
+      GJ_CUDA(cudaStreamSynchronize(s->stream));
+    }
+    found += total;
+  }
+  GJ_CUDA(cudaMemcpyAsync(&s->h_status[3], d_status, sizeof(DevStatus), cudaMemcpyDeviceToHost, s->stream));
+  GJ_CUDA(cudaStreamSynchronize(s->stream));
+  *n_candidates = found;
+  return status_to_code(s->h_status[3], bad_index);
+}
+
 int gj_cells_from_points_host(gj_session* s, const double* latlng, uint64_t n, int level, uint64_t* out_raw,
                               uint64_t* bad_index) {
   if (!s || (n && (!latlng || !out_raw))) return GJ_INVALID_ARGUMENT;

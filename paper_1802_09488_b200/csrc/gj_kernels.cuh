@@ -595,6 +595,49 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
   }
 }
 
+// Does the entry hold at least one candidate (non-interior) reference?  The
+// test Act::train applies to every training point (act.cpp:414-440).
+__device__ __forceinline__ bool entry_has_candidate(const DevIndex& ix, uint64_t e) {
+  const uint32_t tag = static_cast<uint32_t>(e) & 3u;
+  if (e == 0 || tag == 0u) return false;
+  if (tag == 1u) return ((e >> 2) & 1u) == 0u;
+  if (tag == 2u) return ((e >> 33) & 1u) == 0u || ((e >> 2) & 1u) == 0u;
+  const uint32_t off = static_cast<uint32_t>(e >> 2) & 0x7fffffffu;  // [t, ids, c, ids]
+  return __ldg(ix.lut + off + 1u + __ldg(ix.lut + off)) != 0u;
+}
+
+// Training pre-pass: flag[i] = 1 when point i probes into a candidate-bearing
+// cell, else 0 (as u32, ready for the exclusive scan that orders the output).
+__global__ void __launch_bounds__(256)
+candidate_flags_kernel(const __grid_constant__ DevIndex ix, const double2* __restrict__ pts, uint64_t n,
+                       uint64_t base_index, uint32_t* __restrict__ flags, DevStatus* status) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  uint32_t* s_table = reinterpret_cast<uint32_t*>(smem);
+  for (uint32_t i = threadIdx.x; i < ix.dir.n_table; i += blockDim.x) s_table[i] = __ldg(ix.dir.table + i);
+  __syncthreads();
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const double2 p = __ldcs(pts + i);
+    uint32_t f = 0;
+    if (latlng_valid(p.x, p.y)) {
+      f = entry_has_candidate(ix, probe_point(ix, s_table, p.x, p.y)) ? 1u : 0u;
+    } else {
+      flag_error(status, kErrInvalidPoint, base_index + i);
+    }
+    flags[i] = f;
+  }
+}
+
+// out[offset[i]] = base_index + i for every flagged point (offsets from the scan).
+__global__ void __launch_bounds__(256)
+candidate_scatter_kernel(const uint32_t* __restrict__ flags, const uint64_t* __restrict__ offset, uint64_t n,
+                         uint64_t base_index, uint64_t* __restrict__ out) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) {
+    if (flags[i]) out[offset[i]] = base_index + i;
+  }
+}
+
 // Entries only: bitwise Act::probe(cell_from_point(p, k_max/2)).
 __global__ void __launch_bounds__(256)
 probe_points_kernel(const __grid_constant__ DevIndex ix, const double2* __restrict__ pts, uint64_t n,

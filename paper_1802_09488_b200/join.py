@@ -238,6 +238,18 @@ class Session:
         _check(capi.lib().gj_probe_cells_host(self._h, _vp(r), len(r), _vp(out)))
         return out
 
+    # ---- training pre-pass ----
+    def training_candidates(self, points, base_index: int = 0) -> np.ndarray:
+        """Ascending global indices of the points whose probe lands in a
+        candidate-bearing cell: the `any_candidate` test of Act::train
+        (src/act.cpp:414-440)."""
+        p = _points(points)
+        out = np.empty(len(p), np.uint64)
+        found, bad = C.c_uint64(0), C.c_uint64(0)
+        _check(capi.lib().gj_training_candidates_host(self._h, _vp(p), len(p), C.c_uint64(base_index), _vp(out),
+                                                      C.c_uint64(len(out)), C.byref(found), C.byref(bad)), bad)
+        return out[:found.value].copy()
+
     # ---- streaming join ----
     def join_count(self, points, mode=capi.GJ_MODE_BUNDLE, stats: JoinStats | None = None,
                    want_ids: bool = False, base_index: int = 0, overflow_capacity: int | None = None):
@@ -347,3 +359,16 @@ def collect_metrics(bundle: IndexBundle, points) -> IndexMetrics:
     s = JoinStats()
     accumulate_probe_stats(bundle, points, s)
     return metrics_from_stats(s, int(bundle.info.node_count))
+
+
+def training_candidates(bundle: IndexBundle, points) -> np.ndarray:
+    """The work list of Act::train (src/act.cpp:414-440): indices of the
+    training points that hit a cell with at least one candidate reference."""
+    return bundle.session().training_candidates(points)
+
+
+def expensive_fraction(bundle: IndexBundle, points) -> float:
+    """TrainingStats::expensive_fraction_before/after (src/act.cpp:414-426):
+    share of the points whose probe meets a candidate reference; 0 for no points."""
+    p = _points(points)
+    return 0.0 if len(p) == 0 else len(training_candidates(bundle, p)) / len(p)

@@ -73,6 +73,20 @@ void compare(const IndexBundle& bundle, const std::vector<LatLng>& points) {
   EXPECT(cm.tree_nodes == gm.tree_nodes && cm.false_hit_fraction == gm.false_hit_fraction &&
          cm.solely_true_hit_fraction == gm.solely_true_hit_fraction && cm.avg_candidates == gm.avg_candidates);
 
+  // the probe half of Act::train (act.cpp:414-440) as a pre-pass: the work list and expensive_fraction
+  std::vector<size_t> want_candidates;
+  for (size_t i = 0; i < points.size(); ++i) {
+    const uint64_t e = bundle.act().probe(cell_from_point(points[i], bundle.act().max_indexed_level()));
+    bool any_candidate = false;
+    bundle.act().for_each_reference(e, [&](uint32_t, bool interior) {
+      if (!interior) any_candidate = true;
+    });
+    if (any_candidate) want_candidates.push_back(i);
+  }
+  EXPECT(gpu::training_candidates(dev, points) == want_candidates);
+  EXPECT(gpu::expensive_fraction(dev, points) ==
+         static_cast<double>(want_candidates.size()) / static_cast<double>(points.size()));
+
   // a single bad coordinate aborts the join with std::invalid_argument on both sides
   std::vector<LatLng> bad = points;
   bad[bad.size() / 2].lat = 91.0;

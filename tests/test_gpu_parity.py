@@ -220,3 +220,37 @@ def test_multi_chunk_inputs_match_oracle():
     assert np.array_equal(ids, pid)
     assert st.as_tuple() == tuple(int(v) for v in ost)
     assert int(row_ptr[-1]) == len(pid) and int(row_ptr[0]) == 0
+
+
+@pytest.mark.parametrize("name", JOIN_FIXTURES)
+def test_training_candidates_match_reference(name):
+    """The training pre-pass (the probe half of Act::train, act.cpp:414-440):
+    ordered indices equal to the compiled reference's fixture; the count equals
+    JoinStats::refinement_entered of the reference's probe pass."""
+    fx, bundle = setup(name)
+    want = golden_util.load("training_candidates")[name].astype(np.uint64)
+    s = bundle.session()
+    got = s.training_candidates(fx["points"])
+    assert np.array_equal(got, want)
+    assert len(got) == int(fx["probe_stats"][4])
+    n = len(fx["points"])
+    assert join.expensive_fraction(bundle, fx["points"]) == (len(want) / n if n else 0.0)
+    # a base index shifts the output; an empty input gives an empty list
+    assert np.array_equal(s.training_candidates(fx["points"][:777], base_index=1 << 33),
+                          want[want < 777] + np.uint64(1 << 33))
+    assert len(s.training_candidates(np.zeros((0, 2)))) == 0
+
+
+def test_training_candidates_multi_chunk_and_errors():
+    fx, bundle = setup("cfg3_tess16_exact_trained")
+    ox = golden_util.oracle_index(fx)
+    rng = np.random.default_rng(0x7A12)
+    lat, lng = fx["points"][:, 0], fx["points"][:, 1]
+    n = 4_300_000  # more than one 4 M-point chunk
+    pts = np.stack([rng.uniform(lat.min(), lat.max(), n), rng.uniform(lng.min(), lng.max(), n)], axis=1)
+    s = bundle.session()
+    assert np.array_equal(s.training_candidates(pts), ox.training_candidates(pts))
+    pts[4_200_123, 0] = np.nan
+    with pytest.raises(join.InvalidArgument) as e:
+        s.training_candidates(pts)
+    assert e.value.index == 4_200_123

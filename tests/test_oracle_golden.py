@@ -191,3 +191,29 @@ def test_oracle_against_live_reference(ref_available):
             opi, opid, ost, _ = ox.join(pts, approx=not exact)
             assert np.array_equal(pi, opi) and np.array_equal(pid, opid) and np.array_equal(st, ost)
         assert ox.join_count(pts, b.approx, 4)[0] == b.join_count(pts, 4)
+
+
+# ---- training pre-pass (act.cpp:414-440) ---------------------------------------------
+@pytest.mark.parametrize("name", JOIN_FIXTURES)
+def test_training_candidates_match_reference_fixture(name):
+    """The oracle's restatement of Act::train's any_candidate test against the
+    indices the compiled reference produced (tests/golden/make_training_golden.py),
+    and against JoinStats::refinement_entered of the same reference run."""
+    fx = golden_util.load(name)
+    want = golden_util.load("training_candidates")[name].astype(np.uint64)
+    got = golden_util.oracle_index(fx).training_candidates(fx["points"])
+    assert np.array_equal(got, want)
+    assert len(got) == int(fx["probe_stats"][4])
+
+
+def test_training_candidates_match_live_reference():
+    from oracle import ref
+    if not ref.available():
+        pytest.skip("oracle/_ref not built")
+    fx = golden_util.load("cfg3_tess16_exact_trained")
+    b = ref.RefBundle.load(golden_util.bundle_file("cfg3_tess16_exact_trained"))
+    rng = np.random.default_rng(0x7A11)
+    lat = fx["points"][:, 0]
+    lng = fx["points"][:, 1]
+    pts = np.stack([rng.uniform(lat.min(), lat.max(), 50_000), rng.uniform(lng.min(), lng.max(), 50_000)], axis=1)
+    assert np.array_equal(golden_util.oracle_index(fx).training_candidates(pts), b.training_candidates(pts))
