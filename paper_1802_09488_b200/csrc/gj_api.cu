@@ -393,12 +393,36 @@ int run_host_join(gj_session* s, const double* latlng, uint64_t n, uint64_t base
 // the pipeline comment in gj_kernels.cuh).  Chunks are processed one after
 // the other; a chunk's pair count is only known after its scan, so the id
 // buffer is sized then.
+// Grow `buf` to at least `want` bytes keeping its first `keep` bytes.
+int grow_keep(gj_session* s, DeviceBuffer& buf, size_t want, size_t keep) {
+  if (want <= buf.bytes) return GJ_OK;
+  void* fresh = nullptr;
+  GJ_CUDA(cudaMalloc(&fresh, want));
+  if (keep) {
+    cudaError_t e = cudaMemcpyAsync(fresh, buf.ptr, keep, cudaMemcpyDeviceToDevice, s->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s->stream);
+    if (e != cudaSuccess) {
+      cudaFree(fresh);
+      return cuda_fail(e, "grow_keep");
+    }
+  }
+  buf.release();
+  buf.ptr = fresh;
+  buf.bytes = want;
+  return GJ_OK;
+}
+
+// Materialised pairs.  Chunks of points go H2D on the copy stream one chunk
+// ahead of the kernels (two point buffers); every chunk's row offsets (with
+// the running global base) and polygon ids are appended to session buffers in
+// HBM, and gj_pairs_copy later copies them straight into the caller's arrays.
 int run_host_pairs(gj_session* s, const double* latlng, uint64_t n, bool exact, gj_stats* stats,
                    uint64_t* bad_index) {
   gj_index& ix = *s->ix;
   GJ_CUDA(cudaSetDevice(ix.device));
-  s->pairs_row_ptr.assign(n + 1, 0);
-  s->pairs_id.clear();
+  s->pairs_valid = false;
+  s->pairs_n = n;
+  s->pairs_total = 0;
   const uint64_t max_cand = std::max<uint64_t>(1, ix.max_cand_refs);
   const uint64_t per_point = 48 + (exact ? max_cand * 13 : 0);
   uint64_t chunk = std::min<uint64_t>(4ull << 20, std::max<uint64_t>(4096, kScratchBudget / per_point));
@@ -415,28 +439,45 @@ int run_host_pairs(gj_session* s, const double* latlng, uint64_t n, bool exact, 
   }
   const uint32_t n_blocks_max = static_cast<uint32_t>((chunk + kScanTile - 1) / kScanTile);
   GJ_CUDA(s->d_points[0].reserve(chunk * 16));
+  GJ_CUDA(s->d_points[1].reserve(chunk * 16));
   GJ_CUDA(s->d_entries.reserve(chunk * 8));
   GJ_CUDA(s->d_nrefs.reserve(chunk * 4));
   GJ_CUDA(s->d_task_base.reserve(chunk * 4));
   GJ_CUDA(s->d_pair_count.reserve(chunk * 4));
-  GJ_CUDA(s->d_row_ptr.reserve((chunk + 1) * 8));
   GJ_CUDA(s->d_block_sums.reserve((static_cast<size_t>(n_blocks_max) + 2) * 8));
   GJ_CUDA(s->d_stats.reserve(6 * 8));
+  GJ_CUDA(s->d_all_row_ptr.reserve((n + 1) * 8));
+  GJ_CUDA(s->d_all_ids.reserve(std::max<uint64_t>(n + n / 4, 1024) * 4));  // grows when a chunk needs more
   GJ_CUDA(cudaMemsetAsync(s->d_stats.ptr, 0, 6 * 8, s->stream));
   DevStatus* d_status = s->d_status.as<DevStatus>() + 3;
   const size_t probe_smem = align16(std::max<size_t>(ix.dev.dir.n_table * 4, 16));
   GJ_CUDA(cudaFuncSetAttribute(probe_points_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(probe_smem)));
   const unsigned wide = static_cast<unsigned>(ix.sm_count) * 8u;
+  uint64_t* d_row_all = s->d_all_row_ptr.as<uint64_t>();
 
-  for (uint64_t begin = 0; begin < n; begin += chunk) {
+  auto copy_in = [&](uint64_t begin, int b) -> int {  // chunk at `begin` -> point buffer b, on the copy stream
+    const uint64_t len = std::min(chunk, n - begin);
+    GJ_CUDA(cudaStreamWaitEvent(s->copy_in, s->ev_done[b], 0));  // the kernels that read buffer b last
+    GJ_CUDA(cudaMemcpyAsync(s->d_points[b].ptr, latlng + 2 * begin, len * 16, cudaMemcpyHostToDevice, s->copy_in));
+    GJ_CUDA(cudaEventRecord(s->ev_in[b], s->copy_in));
+    return GJ_OK;
+  };
+  GJ_CUDA(cudaEventRecord(s->ev_done[0], s->stream));
+  GJ_CUDA(cudaEventRecord(s->ev_done[1], s->stream));
+  if (n && (rc = copy_in(0, 0)) != GJ_OK) return rc;
+
+  uint64_t id_base = 0;
+  int b = 0;
+  for (uint64_t begin = 0; begin < n; begin += chunk, b ^= 1) {
     const uint64_t len = std::min(chunk, n - begin);
     const uint32_t n_blocks = static_cast<uint32_t>((len + kScanTile - 1) / kScanTile);
-    GJ_CUDA(cudaMemcpyAsync(s->d_points[0].ptr, latlng + 2 * begin, len * 16, cudaMemcpyHostToDevice, s->stream));
+    if (begin + chunk < n && (rc = copy_in(begin + chunk, b ^ 1)) != GJ_OK) return rc;
+    GJ_CUDA(cudaStreamWaitEvent(s->stream, s->ev_in[b], 0));
     if ((rc = reset_status(s, d_status)) != GJ_OK) return rc;
+    const double2* d_pts = s->d_points[b].as<double2>();
     probe_points_kernel<<<static_cast<unsigned>(std::min<uint64_t>((len + 255) / 256, ix.sm_count * 4ull)), 256,
-                          probe_smem, s->stream>>>(ix.dev, s->d_points[0].as<double2>(), len, begin,
-                                                   s->d_entries.as<uint64_t>(), d_status);
+                          probe_smem, s->stream>>>(ix.dev, d_pts, len, begin, s->d_entries.as<uint64_t>(), d_status);
     PairsParams pp{};
     pp.entries = s->d_entries.as<uint64_t>();
     pp.n = len;
@@ -449,7 +490,7 @@ int run_host_pairs(gj_session* s, const double* latlng, uint64_t n, bool exact, 
     pp.task_cap = task_cap;
     pp.task_pass = s->d_task_pass.as<uint8_t>();
     pp.count = s->d_pair_count.as<uint32_t>();
-    pp.row_ptr = s->d_row_ptr.as<uint64_t>();
+    pp.row_ptr = d_row_all + begin;
     pp.stats = stats ? s->d_stats.as<unsigned long long>() : nullptr;
     pp.status = d_status;
     pp.exact = exact ? 1 : 0;
@@ -457,7 +498,7 @@ int run_host_pairs(gj_session* s, const double* latlng, uint64_t n, bool exact, 
     s->launches += 2;
     if (exact) {
       RefineParams rp{};
-      rp.pts = s->d_points[0].as<double2>();
+      rp.pts = d_pts;
       rp.base_index = begin;
       rp.task_point = pp.task_point;
       rp.task_slot = pp.task_slot;
@@ -471,12 +512,13 @@ int run_host_pairs(gj_session* s, const double* latlng, uint64_t n, bool exact, 
                       s->stream>>>(ix.dev, rp);
       ++s->launches;
     }
+    GJ_CUDA(cudaEventRecord(s->ev_done[b], s->stream));  // the point buffer is free again
     pairs_emit_kernel<false><<<wide, 256, 0, s->stream>>>(ix.dev, pp);
     scan_block_sums_kernel<<<n_blocks, kScanThreads, 0, s->stream>>>(pp.count, len, s->d_block_sums.as<uint64_t>());
     uint64_t* d_total = s->d_block_sums.as<uint64_t>() + n_blocks_max + 1;
     scan_sums_kernel<<<1, kScanThreads, 0, s->stream>>>(s->d_block_sums.as<uint64_t>(), n_blocks, d_total);
-    scan_apply_kernel<<<n_blocks, kScanThreads, 0, s->stream>>>(pp.count, len, s->d_block_sums.as<uint64_t>(),
-                                                                s->d_row_ptr.as<uint64_t>());
+    scan_apply_kernel<<<n_blocks, kScanThreads, 0, s->stream>>>(pp.count, len, s->d_block_sums.as<uint64_t>(), id_base,
+                                                                d_row_all + begin);
     s->launches += 4;
     GJ_CUDA(cudaGetLastError());
     uint64_t total = 0;
@@ -484,23 +526,20 @@ int run_host_pairs(gj_session* s, const double* latlng, uint64_t n, bool exact, 
     GJ_CUDA(cudaMemcpyAsync(&s->h_status[3], d_status, sizeof(DevStatus), cudaMemcpyDeviceToHost, s->stream));
     GJ_CUDA(cudaStreamSynchronize(s->stream));
     if ((rc = status_to_code(s->h_status[3], bad_index)) != GJ_OK) return rc;
-    GJ_CUDA(s->d_pair_ids.reserve(std::max<uint64_t>(total, 1) * 4));
-    pp.out_id = s->d_pair_ids.as<uint32_t>();
+    if ((id_base + total) * 4 > s->d_all_ids.bytes) {  // at least double, so appends stay amortised
+      const size_t want = std::max<size_t>((id_base + total) * 4, s->d_all_ids.bytes * 2);
+      if ((rc = grow_keep(s, s->d_all_ids, want, id_base * 4)) != GJ_OK) return rc;
+    }
+    pp.out_id = s->d_all_ids.as<uint32_t>();  // row_ptr already carries the global base
     pairs_emit_kernel<true><<<wide, 256, 0, s->stream>>>(ix.dev, pp);
     ++s->launches;
     GJ_CUDA(cudaGetLastError());
-    const uint64_t id_base = s->pairs_id.size();
-    s->pairs_id.resize(id_base + total);
-    GJ_CUDA(cudaMemcpyAsync(s->pairs_row_ptr.data() + begin, s->d_row_ptr.ptr, len * 8, cudaMemcpyDeviceToHost, s->stream));
-    if (total) {
-      GJ_CUDA(cudaMemcpyAsync(s->pairs_id.data() + id_base, s->d_pair_ids.ptr, total * 4, cudaMemcpyDeviceToHost, s->stream));
-    }
-    GJ_CUDA(cudaStreamSynchronize(s->stream));
-    if (id_base) {
-      for (uint64_t i = begin; i < begin + len; ++i) s->pairs_row_ptr[i] += id_base;
-    }
+    id_base += total;
   }
-  s->pairs_row_ptr[n] = s->pairs_id.size();
+  GJ_CUDA(cudaMemcpyAsync(d_row_all + n, &id_base, 8, cudaMemcpyHostToDevice, s->stream));
+  GJ_CUDA(cudaStreamSynchronize(s->stream));
+  s->pairs_total = id_base;
+  s->pairs_valid = true;
   if (stats) {
     unsigned long long h_stats[6];
     GJ_CUDA(cudaMemcpy(h_stats, s->d_stats.ptr, sizeof h_stats, cudaMemcpyDeviceToHost));
@@ -700,7 +739,7 @@ int gj_training_candidates_host(gj_session* s, const double* latlng, uint64_t n,
                                                            base_index + begin, d_flags, d_status);
     scan_block_sums_kernel<<<n_blocks, kScanThreads, 0, s->stream>>>(d_flags, len, d_sums);
     scan_sums_kernel<<<1, kScanThreads, 0, s->stream>>>(d_sums, n_blocks, d_total);
-    scan_apply_kernel<<<n_blocks, kScanThreads, 0, s->stream>>>(d_flags, len, d_sums, s->d_row_ptr.as<uint64_t>());
+    scan_apply_kernel<<<n_blocks, kScanThreads, 0, s->stream>>>(d_flags, len, d_sums, 0, s->d_row_ptr.as<uint64_t>());
     candidate_scatter_kernel<<<grid, 256, 0, s->stream>>>(d_flags, s->d_row_ptr.as<uint64_t>(), len,
                                                           base_index + begin, s->d_entries.as<uint64_t>());
     s->launches += 5;
@@ -851,18 +890,27 @@ int gj_join_pairs_host(gj_session* s, const double* latlng, uint64_t n, int mode
   if (!resolve_exact(*s->ix, mode, &exact)) return GJ_INVALID_ARGUMENT;
   const int rc = run_host_pairs(s, latlng, n, exact, stats, bad_index);
   if (rc != GJ_OK) {
-    s->pairs_row_ptr.clear();
-    s->pairs_id.clear();
+    s->pairs_valid = false;
     return rc;
   }
-  if (n_pairs) *n_pairs = s->pairs_id.size();
+  if (n_pairs) *n_pairs = s->pairs_total;
   return GJ_OK;
 }
 
 int gj_pairs_copy(gj_session* s, uint64_t* row_ptr, uint32_t* polygon_id) {
   if (!s || !row_ptr) return GJ_INVALID_ARGUMENT;
-  std::copy(s->pairs_row_ptr.begin(), s->pairs_row_ptr.end(), row_ptr);
-  if (polygon_id) std::copy(s->pairs_id.begin(), s->pairs_id.end(), polygon_id);
+  if (!s->pairs_valid) {
+    set_error("gj_pairs_copy: no completed gj_join_pairs_host call to copy from");
+    return GJ_INVALID_ARGUMENT;
+  }
+  GJ_CUDA(cudaSetDevice(s->ix->device));
+  // straight from HBM into the caller's arrays (full PCIe rate when they are pinned, gj_host_alloc)
+  GJ_CUDA(cudaMemcpyAsync(row_ptr, s->d_all_row_ptr.ptr, (s->pairs_n + 1) * 8, cudaMemcpyDeviceToHost, s->stream));
+  if (polygon_id && s->pairs_total) {
+    GJ_CUDA(cudaMemcpyAsync(polygon_id, s->d_all_ids.ptr, s->pairs_total * 4, cudaMemcpyDeviceToHost, s->copy_out));
+    GJ_CUDA(cudaStreamSynchronize(s->copy_out));
+  }
+  GJ_CUDA(cudaStreamSynchronize(s->stream));
   return GJ_OK;
 }
 

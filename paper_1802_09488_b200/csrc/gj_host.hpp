@@ -85,9 +85,11 @@ struct gj_session {
   gj::DeviceBuffer d_nrefs, d_task_base, d_pair_count, d_row_ptr, d_block_sums, d_pair_ids;
   cudaEvent_t ev_in[3]{}, ev_done[3]{}, ev_out[3]{};
   gj::DevStatus* h_status = nullptr;   // pinned
-  // materialised pairs kept for gj_pairs_copy
-  std::vector<uint64_t> pairs_row_ptr;
-  std::vector<uint32_t> pairs_id;
+  // materialised pairs of the last gj_join_pairs_host call, kept in HBM for gj_pairs_copy:
+  // row_ptr[n + 1] (global offsets) and the polygon ids
+  gj::DeviceBuffer d_all_row_ptr, d_all_ids;
+  uint64_t pairs_n = 0, pairs_total = 0;
+  bool pairs_valid = false;
   int latched_status = 0;
   uint64_t latched_bad = ~0ull;
 };

@@ -1068,7 +1068,7 @@ scan_sums_kernel(uint64_t* __restrict__ block_sums, uint32_t n_blocks, uint64_t*
 
 __global__ void __launch_bounds__(kScanThreads)
 scan_apply_kernel(const uint32_t* __restrict__ in, uint64_t n, const uint64_t* __restrict__ block_sums,
-                  uint64_t* __restrict__ out) {
+                  uint64_t offset, uint64_t* __restrict__ out) {
   __shared__ uint64_t s_total;
   const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kScanTile + threadIdx.x * kScanItems;
   uint32_t item[kScanItems];
@@ -1078,7 +1078,7 @@ scan_apply_kernel(const uint32_t* __restrict__ in, uint64_t n, const uint64_t* _
     item[k] = base + k < n ? in[base + k] : 0u;
     v += item[k];
   }
-  uint64_t run = block_sums[blockIdx.x] + block_exclusive_scan(v, &s_total);
+  uint64_t run = offset + block_sums[blockIdx.x] + block_exclusive_scan(v, &s_total);
 #pragma unroll
   for (int k = 0; k < kScanItems; ++k) {
     if (base + k < n) out[base + k] = run;

@@ -23,7 +23,8 @@ from paper_1802_09488_b200 import capi, join, synth  # noqa: E402
 from tools import build_bundles  # noqa: E402
 
 
-def run_config(config: int, n_points: int, scale: float, reps: int, check: int, want_ids: bool = True):
+def run_config(config: int, n_points: int, scale: float, reps: int, check: int, want_ids: bool = True,
+               pairs_points: int = 0):
     import torch
 
     spec = synth.SPECS[config]
@@ -87,6 +88,15 @@ def run_config(config: int, n_points: int, scale: float, reps: int, check: int, 
     gpi = np.repeat(np.arange(mp, dtype=np.uint64), np.diff(row_ptr.astype(np.int64)))
     ok_pairs = bool(np.array_equal(gpi, pi) and np.array_equal(ids, pid))
 
+    pairs_res = None
+    if pairs_points:  # throughput of the materialised-pairs call (CSR), host buffers in and out
+        mq = min(pairs_points, n)
+        sess.join_pairs(pts[:min(mq, 1_000_000)], mode)
+        t0 = time.time()
+        rp, pid2 = sess.join_pairs(pts[:mq], mode)
+        dt = time.time() - t0
+        pairs_res = {"points": mq, "pairs": int(rp[-1]), "seconds": dt, "mpoints_per_s": mq / dt / 1e6,
+                     "mpairs_per_s": int(rp[-1]) / dt / 1e6}
     res = {
         "config": config, "name": name, "mode": "exact" if spec.exact else "approx", "points": n,
         "ms": ms, "gpoints_per_s": n / ms / 1e6, "launches_per_step": (launches1 - launches0) // reps, "ids": want_ids,
@@ -97,6 +107,7 @@ def run_config(config: int, n_points: int, scale: float, reps: int, check: int, 
         "pairs_per_point": float(counts.sum()) / n,
         "oracle_counts_equal": bool(ok), "oracle_pairs_equal": ok_pairs, "oracle_prefix": m,
         "cpu_oracle_prefix_mpts_per_s_16thr": m / cpu_s / 1e6, "gen_s": gen_s,
+        "join_pairs_host": pairs_res,
     }
     print(json.dumps(res), flush=True)
     sess.close()
@@ -112,8 +123,10 @@ def main():
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--check", type=int, default=5_000_000)
     ap.add_argument("--no-ids", action="store_true", help="counts + stats only (no first id per point)")
+    ap.add_argument("--pairs", type=int, default=0, help="also time gj_join_pairs_host on this many points")
     args = ap.parse_args()
-    out = [run_config(c, args.points, args.scale, args.reps, args.check, not args.no_ids) for c in args.configs]
+    out = [run_config(c, args.points, args.scale, args.reps, args.check, not args.no_ids, args.pairs)
+           for c in args.configs]
     (ROOT / "gpurun_out").mkdir(exist_ok=True)
     (ROOT / "gpurun_out" / "bench_configs.json").write_text(json.dumps(out, indent=1))
 
