@@ -73,11 +73,8 @@ struct StripMeta {
   uint32_t ptr_base;  // first entry of this polygon in strip_ptr (k + 1 entries)
 };
 
-struct EdgeRecord {  // x = lng, y = lat (geometry.cpp:35); 64 bytes
+struct __align__(32) EdgeRecord {  // x = lng, y = lat (geometry.cpp:35); 32 bytes, one 256-bit load
   double ax, ay, bx, by;
-  // the edge's bounding box widened by pip_edge_classify's 1e-9 deg margin:
-  // fmin(ax, bx) - m, fmax(ax, bx) + m, fmin(ay, by) - m, fmax(ay, by) + m
-  double x_lo, x_hi, y_lo, y_hi;
 };
 
 // Strip of latitude y.  The same monotone fp64 expression runs on the host
@@ -357,11 +354,24 @@ __device__ __forceinline__ double point_segment_dist_sq(double px, double py, do
 // reference's comparison is false as well.
 constexpr double kPipBoxMargin = 1e-9;
 
-__device__ __forceinline__ uint32_t pip_edge_classify(double qx, double qy, double ay, double by, double x_lo,
-                                                      double x_hi, double y_lo, double y_hi) {
-  const bool near_box = qx >= x_lo && qx <= x_hi && qy >= y_lo && qy <= y_hi;
+// The box is the edge's bounding box widened by the margin:
+// [min(ax,bx) - m, max(ax,bx) + m] x [min(ay,by) - m, max(ay,by) + m].  Rounding
+// is monotone, so RN(min(a,b) - m) = min(RN(a - m), RN(b - m)): the test needs
+// no min/max, only the four widened coordinates per axis.
+__device__ __forceinline__ uint32_t pip_edge_classify(double qx, double qy, double ax, double ay, double bx,
+                                                      double by) {
+  const double m = kPipBoxMargin;
+  const bool near_x = (qx >= __dsub_rn(ax, m) || qx >= __dsub_rn(bx, m)) &&
+                      (qx <= __dadd_rn(ax, m) || qx <= __dadd_rn(bx, m));
+  const bool near_y = (qy >= __dsub_rn(ay, m) || qy >= __dsub_rn(by, m)) &&
+                      (qy <= __dadd_rn(ay, m) || qy <= __dadd_rn(by, m));
   const bool straddles = (ay > qy) != (by > qy);  // geometry.cpp:197
-  return (near_box ? 1u : 0u) | (straddles ? 2u : 0u);
+  return (near_x && near_y ? 1u : 0u) | (straddles ? 2u : 0u);
+}
+
+// One edge record with a single 256-bit load (sm_100+).
+__device__ __forceinline__ void load_edge(const EdgeRecord* rec, double* ax, double* ay, double* bx, double* by) {
+  asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(*ax), "=d"(*ay), "=d"(*bx), "=d"(*by) : "l"(rec));
 }
 
 // geometry.cpp:186-193: on an edge or vertex

@@ -487,8 +487,7 @@ int create_index(const gj_index_desc& d, int device, gj_index** out) {
         strip_ptr.push_back(static_cast<uint32_t>(strip_edges.size()));
         for (uint32_t e : lists[st]) {
           const double2 a = v[e], b = v[e + 1];
-          strip_edges.push_back(EdgeRecord{a.x, a.y, b.x, b.y, std::min(a.x, b.x) - margin, std::max(a.x, b.x) + margin,
-                                           std::min(a.y, b.y) - margin, std::max(a.y, b.y) + margin});
+          strip_edges.push_back(EdgeRecord{a.x, a.y, b.x, b.y});
         }
       }
       strip_ptr.push_back(static_cast<uint32_t>(strip_edges.size()));

@@ -780,10 +780,10 @@ refine_kernel(const __grid_constant__ DevIndex ix, RefineParams rp) {
       const double ox = __shfl_sync(0xffffffffu, qx, owner);
       const double oy = __shfl_sync(0xffffffffu, qy, owner);
       if (lane < take) {
-        const double2 a = __ldg(reinterpret_cast<const double2*>(ix.strip_edges + item.x));
-        const double2 b = __ldg(reinterpret_cast<const double2*>(ix.strip_edges + item.x) + 1);
-        if ((item.y & 1u) && pip_edge_on_boundary(ox, oy, a.x, a.y, b.x, b.y)) atomicOr(&s_result[warp][owner], 1u);
-        if ((item.y & 2u) && pip_edge_crosses(ox, oy, a.x, a.y, b.x, b.y)) atomicXor(&s_result[warp][owner], 2u);
+        double ax, ay, bx, by;
+        load_edge(ix.strip_edges + item.x, &ax, &ay, &bx, &by);
+        if ((item.y & 1u) && pip_edge_on_boundary(ox, oy, ax, ay, bx, by)) atomicOr(&s_result[warp][owner], 1u);
+        if ((item.y & 2u) && pip_edge_crosses(ox, oy, ax, ay, bx, by)) atomicXor(&s_result[warp][owner], 2u);
       }
     };
 
@@ -814,11 +814,9 @@ refine_kernel(const __grid_constant__ DevIndex ix, RefineParams rp) {
       const double oy = __shfl_sync(0xffffffffu, qy, src);
       uint32_t kinds = 0;
       if (real) {
-        const double2* rec = reinterpret_cast<const double2*>(ix.strip_edges + e);
-        const double ay = __ldg(reinterpret_cast<const double*>(rec) + 1);
-        const double by = __ldg(reinterpret_cast<const double*>(rec) + 3);
-        const double2 bx = __ldg(rec + 2), byr = __ldg(rec + 3);
-        kinds = pip_edge_classify(ox, oy, ay, by, bx.x, bx.y, byr.x, byr.y);
+        double ax, ay, bx, by;
+        load_edge(ix.strip_edges + e, &ax, &ay, &bx, &by);
+        kinds = pip_edge_classify(ox, oy, ax, ay, bx, by);
       }
       const uint32_t mask = __ballot_sync(0xffffffffu, kinds != 0u);
       if (kinds) s_list[warp][n_list + __popc(mask & lane_lt)] = make_uint2(e, (src << 2) | kinds);

@@ -24,7 +24,7 @@ from tools import build_bundles  # noqa: E402
 
 
 def run_config(config: int, n_points: int, scale: float, reps: int, check: int, want_ids: bool = True,
-               pairs_points: int = 0):
+               pairs_points: int = 0, want_stats: bool = True):
     import torch
 
     spec = synth.SPECS[config]
@@ -48,7 +48,8 @@ def run_config(config: int, n_points: int, scale: float, reps: int, check: int, 
     stream = torch.cuda.ExternalStream(sess.stream)
 
     def step():
-        sess.join_count_device(d_pts.data_ptr(), n, d_counts.data_ptr(), mode, d_stats_ptr=d_stats.data_ptr(),
+        sess.join_count_device(d_pts.data_ptr(), n, d_counts.data_ptr(), mode,
+                               d_stats_ptr=d_stats.data_ptr() if want_stats else 0,
                                d_first_id_ptr=d_first.data_ptr() if want_ids else 0)
 
     for _ in range(3):
@@ -99,7 +100,7 @@ def run_config(config: int, n_points: int, scale: float, reps: int, check: int, 
                      "mpairs_per_s": int(rp[-1]) / dt / 1e6}
     res = {
         "config": config, "name": name, "mode": "exact" if spec.exact else "approx", "points": n,
-        "ms": ms, "gpoints_per_s": n / ms / 1e6, "launches_per_step": (launches1 - launches0) // reps, "ids": want_ids,
+        "ms": ms, "gpoints_per_s": n / ms / 1e6, "launches_per_step": (launches1 - launches0) // reps, "ids": want_ids, "stats_collected": want_stats,
         "index_nodes": int(info.node_count), "index_mb": info.device_bytes / 1e6, "n_polygons": int(info.n_polygons),
         "dir1_level": info.dir_level, "dir2_level": info.dir2_level,
         "stats": dict(zip(["probes", "pip_tests", "false_hits", "solely_true_hits", "refinement_entered",
@@ -123,9 +124,10 @@ def main():
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--check", type=int, default=5_000_000)
     ap.add_argument("--no-ids", action="store_true", help="counts + stats only (no first id per point)")
+    ap.add_argument("--no-stats", action="store_true", help="do not collect JoinStats")
     ap.add_argument("--pairs", type=int, default=0, help="also time gj_join_pairs_host on this many points")
     args = ap.parse_args()
-    out = [run_config(c, args.points, args.scale, args.reps, args.check, not args.no_ids, args.pairs)
+    out = [run_config(c, args.points, args.scale, args.reps, args.check, not args.no_ids, args.pairs, not args.no_stats)
            for c in args.configs]
     (ROOT / "gpurun_out").mkdir(exist_ok=True)
     (ROOT / "gpurun_out" / "bench_configs.json").write_text(json.dumps(out, indent=1))
