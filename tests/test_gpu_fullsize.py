@@ -1,0 +1,117 @@
+"""GPU tests at BASELINE.json's full sizes (configs[1] / configs[2]: 289
+polygons, 100 M points), through size-independent properties of the join —
+no CPU oracle can finish these sizes in seconds:
+
+  * conservation: per-polygon counts == histogram of (first ids + overflow ids);
+  * JoinStats identities: probes == n, the three probe outcomes partition n,
+    candidate_refs bounds the refined pairs;
+  * linearity / shard invariance: the join of the whole input equals the sum of
+    the joins of its ranges (what the multi-GPU split relies on), and global
+    point indices (base_index) only relabel;
+  * exact ⊆ approx: refining can only remove pairs;
+  * the device-resident and the host-buffer entry points agree.
+
+The indexes are the bench's cached reference-built bundles (.cache/, built
+offline by tools/build_bundles.py); the tests skip when the cache is absent."""
+import numpy as np
+import pytest
+
+from paper_1802_09488_b200 import capi, join, synth
+from tools import build_bundles
+
+pytestmark = pytest.mark.gpu
+
+N_FULL = 100_000_000
+
+
+def _bundle(config):
+    name = build_bundles.workload_name(config)
+    if not build_bundles.have_bundle(name):
+        pytest.skip(f"no cached index for config {config} (tools/build_bundles.py needs the reference)")
+    return join.IndexBundle.load(build_bundles.bundle_file(name), device=0)
+
+
+def _hist(bundle, first, ovf_id):
+    """Per-slot histogram of every emitted pair: first ids (flag stripped) + overflow ids."""
+    hit = first[first < capi.GJ_DEFERRED] & np.uint32(~capi.GJ_MORE_FLAG & 0xFFFFFFFF)
+    ids = np.concatenate([hit, ovf_id])
+    return np.bincount(np.searchsorted(bundle.ids, ids), minlength=len(bundle.ids)).astype(np.uint64)
+
+
+def test_config2_full_size_properties():
+    bundle = _bundle(2)
+    s = bundle.session()
+    pts = synth.points_for(2, N_FULL, None)
+    assert pts.shape == (N_FULL, 2)
+    st = join.JoinStats()
+    counts, first, (ovf_pt, ovf_id) = s.join_count(pts, capi.GJ_MODE_APPROX, stats=st, want_ids=True)
+    # conservation
+    assert np.array_equal(counts, _hist(bundle, first, ovf_id))
+    assert not np.any(first == capi.GJ_DEFERRED)  # approx mode defers nothing
+    more = (first != capi.GJ_NO_MATCH) & ((first & capi.GJ_MORE_FLAG) != 0)
+    assert np.array_equal(np.unique(ovf_pt), np.flatnonzero(more).astype(np.uint64))
+    assert np.all(np.diff(ovf_pt.astype(np.int64)) >= 0)  # overflow records ascend by point
+    # JoinStats identities (join.hpp:77-84)
+    probes, pip_tests, false_hits, solely_true, refined, cand_refs = st.as_tuple()
+    assert probes == N_FULL and pip_tests == 0
+    assert false_hits + solely_true + refined == N_FULL
+    assert false_hits == int(np.count_nonzero(first == capi.GJ_NO_MATCH))
+    assert int(counts.sum()) >= N_FULL - false_hits and cand_refs >= refined
+    # linearity over ranges, with global indices
+    cut = 37_123_457  # not a multiple of any tile or chunk size
+    c0, f0, (p0, i0) = s.join_count(pts[:cut], capi.GJ_MODE_APPROX, want_ids=True)
+    c1, f1, (p1, i1) = s.join_count(pts[cut:], capi.GJ_MODE_APPROX, want_ids=True, base_index=cut)
+    assert np.array_equal(c0 + c1, counts)
+    assert np.array_equal(np.concatenate([f0, f1]), first)
+    assert np.array_equal(np.concatenate([p0, p1]), ovf_pt) and np.array_equal(np.concatenate([i0, i1]), ovf_id)
+    # count-only entry point agrees
+    c_only, _, _ = s.join_count(pts, capi.GJ_MODE_APPROX)
+    assert np.array_equal(c_only, counts)
+
+
+def test_config2_device_resident_equals_host_path():
+    import torch
+    bundle = _bundle(2)
+    s = bundle.session()
+    n = N_FULL
+    pts = synth.points_for(2, n, None)
+    d_pts = torch.from_numpy(pts).cuda()
+    d_counts = torch.zeros(len(bundle.ids), dtype=torch.int64, device="cuda")
+    d_stats = torch.zeros(6, dtype=torch.int64, device="cuda")
+    d_first = torch.empty(n, dtype=torch.int32, device="cuda")
+    s.join_count_device(d_pts.data_ptr(), n, d_counts.data_ptr(), capi.GJ_MODE_APPROX,
+                        d_stats_ptr=d_stats.data_ptr(), d_first_id_ptr=d_first.data_ptr(), sync=True)
+    st = join.JoinStats()
+    counts, first, _ = s.join_count(pts, capi.GJ_MODE_APPROX, stats=st, want_ids=True)
+    assert np.array_equal(d_counts.cpu().numpy().astype(np.uint64), counts)
+    assert np.array_equal(d_first.cpu().numpy().view(np.uint32), first)
+    assert tuple(int(v) for v in d_stats.cpu().numpy()) == st.as_tuple()
+    # idempotence: a second launch over the same input adds exactly the same counts
+    s.join_count_device(d_pts.data_ptr(), n, d_counts.data_ptr(), capi.GJ_MODE_APPROX, sync=True)
+    assert np.array_equal(d_counts.cpu().numpy().astype(np.uint64), 2 * counts)
+
+
+def test_config3_exact_is_subset_of_approx_full_size():
+    bundle = _bundle(3)
+    s = bundle.session()
+    polys = synth.polygons_for(3, 1.0)
+    pts = synth.points_for(3, N_FULL, polys)
+    se, sa = join.JoinStats(), join.JoinStats()
+    ce, fe, (pe, ie) = s.join_count(pts, capi.GJ_MODE_EXACT, stats=se, want_ids=True)
+    ca, fa, (pa, ia) = s.join_count(pts, capi.GJ_MODE_APPROX, stats=sa, want_ids=True)
+    assert np.array_equal(ce, _hist(bundle, fe, ie)) and np.array_equal(ca, _hist(bundle, fa, ia))
+    assert np.all(ce <= ca)  # refinement only removes pairs
+    # probe-side counters do not depend on the mode; pip_tests == candidate_refs in exact mode (join.cpp:100-118)
+    assert se.as_tuple()[0] == sa.as_tuple()[0] == N_FULL
+    assert se.as_tuple()[2:] == sa.as_tuple()[2:]
+    assert se.as_tuple()[1] == se.as_tuple()[5] and sa.as_tuple()[1] == 0
+    assert int(ca.sum()) - int(ce.sum()) <= se.as_tuple()[1]  # at most one pair lost per PIP test
+    # a point with no approx match has no exact match; exact first ids are approx pairs of that point
+    assert np.all(fe[fa == capi.GJ_NO_MATCH] == capi.GJ_NO_MATCH)
+    single = (fa != capi.GJ_NO_MATCH) & ((fa & capi.GJ_MORE_FLAG) == 0) & (fe < capi.GJ_DEFERRED)
+    assert np.array_equal(fe[single] & np.uint32(0x7FFFFFFF), fa[single])
+    # shard invariance in exact mode
+    cut = 61_000_003
+    c0, _, _ = s.join_count(pts[:cut], capi.GJ_MODE_EXACT)
+    c1, _, _ = s.join_count(pts[cut:], capi.GJ_MODE_EXACT, base_index=cut)
+    assert np.array_equal(c0 + c1, ce)
