@@ -119,6 +119,14 @@ struct DevIndex {
   // of `dir` when present; `table` then points at uint16 data.
   DevDirectory dir16;
   DevQueueCoding qc;  // for the 32-bit tier behind dir16 (dir2 when present, else dir)
+  // Optional palette form of every trie node, 128 bytes (one L2 line / DRAM
+  // burst) instead of 2 KB: [4 distinct entries (u64) | 256 two-bit codes (64 B) |
+  // pad].  A boundary node of a tessellation holds 2-4 distinct entries (two
+  // true hits, their candidate pair, empty), so the whole tree shrinks 16x and
+  // stays in L2 where the arena cannot (a random arena read is a 128-byte DRAM
+  // burst).  Nodes with more than 4 distinct entries keep word 0 == ~0 and are
+  // read from the arena.  Null when absent.
+  const uint64_t* node_pal;
   const uint64_t* dict;  // [n_dict], dict[0] == 0
   uint32_t n_dict;
 };

@@ -24,10 +24,11 @@ thread_local std::string g_error;
 
 constexpr uint64_t kMaxDirEntries = 32768;         // 128 KB of u32 codes (shared memory)
 constexpr uint64_t kMaxDir2Entries = 16ull << 20;  // 64 MB of u32 codes (stays in the 126 MB L2)
-// 68 KB of u16 codes: with K1's queues and histogram that stays inside the
-// 132 KB shared-memory carve-out step, which leaves the SM 124 KB of L1 for loads
-// in flight (a finer tier at 196 KB measured slower, see plan_smem in gj_api.cu)
-constexpr uint64_t kMaxDir16Entries = 34816;
+// 136 KB of u16 codes: with K1's queues and histogram that stays inside the
+// 196 KB shared-memory carve-out step (60 KB of L1 left for loads in flight);
+// the next step up (228 KB) is a cliff, see plan_smem in gj_api.cu
+constexpr uint64_t kMaxDir16Entries = 69632;
+constexpr uint64_t kMaxNodePalBytes = 32ull << 20;  // palette nodes are only worth it while they stay in L2
 constexpr uint64_t kMaxPolygonId = (1u << 30) - 1;
 
 struct Bitmap {
@@ -523,8 +524,46 @@ int create_index(const gj_index_desc& d, int device, gj_index** out) {
   if ((rc = upload(ix->d_dir2_table, an.dir2.table.data(), an.dir2.table.size(), &bytes)) != GJ_OK) return rc;
   if ((rc = upload(ix->d_dir16_table, an.dir16.table16.data(), an.dir16.table16.size(), &bytes)) != GJ_OK) return rc;
 
+  // Palette form of the nodes (DevIndex::node_pal), for K1's deep descents.
+  bool have_pal = false;
+  {
+    uint64_t max_pal = kMaxNodePalBytes;
+    if (const char* e = std::getenv("GJ_NODE_PAL_MAX_MB")) max_pal = std::strtoull(e, nullptr, 10) << 20;  // tuning knob
+    if (d.node_count != 0 && d.node_count * 128 <= max_pal && d.node_count <= (1ull << 23)) {
+      std::vector<uint64_t> pal(d.node_count * 16, 0);
+      for (uint64_t node = 0; node < d.node_count; ++node) {
+        const uint64_t* slots = d.arena + node * kNodeSlots;
+        uint64_t* rec = pal.data() + node * 16;
+        uint64_t values[4];
+        int n_values = 0;
+        bool fits = true;
+        for (int sl = 0; sl < kNodeSlots && fits; ++sl) {
+          int code = 0;
+          while (code < n_values && values[code] != slots[sl]) ++code;
+          if (code == n_values) {
+            if (n_values == 4) {
+              fits = false;
+              break;
+            }
+            values[n_values++] = slots[sl];
+          }
+          rec[4 + sl / 32] |= static_cast<uint64_t>(code) << (2 * (sl % 32));
+        }
+        if (fits) {
+          for (int c = 0; c < 4; ++c) rec[c] = c < n_values ? values[c] : 0;
+        } else {
+          for (int w = 0; w < 16; ++w) rec[w] = 0;
+          rec[0] = ~0ull;  // more than 4 distinct entries: read the arena
+        }
+      }
+      if ((rc = upload(ix->d_node_pal, pal.data(), pal.size(), &bytes)) != GJ_OK) return rc;
+      have_pal = true;
+    }
+  }
+
   DevIndex& dv = ix->dev;
   dv.arena = ix->d_arena.as<uint64_t>();
+  dv.node_pal = have_pal ? ix->d_node_pal.as<uint64_t>() : nullptr;
   dv.lut = ix->d_lut.as<uint32_t>();
   dv.ids = ix->d_ids.as<uint32_t>();
   dv.ring_off = ix->d_ring_off.as<uint64_t>();

@@ -378,7 +378,17 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
         bool walk = true;
         if (ix.qc.packed) {  // the word is (node - 1) * 256 + (y sub-cell bits << 4 | x sub-cell bits)
           const uint32_t slot = (spread4((c >> 4) & 0xFu) << 1) | spread4(c & 0xFu);  // chunk_slot
-          entry = ld_arena(ix.arena + ((node & ~0xFFull) | slot));
+          const uint64_t at = (node & ~0xFFull) | slot;
+          bool from_arena = true;
+          if (ix.node_pal) {  // the node's 128-byte palette form, usually an L2 hit
+            const uint64_t* rec = ix.node_pal + (at >> 8) * 16u;
+            const uint32_t codes = __ldg(reinterpret_cast<const uint32_t*>(rec + 4) + (slot >> 4));
+            const uint64_t v = __ldg(rec + ((codes >> ((slot & 15u) * 2u)) & 3u));
+            const uint64_t first = __ldg(rec);
+            from_arena = first == ~0ull;
+            entry = v;
+          }
+          if (from_arena) entry = ld_arena(ix.arena + at);
           walk = (entry & 3u) == 0u && entry != 0u;  // a link again: deeper than the queued bits reach
           node = entry >> 2;
           level += 4;

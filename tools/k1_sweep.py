@@ -25,8 +25,8 @@ VARIANTS = {
     "pf0": ["GJ_PF_DIST=0"],
     "pf2": ["GJ_PF_DIST=2"],
     "ppt3": ["GJ_PPT=3"],
+    "ppt5": ["GJ_PPT=5"],
     "ppt6": ["GJ_PPT=6"],
-    "t512_b2_ppt4": ["GJ_JOIN_THREADS=512", "GJ_JOIN_MIN_BLOCKS=2", "GJ_PPT=4", "GJ_SMEM_LIMIT_KB=99"],
     "exp_phase1_only": ["GJ_EXP_PHASE1_ONLY"],
     "exp_no_phase3": ["GJ_EXP_NO_PHASE3"],
 }
