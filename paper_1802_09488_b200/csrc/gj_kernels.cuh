@@ -11,6 +11,8 @@
 // All of it is HBM/L2-bound integer and fp64 scalar work; no tensor cores.
 #pragma once
 
+#include <type_traits>
+
 #include "gj_device.cuh"
 
 namespace gj {
@@ -524,21 +526,24 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
   };
 #pragma unroll 1
   for (uint32_t k = 0; k < kPrefetchTiles; ++k) prefetch_chunk(blockIdx.x + k * gridDim.x);
-  for (uint32_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+  // One tile of this warp.  kFull: every point of the tile exists (all tiles
+  // but possibly the last), so neither the loads nor population 1 test i < n.
+  auto tile_body = [&](uint32_t tile, auto full_tag) {
+    constexpr bool kFull = decltype(full_tag)::value;
     const uint32_t base = tile * kTile + warp * kChunkPoints + lane;  // point of slot j: base + 32 j
     prefetch_chunk(tile + kPrefetchTiles * gridDim.x);
     double2 p[kPointsPerThread];
 #pragma unroll
     for (int j = 0; j < kPointsPerThread; ++j) {
-      // streaming read, touched once: evict-first.  Lanes past the end re-read
-      // the last point and are masked below.
-      p[j] = __ldcs(pts + min(base + j * 32u, n - 1u));
+      // streaming read, touched once: evict-first.  In the last tile lanes past
+      // the end re-read the last point and are masked below.
+      p[j] = __ldcs(pts + (kFull ? base + j * 32u : min(base + j * 32u, n - 1u)));
     }
     // ---- population 1: shared-memory tier, no branches, no calls ----
 #pragma unroll
     for (int j = 0; j < kPointsPerThread; ++j) {
       const uint32_t i = base + j * 32u;
-      const bool live = i < n;
+      const bool live = kFull || i < n;
       uint32_t x, y;  // left-aligned to 32 bits
       const bool ok = grid_xy_try(p[j].x, p[j].y, &x, &y) && live;  // valid, coordinates exact
       const uint32_t cx = min((x >> d1_shift) - d1_x0, d1_w);  // clamps into the all-miss padding
@@ -574,7 +579,11 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
       q2_count = enqueue(s_q2, q2_count, open, ok ? i : i | 0x80000000u, qy * qc_mul + qx);
     }
     drain2(false);
-  }
+  };
+  const uint32_t n_full_tiles = n / kTile;
+  uint32_t tile = blockIdx.x;
+  for (; tile < n_full_tiles; tile += gridDim.x) tile_body(tile, std::true_type{});
+  if (tile < n_tiles) tile_body(tile, std::false_type{});  // the partial last tile, in one CTA
   drain2(true);
   settle_batch();
   drain3(true);
