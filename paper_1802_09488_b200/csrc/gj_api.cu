@@ -610,35 +610,10 @@ int gj_session_create(gj_index* ix, gj_session** out) {
   }
   GJ_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&s->h_status), 4 * sizeof(DevStatus), cudaHostAllocDefault));
   GJ_CUDA(s->d_status.reserve(4 * sizeof(DevStatus)));
-  if (const char* e = std::getenv("GJ_L2_FETCH")) {  // tuning knob: 32 / 64 / 128
-    if (cudaDeviceSetLimit(cudaLimitMaxL2FetchGranularity, static_cast<size_t>(std::atoi(e))) != cudaSuccess) cudaGetLastError();
-  }
-#ifndef GJ_NO_L2_PERSIST
-  // Keep the second directory tier resident in L2: it is small (<= 64 MB),
-  // gathered at random by ~30 % of the points, and would otherwise be churned
-  // out by the point stream that passes through the same cache.
-  if (ix->dev.dir2.n_table) {
-    cudaDeviceProp prop{};
-    GJ_CUDA(cudaGetDeviceProperties(&prop, ix->device));
-    const size_t table_bytes = static_cast<size_t>(ix->dev.dir2.n_table) * 4;
-    const size_t window = std::min<size_t>(table_bytes, static_cast<size_t>(prop.accessPolicyMaxWindowSize));
-    const size_t carve = std::min<size_t>(window, static_cast<size_t>(prop.persistingL2CacheMaxSize));
-    if (carve > 0) {
-      size_t current = 0;
-      cudaDeviceGetLimit(&current, cudaLimitPersistingL2CacheSize);
-      if (current < carve) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, carve);
-      cudaStreamAttrValue attr{};
-      attr.accessPolicyWindow.base_ptr = const_cast<uint32_t*>(ix->dev.dir2.table);
-      attr.accessPolicyWindow.num_bytes = window;
-      attr.accessPolicyWindow.hitRatio = static_cast<float>(std::min(1.0, static_cast<double>(carve) / window));
-      attr.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-      attr.accessPolicyWindow.missProp = cudaAccessPropertyNormal;
-      if (cudaStreamSetAttribute(s->stream, cudaStreamAttributeAccessPolicyWindow, &attr) != cudaSuccess) {
-        cudaGetLastError();  // persistence is an optimisation, never a requirement
-      }
-    }
-  }
-#endif
+  // No L2 persistence window for the second directory tier: it is hot enough
+  // to stay resident by itself (98 % hit rate with and without a window), and a
+  // persisting carve-out is a device-wide limit that takes L2 away from
+  // everything else (a 70 MB carve-out made K1 1.5x slower).
   *out = s.release();
   return GJ_OK;
 }
