@@ -100,6 +100,11 @@ int reset_status(gj_session* s, DevStatus* d_status) {
   return GJ_OK;
 }
 
+HostStager& stager_of(gj_session* s) {
+  if (!s->stager) s->stager = std::make_unique<HostStager>();
+  return *s->stager;
+}
+
 struct JoinRequest {
   const double2* d_pts;
   uint64_t n;
@@ -297,9 +302,17 @@ int run_host_join(gj_session* s, const double* latlng, uint64_t n, uint64_t base
   int final_rc = GJ_OK;
   DevStatus worst{kNoBadIndex, 0, 0, 0, 0};
 
+  // First ids go straight to pinned caller memory on the copy-out stream; for
+  // pageable memory they are staged when the chunk is drained.
+  const bool ids_direct = want_ids && HostStager::is_pinned(out_first_id);
+
   auto drain = [&](uint64_t c) -> int {  // chunk c finished on the device?
     const int b = static_cast<int>(c % 3);
     GJ_CUDA(cudaEventSynchronize(s->ev_done[b]));
+    if (want_ids && !ids_direct) {
+      const uint64_t c_begin = c * chunk, c_len = std::min(chunk, n - c_begin);
+      GJ_CUDA(stager_of(s).to_host(out_first_id + c_begin, s->d_first_id[b].ptr, c_len * 4, s->copy_out));
+    }
     const DevStatus& st = s->h_status[b];
     worst.flags |= st.flags;
     worst.bad_index = std::min(worst.bad_index, st.bad_index);
@@ -333,11 +346,11 @@ int run_host_join(gj_session* s, const double* latlng, uint64_t n, uint64_t base
       GJ_CUDA(cudaStreamWaitEvent(s->copy_in, s->ev_done[b], 0));
       if (!serial && (rc = drain(c - 3)) != GJ_OK) return rc;
     }
-    GJ_CUDA(cudaMemcpyAsync(s->d_points[b].ptr, latlng + 2 * begin, len * 16, cudaMemcpyHostToDevice, s->copy_in));
+    GJ_CUDA(stager_of(s).to_device(s->d_points[b].ptr, latlng + 2 * begin, len * 16, s->copy_in));
     GJ_CUDA(cudaEventRecord(s->ev_in[b], s->copy_in));
     if (serial && c >= 1 && (rc = drain(c - 1)) != GJ_OK) return rc;
     GJ_CUDA(cudaStreamWaitEvent(s->stream, s->ev_in[b], 0));
-    if (want_ids && c >= 3) GJ_CUDA(cudaStreamWaitEvent(s->stream, s->ev_out[b], 0));
+    if (ids_direct && c >= 3) GJ_CUDA(cudaStreamWaitEvent(s->stream, s->ev_out[b], 0));
 
     JoinRequest rq{};
     rq.d_pts = s->d_points[b].as<double2>();
@@ -354,7 +367,7 @@ int run_host_join(gj_session* s, const double* latlng, uint64_t n, uint64_t base
     if ((rc = enqueue_join(s, rq)) != GJ_OK) return rc;
     GJ_CUDA(cudaMemcpyAsync(&s->h_status[b], rq.d_status, sizeof(DevStatus), cudaMemcpyDeviceToHost, s->stream));
     GJ_CUDA(cudaEventRecord(s->ev_done[b], s->stream));
-    if (want_ids) {
+    if (ids_direct) {
       GJ_CUDA(cudaStreamWaitEvent(s->copy_out, s->ev_done[b], 0));
       GJ_CUDA(cudaMemcpyAsync(out_first_id + begin, s->d_first_id[b].ptr, len * 4, cudaMemcpyDeviceToHost, s->copy_out));
       GJ_CUDA(cudaEventRecord(s->ev_out[b], s->copy_out));
@@ -459,7 +472,7 @@ int run_host_pairs(gj_session* s, const double* latlng, uint64_t n, bool exact, 
   auto copy_in = [&](uint64_t begin, int b) -> int {  // chunk at `begin` -> point buffer b, on the copy stream
     const uint64_t len = std::min(chunk, n - begin);
     GJ_CUDA(cudaStreamWaitEvent(s->copy_in, s->ev_done[b], 0));  // the kernels that read buffer b last
-    GJ_CUDA(cudaMemcpyAsync(s->d_points[b].ptr, latlng + 2 * begin, len * 16, cudaMemcpyHostToDevice, s->copy_in));
+    GJ_CUDA(stager_of(s).to_device(s->d_points[b].ptr, latlng + 2 * begin, len * 16, s->copy_in));
     GJ_CUDA(cudaEventRecord(s->ev_in[b], s->copy_in));
     return GJ_OK;
   };
@@ -472,7 +485,6 @@ int run_host_pairs(gj_session* s, const double* latlng, uint64_t n, bool exact, 
   for (uint64_t begin = 0; begin < n; begin += chunk, b ^= 1) {
     const uint64_t len = std::min(chunk, n - begin);
     const uint32_t n_blocks = static_cast<uint32_t>((len + kScanTile - 1) / kScanTile);
-    if (begin + chunk < n && (rc = copy_in(begin + chunk, b ^ 1)) != GJ_OK) return rc;
     GJ_CUDA(cudaStreamWaitEvent(s->stream, s->ev_in[b], 0));
     if ((rc = reset_status(s, d_status)) != GJ_OK) return rc;
     const double2* d_pts = s->d_points[b].as<double2>();
@@ -521,6 +533,8 @@ int run_host_pairs(gj_session* s, const double* latlng, uint64_t n, bool exact, 
                                                                 d_row_all + begin);
     s->launches += 4;
     GJ_CUDA(cudaGetLastError());
+    // stage the next chunk's points while the device works on this one
+    if (begin + chunk < n && (rc = copy_in(begin + chunk, b ^ 1)) != GJ_OK) return rc;
     uint64_t total = 0;
     GJ_CUDA(cudaMemcpyAsync(&total, d_total, 8, cudaMemcpyDeviceToHost, s->stream));
     GJ_CUDA(cudaMemcpyAsync(&s->h_status[3], d_status, sizeof(DevStatus), cudaMemcpyDeviceToHost, s->stream));
@@ -879,13 +893,12 @@ int gj_pairs_copy(gj_session* s, uint64_t* row_ptr, uint32_t* polygon_id) {
     return GJ_INVALID_ARGUMENT;
   }
   GJ_CUDA(cudaSetDevice(s->ix->device));
-  // straight from HBM into the caller's arrays (full PCIe rate when they are pinned, gj_host_alloc)
-  GJ_CUDA(cudaMemcpyAsync(row_ptr, s->d_all_row_ptr.ptr, (s->pairs_n + 1) * 8, cudaMemcpyDeviceToHost, s->stream));
+  // straight from HBM into the caller's arrays: directly when they are pinned (gj_host_alloc), else
+  // through the session's stager
+  GJ_CUDA(stager_of(s).to_host(row_ptr, s->d_all_row_ptr.ptr, (s->pairs_n + 1) * 8, s->copy_out));
   if (polygon_id && s->pairs_total) {
-    GJ_CUDA(cudaMemcpyAsync(polygon_id, s->d_all_ids.ptr, s->pairs_total * 4, cudaMemcpyDeviceToHost, s->copy_out));
-    GJ_CUDA(cudaStreamSynchronize(s->copy_out));
+    GJ_CUDA(stager_of(s).to_host(polygon_id, s->d_all_ids.ptr, s->pairs_total * 4, s->copy_out));
   }
-  GJ_CUDA(cudaStreamSynchronize(s->stream));
   return GJ_OK;
 }
 

@@ -3,9 +3,14 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <condition_variable>
 #include <cstdint>
+#include <cstring>
+#include <memory>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/geojoin_b200.h"
@@ -55,6 +60,161 @@ struct HostDirectory {
   std::vector<uint16_t> table16;  // the 16-bit first tier uses this instead
 };
 
+// Fork-join memcpy over a few worker threads: one thread moves ~10 GB/s between
+// pageable and pinned memory (less when the pages are touched for the first
+// time), the PCIe link 55 GB/s.
+class CopyPool {
+ public:
+  explicit CopyPool(int threads) {
+    for (int w = 0; w < threads; ++w) workers_.emplace_back([this, w] { run(w); });
+  }
+  ~CopyPool() {
+    {
+      std::lock_guard<std::mutex> lk(m_);
+      stop_ = true;
+      ++generation_;
+    }
+    cv_.notify_all();
+    for (std::thread& t : workers_) t.join();
+  }
+  CopyPool(const CopyPool&) = delete;
+  CopyPool& operator=(const CopyPool&) = delete;
+
+  // blocking; the caller's thread takes the last slice
+  void copy(void* dst, const void* src, size_t bytes) {
+    const size_t parts = workers_.size() + 1;
+    if (bytes < (1u << 20) || parts == 1) {
+      std::memcpy(dst, src, bytes);
+      return;
+    }
+    {
+      std::lock_guard<std::mutex> lk(m_);
+      dst_ = static_cast<char*>(dst);
+      src_ = static_cast<const char*>(src);
+      slice_ = ((bytes + parts - 1) / parts + 4095) & ~size_t{4095};
+      bytes_ = bytes;
+      pending_ = static_cast<int>(workers_.size());
+      ++generation_;
+    }
+    cv_.notify_all();
+    copy_slice(parts - 1);
+    std::unique_lock<std::mutex> lk(m_);
+    done_.wait(lk, [this] { return pending_ == 0; });
+  }
+
+ private:
+  void copy_slice(size_t part) {
+    const size_t begin = part * slice_;
+    if (begin < bytes_) std::memcpy(dst_ + begin, src_ + begin, std::min(slice_, bytes_ - begin));
+  }
+  void run(int w) {
+    uint64_t seen = 0;
+    for (;;) {
+      {
+        std::unique_lock<std::mutex> lk(m_);
+        cv_.wait(lk, [&] { return generation_ != seen; });
+        seen = generation_;
+        if (stop_) return;
+      }
+      copy_slice(static_cast<size_t>(w));
+      std::lock_guard<std::mutex> lk(m_);
+      if (--pending_ == 0) done_.notify_one();
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex m_;
+  std::condition_variable cv_, done_;
+  uint64_t generation_ = 0;
+  bool stop_ = false;
+  char* dst_ = nullptr;
+  const char* src_ = nullptr;
+  size_t slice_ = 0, bytes_ = 0;
+  int pending_ = 0;
+};
+
+// Copies between PAGEABLE host memory and the device at close to PCIe rate:
+// the pool moves the data through two pinned pieces while the copy engine works
+// on the other one.  (cudaMemcpyAsync on pageable memory is staged by the
+// driver on one thread, ~5-10 GB/s.)  Pinned or registered host memory
+// (gj_host_alloc) needs none of this and is copied directly.
+class HostStager {
+ public:
+  static constexpr size_t kPiece = 32u << 20;
+  HostStager() : pool_(static_cast<int>(std::min(7u, std::max(1u, std::thread::hardware_concurrency() / 2)))) {}
+  ~HostStager() {
+    for (int b = 0; b < 2; ++b) {
+      if (pinned_[b]) cudaFreeHost(pinned_[b]);
+      if (ev_[b]) cudaEventDestroy(ev_[b]);
+    }
+  }
+  static bool is_pinned(const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeManaged;
+  }
+  // Enqueues on `st`; returns once the last piece has been handed to the copy engine.
+  cudaError_t to_device(void* d_dst, const void* h_src, size_t bytes, cudaStream_t st) {
+    if (bytes < (4u << 20) || is_pinned(h_src)) return cudaMemcpyAsync(d_dst, h_src, bytes, cudaMemcpyHostToDevice, st);
+    cudaError_t e = init();
+    for (size_t off = 0, k = 0; off < bytes && e == cudaSuccess; off += kPiece, ++k) {
+      const int b = static_cast<int>(k & 1);
+      const size_t len = std::min(kPiece, bytes - off);
+      e = cudaEventSynchronize(ev_[b]);  // the copy engine is done with this piece
+      if (e != cudaSuccess) break;
+      pool_.copy(pinned_[b], static_cast<const char*>(h_src) + off, len);
+      e = cudaMemcpyAsync(static_cast<char*>(d_dst) + off, pinned_[b], len, cudaMemcpyHostToDevice, st);
+      if (e == cudaSuccess) e = cudaEventRecord(ev_[b], st);
+    }
+    return e;
+  }
+  // Blocking: the data is in h_dst on return.
+  cudaError_t to_host(void* h_dst, const void* d_src, size_t bytes, cudaStream_t st) {
+    if (bytes < (4u << 20) || is_pinned(h_dst)) {
+      const cudaError_t e = cudaMemcpyAsync(h_dst, d_src, bytes, cudaMemcpyDeviceToHost, st);
+      return e == cudaSuccess ? cudaStreamSynchronize(st) : e;
+    }
+    cudaError_t e = init();
+    if (e != cudaSuccess) return e;
+    const size_t pieces = (bytes + kPiece - 1) / kPiece;
+    auto issue = [&](size_t k) {
+      const int b = static_cast<int>(k & 1);
+      const size_t off = k * kPiece, len = std::min(kPiece, bytes - off);
+      cudaError_t r = cudaMemcpyAsync(pinned_[b], static_cast<const char*>(d_src) + off, len, cudaMemcpyDeviceToHost, st);
+      return r == cudaSuccess ? cudaEventRecord(ev_[b], st) : r;
+    };
+    e = issue(0);
+    for (size_t k = 0; k < pieces && e == cudaSuccess; ++k) {
+      if (k + 1 < pieces) e = issue(k + 1);  // the other piece: its last contents were copied out already
+      if (e != cudaSuccess) break;
+      const int b = static_cast<int>(k & 1);
+      e = cudaEventSynchronize(ev_[b]);
+      if (e != cudaSuccess) break;
+      const size_t off = k * kPiece, len = std::min(kPiece, bytes - off);
+      pool_.copy(static_cast<char*>(h_dst) + off, pinned_[b], len);
+    }
+    return e;
+  }
+
+ private:
+  cudaError_t init() {
+    for (int b = 0; b < 2; ++b) {
+      if (!pinned_[b]) {
+        cudaError_t e = cudaHostAlloc(&pinned_[b], kPiece, cudaHostAllocDefault);
+        if (e != cudaSuccess) return e;
+        e = cudaEventCreateWithFlags(&ev_[b], cudaEventDisableTiming);
+        if (e != cudaSuccess) return e;
+      }
+    }
+    return cudaSuccess;
+  }
+  CopyPool pool_;
+  void* pinned_[2] = {nullptr, nullptr};
+  cudaEvent_t ev_[2] = {nullptr, nullptr};
+};
+
 }  // namespace gj
 
 struct gj_index {
@@ -90,6 +250,7 @@ struct gj_session {
   gj::DeviceBuffer d_all_row_ptr, d_all_ids;
   uint64_t pairs_n = 0, pairs_total = 0;
   bool pairs_valid = false;
+  std::unique_ptr<gj::HostStager> stager;  // created on first use with pageable host memory
   int latched_status = 0;
   uint64_t latched_bad = ~0ull;
 };
