@@ -23,6 +23,7 @@
 #include <span>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "geojoin/join.hpp"
@@ -161,11 +162,19 @@ inline std::vector<JoinPair> pairs(const DeviceIndex& ix, std::span<const LatLng
   std::vector<uint64_t> row_ptr(points.size() + 1);
   std::vector<uint32_t> ids(n_pairs);
   check(gj_pairs_copy(ix.session(), row_ptr.data(), ids.data()));
-  std::vector<JoinPair> out;
-  out.reserve(n_pairs);
-  for (size_t i = 0; i < points.size(); ++i) {
-    for (uint64_t k = row_ptr[i]; k < row_ptr[i + 1]; ++k) out.push_back(JoinPair{i, ids[k]});
-  }
+  // CSR -> the reference's array of {point_index, polygon_id}, a few threads over ranges of points
+  std::vector<JoinPair> out(n_pairs);
+  const size_t n = points.size();
+  const size_t workers = n_pairs < (1u << 22) ? 1 : std::min<size_t>(8, std::max(1u, std::thread::hardware_concurrency()));
+  auto expand = [&](size_t first, size_t last) {
+    for (size_t i = first; i < last; ++i) {
+      for (uint64_t k = row_ptr[i]; k < row_ptr[i + 1]; ++k) out[k] = JoinPair{i, ids[k]};
+    }
+  };
+  std::vector<std::thread> pool;
+  for (size_t w = 1; w < workers; ++w) pool.emplace_back(expand, n * w / workers, n * (w + 1) / workers);
+  expand(0, n / workers);
+  for (std::thread& t : pool) t.join();
   add_stats(s, stats);
   return out;
 }

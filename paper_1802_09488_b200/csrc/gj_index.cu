@@ -104,12 +104,12 @@ struct Analysis {
 // look in tb, otherwise 1 + ((polygon_id << 1) | interior).  Any level up to
 // tb's works (not only trie-node boundaries); the deepest whose padded window
 // has at most `max_entries` cells is taken.
-void build_dir16(const HostDirectory& tb, uint64_t max_entries, HostDirectory* d16) {
+void build_dir16(const HostDirectory& tb, uint64_t max_entries, int max_level, HostDirectory* d16) {
   *d16 = HostDirectory{};
   d16->pitch = 1;
   d16->table16.assign(1, 0);  // an empty window is just its all-miss padding
   if (tb.width == 0 || tb.height == 0) return;
-  for (int level = tb.level; level >= 0; --level) {
+  for (int level = std::min(tb.level, max_level); level >= 0; --level) {
     const int down = tb.level - level;
     const uint32_t x0 = tb.x0 >> down, y0 = tb.y0 >> down;
     const uint32_t w = ((tb.x0 + tb.width - 1) >> down) - x0 + 1;
@@ -507,7 +507,9 @@ int create_index(const gj_index_desc& d, int device, gj_index** out) {
   {
     uint64_t max16 = kMaxDir16Entries;
     if (const char* e = std::getenv("GJ_DIR16_MAX")) max16 = std::strtoull(e, nullptr, 10);  // tuning knob
-    build_dir16(an.dir2.table.empty() ? an.dir : an.dir2, max16, &an.dir16);
+    int max_level = 30;  // tuning knob: a density-matched stand-in over a small box can emulate the full-size tier
+    if (const char* e = std::getenv("GJ_DIR16_LEVEL_MAX")) max_level = std::atoi(e);
+    build_dir16(an.dir2.table.empty() ? an.dir : an.dir2, max16, max_level, &an.dir16);
   }
   size_t bytes = 0;
   if ((rc = upload(ix->d_arena, d.arena, d.node_count * kNodeSlots, &bytes)) != GJ_OK) return rc;

@@ -102,7 +102,8 @@ def run_config(config: int, n_points: int, scale: float, reps: int, check: int, 
         "config": config, "name": name, "mode": "exact" if spec.exact else "approx", "points": n,
         "ms": ms, "gpoints_per_s": n / ms / 1e6, "launches_per_step": (launches1 - launches0) // reps, "ids": want_ids, "stats_collected": want_stats,
         "index_nodes": int(info.node_count), "index_mb": info.device_bytes / 1e6, "n_polygons": int(info.n_polygons),
-        "dir1_level": info.dir_level, "dir2_level": info.dir2_level,
+        "dir1_level": info.dir_level, "dir2_level": info.dir2_level, "dir16_level": info.dir16_level,
+        "dir16_cells": [info.dir16_width, info.dir16_height], "dir2_cells": [info.dir2_width, info.dir2_height],
         "stats": dict(zip(["probes", "pip_tests", "false_hits", "solely_true_hits", "refinement_entered",
                            "candidate_refs"], stats)),
         "pairs_per_point": float(counts.sum()) / n,
@@ -125,8 +126,14 @@ def main():
     ap.add_argument("--check", type=int, default=5_000_000)
     ap.add_argument("--no-ids", action="store_true", help="counts + stats only (no first id per point)")
     ap.add_argument("--no-stats", action="store_true", help="do not collect JoinStats")
+    ap.add_argument("--dir16-level", type=int, default=0,
+                    help="cap the shared-memory tier at this grid level (a stand-in over a scaled-down box otherwise "
+                         "gets a finer first tier than the full-size box would: level 17 for the BASELINE box)")
     ap.add_argument("--pairs", type=int, default=0, help="also time gj_join_pairs_host on this many points")
     args = ap.parse_args()
+    if args.dir16_level:
+        import os
+        os.environ["GJ_DIR16_LEVEL_MAX"] = str(args.dir16_level)
     out = [run_config(c, args.points, args.scale, args.reps, args.check, not args.no_ids, args.pairs, not args.no_stats)
            for c in args.configs]
     (ROOT / "gpurun_out").mkdir(exist_ok=True)
