@@ -362,19 +362,29 @@ __device__ __forceinline__ double point_segment_dist_sq(double px, double py, do
 // reference's comparison is false as well.
 constexpr double kPipBoxMargin = 1e-9;
 
-// The box is the edge's bounding box widened by the margin:
-// [min(ax,bx) - m, max(ax,bx) + m] x [min(ay,by) - m, max(ay,by) + m].  Rounding
-// is monotone, so RN(min(a,b) - m) = min(RN(a - m), RN(b - m)): the test needs
-// no min/max, only the four widened coordinates per axis.
+// Sorts a (point, edge) pair without a division.  The box is the edge's
+// bounding box widened by the margin: [min(ax,bx) - m, max(ax,bx) + m] x
+// [min(ay,by) - m, max(ay,by) + m]; rounding is monotone, so RN(min(a,b) - m) =
+// min(RN(a - m), RN(b - m)) and the test needs no min/max, only the four widened
+// coordinates per axis.  Result bits:
+//   1  inside the box: the distance to the edge must be computed (geometry.cpp:186-193)
+//   2  the edge straddles the point's latitude (geometry.cpp:197) and the point
+//      is inside the box's x range: the crossing abscissa must be computed
+//   4  it straddles and the point is LEFT of the x range: the ray crosses, no
+//      arithmetic needed.  x_cross = ax + t (bx - ax) with t = RN(RN(qy - ay) /
+//      RN(by - ay)) in [0, 1 + 2^-52], so x_cross lies within 360 * 2^-51 <
+//      2e-13 of [min(ax,bx), max(ax,bx)] — far inside the 1e-9 margin — and
+//      qx < min - m implies qx < x_cross (to the right of max + m: no crossing).
 __device__ __forceinline__ uint32_t pip_edge_classify(double qx, double qy, double ax, double ay, double bx,
                                                       double by) {
   const double m = kPipBoxMargin;
-  const bool near_x = (qx >= __dsub_rn(ax, m) || qx >= __dsub_rn(bx, m)) &&
-                      (qx <= __dadd_rn(ax, m) || qx <= __dadd_rn(bx, m));
+  const bool ge_lo = qx >= __dsub_rn(ax, m) || qx >= __dsub_rn(bx, m);
+  const bool le_hi = qx <= __dadd_rn(ax, m) || qx <= __dadd_rn(bx, m);
+  const bool near_x = ge_lo && le_hi;
   const bool near_y = (qy >= __dsub_rn(ay, m) || qy >= __dsub_rn(by, m)) &&
                       (qy <= __dadd_rn(ay, m) || qy <= __dadd_rn(by, m));
   const bool straddles = (ay > qy) != (by > qy);  // geometry.cpp:197
-  return (near_x && near_y ? 1u : 0u) | (straddles ? 2u : 0u);
+  return (near_x && near_y ? 1u : 0u) | (straddles && near_x ? 2u : 0u) | (straddles && !ge_lo ? 4u : 0u);
 }
 
 // One edge record with a single 256-bit load (sm_100+).

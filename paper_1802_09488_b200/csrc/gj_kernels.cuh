@@ -837,6 +837,8 @@ refine_kernel(const __grid_constant__ DevIndex ix, RefineParams rp) {
         load_edge(ix.strip_edges + e, &ax, &ay, &bx, &by);
         kinds = pip_edge_classify(ox, oy, ax, ay, bx, by);
       }
+      if (kinds & 4u) atomicXor(&s_result[warp][src], 2u);  // crosses for certain: no division
+      kinds &= 3u;
       const uint32_t mask = __ballot_sync(0xffffffffu, kinds != 0u);
       if (kinds) s_list[warp][n_list + __popc(mask & lane_lt)] = make_uint2(e, (src << 2) | kinds);
       n_list += __popc(mask);

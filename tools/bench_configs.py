@@ -24,7 +24,7 @@ from tools import build_bundles  # noqa: E402
 
 
 def run_config(config: int, n_points: int, scale: float, reps: int, check: int, want_ids: bool = True,
-               pairs_points: int = 0, want_stats: bool = True):
+               pairs_points: int = 0, want_stats: bool = True, force_mode: str | None = None):
     import torch
 
     spec = synth.SPECS[config]
@@ -38,7 +38,8 @@ def run_config(config: int, n_points: int, scale: float, reps: int, check: int, 
     t0 = time.time()
     pts = synth.points_for(config, n, polys, scale=scale)
     gen_s = time.time() - t0
-    mode = capi.GJ_MODE_EXACT if spec.exact else capi.GJ_MODE_APPROX
+    exact = spec.exact if force_mode is None else force_mode == "exact"
+    mode = capi.GJ_MODE_EXACT if exact else capi.GJ_MODE_APPROX
 
     d_pts = torch.from_numpy(pts).cuda()
     n_ids = len(bundle.ids)
@@ -77,7 +78,7 @@ def run_config(config: int, n_points: int, scale: float, reps: int, check: int, 
     m = min(check, n)
     ox = golden_util.oracle_index(golden_util.parse_gjx(Path(path).read_bytes()))
     t0 = time.time()
-    want, total = ox.join_count(pts[:m], approx=not spec.exact, threads=16)
+    want, total = ox.join_count(pts[:m], approx=not exact, threads=16)
     cpu_s = time.time() - t0
     got, _, _ = sess.join_count(pts[:m], mode)
     got_map = {int(bundle.ids[k]): int(got[k]) for k in np.nonzero(got)[0]}
@@ -85,7 +86,7 @@ def run_config(config: int, n_points: int, scale: float, reps: int, check: int, 
     # ordered pairs on a smaller prefix
     mp = min(200_000, n)
     row_ptr, ids = sess.join_pairs(pts[:mp], mode)
-    pi, pid, ost, _ = ox.join(pts[:mp], approx=not spec.exact)
+    pi, pid, ost, _ = ox.join(pts[:mp], approx=not exact)
     gpi = np.repeat(np.arange(mp, dtype=np.uint64), np.diff(row_ptr.astype(np.int64)))
     ok_pairs = bool(np.array_equal(gpi, pi) and np.array_equal(ids, pid))
 
@@ -99,7 +100,7 @@ def run_config(config: int, n_points: int, scale: float, reps: int, check: int, 
         pairs_res = {"points": mq, "pairs": int(rp[-1]), "seconds": dt, "mpoints_per_s": mq / dt / 1e6,
                      "mpairs_per_s": int(rp[-1]) / dt / 1e6}
     res = {
-        "config": config, "name": name, "mode": "exact" if spec.exact else "approx", "points": n,
+        "config": config, "name": name, "mode": "exact" if exact else "approx", "points": n,
         "ms": ms, "gpoints_per_s": n / ms / 1e6, "launches_per_step": (launches1 - launches0) // reps, "ids": want_ids, "stats_collected": want_stats,
         "index_nodes": int(info.node_count), "index_mb": info.device_bytes / 1e6, "n_polygons": int(info.n_polygons),
         "dir1_level": info.dir_level, "dir2_level": info.dir2_level, "dir16_level": info.dir16_level,
@@ -126,6 +127,7 @@ def main():
     ap.add_argument("--check", type=int, default=5_000_000)
     ap.add_argument("--no-ids", action="store_true", help="counts + stats only (no first id per point)")
     ap.add_argument("--no-stats", action="store_true", help="do not collect JoinStats")
+    ap.add_argument("--mode", choices=["approx", "exact"], default=None, help="override the config's join mode")
     ap.add_argument("--dir16-level", type=int, default=0,
                     help="cap the shared-memory tier at this grid level (a stand-in over a scaled-down box otherwise "
                          "gets a finer first tier than the full-size box would: level 17 for the BASELINE box)")
@@ -134,7 +136,7 @@ def main():
     if args.dir16_level:
         import os
         os.environ["GJ_DIR16_LEVEL_MAX"] = str(args.dir16_level)
-    out = [run_config(c, args.points, args.scale, args.reps, args.check, not args.no_ids, args.pairs, not args.no_stats)
+    out = [run_config(c, args.points, args.scale, args.reps, args.check, not args.no_ids, args.pairs, not args.no_stats, args.mode)
            for c in args.configs]
     (ROOT / "gpurun_out").mkdir(exist_ok=True)
     (ROOT / "gpurun_out" / "bench_configs.json").write_text(json.dumps(out, indent=1))
