@@ -115,3 +115,36 @@ def test_config3_exact_is_subset_of_approx_full_size():
     c0, _, _ = s.join_count(pts[:cut], capi.GJ_MODE_EXACT)
     c1, _, _ = s.join_count(pts[cut:], capi.GJ_MODE_EXACT, base_index=cut)
     assert np.array_equal(c0 + c1, ce)
+
+
+def test_one_billion_points_in_one_launch():
+    """BASELINE configs[3] scale (1 B points per join): one device-resident
+    launch over 16 GB of points (the 100 M config-2 points tiled 10 times in
+    HBM) gives exactly 10x the counts and the same first ids in every copy —
+    exercises point indices up to 2^30 and the 32-bit tile arithmetic."""
+    import torch
+    bundle = _bundle(2)
+    s = bundle.session()
+    reps = 10
+    n = N_FULL * reps
+    pts = synth.points_for(2, N_FULL, None)
+    d_one = torch.from_numpy(pts).cuda()
+    d_pts = d_one.repeat(reps, 1).contiguous()
+    assert d_pts.shape == (n, 2)
+    d_counts = torch.zeros(len(bundle.ids), dtype=torch.int64, device="cuda")
+    d_first = torch.empty(n, dtype=torch.int32, device="cuda")
+    s.join_count_device(d_pts.data_ptr(), n, d_counts.data_ptr(), capi.GJ_MODE_APPROX,
+                        d_first_id_ptr=d_first.data_ptr(), sync=True)
+    d_counts1 = torch.zeros_like(d_counts)
+    d_first1 = torch.empty(N_FULL, dtype=torch.int32, device="cuda")
+    s.join_count_device(d_one.data_ptr(), N_FULL, d_counts1.data_ptr(), capi.GJ_MODE_APPROX,
+                        d_first_id_ptr=d_first1.data_ptr(), sync=True)
+    assert torch.equal(d_counts, d_counts1 * reps)
+    assert bool((d_first.view(reps, N_FULL) == d_first1.unsqueeze(0)).all())
+    # a ragged total (not a multiple of the tile) ending inside the last copy
+    m = n - 12_345
+    d_counts.zero_()
+    s.join_count_device(d_pts.data_ptr(), m, d_counts.data_ptr(), capi.GJ_MODE_APPROX, sync=True)
+    tail, _, _ = s.join_count(pts[N_FULL - 12_345:], capi.GJ_MODE_APPROX)
+    assert np.array_equal(d_counts.cpu().numpy().astype(np.uint64),
+                          d_counts1.cpu().numpy().astype(np.uint64) * reps - tail)
