@@ -254,3 +254,69 @@ def test_training_candidates_multi_chunk_and_errors():
     with pytest.raises(join.InvalidArgument) as e:
         s.training_candidates(pts)
     assert e.value.index == 4_200_123
+
+
+def _write(tmp_path, name, data: bytes):
+    p = tmp_path / name
+    p.write_bytes(data)
+    return p
+
+
+def test_corrupt_index_files_are_rejected(tmp_path):
+    """test_act.cpp:609-624 / test_join.cpp:317-318: empty, bad magic,
+    truncated and garbage snapshots raise CorruptionError, never crash."""
+    good = golden_util.gjx_bytes(golden_util.load("cfg2_tess16_approx4m"))
+    for name, data in [("empty.gjx", b""), ("magic.gjx", b"XXXXYYYYZZZZ"), ("garbage.gjx", b"not an index"),
+                       ("half.gjx", good[: len(good) // 2]), ("short.gjx", good[:100]),
+                       ("almost.gjx", good[:-9])]:
+        with pytest.raises(join.CorruptionError):
+            join.IndexBundle.load(_write(tmp_path, name, data), device=0)
+    with pytest.raises(OSError):
+        join.IndexBundle.load(tmp_path / "missing.gjx", device=0)
+    # the untouched bytes still load
+    join.IndexBundle.load(_write(tmp_path, "good.gjx", good), device=0).close()
+
+
+def test_structurally_corrupt_indexes_are_rejected():
+    """What the reference would only hit lazily while probing (act.cpp:141-153,
+    269, 667-669; join.cpp:111-114) is rejected when the index is created."""
+    fx = golden_util.load("cfg5_stars_scaled")  # has lookup-table records
+    g = golden_util.parse_gjx(golden_util.gjx_bytes(fx))
+
+    def make(**over):
+        a = dict(g)
+        a.update(over)
+        return join.IndexBundle.from_arrays(a["arena"], a["lut"], a["roots"], a["prefixes"], a["prefix_bits"],
+                                            a["k_max"], a["approx"], a["polygon_ids"], a["vtx_off"],
+                                            a["vtx_latlng"], device=0)
+
+    make().close()  # the unmodified arrays are fine
+    arena = g["arena"]
+    n_nodes = len(arena) // 256
+    links = np.flatnonzero(((arena & 3) == 0) & (arena != 0))
+    offsets = np.flatnonzero((arena & 3) == 3)
+    assert len(links) and len(offsets)
+
+    bad = arena.copy()
+    bad[links[0]] = np.uint64((n_nodes + 5) << 2)  # link past the arena
+    with pytest.raises(join.CorruptionError):
+        make(arena=bad)
+    bad = arena.copy()
+    bad[links[-1]] = np.uint64(1 << 2)  # link back to the root: not a forest
+    with pytest.raises(join.CorruptionError):
+        make(arena=bad)
+    bad = arena.copy()
+    bad[offsets[0]] = np.uint64(((len(g["lut"]) + 7) << 2) | 3)  # lookup-table offset out of range
+    with pytest.raises(join.CorruptionError):
+        make(arena=bad)
+    lut = g["lut"].copy()
+    off = int(arena[offsets[0]] >> np.uint64(2)) & 0x7FFFFFFF
+    lut[off] = np.uint32(len(lut))  # record longer than the table
+    with pytest.raises(join.CorruptionError):
+        make(lut=lut)
+    with pytest.raises(join.CorruptionError):
+        make(k_max=50)  # validate_act_config, act.cpp:38-42
+    roots = g["roots"].copy()
+    roots[0] = n_nodes + 1
+    with pytest.raises(join.CorruptionError):
+        make(roots=roots)
