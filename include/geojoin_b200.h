@@ -217,6 +217,9 @@ GJ_API int gj_join_count_host(gj_session* s, const double* latlng, uint64_t n,
 /* Same with points already resident in HBM (device pointers; asynchronous on
  * the session stream unless `sync` != 0).  d_counts/d_stats are device
  * arrays (u64[n_ids], u64[6]) that are ADDED to; d_first_id may be NULL.
+ * No overflow list here: a point with further pairs only carries GJ_MORE_FLAG,
+ * and in exact mode a point whose pairs depend on refinement reads
+ * GJ_DEFERRED (its pairs are in the counts); use the *_host calls for lists.
  * Errors (invalid point, unknown polygon) are latched in the session and
  * returned by gj_session_sync. */
 GJ_API int gj_join_count_device(gj_session* s, const double* d_latlng, uint64_t n,

@@ -116,6 +116,7 @@ struct JoinRequest {
   uint32_t* d_first_id;  // null = counts only
   DevStatus* d_status;
   uint64_t ovf_cap;      // records available in the session overflow buffers
+  bool ovf_discard;      // first ids wanted, the overflow list not (device-resident calls)
   uint64_t task_cap;
   uint8_t* d_task_pass;  // pairs mode
 };
@@ -143,6 +144,7 @@ int enqueue_join(gj_session* s, const JoinRequest& rq) {
   jp.ovf_id = s->d_ovf_id.as<uint32_t>();
   jp.ovf_ord = s->d_ovf_ord.as<uint32_t>();
   jp.ovf_cap = rq.d_first_id ? rq.ovf_cap : 0;
+  jp.ovf_discard = rq.ovf_discard ? 1 : 0;
   jp.task_point = s->d_task_point.as<uint32_t>();
   jp.task_slot = s->d_task_slot.as<uint32_t>();
   jp.task_ord = s->d_task_ord.as<uint32_t>();
@@ -181,7 +183,7 @@ int enqueue_join(gj_session* s, const JoinRequest& rq) {
     rp.ovf_cap = jp.ovf_cap;
     rp.task_pass = rq.d_task_pass;
     rp.status = rq.d_status;
-    rp.want_ids = rq.d_first_id ? 1 : 0;
+    rp.want_ids = rq.d_first_id && !rq.ovf_discard ? 1 : 0;
     const size_t counts_smem = static_cast<size_t>(n_ids) * 4;
     rp.smem_counts = counts_smem <= (32u << 10) ? 1 : 0;
     // persistent grid: exactly the blocks that are resident at once (a partial
@@ -839,14 +841,12 @@ int gj_join_count_device(gj_session* s, const double* d_latlng, uint64_t n, int 
   if (!resolve_exact(ix, mode, &exact)) return GJ_INVALID_ARGUMENT;
   GJ_CUDA(cudaSetDevice(ix.device));
   const uint64_t task_cap = exact ? n * std::max<uint64_t>(1, ix.max_cand_refs) : 0;
-  const uint64_t ovf_cap = d_first_id ? n * std::max<uint64_t>(1, ix.max_refs) : 0;
   if (task_cap >= (1ull << 32)) {
     set_error("candidate task capacity exceeds 2^32; split the launch");
     return GJ_INVALID_ARGUMENT;
   }
   int rc;
   if (exact && (rc = reserve_tasks(s, task_cap)) != GJ_OK) return rc;
-  if (d_first_id && (rc = reserve_overflow(s, ovf_cap)) != GJ_OK) return rc;
   JoinRequest rq{};
   rq.d_pts = reinterpret_cast<const double2*>(d_latlng);
   rq.n = n;
@@ -857,7 +857,8 @@ int gj_join_count_device(gj_session* s, const double* d_latlng, uint64_t n, int 
   rq.d_stats = reinterpret_cast<unsigned long long*>(d_stats);
   rq.d_first_id = d_first_id;
   rq.d_status = s->d_status.as<DevStatus>();
-  rq.ovf_cap = ovf_cap;
+  rq.ovf_cap = 0;  // the overflow list cannot be handed back from here: only the flag in the first id
+  rq.ovf_discard = true;
   rq.task_cap = task_cap;
   if ((rc = enqueue_join(s, rq)) != GJ_OK) return rc;
   if (sync) return gj_session_sync(s, nullptr);

@@ -54,6 +54,7 @@ struct JoinParams {
   uint32_t* ovf_id;
   uint32_t* ovf_ord;
   uint64_t ovf_cap;
+  int32_t ovf_discard;      // device-resident calls: nobody can read the list, do not record (and never fail on) it
   uint32_t* task_point;
   uint32_t* task_slot;
   uint32_t* task_ord;
@@ -214,8 +215,8 @@ __device__ __noinline__ uint32_t emit_general(const DevIndex& ix, const JoinPara
   const bool exact = jp.exact != 0;
   const uint32_t n_now = exact ? e.n_refs - e.n_cand : e.n_refs;
   uint32_t n_ovf = e.n_ovf;
-  if (n_ovf && ovf_base + n_ovf > jp.ovf_cap) {
-    atomicOr(&jp.status->flags, kErrOverflowCap);
+  if (n_ovf && (jp.ovf_discard || ovf_base + n_ovf > jp.ovf_cap)) {
+    if (!jp.ovf_discard) atomicOr(&jp.status->flags, kErrOverflowCap);
     n_ovf = 0;
   }
   const bool tasks_ok = e.n_tasks == 0 || task_base + e.n_tasks <= jp.task_cap;
