@@ -52,7 +52,8 @@ typedef enum {
   GJ_UNKNOWN_POLYGON = 4,  /* CorruptionError, src/join.cpp:111-114 */
   GJ_CUDA_ERROR = 5,
   GJ_CAPACITY = 6,         /* caller-provided output buffer too small */
-  GJ_IO_ERROR = 7
+  GJ_IO_ERROR = 7,
+  GJ_DATA_ERROR = 8        /* DataError: src/csv.cpp:58-77,91-94 */
 } gj_status;
 
 /* Join mode.  GJ_MODE_BUNDLE takes the mode negotiated at build time, as
@@ -166,6 +167,22 @@ GJ_API int gj_probe_points_host(gj_session* s, const double* latlng, uint64_t n,
  * at level k_max/2 (all 8 face values accepted, as in the batch kernels). */
 GJ_API int gj_probe_cells_host(gj_session* s, const uint64_t* raw_ids, uint64_t n,
                                uint64_t* out_entries);
+
+/* ---- point ingestion: CsvPointReader (include/geojoin/io.hpp:43-68,
+ * src/csv.cpp:26-100) over a text buffer, parsed on the device --------------
+ * A header row names the columns; every following non-empty row whose
+ * lat_column / lng_column fields are, after leading blanks, exactly one decimal
+ * number each (std::from_chars semantics, correctly rounded) and form a valid
+ * point is written to out_latlng in order, up to `cap` points; *n_points is
+ * their total (call again with a larger buffer if it exceeds cap).  Other rows
+ * are counted in *n_skipped, or — strict != 0 — end the call with
+ * GJ_DATA_ERROR and their 1-based line number in *bad_line.  GJ_DATA_ERROR
+ * with *bad_line == 0: the input is empty; == 1: the header lacks a column
+ * (gj_last_error names it, like the reference's message). */
+GJ_API int gj_points_from_csv_host(gj_session* s, const char* text, uint64_t n_bytes,
+                                   const char* lat_column, const char* lng_column, int strict,
+                                   double* out_latlng, uint64_t cap, uint64_t* n_points,
+                                   uint64_t* n_skipped, uint64_t* bad_line);
 
 /* ---- training pre-pass: the probe half of Act::train (act.cpp:414-440) ----
  * Finds the points whose probe lands in a candidate-bearing cell, i.e. for

@@ -11,13 +11,16 @@
 //   collect_metrics                 include/geojoin/join.hpp:148-149, src/join.cpp:309-314
 //
 // plus the probe half of Act::train (src/act.cpp:414-440) as a pre-pass:
-// training_candidates / expensive_fraction.
+// training_candidates / expensive_fraction, and load_points_csv
+// (include/geojoin/io.hpp:71-72) parsed on the device.
 //
 // so a call site switches by replacing `geojoin::` with `geojoin::gpu::` and
 // handing over a DeviceIndex made once from its IndexBundle.  Errors come back
 // as the reference's exception types.  Header-only; link libgeojoin_b200.so.
 #pragma once
 
+#include <fstream>
+#include <iterator>
 #include <map>
 #include <memory>
 #include <span>
@@ -26,6 +29,7 @@
 #include <thread>
 #include <vector>
 
+#include "geojoin/io.hpp"
 #include "geojoin/join.hpp"
 #include "geojoin_b200.h"
 
@@ -243,6 +247,27 @@ inline double expensive_fraction(const DeviceIndex& ix, std::span<const LatLng> 
   detail::check(gj_training_candidates_host(ix.session(), detail::as_doubles(points), points.size(), 0, nullptr, 0,
                                             &found, &bad));
   return static_cast<double>(found) / static_cast<double>(points.size());
+}
+
+// load_points_csv (io.hpp:71-72, csv.cpp:102-113) with the rows parsed on the
+// GPU; DataError for an unreadable or empty file, a missing column or — strict —
+// an invalid row, like the reference.
+inline std::vector<LatLng> load_points_csv(const DeviceIndex& ix, const std::string& path,
+                                           CsvPointReader::Options options = CsvPointReader::Options()) {
+  std::ifstream in(path, std::ios::binary);
+  if (!in) throw DataError("cannot open point file: " + path);
+  const std::string text((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+  size_t rows = 1;
+  for (char c : text) rows += c == '\n';
+  std::vector<LatLng> points(rows);
+  uint64_t n = 0, skipped = 0, bad_line = 0;
+  const int rc = gj_points_from_csv_host(ix.session(), text.data(), text.size(), options.lat_column.c_str(),
+                                         options.lng_column.c_str(), options.strict ? 1 : 0,
+                                         reinterpret_cast<double*>(points.data()), points.size(), &n, &skipped, &bad_line);
+  if (rc == GJ_DATA_ERROR) throw DataError(gj_last_error());
+  detail::check(rc);
+  points.resize(n);
+  return points;
 }
 
 }  // namespace geojoin::gpu

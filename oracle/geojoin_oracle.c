@@ -574,3 +574,140 @@ int gjo_join_count_threads(const gjo_index* ix, const double* latlng,
   free(partial);
   return rc;
 }
+
+/* ---- CSV point ingestion (csv.cpp) ------------------------------------- */
+
+/* parse_double, csv.cpp:39-45: leading spaces/tabs skipped, then the whole
+ * rest of the field must be one std::from_chars(general) number.  Restated:
+ * [-] digits [. digits] with at least one digit, optionally [eE][+-]digits —
+ * a malformed exponent is left unconsumed, so the field is rejected.  (The
+ * words inf / nan also parse there, but never to a valid coordinate, so they
+ * are rejected here with everything else that is not a decimal.)  The value is
+ * the correctly rounded double (strtod, like fast_float inside from_chars);
+ * overflow and a nonzero decimal that rounds to zero are range errors,
+ * subnormal results are not. */
+static int csv_parse_double(const char* b, const char* e, double* out) {
+  while (b != e && (*b == ' ' || *b == '\t')) ++b;
+  const char* p = b;
+  if (p != e && *p == '-') ++p;
+  int digits = 0, nonzero = 0;
+  while (p != e && *p >= '0' && *p <= '9') {
+    nonzero |= *p != '0';
+    ++digits;
+    ++p;
+  }
+  if (p != e && *p == '.') {
+    ++p;
+    while (p != e && *p >= '0' && *p <= '9') {
+      nonzero |= *p != '0';
+      ++digits;
+      ++p;
+    }
+  }
+  if (digits == 0) return 0;
+  if (p != e && (*p == 'e' || *p == 'E')) {
+    const char* q = p + 1;
+    if (q != e && (*q == '+' || *q == '-')) ++q;
+    if (q != e && *q >= '0' && *q <= '9') {
+      while (q != e && *q >= '0' && *q <= '9') ++q;
+      p = q;
+    }
+  }
+  if (p != e) return 0; /* ptr == end, csv.cpp:44 */
+  const size_t len = (size_t)(e - b);
+  char stack_buf[128];
+  char* buf = len < sizeof stack_buf ? stack_buf : (char*)malloc(len + 1);
+  if (!buf) return 0;
+  memcpy(buf, b, len);
+  buf[len] = 0;
+  const double v = strtod(buf, NULL);
+  if (buf != stack_buf) free(buf);
+  if (isinf(v) || (v == 0.0 && nonzero)) return 0; /* std::errc::result_out_of_range */
+  *out = v;
+  return 1;
+}
+
+/* The field_index-th comma-separated field of [b, e) (split_row, csv.cpp:26-37). */
+static int csv_field(const char* b, const char* e, uint64_t field_index, const char** fb, const char** fe) {
+  uint64_t k = 0;
+  const char* start = b;
+  for (const char* p = b;; ++p) {
+    if (p == e || *p == ',') {
+      if (k == field_index) {
+        *fb = start;
+        *fe = p;
+        return 1;
+      }
+      if (p == e) return 0;
+      ++k;
+      start = p + 1;
+    }
+  }
+}
+
+int gjo_csv_points(const char* text, uint64_t n_bytes, const char* lat_column,
+                   const char* lng_column, int strict, double* out_latlng,
+                   uint64_t cap, uint64_t* n_points, uint64_t* n_skipped,
+                   uint64_t* bad_line) {
+  const char* end = text + n_bytes;
+  *n_points = 0;
+  *n_skipped = 0;
+  if (bad_line) *bad_line = 0;
+  if (n_bytes == 0) return GJO_DATA_ERROR; /* csv.cpp:58-60: std::getline fails on an empty stream */
+  /* header: read_line strips one trailing CR (csv.cpp:47-51) */
+  const char* p = text;
+  const char* nl = memchr(p, '\n', (size_t)(end - p));
+  const char* le = nl ? nl : end;
+  const char* next = nl ? nl + 1 : end;
+  if (le != p && le[-1] == '\r') --le;
+  const size_t lat_len = strlen(lat_column), lng_len = strlen(lng_column);
+  uint64_t lat_index = 0, lng_index = 0;
+  int lat_found = 0, lng_found = 0;
+  for (uint64_t i = 0;; ++i) { /* csv.cpp:64-72: a later duplicate wins; lat is tested first */
+    const char *fb, *fe;
+    if (!csv_field(p, le, i, &fb, &fe)) break;
+    const size_t flen = (size_t)(fe - fb);
+    if (flen == lat_len && memcmp(fb, lat_column, flen) == 0) {
+      lat_index = i;
+      lat_found = 1;
+    } else if (flen == lng_len && memcmp(fb, lng_column, flen) == 0) {
+      lng_index = i;
+      lng_found = 1;
+    }
+  }
+  if (!lat_found || !lng_found) {
+    if (bad_line) *bad_line = 1;
+    return GJO_DATA_ERROR;
+  }
+  uint64_t line_number = 1, n = 0;
+  for (p = next; p != end;) { /* csv.cpp:80-100 */
+    nl = memchr(p, '\n', (size_t)(end - p));
+    le = nl ? nl : end;
+    next = nl ? nl + 1 : end;
+    if (le != p && le[-1] == '\r') --le;
+    ++line_number;
+    if (le != p) { /* empty lines are skipped without counting */
+      const char *ab, *ae, *ob, *oe;
+      double lat = 0, lng = 0;
+      const int ok = csv_field(p, le, lat_index, &ab, &ae) && csv_field(p, le, lng_index, &ob, &oe) &&
+                     csv_parse_double(ab, ae, &lat) && csv_parse_double(ob, oe, &lng) &&
+                     gjo_latlng_valid(lat, lng);
+      if (ok) {
+        if (n < cap) {
+          out_latlng[2 * n] = lat;
+          out_latlng[2 * n + 1] = lng;
+        }
+        ++n;
+      } else if (strict) {
+        if (bad_line) *bad_line = line_number;
+        *n_points = n;
+        return GJO_DATA_ERROR;
+      } else {
+        ++*n_skipped;
+      }
+    }
+    p = next;
+  }
+  *n_points = n;
+  return GJO_OK;
+}

@@ -11,14 +11,14 @@ import numpy as np
 
 from . import build as _build
 
-OK, INVALID_POINT, INVALID_LEVEL, CORRUPT_INDEX, UNKNOWN_POLYGON, CAPACITY = range(6)
+OK, INVALID_POINT, INVALID_LEVEL, CORRUPT_INDEX, UNKNOWN_POLYGON, CAPACITY, DATA_ERROR = range(7)
 
 _LIB = None
 
 
 class OracleError(RuntimeError):
     def __init__(self, status: int, bad_index: int | None = None):
-        names = ["OK", "INVALID_POINT", "INVALID_LEVEL", "CORRUPT_INDEX", "UNKNOWN_POLYGON", "CAPACITY"]
+        names = ["OK", "INVALID_POINT", "INVALID_LEVEL", "CORRUPT_INDEX", "UNKNOWN_POLYGON", "CAPACITY", "DATA_ERROR"]
         super().__init__(f"oracle status {names[status]} (index {bad_index})")
         self.status = status
         self.bad_index = bad_index
@@ -89,6 +89,19 @@ def pip_test(ring, points) -> np.ndarray:
     out = np.empty(len(p), np.uint8)
     lib().gjo_pip_tests(_p(r), C.c_uint64(len(r)), _p(p), C.c_uint64(len(p)), _p(out))
     return out.astype(bool)
+
+
+def csv_points(text: bytes, lat_column: str = "lat", lng_column: str = "lng", strict: bool = False):
+    """CsvPointReader restated (csv.cpp:26-100) -> (points (n, 2), skipped rows);
+    raises OracleError(DATA_ERROR, line) like the reference's DataError."""
+    cap = max(1, text.count(b"\n") + 1)
+    out = np.empty((cap, 2), np.float64)
+    n, skipped, bad = C.c_uint64(0), C.c_uint64(0), C.c_uint64(0)
+    rc = lib().gjo_csv_points(text, C.c_uint64(len(text)), lat_column.encode(), lng_column.encode(), int(strict),
+                              _p(out), C.c_uint64(cap), C.byref(n), C.byref(skipped), C.byref(bad))
+    if rc:
+        raise OracleError(rc, bad.value)
+    return out[:n.value].copy(), int(skipped.value)
 
 
 class OracleIndex:

@@ -184,6 +184,17 @@ def pip_test(ring, points) -> np.ndarray:
     return out.astype(bool)
 
 
+def csv_points(text: bytes, lat_column: str = "lat", lng_column: str = "lng", strict: bool = False):
+    """The reference's CsvPointReader over a text buffer -> (points (n, 2), skipped rows).
+    DataError (empty input, missing column, strict-mode bad row) raises RefError with the reference's message."""
+    cap = max(1, text.count(b"\n") + 1)
+    out = np.empty((cap, 2), np.float64)
+    n, skipped = C.c_uint64(0), C.c_uint64(0)
+    _check(lib().ref_csv_points(text, C.c_uint64(len(text)), lat_column.encode(), lng_column.encode(), int(strict),
+                                _p(out), C.c_uint64(cap), C.byref(n), C.byref(skipped)))
+    return out[:n.value].copy(), int(skipped.value)
+
+
 class RefBundle:
     """Owns a reference ``IndexBundle`` (join.hpp:89-115)."""
 

@@ -27,6 +27,7 @@
 #include <fstream>
 #include <map>
 #include <span>
+#include <sstream>
 #include <stdexcept>
 #include <string>
 #include <thread>
@@ -35,6 +36,7 @@
 #include "geojoin/act.hpp"
 #include "geojoin/cell_id.hpp"
 #include "geojoin/geometry.hpp"
+#include "geojoin/io.hpp"
 #include "geojoin/join.hpp"
 #include "geojoin/latlng.hpp"
 
@@ -461,6 +463,35 @@ int64_t ref_join_exact_count_threads(const void* h, const double* latlng,
     }
   });
   return rc == kOk ? m : rc;
+}
+
+// CsvPointReader (io.hpp:43-68, csv.cpp:54-100) over a text buffer: every valid
+// point in order.  Returns 0 on success; a DataError (empty input, missing
+// column, strict-mode bad row) comes back as kOther with its message in
+// ref_last_error().  *n_points is the total number of valid points even when it
+// exceeds `cap`.
+int ref_csv_points(const char* text, uint64_t n_bytes, const char* lat_column,
+                   const char* lng_column, int strict, double* out_latlng,
+                   uint64_t cap, uint64_t* n_points, uint64_t* n_skipped) {
+  return guarded([&] {
+    std::istringstream is(std::string(text, n_bytes));
+    CsvPointReader::Options opt;
+    opt.lat_column = lat_column;
+    opt.lng_column = lng_column;
+    opt.strict = strict != 0;
+    CsvPointReader reader(is, opt);
+    LatLng p;
+    uint64_t n = 0;
+    while (reader.next(p)) {
+      if (n < cap) {
+        out_latlng[2 * n] = p.lat;
+        out_latlng[2 * n + 1] = p.lng;
+      }
+      ++n;
+    }
+    *n_points = n;
+    *n_skipped = reader.skipped_rows();
+  });
 }
 
 // The `any_candidate` test Act::train applies to every training point

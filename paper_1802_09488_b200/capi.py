@@ -12,7 +12,7 @@ from pathlib import Path
 from . import _build
 
 GJ_OK, GJ_INVALID_POINT, GJ_INVALID_ARGUMENT, GJ_CORRUPT_INDEX, GJ_UNKNOWN_POLYGON, \
-    GJ_CUDA_ERROR, GJ_CAPACITY, GJ_IO_ERROR = range(8)
+    GJ_CUDA_ERROR, GJ_CAPACITY, GJ_IO_ERROR, GJ_DATA_ERROR = range(9)
 GJ_MODE_BUNDLE, GJ_MODE_APPROX, GJ_MODE_EXACT = 0, 1, 2
 GJ_NO_MATCH = 0xFFFFFFFF
 GJ_DEFERRED = 0xFFFFFFFE
@@ -24,7 +24,7 @@ EXPORTS = [
     "gj_index_get_info", "gj_index_ids", "gj_session_create", "gj_session_destroy", "gj_session_stream",
     "gj_host_alloc", "gj_host_free", "gj_cells_from_points_host", "gj_probe_points_host", "gj_probe_cells_host",
     "gj_join_count_host", "gj_join_count_device", "gj_session_sync", "gj_session_launches",
-    "gj_join_pairs_host", "gj_pairs_copy", "gj_training_candidates_host",
+    "gj_join_pairs_host", "gj_pairs_copy", "gj_training_candidates_host", "gj_points_from_csv_host",
 ]
 
 
@@ -110,6 +110,9 @@ def lib():
         L.gj_join_pairs_host.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_int, C.POINTER(C.c_uint64),
                                          C.POINTER(Stats), C.POINTER(C.c_uint64)]
         L.gj_pairs_copy.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+        L.gj_points_from_csv_host.argtypes = [C.c_void_p, C.c_char_p, C.c_uint64, C.c_char_p, C.c_char_p, C.c_int,
+                                              C.c_void_p, C.c_uint64, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
+                                              C.POINTER(C.c_uint64)]
         L.gj_training_candidates_host.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p,
                                                   C.c_uint64, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
         _LIB = L

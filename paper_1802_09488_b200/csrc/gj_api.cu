@@ -9,6 +9,7 @@
 #include <numeric>
 
 #include "gj_host.hpp"
+#include "gj_csv.cuh"
 #include "gj_kernels.cuh"
 
 namespace gj {
@@ -696,6 +697,156 @@ int gj_probe_points_host(gj_session* s, const double* latlng, uint64_t n, uint64
   GJ_CUDA(cudaMemcpyAsync(&s->h_status[3], d_status, sizeof(DevStatus), cudaMemcpyDeviceToHost, s->stream));
   GJ_CUDA(cudaStreamSynchronize(s->stream));
   return status_to_code(s->h_status[3], bad_index);
+}
+
+int gj_points_from_csv_host(gj_session* s, const char* text, uint64_t n_bytes, const char* lat_column,
+                            const char* lng_column, int strict, double* out_latlng, uint64_t cap, uint64_t* n_points,
+                            uint64_t* n_skipped, uint64_t* bad_line) {
+  if (!s || !lat_column || !lng_column || !n_points || !n_skipped || (n_bytes && !text) || (cap && !out_latlng)) {
+    return GJ_INVALID_ARGUMENT;
+  }
+  *n_points = 0;
+  *n_skipped = 0;
+  if (bad_line) *bad_line = 0;
+  if (n_bytes == 0) {  // csv.cpp:58-60
+    set_error("point file is empty, expected a CSV header");
+    return GJ_DATA_ERROR;
+  }
+  // ---- header, on the host (csv.cpp:54-78) ----
+  const char* end = text + n_bytes;
+  const char* nl = static_cast<const char*>(std::memchr(text, '\n', n_bytes));
+  const char* header_end = nl ? nl : end;
+  const char* data = nl ? nl + 1 : end;
+  if (header_end != text && header_end[-1] == '\r') --header_end;  // read_line, csv.cpp:47-51
+  const std::string lat_name(lat_column), lng_name(lng_column);
+  uint32_t lat_index = 0, lng_index = 0, column = 0;
+  bool lat_found = false, lng_found = false;
+  for (const char* field = text;; ++column) {  // split_row, csv.cpp:26-37
+    const char* comma = static_cast<const char*>(std::memchr(field, ',', static_cast<size_t>(header_end - field)));
+    const char* field_end = comma ? comma : header_end;
+    const std::string name(field, field_end);
+    if (name == lat_name) {  // a later duplicate wins; lat is tested first (csv.cpp:64-72)
+      lat_index = column;
+      lat_found = true;
+    } else if (name == lng_name) {
+      lng_index = column;
+      lng_found = true;
+    }
+    if (!comma) break;
+    field = comma + 1;
+  }
+  if (!lat_found || !lng_found) {
+    set_error("CSV header is missing column '" + (lat_found ? lng_name : lat_name) + "'");
+    if (bad_line) *bad_line = 1;
+    return GJ_DATA_ERROR;
+  }
+
+  gj_index& ix = *s->ix;
+  GJ_CUDA(cudaSetDevice(ix.device));
+  GJ_CUDA(s->d_csv_meta.reserve(16));
+  unsigned long long* d_skipped = s->d_csv_meta.as<unsigned long long>();
+  unsigned long long* d_first_bad = d_skipped + 1;
+  const unsigned wide = static_cast<unsigned>(ix.sm_count) * 8u;
+  constexpr uint64_t kChunkBytes = 64ull << 20;
+  uint64_t found = 0, skipped = 0, lines_before = 0;  // data lines in earlier chunks
+  for (const char* chunk = data; chunk != end;) {
+    // a chunk ends just past a newline (or at the end of the text)
+    const char* chunk_end = end;
+    if (static_cast<uint64_t>(end - chunk) > kChunkBytes) {
+      const char* back = static_cast<const char*>(memrchr(chunk, '\n', kChunkBytes));
+      const char* fwd = back ? back : static_cast<const char*>(std::memchr(chunk + kChunkBytes, '\n',
+                                                                            static_cast<size_t>(end - chunk - kChunkBytes)));
+      chunk_end = fwd ? fwd + 1 : end;
+    }
+    const uint64_t len = static_cast<uint64_t>(chunk_end - chunk);
+    const uint64_t n_pieces = (len + 15) / 16;
+    const uint32_t piece_blocks = static_cast<uint32_t>((n_pieces + kScanTile - 1) / kScanTile);
+    GJ_CUDA(s->d_csv_text.reserve(n_pieces * 16 + 16));
+    GJ_CUDA(s->d_csv_counts.reserve(n_pieces * 4));
+    GJ_CUDA(s->d_csv_offsets.reserve((n_pieces + 1) * 8));
+    GJ_CUDA(s->d_block_sums.reserve((static_cast<size_t>(piece_blocks) + 2) * 8));
+    char* d_text = s->d_csv_text.as<char>();
+    GJ_CUDA(stager_of(s).to_device(d_text, chunk, len, s->stream));
+    uint64_t* d_sums = s->d_block_sums.as<uint64_t>();
+    uint64_t* d_total = d_sums + piece_blocks + 1;
+    csv_count_newlines_kernel<<<wide, 256, 0, s->stream>>>(d_text, len, s->d_csv_counts.as<uint32_t>());
+    scan_block_sums_kernel<<<piece_blocks, kScanThreads, 0, s->stream>>>(s->d_csv_counts.as<uint32_t>(), n_pieces, d_sums);
+    scan_sums_kernel<<<1, kScanThreads, 0, s->stream>>>(d_sums, piece_blocks, d_total);
+    scan_apply_kernel<<<piece_blocks, kScanThreads, 0, s->stream>>>(s->d_csv_counts.as<uint32_t>(), n_pieces, d_sums, 0,
+                                                                    s->d_csv_offsets.as<uint64_t>());
+    s->launches += 4;
+    GJ_CUDA(cudaGetLastError());
+    uint64_t n_newlines = 0;
+    GJ_CUDA(cudaMemcpyAsync(&n_newlines, d_total, 8, cudaMemcpyDeviceToHost, s->stream));
+    GJ_CUDA(cudaStreamSynchronize(s->stream));
+    const bool open_last = chunk_end[-1] != '\n';  // only the last chunk can end without a newline
+    const uint64_t n_lines = n_newlines + (open_last ? 1 : 0);
+    const uint32_t line_blocks = static_cast<uint32_t>((n_lines + kScanTile - 1) / kScanTile);
+    GJ_CUDA(s->d_csv_lines.reserve((n_lines + 2) * 8));
+    GJ_CUDA(s->d_csv_status.reserve(n_lines * 4 + 16));
+    GJ_CUDA(s->d_csv_valid.reserve(n_lines * 4 + 16));
+    GJ_CUDA(s->d_csv_points.reserve(n_lines * 16 + 16));
+    GJ_CUDA(s->d_row_ptr.reserve((n_lines + 1) * 8));
+    GJ_CUDA(s->d_block_sums.reserve((static_cast<size_t>(std::max(piece_blocks, line_blocks)) + 2) * 8));
+    d_sums = s->d_block_sums.as<uint64_t>();
+    uint64_t* d_lines = s->d_csv_lines.as<uint64_t>();
+    const uint64_t edge[2] = {0, len + 1};  // start of line 0; the end sentinel of an unterminated last line
+    GJ_CUDA(cudaMemcpyAsync(d_lines, &edge[0], 8, cudaMemcpyHostToDevice, s->stream));
+    if (open_last) GJ_CUDA(cudaMemcpyAsync(d_lines + n_lines, &edge[1], 8, cudaMemcpyHostToDevice, s->stream));
+    const unsigned long long meta[2] = {0ull, ~0ull};
+    GJ_CUDA(cudaMemcpyAsync(d_skipped, meta, 16, cudaMemcpyHostToDevice, s->stream));
+    csv_line_starts_kernel<<<wide, 256, 0, s->stream>>>(d_text, len, s->d_csv_offsets.as<uint64_t>(), d_lines);
+    CsvParams cp{};
+    cp.text = d_text;
+    cp.n_bytes = len;
+    cp.line_start = d_lines;
+    cp.n_lines = n_lines;
+    cp.lat_index = lat_index;
+    cp.lng_index = lng_index;
+    cp.status = s->d_csv_status.as<uint32_t>();
+    cp.valid = s->d_csv_valid.as<uint32_t>();
+    cp.point = s->d_csv_points.as<double2>();
+    cp.n_skipped = d_skipped;
+    cp.first_bad = d_first_bad;
+    uint64_t n_valid = 0;
+    unsigned long long h_meta[2] = {0, ~0ull};
+    if (n_lines) {
+      uint64_t* d_vtotal = d_sums + line_blocks + 1;
+      csv_parse_rows_kernel<<<wide, 128, 0, s->stream>>>(cp);
+      scan_block_sums_kernel<<<line_blocks, kScanThreads, 0, s->stream>>>(cp.valid, n_lines, d_sums);
+      scan_sums_kernel<<<1, kScanThreads, 0, s->stream>>>(d_sums, line_blocks, d_vtotal);
+      scan_apply_kernel<<<line_blocks, kScanThreads, 0, s->stream>>>(cp.valid, n_lines, d_sums, 0,
+                                                                     s->d_row_ptr.as<uint64_t>());
+      s->launches += 5;
+      GJ_CUDA(cudaGetLastError());
+      GJ_CUDA(cudaMemcpyAsync(&n_valid, d_vtotal, 8, cudaMemcpyDeviceToHost, s->stream));
+      GJ_CUDA(cudaMemcpyAsync(h_meta, d_skipped, 16, cudaMemcpyDeviceToHost, s->stream));
+      GJ_CUDA(cudaStreamSynchronize(s->stream));
+    }
+    if (strict && h_meta[1] != ~0ull) {  // csv.cpp:91-94; the header is line 1
+      if (bad_line) *bad_line = lines_before + h_meta[1] + 2;
+      set_error("line " + std::to_string(lines_before + h_meta[1] + 2) + ": invalid point row");
+      return GJ_DATA_ERROR;
+    }
+    if (n_valid) {
+      GJ_CUDA(s->d_csv_out.reserve(n_valid * 16));
+      csv_scatter_kernel<<<wide, 256, 0, s->stream>>>(cp.valid, s->d_row_ptr.as<uint64_t>(), cp.point, n_lines,
+                                                      s->d_csv_out.as<double2>());
+      ++s->launches;
+      GJ_CUDA(cudaGetLastError());
+      const uint64_t room = cap > found ? cap - found : 0;
+      const uint64_t take = std::min(n_valid, room);
+      if (take) GJ_CUDA(stager_of(s).to_host(out_latlng + 2 * found, s->d_csv_out.ptr, take * 16, s->stream));
+      GJ_CUDA(cudaStreamSynchronize(s->stream));
+    }
+    found += n_valid;
+    skipped += h_meta[0];
+    lines_before += n_lines;
+    chunk = chunk_end;
+  }
+  *n_points = found;
+  *n_skipped = skipped;
+  return GJ_OK;
 }
 
 int gj_training_candidates_host(gj_session* s, const double* latlng, uint64_t n, uint64_t base_index,

@@ -248,6 +248,9 @@ struct gj_session {
   // materialised pairs of the last gj_join_pairs_host call, kept in HBM for gj_pairs_copy:
   // row_ptr[n + 1] (global offsets) and the polygon ids
   gj::DeviceBuffer d_all_row_ptr, d_all_ids;
+  // CSV ingestion scratch
+  gj::DeviceBuffer d_csv_text, d_csv_counts, d_csv_offsets, d_csv_lines, d_csv_status, d_csv_valid, d_csv_points,
+      d_csv_out, d_csv_meta;
   uint64_t pairs_n = 0, pairs_total = 0;
   bool pairs_valid = false;
   std::unique_ptr<gj::HostStager> stager;  // created on first use with pageable host memory

@@ -48,6 +48,15 @@ class CudaError(RuntimeError):
     pass
 
 
+class DataError(RuntimeError):
+    """geojoin::DataError (io.hpp:27-31): empty point file, missing CSV column,
+    or — strict mode — an invalid row; ``line`` is its 1-based line number."""
+
+    def __init__(self, msg, line=None):
+        super().__init__(msg)
+        self.line = line
+
+
 def _raise(rc: int, bad_index=None):
     msg = capi.lib().gj_last_error().decode()
     if rc == capi.GJ_INVALID_POINT:
@@ -60,6 +69,8 @@ def _raise(rc: int, bad_index=None):
         raise CapacityError(msg)
     if rc == capi.GJ_IO_ERROR:
         raise OSError(msg)
+    if rc == capi.GJ_DATA_ERROR:
+        raise DataError(msg, bad_index)
     raise CudaError(msg)
 
 
@@ -238,6 +249,19 @@ class Session:
         _check(capi.lib().gj_probe_cells_host(self._h, _vp(r), len(r), _vp(out)))
         return out
 
+    # ---- point ingestion ----
+    def points_from_csv(self, text: bytes, lat_column: str = "lat", lng_column: str = "lng", strict: bool = False):
+        """CsvPointReader (io.hpp:43-68, csv.cpp:54-100) over a text buffer, parsed on
+        the GPU -> (points float64 (n, 2), skipped rows)."""
+        text = bytes(text)
+        cap = max(1, text.count(b"\n") + 1)
+        out = np.empty((cap, 2), np.float64)
+        n, skipped, bad = C.c_uint64(0), C.c_uint64(0), C.c_uint64(0)
+        _check(capi.lib().gj_points_from_csv_host(self._h, text, len(text), lat_column.encode(), lng_column.encode(),
+                                                  int(strict), _vp(out), cap, C.byref(n), C.byref(skipped),
+                                                  C.byref(bad)), bad)
+        return out[:n.value].copy() if n.value < cap else out, int(skipped.value)
+
     # ---- training pre-pass ----
     def training_candidates(self, points, base_index: int = 0) -> np.ndarray:
         """Ascending global indices of the points whose probe lands in a
@@ -372,3 +396,14 @@ def expensive_fraction(bundle: IndexBundle, points) -> float:
     share of the points whose probe meets a candidate reference; 0 for no points."""
     p = _points(points)
     return 0.0 if len(p) == 0 else len(training_candidates(bundle, p)) / len(p)
+
+
+def load_points_csv(bundle: IndexBundle, path, lat_column: str = "lat", lng_column: str = "lng",
+                    strict: bool = False) -> np.ndarray:
+    """load_points_csv (io.hpp:71-72, csv.cpp:102-113): the valid points of a CSV
+    file, parsed on the bundle's GPU."""
+    try:
+        text = open(path, "rb").read()
+    except OSError as exc:
+        raise DataError(f"cannot open point file: {path}") from exc
+    return bundle.session().points_from_csv(text, lat_column, lng_column, strict)[0]

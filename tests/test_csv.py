@@ -1,0 +1,144 @@
+"""Point ingestion: the reference's CsvPointReader
+(io.hpp:43-68, csv.cpp:26-100).  CPU: the C oracle against the fixture the
+compiled reference produced (tests/golden/make_csv_golden.py) and against the
+live reference; GPU: the device parser through the C ABI against both,
+bit-exact (decimal -> double correctly rounded, like std::from_chars)."""
+import numpy as np
+import pytest
+
+from oracle import oracle
+from tests import golden_util
+
+CASES = ["edge", "random_a", "random_b", "random_c", "dup_columns", "renamed", "header_only"]
+
+
+def _case(name):
+    fx = golden_util.load("csv_points")
+    text = fx[f"{name}__text"].tobytes()
+    lat, lng = fx[f"{name}__cols"].tobytes().decode().split(",")
+    return text, lat, lng, fx[f"{name}__points"], int(fx[f"{name}__skipped"][0])
+
+
+def _same_bits(a, b):
+    return a.shape == b.shape and np.array_equal(np.ascontiguousarray(a).view(np.uint64),
+                                                 np.ascontiguousarray(b).view(np.uint64))
+
+
+def _stress_text(seed, n):
+    """Rows in every number style std::from_chars accepts, with long digit
+    strings, ties, subnormals and junk mixed in."""
+    rng = np.random.default_rng(seed)
+    lat = rng.uniform(-91, 91, n)
+    lng = rng.uniform(-181, 181, n)
+    rows = ["a,lat,b,lng"]
+    junk = ["", "x", "1e", "+1", "1 ", "nan", "inf", "1e400", "1e-400", "0x1p3", "--1", "1..2", ".", "1,2"]
+    for k in range(n):
+        s = int(rng.integers(0, 10))
+        if s == 0:
+            a, o = repr(float(lat[k])), repr(float(lng[k]))
+        elif s == 1:
+            a, o = f"{lat[k]:.{int(rng.integers(0, 25))}f}", f"{lng[k]:.{int(rng.integers(0, 40))}f}"
+        elif s == 2:
+            a, o = f"{lat[k]:.{int(rng.integers(0, 20))}e}", f"{lng[k]:.{int(rng.integers(0, 30))}E}"
+        elif s == 3:  # exact binary expansions: ties and near-ties at 60+ digits
+            a, o = f"{lat[k]:.70f}", f"{np.nextafter(lng[k], 0) / 2 + lng[k] / 2:.80f}"
+        elif s == 4:
+            a, o = f"{lat[k] * 1e-300:.17e}", f"{lng[k] * 1e-310:.17e}"  # tiny, subnormal
+        elif s == 5:
+            a, o = f"{lat[k] * 10 ** -int(rng.integers(20, 330)):.{int(rng.integers(0, 19))}e}", f"{int(lng[k])}"
+        elif s == 6:
+            a, o = f" \t{lat[k]:.12g}", f"\t {lng[k]:.7g}"
+        elif s == 7:
+            a, o = f"{int(lat[k] * 1e15)}e-15", f"{int(lng[k] * 1e18)}E-18"
+        elif s == 8:
+            a, o = junk[int(rng.integers(0, len(junk)))], f"{lng[k]:.5f}"
+        else:
+            a, o = f"{lat[k]:.5f}", junk[int(rng.integers(0, len(junk)))]
+        rows.append(f"{k},{a},z,{o}")
+        if rng.random() < 0.02:
+            rows.append("")
+    return ("\n".join(rows) + "\n").encode()
+
+
+# ---- CPU: the oracle is pinned to the reference -------------------------------------------------
+@pytest.mark.parametrize("name", CASES)
+def test_oracle_csv_matches_reference_fixture(name):
+    text, lat, lng, want, skipped = _case(name)
+    got, sk = oracle.csv_points(text, lat, lng)
+    assert _same_bits(got, want) and sk == skipped
+
+
+def test_oracle_csv_matches_live_reference():
+    from oracle import ref
+    if not ref.available():
+        pytest.skip("oracle/_ref not built")
+    text = _stress_text(0xC5B1, 20000)
+    want, wsk = ref.csv_points(text, "lat", "lng")
+    got, sk = oracle.csv_points(text, "lat", "lng")
+    assert _same_bits(got, want) and sk == wsk and len(got) > 10000 and sk > 1000
+
+
+def test_oracle_csv_errors():
+    for text, line in [(b"", 0), (b"\n1,2\n", 1), (b"lat,x\n1,2\n", 1), (b"x,lng\n1,2\n", 1)]:
+        with pytest.raises(oracle.OracleError) as e:
+            oracle.csv_points(text)
+        assert e.value.status == oracle.DATA_ERROR and e.value.bad_index == line
+    with pytest.raises(oracle.OracleError) as e:  # csv.cpp:91-94: the header is line 1, empty lines count
+        oracle.csv_points(b"lat,lng\n1,2\n\nbad,3\n4,5\n", strict=True)
+    assert e.value.bad_index == 4
+    assert len(oracle.csv_points(b"lat,lng\n1,2\n\n4,5\n", strict=True)[0]) == 2
+
+
+# ---- GPU: the device parser -----------------------------------------------------------------------
+def _session():
+    from paper_1802_09488_b200 import join
+    bundle = join.IndexBundle.load(golden_util.bundle_file("join_small_exact"), device=0)
+    return bundle, bundle.session()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", CASES)
+def test_gpu_csv_matches_reference_fixture(name):
+    text, lat, lng, want, skipped = _case(name)
+    bundle, s = _session()
+    got, sk = s.points_from_csv(text, lat, lng)
+    assert _same_bits(got, want) and sk == skipped
+    bundle.close()
+
+
+@pytest.mark.gpu
+def test_gpu_csv_stress_matches_oracle():
+    bundle, s = _session()
+    text = _stress_text(0xC5B2, 400_000)
+    want, wsk = oracle.csv_points(text, "lat", "lng")
+    got, sk = s.points_from_csv(text, "lat", "lng")
+    assert _same_bits(got, want) and sk == wsk and len(got) > 200_000
+    # CRLF, no trailing newline, other column order
+    text2 = text.replace(b"\n", b"\r\n").rstrip(b"\r\n")
+    got2, sk2 = s.points_from_csv(text2, "lat", "lng")
+    assert _same_bits(got2, want) and sk2 == wsk
+    bundle.close()
+
+
+@pytest.mark.gpu
+def test_gpu_csv_errors_and_file_loader(tmp_path):
+    from paper_1802_09488_b200 import join
+    bundle, s = _session()
+    for text, line in [(b"", 0), (b"\n1,2\n", 1), (b"lat,x\n1,2\n", 1), (b"x,lng\n1,2\n", 1)]:
+        with pytest.raises(join.DataError) as e:
+            s.points_from_csv(text)
+        assert e.value.line == line
+    with pytest.raises(join.DataError) as e:
+        s.points_from_csv(b"lat,lng\n1,2\n\nbad,3\n4,5\n", strict=True)
+    assert e.value.line == 4 and "line 4" in str(e.value)
+    with pytest.raises(join.DataError) as e:
+        s.points_from_csv(b"lat,x\n1,2\n")
+    assert "missing column 'lng'" in str(e.value)
+    pts, sk = s.points_from_csv(b"lat,lng\n1,2\n\n4,5\n", strict=True)
+    assert pts.tolist() == [[1.0, 2.0], [4.0, 5.0]] and sk == 0
+    p = tmp_path / "pts.csv"
+    p.write_bytes(b"id,lat,lng\n7,40.5,-73.25\n8,91,0\n9,-12.125,179.5\n")
+    assert join.load_points_csv(bundle, p).tolist() == [[40.5, -73.25], [-12.125, 179.5]]
+    with pytest.raises(join.DataError):
+        join.load_points_csv(bundle, tmp_path / "missing.csv")
+    bundle.close()
