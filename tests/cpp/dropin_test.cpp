@@ -7,6 +7,7 @@
 // /root/reference exists; run on the GPU box by tests/test_gpu_dropin.py.
 #include <cmath>
 #include <cstdio>
+#include <fstream>
 #include <random>
 #include <vector>
 
@@ -86,6 +87,33 @@ void compare(const IndexBundle& bundle, const std::vector<LatLng>& points) {
   EXPECT(gpu::training_candidates(dev, points) == want_candidates);
   EXPECT(gpu::expensive_fraction(dev, points) ==
          static_cast<double>(want_candidates.size()) / static_cast<double>(points.size()));
+
+  // load_points_csv (csv.cpp:102-113): rows parsed on the GPU against the reference's reader
+  {
+    const std::string path = "/tmp/geojoin_dropin_points.csv";
+    {
+      std::ofstream csv(path);
+      csv << "id,lng,note,lat\n";
+      csv.precision(17);
+      for (size_t i = 0; i < 5000; ++i) {
+        csv << i << ',' << points[i].lng << ",x," << points[i].lat << (i % 3 ? "\n" : "\r\n");
+        if (i % 500 == 0) csv << "bad,row\n\n" << i << ",181,y,5\n";
+      }
+    }
+    const std::vector<LatLng> want = load_points_csv(path);
+    const std::vector<LatLng> got = gpu::load_points_csv(dev, path);
+    EXPECT(got.size() == want.size() && got.size() == 5000);
+    bool same = got.size() == want.size();
+    for (size_t i = 0; same && i < got.size(); ++i) same = got[i].lat == want[i].lat && got[i].lng == want[i].lng;
+    EXPECT(same);
+    CsvPointReader::Options strict;
+    strict.strict = true;
+    bool cpu_threw = false, gpu_threw = false;
+    try { load_points_csv(path, strict); } catch (const DataError&) { cpu_threw = true; }
+    try { gpu::load_points_csv(dev, path, strict); } catch (const DataError&) { gpu_threw = true; }
+    EXPECT(cpu_threw && gpu_threw);
+    std::remove(path.c_str());
+  }
 
   // a single bad coordinate aborts the join with std::invalid_argument on both sides
   std::vector<LatLng> bad = points;

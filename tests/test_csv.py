@@ -142,3 +142,33 @@ def test_gpu_csv_errors_and_file_loader(tmp_path):
     with pytest.raises(join.DataError):
         join.load_points_csv(bundle, tmp_path / "missing.csv")
     bundle.close()
+
+
+@pytest.mark.gpu
+def test_gpu_csv_multi_chunk_and_throughput():
+    """More text than one 64 MB device chunk: chunk seams fall on line ends and
+    do not show in the result; prints the device parser's throughput."""
+    import time
+    bundle, s = _session()
+    rng = np.random.default_rng(0xC5B3)
+    n = 3_000_000
+    lat = rng.uniform(-90, 90, n)
+    lng = rng.uniform(-180, 180, n)
+    body = "\n".join(f"{a!r},{o:.9f}" for a, o in zip(lat.tolist(), lng.tolist()))
+    text = ("lat,lng\n" + body + "\n").encode()
+    assert len(text) > (64 << 20)
+    s.points_from_csv(text[:1 << 20].rsplit(b"\n", 1)[0])
+    t0 = time.time()
+    got, sk = s.points_from_csv(text)
+    dt = time.time() - t0
+    print(f"\ncsv: {len(text) / 1e6:.0f} MB, {n} rows in {dt:.3f} s = {len(text) / dt / 1e9:.2f} GB/s, {n / dt / 1e6:.1f} M rows/s")
+    assert sk == 0 and len(got) == n
+    assert np.array_equal(got[:, 0], lat)  # repr() round-trips exactly
+    assert np.array_equal(got[:, 1], np.array([float(f"{o:.9f}") for o in lng[:200_000].tolist()]
+                                              + got[200_000:, 1].tolist()))
+    t0 = time.time()
+    want, _ = oracle.csv_points(text)
+    cpu = time.time() - t0
+    print(f"csv: CPU oracle (strtod, one thread) {cpu:.2f} s = {len(text) / cpu / 1e6:.0f} MB/s")
+    assert _same_bits(got, want)
+    bundle.close()
