@@ -30,6 +30,16 @@ struct SmemPlan {
   size_t total;
 };
 
+}  // namespace
+
+size_t k1_smem_besides_tier(size_t n_ids) {
+  const size_t queues = static_cast<size_t>(kJoinThreads / 32) * kQueueBytesPerWarp;
+  const size_t hist_row = (n_ids + 1) * 4;
+  return queues + (hist_row <= (64u << 10) ? hist_row : 0) + 64;  // + alignment slack
+}
+
+namespace {
+
 // Shared memory of K1: [16-bit tier | per-warp queues | histogram].  The SM's
 // L1 is what shared memory leaves of 256 KB, in carve-out steps, and K1 needs
 // L1 for its loads in flight (measured on config 2: 0.53 ms per 100 M points
@@ -50,7 +60,9 @@ SmemPlan plan_smem(const gj_index& ix) {
 #endif
   const size_t one = (static_cast<size_t>(ix.dev.n_ids) + 1) * 4;  // + the spare row non-emitting lanes count into
   uint32_t rep = 0;
-  if (ix.dev.n_ids && at + one <= limit) {
+  const size_t last_good_step = (196u - 1u) << 10;  // above it: the 228 KB carve-out cliff
+  const bool hist_fits = at + one <= limit && (at + one <= last_good_step || at > last_good_step);
+  if (ix.dev.n_ids && hist_fits) {
     size_t step = limit;  // carve-out steps hold 1 KB of system shared memory per CTA
     for (size_t kb : {64, 100, 132, 164, 196}) {
       if (at + one <= (kb - 1) << 10) {
@@ -154,6 +166,20 @@ int enqueue_join(gj_session* s, const JoinRequest& rq) {
   jp.smem_queue_off = sp.queue_off;
   jp.smem_hist_off = sp.hist_off;
   jp.hist_rep = sp.hist_rep;
+  // No room for the histogram in shared memory: count into per-SM copies (at most 1 GB of them)
+  const size_t priv_bytes = static_cast<size_t>(ix.sm_count) * n_ids * 4;
+  const bool k2_local = static_cast<size_t>(n_ids) * 4 <= (32u << 10);
+  const bool want_priv = n_ids != 0 && priv_bytes <= (1ull << 30) && (sp.hist_rep == 0 || (rq.exact && !k2_local));
+  uint32_t* d_priv = nullptr;
+  if (want_priv) {
+    if (s->d_counts_priv.bytes < priv_bytes) {
+      GJ_CUDA(s->d_counts_priv.reserve(priv_bytes));
+      GJ_CUDA(cudaMemsetAsync(s->d_counts_priv.ptr, 0, priv_bytes, s->stream));
+    }
+    d_priv = s->d_counts_priv.as<uint32_t>();
+  }
+  jp.counts_priv = sp.hist_rep == 0 ? d_priv : nullptr;
+  jp.n_priv = static_cast<uint32_t>(ix.sm_count);
   jp.exact = rq.exact ? 1 : 0;
 
   const int variant = (rq.d_first_id ? 4 : 0) | (rq.want_stats ? 2 : 0) | (ix.dev.ids_dense && sp.hist_rep ? 1 : 0);
@@ -187,6 +213,8 @@ int enqueue_join(gj_session* s, const JoinRequest& rq) {
     rp.want_ids = rq.d_first_id && !rq.ovf_discard ? 1 : 0;
     const size_t counts_smem = static_cast<size_t>(n_ids) * 4;
     rp.smem_counts = counts_smem <= (32u << 10) ? 1 : 0;
+    rp.counts_priv = rp.smem_counts ? nullptr : d_priv;
+    rp.n_priv = static_cast<uint32_t>(ix.sm_count);
     // persistent grid: exactly the blocks that are resident at once (a partial
     // second wave of a grid-stride kernel only adds a tail)
     int per_sm = 0;
@@ -194,6 +222,12 @@ int enqueue_join(gj_session* s, const JoinRequest& rq) {
                                                           rp.smem_counts ? counts_smem : 0));
     const unsigned blocks = static_cast<unsigned>(ix.sm_count) * static_cast<unsigned>(std::max(per_sm, 1));
     refine_kernel<<<blocks, kRefineThreads, rp.smem_counts ? counts_smem : 0, s->stream>>>(ix.dev, rp);
+    ++s->launches;
+    GJ_CUDA(cudaGetLastError());
+  }
+  if (d_priv) {
+    fold_private_counts_kernel<<<std::max(1u, std::min((n_ids + 255u) / 256u, static_cast<unsigned>(ix.sm_count) * 8u)), 256, 0,
+                                 s->stream>>>(d_priv, static_cast<uint32_t>(ix.sm_count), n_ids, rq.d_counts);
     ++s->launches;
     GJ_CUDA(cudaGetLastError());
   }

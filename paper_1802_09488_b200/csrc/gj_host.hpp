@@ -20,6 +20,10 @@ namespace gj {
 
 void set_error(const std::string& msg);
 int cuda_fail(cudaError_t e, const char* what);
+// Shared memory K1 needs besides its first tier (per-warp queues, one histogram row set for `n_ids`
+// polygons when that fits), so the index builder can size the tier to stay below the 228 KB carve-out
+// step (defined next to the kernel's launch plan, gj_api.cu).
+size_t k1_smem_besides_tier(size_t n_ids);
 
 #define GJ_CUDA(call)                                  \
   do {                                                 \
@@ -238,6 +242,7 @@ struct gj_session {
   uint64_t launches = 0;
   // scratch
   gj::DeviceBuffer d_status, d_counts, d_stats;
+  gj::DeviceBuffer d_counts_priv;  // [sm_count][n_ids] u32, kept zero between launches
   gj::DeviceBuffer d_points[3], d_first_id[3], d_entries;
   gj::DeviceBuffer d_ovf_point, d_ovf_id, d_ovf_ord;
   gj::DeviceBuffer d_task_point, d_task_slot, d_task_ord, d_task_pass;

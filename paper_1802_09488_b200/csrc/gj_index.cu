@@ -507,7 +507,10 @@ int create_index(const gj_index_desc& d, int device, gj_index** out) {
     an.dir.table.assign(1, 0u);
   }
   {
-    uint64_t max16 = kMaxDir16Entries;
+    // the tier, K1's queues and one histogram row set must stay inside the 196 KB carve-out step
+    const size_t besides = k1_smem_besides_tier(n_ids);
+    const size_t step = (196u - 1u) << 10;
+    uint64_t max16 = std::min<uint64_t>(kMaxDir16Entries, step > besides ? (step - besides) / 2 : 0);
     if (const char* e = std::getenv("GJ_DIR16_MAX")) max16 = std::strtoull(e, nullptr, 10);  // tuning knob
     int max_level = 30;  // tuning knob: a density-matched stand-in over a small box can emulate the full-size tier
     if (const char* e = std::getenv("GJ_DIR16_LEVEL_MAX")) max_level = std::atoi(e);

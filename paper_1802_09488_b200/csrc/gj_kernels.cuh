@@ -62,7 +62,9 @@ struct JoinParams {
   DevStatus* status;
   uint32_t smem_queue_off;  // bytes: per-warp open-point queues
   uint32_t smem_hist_off;   // bytes
-  uint32_t hist_rep;        // replicas per slot (power of two), 0 = global atomics
+  uint32_t hist_rep;        // replicas per slot (power of two), 0 = not in shared memory
+  uint32_t* counts_priv;    // hist_rep == 0: [n_priv][n_ids] u32 copies, zero on entry; may be null
+  uint32_t n_priv;          // CTA b counts into copy b % n_priv
   int32_t exact;
 };
 
@@ -132,11 +134,16 @@ __device__ __forceinline__ void st32_if(uint32_t* p, uint32_t v, bool pred) {
 }
 
 // Where K1 counts: a replicated shared-memory histogram (slot * rep + lane
-// replica) or, for id tables too large for it, global atomics.
+// replica) or, for id tables too large for it, a private u32 copy of the counts in
+// global memory, one per resident CTA (folded into the caller's u64 counts afterwards).
+// Atomics of all SMs on ONE shared copy serialise in L2 on every hot polygon:
+// measured 13.4 ms instead of 0.36 ms per 100 M points with 289 polygons, 7.5 ms
+// instead of 0.9 ms with 1600.
 struct HistRef {
   uint32_t smem;      // shared address of the histogram
-  uint32_t rep;       // replicas per slot (power of two), 0 = global atomics
+  uint32_t rep;       // replicas per slot (power of two), 0 = not in shared memory
   uint32_t lane_rep;  // lane & (rep - 1)
+  uint32_t* priv;     // rep == 0: this SM's copy (null: straight into jp.counts)
 };
 
 template <bool kDense>
@@ -145,6 +152,8 @@ __device__ __forceinline__ void count_slot(const DevIndex& ix, const JoinParams&
   const uint32_t slot = kDense ? id : id_to_slot(ix, id);
   if (h.rep) {
     red_inc_shared_if(h.smem + (slot * h.rep + h.lane_rep) * 4u, true);
+  } else if (h.priv) {
+    atomicAdd(h.priv + slot, 1u);
   } else {
     atomicAdd(&jp.counts[slot], 1ull);
   }
@@ -310,7 +319,8 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
 
   // loop invariants in registers
   const uint32_t s_table = smem_addr(smem);
-  const HistRef hist{smem_addr(smem + jp.smem_hist_off), jp.hist_rep, lane & (jp.hist_rep ? jp.hist_rep - 1u : 0u)};
+  const HistRef hist{smem_addr(smem + jp.smem_hist_off), jp.hist_rep, lane & (jp.hist_rep ? jp.hist_rep - 1u : 0u),
+                     jp.counts_priv ? jp.counts_priv + static_cast<size_t>(blockIdx.x % jp.n_priv) * ix.n_ids : nullptr};
   const uint32_t s_q2 = smem_addr(smem + jp.smem_queue_off) + warp * kQueueBytesPerWarp;
   const uint32_t s_q3 = s_q2 + kQueue2Cap * 8u;
   const uint32_t hist_spare = ix.n_ids;  // the histogram has n_ids + 1 rows
@@ -658,6 +668,24 @@ candidate_scatter_kernel(const uint32_t* __restrict__ flags, const uint64_t* __r
   }
 }
 
+// counts[s] += sum over the SMs' private copies, which are left zero for the next launch.
+__global__ void __launch_bounds__(256)
+fold_private_counts_kernel(uint32_t* __restrict__ priv, uint32_t n_copies, uint32_t n_ids,
+                           unsigned long long* __restrict__ counts) {
+  for (uint32_t s = blockIdx.x * blockDim.x + threadIdx.x; s < n_ids; s += gridDim.x * blockDim.x) {
+    unsigned long long sum = 0;
+    for (uint32_t c = 0; c < n_copies; ++c) {
+      const size_t at = static_cast<size_t>(c) * n_ids + s;
+      const uint32_t v = priv[at];
+      if (v) {
+        sum += v;
+        priv[at] = 0;
+      }
+    }
+    if (sum) counts[s] += sum;  // one thread per slot, and the join kernels have finished
+  }
+}
+
 // Entries only: bitwise Act::probe(cell_from_point(p, k_max/2)).
 __global__ void __launch_bounds__(256)
 probe_points_kernel(const __grid_constant__ DevIndex ix, const double2* __restrict__ pts, uint64_t n,
@@ -744,6 +772,8 @@ struct RefineParams {
   DevStatus* status;
   int32_t want_ids;
   int32_t smem_counts;  // the launch carries n_ids * 4 bytes of dynamic shared memory
+  uint32_t* counts_priv;  // otherwise: [n_priv][n_ids] u32 private copies (may be null)
+  uint32_t n_priv;
 };
 
 __global__ void __launch_bounds__(kRefineThreads, 4)
@@ -862,6 +892,8 @@ refine_kernel(const __grid_constant__ DevIndex ix, RefineParams rp) {
     if (pass) {
       if (local_counts) {
         atomicAdd(&s_counts[slot], 1u);
+      } else if (rp.counts_priv) {
+        atomicAdd(rp.counts_priv + static_cast<size_t>(blockIdx.x % rp.n_priv) * ix.n_ids + slot, 1u);
       } else {
         atomicAdd(&rp.counts[slot], 1ull);
       }

@@ -320,3 +320,30 @@ def test_structurally_corrupt_indexes_are_rejected():
     roots[0] = n_nodes + 1
     with pytest.raises(join.CorruptionError):
         make(roots=roots)
+
+
+def test_large_id_table_counts_through_private_copies(monkeypatch):
+    """Id tables too large for the shared-memory histograms (K1: forced here
+    with the tuning knob; K2: more than 8192 ids) count into per-CTA copies in
+    global memory that are folded afterwards: same counts, pairs and stats."""
+    fx = golden_util.load("join_small_exact")
+    g = golden_util.parse_gjx(golden_util.gjx_bytes(fx))
+    extra = 9000  # far-away dummy triangles with sparse ids: referenced by no cell
+    ids = np.concatenate([g["polygon_ids"], 100_000 + 7 * np.arange(extra, dtype=np.uint32)])
+    tri = np.array([[-80.0, 10.0], [-80.0, 10.001], [-79.999, 10.0]])
+    vtx = np.concatenate([g["vtx_latlng"].reshape(-1, 2), np.tile(tri, (extra, 1))])
+    off = np.concatenate([g["vtx_off"], g["vtx_off"][-1] + 3 * np.arange(1, extra + 1, dtype=np.uint64)])
+    monkeypatch.setenv("GJ_HIST_REP", "0")
+    b = join.IndexBundle.from_arrays(g["arena"], g["lut"], g["roots"], g["prefixes"], g["prefix_bits"], g["k_max"],
+                                     g["approx"], ids, off, vtx, device=0)
+    assert len(b.ids) > 8192
+    want = dict(zip(fx["count_ids"].tolist(), fx["count_values"].tolist()))
+    for _ in range(2):  # the copies are left zero for the next launch
+        assert join.join_count_per_polygon(b, fx["points"]) == want
+    for kind, mode in (("exact", capi.GJ_MODE_EXACT), ("approx", capi.GJ_MODE_APPROX)):
+        st = join.JoinStats()
+        counts, first, (ovf_pt, ovf_id) = b.session().join_count(fx["points"], mode, stats=st, want_ids=True)
+        epi, epid = golden_util.pairs_of(fx, kind)
+        assert np.array_equal(counts, np.bincount(np.searchsorted(b.ids, epid), minlength=len(b.ids)).astype(np.uint64))
+        assert st.as_tuple() == tuple(int(v) for v in fx[f"{kind}_stats"])
+    b.close()
