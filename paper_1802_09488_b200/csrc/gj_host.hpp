@@ -247,7 +247,7 @@ struct gj_session {
   gj::DeviceBuffer d_ovf_point, d_ovf_id, d_ovf_ord;
   gj::DeviceBuffer d_task_point, d_task_slot, d_task_ord, d_task_pass;
   // CSR pairs pipeline
-  gj::DeviceBuffer d_nrefs, d_task_base, d_pair_count, d_row_ptr, d_block_sums, d_pair_ids;
+  gj::DeviceBuffer d_nrefs, d_task_base, d_pair_count, d_row_ptr, d_block_sums;
   cudaEvent_t ev_in[3]{}, ev_done[3]{}, ev_out[3]{};
   gj::DevStatus* h_status = nullptr;   // pinned
   // materialised pairs of the last gj_join_pairs_host call, kept in HBM for gj_pairs_copy:
