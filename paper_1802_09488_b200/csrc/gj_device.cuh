@@ -49,7 +49,7 @@ struct DevDirectory {
 // the tier index ((Y >> 4) * pitch + (X >> 4)) and the 4 + 4 sub-cell bits that
 // select the slot in the trie node under a link — population 3 then reads the
 // arena without re-reading the point (a random 16-byte read costs a 128-byte
-// DRAM burst).  Unpacked (window too wide for 32 bits, arena above 2^23 nodes,
+// DRAM burst).  Unpacked (window too wide for 32 bits, arena of 2^24 nodes or more,
 // tier deeper than level 28): the word is the tier index and population 3
 // re-reads the point.  Both forms are  min((v32 >> shift) - origin, clamp)  per
 // axis, word = qy * mul + qx, where v32 is the grid coordinate left-aligned to 32 bits.

@@ -36,6 +36,7 @@ constexpr int kPointsPerThread = GJ_PPT;
 #ifndef GJ_PF_DIST
 #define GJ_PF_DIST 1
 #endif
+constexpr uint32_t kQueueSlow = 0xFFFFFFFFu;  // queue word of a point population 1 would not decide
 constexpr uint32_t kPrefetchTiles = GJ_PF_DIST;  // K1: L2 prefetch distance in tiles, 0 = off
 constexpr int kQueue2Cap = 32 * (kPointsPerThread + 1);
 constexpr int kQueue3Cap = 64;
@@ -368,14 +369,17 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
   };
 
   // Population 3, one batch of open points (one per lane, `mine` = the lane
-  // holds one; bit 31 of `iw` marks a slow point): arena descent / dictionary
-  // / candidates.  All 32 lanes go through it together because the record
-  // reservations are per warp.
+  // holds one): arena descent / dictionary / candidates.  Bit 31 of `iw`
+  // marks an item whose word `c` is not a directory code: kQueueSlow for a slow
+  // point, else — packed coding — the arena slot under a link, all 32 bits of
+  // it, so arenas up to 2^24 nodes (32 GB) qualify.  All 32 lanes go through it
+  // together because the record reservations are per warp.
   auto resolve_open = [&](bool mine, uint32_t iw, uint32_t c) {
     const uint32_t i = iw & 0x7FFFFFFFu;
+    const bool flagged = (iw & 0x80000000u) != 0u;
     uint64_t entry = 0;
     if (mine) {
-      if (iw & 0x80000000u) {  // nothing decided yet: the reference's own sequence
+      if (flagged && c == kQueueSlow) {  // nothing decided yet: the reference's own sequence
         const double2 q = __ldg(pts + i);
         if (!latlng_valid(q.x, q.y)) {
           flag_error(jp.status, kErrInvalidPoint, jp.base_index + i);  // cell_id.cpp:83-85
@@ -384,14 +388,14 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
           if (kStats) ++n_valid;
           entry = probe_raw(ix, cell_from_point(q.x, q.y, ix.leaf_level));
         }
-      } else if (c & kDirLink) {
+      } else if (flagged || (c & kDirLink)) {
         const int walk_level = ix.prefix_level0 + 4 * tb.chunks;
-        uint64_t node = c & ~kDirLink;
+        uint64_t node = c & ~kDirLink;  // unpacked coding: the node under the link
         int level = walk_level;
         bool walk = true;
-        if (ix.qc.packed) {  // the word is (node - 1) * 256 + (y sub-cell bits << 4 | x sub-cell bits)
+        if (flagged) {  // the word is (node - 1) * 256 + (y sub-cell bits << 4 | x sub-cell bits)
           const uint32_t slot = (spread4((c >> 4) & 0xFu) << 1) | spread4(c & 0xFu);  // chunk_slot
-          const uint64_t at = (node & ~0xFFull) | slot;
+          const uint64_t at = (static_cast<uint64_t>(c) & ~0xFFull) | slot;
           bool from_arena = true;
           if (ix.node_pal) {  // the node's 128-byte palette form, usually an L2 hit
             const uint64_t* rec = ix.node_pal + (at >> 8) * 16u;
@@ -489,9 +493,12 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
     const bool mine = lane < batch_take;
     const bool lookup = mine && (batch_point & 0x80000000u) == 0u;
     const bool done = settle(batch_code, lookup, batch_point);
-    uint32_t fwd = batch_code;
-    if (ix.qc.packed && (fwd & kDirLink)) fwd = kDirLink | (((fwd & ~kDirLink) - 1u) * kNodeSlots + batch_slot);
-    q3_count = enqueue(s_q3, q3_count, mine && !done, batch_point, fwd);
+    uint32_t fwd = batch_code, fwd_point = batch_point;  // a slow item travels on as it is (flag + kQueueSlow)
+    if (lookup && ix.qc.packed && (fwd & kDirLink)) {
+      fwd = ((fwd & ~kDirLink) - 1u) * kNodeSlots + batch_slot;
+      fwd_point |= 0x80000000u;
+    }
+    q3_count = enqueue(s_q3, q3_count, mine && !done, fwd_point, fwd);
 #ifdef GJ_EXP_NO_PHASE3  // timing experiment: results are wrong
     q3_count = 0;
 #endif
@@ -510,7 +517,7 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
       idx = (Y >> 4) * tb.pitch + (X >> 4);
       batch_slot = ((Y & ix.qc.sub_mask) << 4) | (X & ix.qc.sub_mask);  // spread into a node slot in population 3
     }
-    batch_code = ldg32_if(table2 + idx, lane < take && (item.x & 0x80000000u) == 0u, 0u);
+    batch_code = ldg32_if(table2 + idx, lane < take && (item.x & 0x80000000u) == 0u, kQueueSlow);
     batch_open = true;
   };
 
