@@ -616,7 +616,8 @@ int create_index(const gj_index_desc& d, int device, gj_index** out) {
     const uint32_t ybits = bits_for((static_cast<uint64_t>(tb.height) + 1) * 16);
     DevQueueCoding& qc = dv.qc;
     qc = DevQueueCoding{};
-    if (tb_shift >= 2 && xbits + ybits <= 32 && d.node_count < (1ull << 24)) {  // arena slots fit 32 bits, below kQueueSlow
+    const bool force_unpacked = std::getenv("GJ_QUEUE_UNPACKED") != nullptr;  // test hook for the fallback coding
+    if (!force_unpacked && tb_shift >= 2 && xbits + ybits <= 32 && d.node_count < (1ull << 24)) {  // arena slots fit 32 bits, below kQueueSlow
       qc.packed = 1;
       qc.shift = static_cast<uint32_t>(tb_shift + 2 - 4);
       qc.x0 = tb.x0 * 16;

@@ -347,3 +347,23 @@ def test_large_id_table_counts_through_private_copies(monkeypatch):
         assert np.array_equal(counts, np.bincount(np.searchsorted(b.ids, epid), minlength=len(b.ids)).astype(np.uint64))
         assert st.as_tuple() == tuple(int(v) for v in fx[f"{kind}_stats"])
     b.close()
+
+
+@pytest.mark.parametrize("name", ["cfg2_tess16_approx4m", "cfg3_tess16_exact_trained", "cfg4_tess36_approx1m_k56",
+                                  "cfg5_stars_scaled", "kmax60_sparse_ids"])
+def test_unpacked_queue_coding_matches_reference(name, monkeypatch):
+    """The fallback queue coding (window too wide for 32 bits, arenas of 2^24+
+    nodes): the queue word is the tier index and population 3 re-reads the
+    point.  Forced with the test hook; results must not change."""
+    monkeypatch.setenv("GJ_QUEUE_UNPACKED", "1")
+    fx = golden_util.load(name)
+    b = join.IndexBundle.load(golden_util.bundle_file(name), device=0)
+    want = dict(zip(fx["count_ids"].tolist(), fx["count_values"].tolist()))
+    assert join.join_count_per_polygon(b, fx["points"]) == want
+    for kind, mode in (("exact", capi.GJ_MODE_EXACT), ("approx", capi.GJ_MODE_APPROX)):
+        st = join.JoinStats()
+        counts, first, _ = b.session().join_count(fx["points"], mode, stats=st, want_ids=True)
+        epi, epid = golden_util.pairs_of(fx, kind)
+        assert np.array_equal(counts, np.bincount(np.searchsorted(b.ids, epid), minlength=len(b.ids)).astype(np.uint64))
+        assert st.as_tuple() == tuple(int(v) for v in fx[f"{kind}_stats"])
+    b.close()
