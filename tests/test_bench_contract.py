@@ -36,3 +36,31 @@ def test_reference_arm_other_ranks_exit_quietly():
     res = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--impl", "reference", "--gpus", "2", "--steps", "1",
                           "--warmup", "0"], capture_output=True, text=True, timeout=120, cwd=ROOT, env=env)
     assert res.returncode == 0 and res.stdout.strip() == ""
+
+
+@pytest.mark.gpu
+def test_own_arm_prints_one_contract_line():
+    from tools import build_bundles
+    if not build_bundles.have_bundle(build_bundles.workload_name(2)):
+        pytest.skip("no cached config-2 index")
+    res = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "1", "--steps", "4", "--warmup", "3",
+                          "--points", "4000000", "--ref-points", "4000000", "--e2e-steps", "2"],
+                         capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert res.returncode == 0, res.stderr[-2000:]
+    lines = [l for l in res.stdout.splitlines() if l.strip()]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert "impl" not in d and d["metric"] == "joined_points_per_sec" and d["unit"] == "points/s"
+    assert d["n_gpus"] == 1 and d["steps"] == 4 and d["warmup"] == 3 and d["higher_is_better"] is True
+    assert d["value"] > 0 and d["ms_per_step"] > 0 and d["vs_baseline"] is None and d["scaling"] == "weak"
+    assert d["dtype"] == "f64" and d["data"] == "synthetic" and "workload" in d["config"]
+    assert d["gpu_launches"] == 4  # one join_kernel launch per step
+    assert set(d["clocks"]) >= {"sm_mhz", "sm_max_mhz", "reasons"}
+    e = d["e2e"]
+    assert e["value"] > 0 and e["unit"] == "points/s" and e["h2d_bytes_per_step"] == 16 * 4000000
+    assert e["d2h_bytes_per_step"] >= 4 * 4000000
+    r = d["roofline"]
+    assert r["bound"] == "hbm" and r["unit"] == "GB/s" and 0 < r["frac"] < 1.2 and r["peak"] > 1000
+    assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9 and "traffic" in r
+    cb = d["cpu_baseline"]
+    assert cb["kind"] in ("reference", "port") and cb["cores"] >= 1 and cb["value"] > 0 and cb["sample"]
