@@ -367,3 +367,29 @@ def test_unpacked_queue_coding_matches_reference(name, monkeypatch):
         assert np.array_equal(counts, np.bincount(np.searchsorted(b.ids, epid), minlength=len(b.ids)).astype(np.uint64))
         assert st.as_tuple() == tuple(int(v) for v in fx[f"{kind}_stats"])
     b.close()
+
+
+def test_index_and_session_lifecycle_releases_device_memory():
+    """Create / use / destroy indexes and sessions repeatedly: HBM comes back."""
+    import torch
+    fx = golden_util.load("cfg2_tess16_approx4m")
+    path = golden_util.bundle_file("cfg2_tess16_approx4m")
+    _cache.clear()
+    torch.cuda.synchronize()
+
+    def cycle():
+        b = join.IndexBundle.load(path, device=0)
+        s = b.session()
+        s.join_count(fx["points"], capi.GJ_MODE_EXACT, want_ids=True)
+        s.join_pairs(fx["points"][:5000], capi.GJ_MODE_APPROX)
+        s.training_candidates(fx["points"][:5000])
+        s.points_from_csv(b"lat,lng\n1,2\n")
+        s.close()
+        b.close()
+
+    cycle()  # first use may create the context's own pools
+    free0, _ = torch.cuda.mem_get_info()
+    for _ in range(20):
+        cycle()
+    free1, _ = torch.cuda.mem_get_info()
+    assert free0 - free1 < (8 << 20), (free0, free1)
