@@ -85,12 +85,22 @@ SmemPlan plan_smem(const gj_index& ix) {
   return p;
 }
 
+// Dynamic shared memory above 48 KB needs an opt-in per kernel.  The limit is
+// a property of the kernel, not of the launch, so it is raised to the device
+// maximum — a per-call value would race between sessions of differently
+// sized indexes.  (The L1 carve-out follows the launch's actual size.)
+template <typename Kernel>
+int allow_max_smem(const gj_index& ix, Kernel kernel) {
+  GJ_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ix.smem_optin)));
+  return GJ_OK;
+}
+
 template <bool kIds, bool kStats, bool kDense>
 int launch_join_variant(gj_session* s, const JoinParams& jp, const SmemPlan& sp) {
   const gj_index& ix = *s->ix;
   auto kernel = join_kernel<kIds, kStats, kDense>;
-  GJ_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(sp.total)));
+  int rc = allow_max_smem(ix, kernel);
+  if (rc != GJ_OK) return rc;
   int occ = 0;
   GJ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kJoinThreads, sp.total));
   if (occ < 1) {
@@ -501,8 +511,7 @@ int run_host_pairs(gj_session* s, const double* latlng, uint64_t n, bool exact, 
   GJ_CUDA(cudaMemsetAsync(s->d_stats.ptr, 0, 6 * 8, s->stream));
   DevStatus* d_status = s->d_status.as<DevStatus>() + 3;
   const size_t probe_smem = align16(std::max<size_t>(ix.dev.dir.n_table * 4, 16));
-  GJ_CUDA(cudaFuncSetAttribute(probe_points_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(probe_smem)));
+  if (int rc_attr = allow_max_smem(ix, probe_points_kernel)) return rc_attr;
   const unsigned wide = static_cast<unsigned>(ix.sm_count) * 8u;
   uint64_t* d_row_all = s->d_all_row_ptr.as<uint64_t>();
 
@@ -715,8 +724,7 @@ int gj_probe_points_host(gj_session* s, const double* latlng, uint64_t n, uint64
   int rc = reset_status(s, d_status);
   if (rc != GJ_OK) return rc;
   const size_t smem = align16(std::max<size_t>(ix.dev.dir.n_table * 4, 16));
-  GJ_CUDA(cudaFuncSetAttribute(probe_points_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(smem)));
+  if (int rc_attr = allow_max_smem(ix, probe_points_kernel)) return rc_attr;
   for (uint64_t begin = 0; begin < n; begin += chunk) {
     const uint64_t len = std::min(chunk, n - begin);
     GJ_CUDA(cudaMemcpyAsync(s->d_points[0].ptr, latlng + 2 * begin, len * 16, cudaMemcpyHostToDevice, s->stream));
@@ -900,8 +908,7 @@ int gj_training_candidates_host(gj_session* s, const double* latlng, uint64_t n,
   int rc = reset_status(s, d_status);
   if (rc != GJ_OK) return rc;
   const size_t smem = align16(std::max<size_t>(ix.dev.dir.n_table * 4, 16));
-  GJ_CUDA(cudaFuncSetAttribute(candidate_flags_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               static_cast<int>(smem)));
+  if (int rc_attr = allow_max_smem(ix, candidate_flags_kernel)) return rc_attr;
   uint64_t found = 0;
   for (uint64_t begin = 0; begin < n; begin += chunk) {
     const uint64_t len = std::min(chunk, n - begin);

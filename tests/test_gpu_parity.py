@@ -393,3 +393,42 @@ def test_index_and_session_lifecycle_releases_device_memory():
         cycle()
     free1, _ = torch.cuda.mem_get_info()
     assert free0 - free1 < (8 << 20), (free0, free1)
+
+
+def test_concurrent_sessions_on_one_index_and_on_two_indexes():
+    """An index is immutable and shared; sessions are per thread.
+    Threads joining at the same time — on one index and on indexes with
+    different shared-memory plans — get the serial results."""
+    import threading
+    from paper_1802_09488_b200.join import Session
+    fxa, fxb = golden_util.load("cfg2_tess16_approx4m"), golden_util.load("cfg5_stars_scaled")
+    ba = join.IndexBundle.load(golden_util.bundle_file("cfg2_tess16_approx4m"), device=0)
+    bb = join.IndexBundle.load(golden_util.bundle_file("cfg5_stars_scaled"), device=0)
+    want = {}
+    for key, (b, fx) in {"a": (ba, fxa), "b": (bb, fxb)}.items():
+        c, f, (op, oi) = b.session().join_count(fx["points"], capi.GJ_MODE_EXACT, want_ids=True)
+        want[key] = (c.copy(), f.copy(), op.copy(), oi.copy())
+    errors = []
+
+    def worker(key, b, fx):
+        try:
+            s = Session(b)
+            for _ in range(25):
+                c, f, (op, oi) = s.join_count(fx["points"], capi.GJ_MODE_EXACT, want_ids=True)
+                w = want[key]
+                if not (np.array_equal(c, w[0]) and np.array_equal(f, w[1]) and np.array_equal(op, w[2])
+                        and np.array_equal(oi, w[3])):
+                    errors.append(key)
+            s.close()
+        except Exception as exc:  # noqa: BLE001
+            errors.append(repr(exc))
+
+    threads = [threading.Thread(target=worker, args=(k, b, fx))
+               for k, b, fx in [("a", ba, fxa), ("b", bb, fxb), ("a", ba, fxa), ("b", bb, fxb)]]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert errors == []
+    ba.close()
+    bb.close()
