@@ -234,42 +234,53 @@ __device__ __noinline__ uint32_t emit_general(const DevIndex& ix, const JoinPara
 
   uint32_t first = e.defer ? kDeferred : kNoMatch;
   uint32_t emitted = 0, tasks = 0;
-  for (uint32_t k = 0; k < e.n_refs; ++k) {
-    // k-th reference in the reference's emit order (act.hpp:169-196)
-    uint32_t p;
-    if (e.tag == 1u) {
-      p = static_cast<uint32_t>(entry >> 2) & 0x7fffffffu;
-    } else if (e.tag == 2u) {
-      p = static_cast<uint32_t>(k == 0 ? entry >> 33 : entry >> 2) & 0x7fffffffu;
-    } else {
-      p = k < e.t ? (__ldg(ix.lut + e.off + 1 + k) << 1) | 1u : (__ldg(ix.lut + e.off + 2 + k) << 1);
+  // the k-th reference emits a pair now (a true hit, or any reference in approximate mode) ...
+  auto emit_pair = [&](uint32_t id, uint32_t k) {
+    count_slot<kDense>(ix, jp, h, id);
+    if (kIds) {
+      if (!e.defer && emitted == 0) {
+        first = id | (n_now > 1 ? kMoreFlag : 0u);
+      } else if (n_ovf) {
+        const uint64_t w = ovf_base + (e.defer ? emitted : emitted - 1);
+        jp.ovf_point[w] = jp.base_index + local;
+        jp.ovf_id[w] = id;
+        jp.ovf_ord[w] = k;
+      }
     }
-    const uint32_t id = p >> 1;
-    if ((p & 1u) != 0u || !exact) {
-      count_slot<kDense>(ix, jp, h, id);
-      if (kIds) {
-        if (!e.defer && emitted == 0) {
-          first = id | (n_now > 1 ? kMoreFlag : 0u);
-        } else if (n_ovf) {
-          const uint64_t w = ovf_base + (e.defer ? emitted : emitted - 1);
-          jp.ovf_point[w] = jp.base_index + local;
-          jp.ovf_id[w] = id;
-          jp.ovf_ord[w] = k;
-        }
-      }
-      ++emitted;
+    ++emitted;
+  };
+  // ... or becomes a candidate task for K2 (exact mode)
+  auto emit_task = [&](uint32_t id, uint32_t k) {
+    const uint32_t slot = kDense ? id : id_to_slot(ix, id);
+    if (__ldg(ix.ring_len + slot) == 0u) {  // join.cpp:111-114
+      flag_error(jp.status, kErrUnknownPolygon, jp.base_index + local);
+    }
+    if (tasks_ok) {
+      const uint64_t w = task_base + tasks;
+      jp.task_point[w] = local;
+      jp.task_slot[w] = slot;
+      jp.task_ord[w] = k;
+    }
+    ++tasks;
+  };
+  // references in the reference's emit order (act.hpp:169-196)
+  if (e.tag == 3u) {  // record [t, true ids, c, candidate ids]: two plain loops (overlapping polygon sets live here)
+    const uint32_t* true_ids = ix.lut + e.off + 1;
+    const uint32_t* cand_ids = ix.lut + e.off + 2;  // indexed by k as well
+    for (uint32_t k = 0; k < e.t; ++k) emit_pair(__ldg(true_ids + k), k);
+    if (exact) {
+      for (uint32_t k = e.t; k < e.n_refs; ++k) emit_task(__ldg(cand_ids + k), k);
     } else {
-      const uint32_t slot = kDense ? id : id_to_slot(ix, id);
-      if (__ldg(ix.ring_len + slot) == 0u) {  // join.cpp:111-114
-        flag_error(jp.status, kErrUnknownPolygon, jp.base_index + local);
+      for (uint32_t k = e.t; k < e.n_refs; ++k) emit_pair(__ldg(cand_ids + k), k);
+    }
+  } else {
+    for (uint32_t k = 0; k < e.n_refs; ++k) {
+      const uint32_t p = static_cast<uint32_t>(e.tag == 2u && k == 0 ? entry >> 33 : entry >> 2) & 0x7fffffffu;
+      if ((p & 1u) != 0u || !exact) {
+        emit_pair(p >> 1, k);
+      } else {
+        emit_task(p >> 1, k);
       }
-      if (tasks_ok) {
-        const uint64_t w = task_base + tasks;
-        jp.task_point[w] = local;
-        jp.task_slot[w] = slot;
-        jp.task_ord[w] = k;
-      }
-      ++tasks;
     }
   }
   return first;
