@@ -186,7 +186,11 @@ class HostStager {
     auto issue = [&](size_t k) {
       const int b = static_cast<int>(k & 1);
       const size_t off = k * kPiece, len = std::min(kPiece, bytes - off);
-      cudaError_t r = cudaMemcpyAsync(pinned_[b], static_cast<const char*>(d_src) + off, len, cudaMemcpyDeviceToHost, st);
+      // the piece may still feed an earlier to_device() on another stream
+      cudaError_t r = cudaEventSynchronize(ev_[b]);
+      if (r == cudaSuccess) {
+        r = cudaMemcpyAsync(pinned_[b], static_cast<const char*>(d_src) + off, len, cudaMemcpyDeviceToHost, st);
+      }
       return r == cudaSuccess ? cudaEventRecord(ev_[b], st) : r;
     };
     e = issue(0);
