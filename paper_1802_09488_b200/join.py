@@ -314,7 +314,10 @@ class Session:
     def join_count_device(self, d_points_ptr: int, n: int, d_counts_ptr: int, mode=capi.GJ_MODE_BUNDLE,
                           d_stats_ptr: int = 0, d_first_id_ptr: int = 0, sync: bool = False):
         """Points already in HBM (raw device pointers, e.g. ``tensor.data_ptr()``);
-        asynchronous on ``self.stream`` unless ``sync``."""
+        asynchronous on ``self.stream`` unless ``sync``.  The session stream does
+        not wait for other streams: buffers filled by another library (torch
+        copies, ``zero_()``) must be complete — synchronise, or record an event
+        and make ``self.stream`` wait for it — before this call."""
         _check(capi.lib().gj_join_count_device(self._h, C.c_void_p(d_points_ptr), n, mode,
                                                C.c_void_p(d_counts_ptr),
                                                C.c_void_p(d_stats_ptr) if d_stats_ptr else None,

@@ -79,6 +79,7 @@ def test_config2_device_resident_equals_host_path():
     d_counts = torch.zeros(len(bundle.ids), dtype=torch.int64, device="cuda")
     d_stats = torch.zeros(6, dtype=torch.int64, device="cuda")
     d_first = torch.empty(n, dtype=torch.int32, device="cuda")
+    torch.cuda.synchronize()  # the session has its own stream: torch's fills and copies must have landed
     s.join_count_device(d_pts.data_ptr(), n, d_counts.data_ptr(), capi.GJ_MODE_APPROX,
                         d_stats_ptr=d_stats.data_ptr(), d_first_id_ptr=d_first.data_ptr(), sync=True)
     st = join.JoinStats()
@@ -133,10 +134,11 @@ def test_one_billion_points_in_one_launch():
     assert d_pts.shape == (n, 2)
     d_counts = torch.zeros(len(bundle.ids), dtype=torch.int64, device="cuda")
     d_first = torch.empty(n, dtype=torch.int32, device="cuda")
-    s.join_count_device(d_pts.data_ptr(), n, d_counts.data_ptr(), capi.GJ_MODE_APPROX,
-                        d_first_id_ptr=d_first.data_ptr(), sync=True)
     d_counts1 = torch.zeros_like(d_counts)
     d_first1 = torch.empty(N_FULL, dtype=torch.int32, device="cuda")
+    torch.cuda.synchronize()  # the session has its own stream: torch's fills and copies must have landed
+    s.join_count_device(d_pts.data_ptr(), n, d_counts.data_ptr(), capi.GJ_MODE_APPROX,
+                        d_first_id_ptr=d_first.data_ptr(), sync=True)
     s.join_count_device(d_one.data_ptr(), N_FULL, d_counts1.data_ptr(), capi.GJ_MODE_APPROX,
                         d_first_id_ptr=d_first1.data_ptr(), sync=True)
     assert torch.equal(d_counts, d_counts1 * reps)
@@ -144,6 +146,7 @@ def test_one_billion_points_in_one_launch():
     # a ragged total (not a multiple of the tile) ending inside the last copy
     m = n - 12_345
     d_counts.zero_()
+    torch.cuda.synchronize()
     s.join_count_device(d_pts.data_ptr(), m, d_counts.data_ptr(), capi.GJ_MODE_APPROX, sync=True)
     tail, _, _ = s.join_count(pts[N_FULL - 12_345:], capi.GJ_MODE_APPROX)
     assert np.array_equal(d_counts.cpu().numpy().astype(np.uint64),

@@ -202,7 +202,7 @@ def test_cell_ids_adversarial_grid_lines_vs_oracle():
 
 
 def test_multi_chunk_inputs_match_oracle():
-    """Inputs larger than the internal chunk sizes (4 M points for pairs, 8 M
+    """Inputs larger than the internal chunk sizes (4 M points for pairs, 3 M
     for counts): chunk seams must not show in pairs, row offsets or counts."""
     fx, bundle = setup("join_small_exact")
     ox = golden_util.oracle_index(fx)

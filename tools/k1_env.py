@@ -41,6 +41,7 @@ def main():
             step()
         sess.sync()
         d_counts.zero_()
+        torch.cuda.synchronize()  # the session launches on its own stream
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         with torch.cuda.stream(stream):
             e0.record()

@@ -85,11 +85,12 @@ def run_all(n_points: int):
             print(f"   {name}: prefix counts differ from the oracle: sum {chk.sum()} vs {truth.sum()}, "
                   f"{(chk != truth).sum()} slots", flush=True)
         d_counts.zero_()
+        torch.cuda.synchronize()  # the session launches on its own stream
         for _ in range(3):
             step()
         sess.sync()
         d_counts.zero_()
-        torch.cuda.synchronize()
+        torch.cuda.synchronize()  # the session launches on its own stream
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         reps = 10
         with torch.cuda.stream(stream):
