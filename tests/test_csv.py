@@ -172,3 +172,61 @@ def test_gpu_csv_multi_chunk_and_throughput():
     print(f"csv: CPU oracle (strtod, one thread) {cpu:.2f} s = {len(text) / cpu / 1e6:.0f} MB/s")
     assert _same_bits(got, want)
     bundle.close()
+
+
+def _random_decimals(seed, n):
+    """Random decimal strings: 1-45 digits, a point anywhere, exponents that put
+    the value anywhere from the subnormals to a few hundred."""
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(n):
+        nd = int(rng.integers(1, 46))
+        digits = "".join(str(int(d)) for d in rng.integers(0, 10, nd))
+        pos = int(rng.integers(0, nd + 1))
+        mant = digits[:pos] + ("." + digits[pos:] if rng.random() < 0.8 else digits[pos:])
+        if mant in ("", "."):
+            mant = "0"
+        target = int(rng.choice([2, 1, 0, -1, -5, -17, -40, -100, -300, -308, -320, -323, -324, -325, -330, -340]))
+        lead = len(digits[:pos].lstrip("0")) if digits[:pos].strip("0") else -(len(digits[pos:]) - len(digits[pos:].lstrip("0")))
+        exp = target - lead
+        s = ("-" if rng.random() < 0.3 else "") + mant
+        if exp != 0 or rng.random() < 0.3:
+            s += ("e" if rng.random() < 0.5 else "E") + (("+" if exp >= 0 and rng.random() < 0.5 else "") + str(exp))
+        out.append(s)
+    return out
+
+
+def test_oracle_number_parsing_matches_python_float():
+    """parse_double's value is the correctly rounded double (std::from_chars);
+    so is Python's float().  Rows are valid iff both fields parse, neither
+    overflows nor rounds a nonzero decimal to zero, and the point is in range."""
+    nums = _random_decimals(0xC5B4, 30000)
+    text = ("lat,lng\n" + "\n".join(f"{s},1.5" for s in nums) + "\n").encode()
+    got, skipped = oracle.csv_points(text)
+    want = []
+    for s in nums:
+        v = float(s)
+        nonzero = any(c in "123456789" for c in s.lower().split("e")[0])
+        if np.isfinite(v) and not (v == 0.0 and nonzero) and abs(v) <= 90.0:
+            want.append(v)
+    want = np.array(want)
+    assert skipped == len(nums) - len(want) and len(want) > 10000
+    assert _same_bits(got[:, 0], want) and np.all(got[:, 1] == 1.5)
+
+
+@pytest.mark.gpu
+def test_gpu_number_parsing_matches_python_float():
+    bundle, s = _session()
+    nums = _random_decimals(0xC5B5, 300000)
+    text = ("lat,lng\n" + "\n".join(f"{x},1.5" for x in nums) + "\n").encode()
+    got, skipped = s.points_from_csv(text)
+    want = []
+    for x in nums:
+        v = float(x)
+        nonzero = any(c in "123456789" for c in x.lower().split("e")[0])
+        if np.isfinite(v) and not (v == 0.0 and nonzero) and abs(v) <= 90.0:
+            want.append(v)
+    want = np.array(want)
+    assert skipped == len(nums) - len(want)
+    assert _same_bits(got[:, 0], want)
+    bundle.close()
