@@ -20,7 +20,16 @@ int load_index_file(const char* path, int device, gj_index** out);
 
 namespace {
 
-constexpr uint64_t kMaxLaunchPoints = (1ull << 31) - 1;  // point indices are u32 with a flag bit
+// Point indices travel in K1's queue words next to flag bits: 2^31 - 1 points per launch, fewer for arenas of
+// 2^24 nodes and more (DevQueueCoding::index_bits).
+uint64_t max_launch_points(const gj_index& ix) {
+  uint64_t cap = (1ull << ix.dev.qc.index_bits) - 1;
+  if (const char* e = std::getenv("GJ_MAX_LAUNCH_POINTS")) {  // test hook: exercise the splitting of device-resident calls
+    const long long v = std::atoll(e);
+    if (v > 0) cap = std::min<uint64_t>(cap, static_cast<uint64_t>(v));
+  }
+  return cap;
+}
 constexpr size_t kScratchBudget = 3ull << 30;      // per-chunk task + overflow scratch
 
 size_t align16(size_t v) { return (v + 15) & ~size_t{15}; }
@@ -142,17 +151,23 @@ struct JoinRequest {
   bool ovf_discard;      // first ids wanted, the overflow list not (device-resident calls)
   uint64_t task_cap;
   uint8_t* d_task_pass;  // pairs mode
+  bool keep_errors;      // do not clear the error flags / bad index of the status block (see gj_join_count_device)
 };
 
 // Enqueue K1 (+ bucket + K2 in exact mode) on the session stream.
 int enqueue_join(gj_session* s, const JoinRequest& rq) {
   gj_index& ix = *s->ix;
-  if (rq.n > kMaxLaunchPoints) {
-    set_error("more than 2^31 points in one launch");
+  if (rq.n > max_launch_points(ix)) {
+    set_error("too many points for one launch");
     return GJ_INVALID_ARGUMENT;
   }
   const uint32_t n_ids = ix.dev.n_ids;
-  int rc = reset_status(s, rq.d_status);
+  int rc = GJ_OK;
+  if (rq.keep_errors) {  // a later piece of one call: only the per-launch cursors start over
+    GJ_CUDA(cudaMemsetAsync(&rq.d_status->overflow_count, 0, 2 * sizeof(unsigned long long), s->stream));
+  } else {
+    rc = reset_status(s, rq.d_status);
+  }
   if (rc != GJ_OK) return rc;
   const SmemPlan sp = plan_smem(ix);
 
@@ -1034,27 +1049,34 @@ int gj_join_count_device(gj_session* s, const double* d_latlng, uint64_t n, int 
   bool exact = false;
   if (!resolve_exact(ix, mode, &exact)) return GJ_INVALID_ARGUMENT;
   GJ_CUDA(cudaSetDevice(ix.device));
-  const uint64_t task_cap = exact ? n * std::max<uint64_t>(1, ix.max_cand_refs) : 0;
+  // One launch per `piece` points: all of them, unless the index caps a launch lower (arenas of 2^24 nodes and more)
+  const uint64_t piece = std::max<uint64_t>(1, std::min(n, max_launch_points(ix)));
+  const uint64_t task_cap = exact ? piece * std::max<uint64_t>(1, ix.max_cand_refs) : 0;
   if (task_cap >= (1ull << 32)) {
     set_error("candidate task capacity exceeds 2^32; split the launch");
     return GJ_INVALID_ARGUMENT;
   }
   int rc;
   if (exact && (rc = reserve_tasks(s, task_cap)) != GJ_OK) return rc;
-  JoinRequest rq{};
-  rq.d_pts = reinterpret_cast<const double2*>(d_latlng);
-  rq.n = n;
-  rq.base_index = 0;
-  rq.exact = exact;
-  rq.want_stats = d_stats != nullptr;
-  rq.d_counts = reinterpret_cast<unsigned long long*>(d_counts);
-  rq.d_stats = reinterpret_cast<unsigned long long*>(d_stats);
-  rq.d_first_id = d_first_id;
-  rq.d_status = s->d_status.as<DevStatus>();
-  rq.ovf_cap = 0;  // the overflow list cannot be handed back from here: only the flag in the first id
-  rq.ovf_discard = true;
-  rq.task_cap = task_cap;
-  if ((rc = enqueue_join(s, rq)) != GJ_OK) return rc;
+  for (uint64_t begin = 0; begin == 0 || begin < n; begin += piece) {
+    const uint64_t len = std::min(piece, n - begin);
+    JoinRequest rq{};
+    rq.d_pts = reinterpret_cast<const double2*>(d_latlng) + begin;
+    rq.n = len;
+    rq.base_index = begin;
+    rq.exact = exact;
+    rq.want_stats = d_stats != nullptr;
+    rq.d_counts = reinterpret_cast<unsigned long long*>(d_counts);
+    rq.d_stats = reinterpret_cast<unsigned long long*>(d_stats);
+    rq.d_first_id = d_first_id ? d_first_id + begin : nullptr;
+    rq.d_status = s->d_status.as<DevStatus>();
+    rq.ovf_cap = 0;  // the overflow list cannot be handed back from here: only the flag in the first id
+    rq.ovf_discard = true;
+    rq.task_cap = task_cap;
+    rq.keep_errors = begin != 0;  // the smallest offending index of the whole call survives the later pieces
+    if ((rc = enqueue_join(s, rq)) != GJ_OK) return rc;
+    if (n == 0) break;
+  }
   if (sync) return gj_session_sync(s, nullptr);
   return GJ_OK;
 }

@@ -49,9 +49,13 @@ struct DevDirectory {
 // the tier index ((Y >> 4) * pitch + (X >> 4)) and the 4 + 4 sub-cell bits that
 // select the slot in the trie node under a link — population 3 then reads the
 // arena without re-reading the point (a random 16-byte read costs a 128-byte
-// DRAM burst).  Unpacked (window too wide for 32 bits, arena of 2^24 nodes or more,
-// tier deeper than level 28): the word is the tier index and population 3
-// re-reads the point.  Both forms are  min((v32 >> shift) - origin, clamp)  per
+// DRAM burst).  An arena slot under a link needs 8 + log2(nodes) bits: up to
+// 2^24 nodes that is the 32-bit second queue word; larger arenas (2^25 / 2^26
+// nodes = 64 / 128 GB) borrow 1 / 2 bits from the point index in the first
+// word (`index_bits`), which caps one launch at 2^30 / 2^29 points (the API
+// splits longer device-resident calls).  Unpacked (window too wide for 32
+// bits, arena of 2^26 nodes or more, tier deeper than level 28): the word is
+// the tier index and population 3 re-reads the point.  Both forms are  min((v32 >> shift) - origin, clamp)  per
 // axis, word = qy * mul + qx, where v32 is the grid coordinate left-aligned to 32 bits.
 struct DevQueueCoding {
   uint32_t packed;
@@ -61,6 +65,8 @@ struct DevQueueCoding {
   uint32_t mul;             // packed: 1 << xbits, unpacked: tb.pitch
   uint32_t xbits;           // packed only
   uint32_t sub_mask;        // packed only: the sub-cell bits at or above the leaf level (cell_id.cpp:93-94)
+  uint32_t index_bits;      // bits of the first queue word that hold the point index (31, or 30 / 29 for wide arenas)
+  uint32_t slow_mark;       // bit 31 and every bit between index_bits and 31: marks a slow point's first word
 };
 
 // Latitude strips of one polygon: its widened latitude range [y0, y0 + k / inv_h]

@@ -617,8 +617,18 @@ int create_index(const gj_index_desc& d, int device, gj_index** out) {
     DevQueueCoding& qc = dv.qc;
     qc = DevQueueCoding{};
     const bool force_unpacked = std::getenv("GJ_QUEUE_UNPACKED") != nullptr;  // test hook for the fallback coding
-    if (!force_unpacked && tb_shift >= 2 && xbits + ybits <= 32 && d.node_count < (1ull << 24)) {  // arena slots fit 32 bits, below kQueueSlow
+    // high bits of an arena slot that travel in the first queue word (see DevQueueCoding)
+    uint32_t slot_hi_bits = 0;
+    while (slot_hi_bits < 3 && d.node_count >= (1ull << (24 + slot_hi_bits))) ++slot_hi_bits;
+    if (const char* e = std::getenv("GJ_QUEUE_SLOT_HI_BITS")) {  // test hook: the wide-arena coding on a small index
+      slot_hi_bits = std::max<uint32_t>(slot_hi_bits, static_cast<uint32_t>(std::atoi(e)));
+    }
+    qc.index_bits = 31;
+    qc.slow_mark = 0x80000000u;
+    if (!force_unpacked && tb_shift >= 2 && xbits + ybits <= 32 && slot_hi_bits <= 2) {  // slots below the kQueueSlow pattern
       qc.packed = 1;
+      qc.index_bits = 31 - slot_hi_bits;
+      qc.slow_mark = 0x80000000u | (((1u << slot_hi_bits) - 1u) << qc.index_bits);
       qc.shift = static_cast<uint32_t>(tb_shift + 2 - 4);
       qc.x0 = tb.x0 * 16;
       qc.y0 = tb.y0 * 16;

@@ -344,9 +344,11 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
   const uint32_t* __restrict__ table2 = tb.table;
   const uint32_t qc_shift = ix.qc.shift, qc_mul = ix.qc.mul;
   const uint32_t qc_x0 = ix.qc.x0, qc_y0 = ix.qc.y0, qc_xc = ix.qc.x_clamp, qc_yc = ix.qc.y_clamp;
+  const uint32_t q_index_bits = ix.qc.index_bits, q_index_mask = (1u << q_index_bits) - 1u;
+  const uint32_t q_slow_mark = ix.qc.slow_mark;
   const double2* __restrict__ pts = jp.pts;
   uint32_t* __restrict__ first_id = jp.first_id;
-  const uint32_t n = static_cast<uint32_t>(jp.n);  // 1 <= n < 2^31 per launch (bit 31 of an index is a queue flag)
+  const uint32_t n = static_cast<uint32_t>(jp.n);  // 1 <= n < 2^index_bits per launch (the bits above are queue flags)
   // A code resolves where it is read when it is one inlined payload that
   // emits: a true hit, or a candidate in approximate mode (join.cpp:100-108).
   const uint32_t need_interior = jp.exact ? 1u : 0u;
@@ -381,16 +383,17 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
 
   // Population 3, one batch of open points (one per lane, `mine` = the lane
   // holds one): arena descent / dictionary / candidates.  Bit 31 of `iw`
-  // marks an item whose word `c` is not a directory code: kQueueSlow for a slow
-  // point, else — packed coding — the arena slot under a link, all 32 bits of
-  // it, so arenas up to 2^24 nodes (32 GB) qualify.  All 32 lanes go through it
-  // together because the record reservations are per warp.
+  // marks an item whose word `c` is not a directory code: kQueueSlow (under
+  // the slow mark) for a slow point, else — packed coding — the arena slot
+  // under a link: its low 32 bits in `c`, the bits above them (arenas of 2^24
+  // nodes = 32 GB and more) between the point index and bit 31 of `iw`.  All
+  // 32 lanes go through it together because the record reservations are per warp.
   auto resolve_open = [&](bool mine, uint32_t iw, uint32_t c) {
-    const uint32_t i = iw & 0x7FFFFFFFu;
+    const uint32_t i = iw & q_index_mask;
     const bool flagged = (iw & 0x80000000u) != 0u;
     uint64_t entry = 0;
     if (mine) {
-      if (flagged && c == kQueueSlow) {  // nothing decided yet: the reference's own sequence
+      if (c == kQueueSlow && (iw & q_slow_mark) == q_slow_mark) {  // nothing decided yet: the reference's own sequence
         const double2 q = __ldg(pts + i);
         if (!latlng_valid(q.x, q.y)) {
           flag_error(jp.status, kErrInvalidPoint, jp.base_index + i);  // cell_id.cpp:83-85
@@ -406,7 +409,8 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
         bool walk = true;
         if (flagged) {  // the word is (node - 1) * 256 + (y sub-cell bits << 4 | x sub-cell bits)
           const uint32_t slot = (spread4((c >> 4) & 0xFu) << 1) | spread4(c & 0xFu);  // chunk_slot
-          const uint64_t at = (static_cast<uint64_t>(c) & ~0xFFull) | slot;
+          const uint64_t at = (static_cast<uint64_t>((iw & 0x7FFFFFFFu) >> q_index_bits) << 32) |
+                              (static_cast<uint64_t>(c) & ~0xFFull) | slot;
           bool from_arena = true;
           if (ix.node_pal) {  // the node's 128-byte palette form, usually an L2 hit
             const uint64_t* rec = ix.node_pal + (at >> 8) * 16u;
@@ -506,8 +510,9 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
     const bool done = settle(batch_code, lookup, batch_point);
     uint32_t fwd = batch_code, fwd_point = batch_point;  // a slow item travels on as it is (flag + kQueueSlow)
     if (lookup && ix.qc.packed && (fwd & kDirLink)) {
-      fwd = ((fwd & ~kDirLink) - 1u) * kNodeSlots + batch_slot;
-      fwd_point |= 0x80000000u;
+      const uint64_t at = static_cast<uint64_t>((fwd & ~kDirLink) - 1u) * kNodeSlots + batch_slot;
+      fwd = static_cast<uint32_t>(at);
+      fwd_point |= 0x80000000u | (static_cast<uint32_t>(at >> 32) << q_index_bits);
     }
     q3_count = enqueue(s_q3, q3_count, mine && !done, fwd_point, fwd);
 #ifdef GJ_EXP_NO_PHASE3  // timing experiment: results are wrong
@@ -605,7 +610,7 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
       const uint32_t qx = min((x >> qc_shift) - qc_x0, qc_xc);
       const uint32_t qy = min((y >> qc_shift) - qc_y0, qc_yc);
       const bool open = live && !emit && !(ok && e == 0xFFFFFFFFu);
-      q2_count = enqueue(s_q2, q2_count, open, ok ? i : i | 0x80000000u, qy * qc_mul + qx);
+      q2_count = enqueue(s_q2, q2_count, open, ok ? i : i | q_slow_mark, qy * qc_mul + qx);
     }
     drain2(false);
   };

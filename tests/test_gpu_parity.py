@@ -369,6 +369,111 @@ def test_unpacked_queue_coding_matches_reference(name, monkeypatch):
     b.close()
 
 
+def _check_join_against_fixture(b, fx):
+    want = dict(zip(fx["count_ids"].tolist(), fx["count_values"].tolist()))
+    assert join.join_count_per_polygon(b, fx["points"]) == want
+    for kind, mode in (("exact", capi.GJ_MODE_EXACT), ("approx", capi.GJ_MODE_APPROX)):
+        st = join.JoinStats()
+        counts, first, _ = b.session().join_count(fx["points"], mode, stats=st, want_ids=True)
+        epi, epid = golden_util.pairs_of(fx, kind)
+        assert np.array_equal(counts, np.bincount(np.searchsorted(b.ids, epid), minlength=len(b.ids)).astype(np.uint64))
+        assert st.as_tuple() == tuple(int(v) for v in fx[f"{kind}_stats"])
+
+
+@pytest.mark.parametrize("hi_bits", [1, 2])
+@pytest.mark.parametrize("name", ["cfg2_tess16_approx4m", "cfg3_tess16_exact_trained", "cfg4_tess36_approx1m_k56",
+                                  "cfg5_stars_scaled"])
+def test_wide_arena_queue_coding_matches_reference(name, hi_bits, monkeypatch):
+    """Arenas of 2^24 / 2^25 nodes and more keep the packed queue coding by carrying
+    1 / 2 high bits of the arena slot next to the point index (DevQueueCoding::index_bits).
+    Forced on a small index with the test hook; results must not change."""
+    monkeypatch.setenv("GJ_QUEUE_SLOT_HI_BITS", str(hi_bits))
+    fx = golden_util.load(name)
+    b = join.IndexBundle.load(golden_util.bundle_file(name), device=0)
+    _check_join_against_fixture(b, fx)
+    b.close()
+
+
+def test_arena_beyond_2_24_nodes_matches_reference():
+    """A REAL arena of more than 2^24 nodes (34 GB): the nodes of a fixture index
+    renumbered to sit above 2^24 empty, unreachable nodes, so every arena slot the
+    join touches needs more than 32 bits.  Entries, counts and stats must equal the
+    fixture's.  (BASELINE config 4 at full size has 18.3 M nodes.)"""
+    import torch
+    shift = 1 << 24
+    free_dev, _ = torch.cuda.mem_get_info()
+    try:
+        avail_host = int([l for l in open("/proc/meminfo") if l.startswith("MemAvailable")][0].split()[1]) * 1024
+    except Exception:
+        avail_host = 0
+    if free_dev < 60 << 30 or avail_host < 60 << 30:
+        pytest.skip("needs 60 GB of free device and host memory")
+    _cache.clear()
+    fx = golden_util.load("cfg4_tess36_approx1m_k56")
+    g = golden_util.parse_gjx(golden_util.gjx_bytes(fx))
+    small = np.asarray(g["arena"], np.uint64)
+    k = len(small) // 256
+    arena = np.zeros((shift + k) * 256, np.uint64)  # untouched pages are not backed by memory
+    link = ((small & np.uint64(3)) == 0) & (small != 0)
+    moved = small.copy()
+    moved[link] += np.uint64(shift << 2)  # a link is node id << 2 (act.hpp:55-60)
+    arena[shift * 256:] = moved
+    roots = np.asarray(g["roots"], np.uint64).copy()
+    roots[roots != 0] += np.uint64(shift)
+    b = join.IndexBundle.from_arrays(arena, g["lut"], roots, g["prefixes"], g["prefix_bits"], g["k_max"], g["approx"],
+                                     g["polygon_ids"], g["vtx_off"], g["vtx_latlng"], device=0)
+    del arena
+    assert b.info.node_count == shift + k
+    assert np.array_equal(b.session().probe_points(fx["points"]), fx["entries"])
+    _check_join_against_fixture(b, fx)
+    b.close()
+
+
+def test_device_resident_call_is_split_into_launches(monkeypatch):
+    """A device-resident call longer than one launch may be (the cap depends on the
+    arena size) runs as several launches: same counts, first ids and stats, and the
+    smallest offending index of the whole call survives the later pieces."""
+    import torch
+    fx = golden_util.load("cfg3_tess16_exact_trained")
+    b = join.IndexBundle.load(golden_util.bundle_file("cfg3_tess16_exact_trained"), device=0)
+    s = b.session()
+    pts = np.ascontiguousarray(fx["points"])
+    n = len(pts)
+    d_pts = torch.from_numpy(pts).cuda()
+
+    def run(mode):
+        d_counts = torch.zeros(len(b.ids), dtype=torch.int64, device="cuda")
+        d_stats = torch.zeros(6, dtype=torch.int64, device="cuda")
+        d_first = torch.empty(n, dtype=torch.int32, device="cuda")
+        torch.cuda.synchronize()
+        s.join_count_device(d_pts.data_ptr(), n, d_counts.data_ptr(), mode, d_stats_ptr=d_stats.data_ptr(),
+                            d_first_id_ptr=d_first.data_ptr(), sync=True)
+        return d_counts.cpu().numpy(), d_stats.cpu().numpy(), d_first.cpu().numpy()
+
+    for mode in (capi.GJ_MODE_EXACT, capi.GJ_MODE_APPROX):
+        monkeypatch.delenv("GJ_MAX_LAUNCH_POINTS", raising=False)
+        l0 = s.launches
+        one = run(mode)
+        per_call = s.launches - l0
+        monkeypatch.setenv("GJ_MAX_LAUNCH_POINTS", str(n // 7 + 1))
+        l0 = s.launches
+        many = run(mode)
+        assert s.launches - l0 == 7 * per_call
+        for a, c in zip(one, many):
+            assert np.array_equal(a, c)
+    bad = pts.copy()
+    bad[n // 7 - 3, 0] = 95.0   # in the first piece
+    bad[n - 5, 1] = np.nan      # in the last piece
+    d_bad = torch.from_numpy(bad).cuda()
+    d_counts = torch.zeros(len(b.ids), dtype=torch.int64, device="cuda")
+    torch.cuda.synchronize()
+    with pytest.raises(join.InvalidArgument) as e:
+        s.join_count_device(d_bad.data_ptr(), n, d_counts.data_ptr(), capi.GJ_MODE_APPROX)
+        s.sync()
+    assert e.value.index == n // 7 - 3
+    b.close()
+
+
 def test_index_and_session_lifecycle_releases_device_memory():
     """Create / use / destroy indexes and sessions repeatedly: HBM comes back."""
     import torch
