@@ -48,7 +48,7 @@ def rss_gb() -> float:
 
 
 def run(config: int, scale: float, n_points: int, launch: int, check: int, reps: int, threads: int,
-        want_ids: bool, want_stats: bool, host_points: int):
+        want_ids: bool, want_stats: bool, host_points: int, pairs_points: int = 0):
     import torch
     from oracle import ref
 
@@ -205,6 +205,18 @@ def run(config: int, scale: float, n_points: int, launch: int, check: int, reps:
         has = np.diff(row_ptr.astype(np.int64)) > 0
         res["first_ids_device_equal_host"] = bool(np.array_equal(first, f2))
         res["first_id_present_iff_reference_pair"] = bool(np.array_equal(first != capi.GJ_NO_MATCH, has))
+    if pairs_points:  # the materialised-pairs call (CSR through host buffers), the config's own output form
+        mq = min(pairs_points, n)
+        t0 = time.time()
+        rp2, pid2 = sess.join_pairs(pts[:mq], mode)
+        dt = time.time() - t0
+        t0 = time.time()
+        rp2, pid2 = sess.join_pairs(pts[:mq], mode)
+        dt2 = time.time() - t0
+        res["join_pairs_host"] = {"points": mq, "pairs": int(rp2[-1]), "seconds_first_call": dt, "seconds": dt2,
+                                  "mpoints_per_s": mq / dt2 / 1e6, "mpairs_per_s": int(rp2[-1]) / dt2 / 1e6}
+        log(f"join_pairs (CSR, host buffers): {dt2:.3f} s per {mq} points, {int(rp2[-1])} pairs")
+        del rp2, pid2
     res["peak_rss_gb"] = rss_gb()
     print(json.dumps(res), flush=True)
     sess.close()
@@ -224,10 +236,11 @@ def main():
     ap.add_argument("--no-ids", action="store_true")
     ap.add_argument("--no-stats", action="store_true")
     ap.add_argument("--host-points", type=int, default=1 << 62, help="points of the host-buffer call (0 = skip)")
+    ap.add_argument("--pairs", type=int, default=0, help="also time gj_join_pairs_host + gj_pairs_copy on this many points")
     ap.add_argument("--out", default="")
     a = ap.parse_args()
     r = run(a.config, a.scale, a.points, a.launch, a.check, a.reps, a.threads, not a.no_ids, not a.no_stats,
-            a.host_points)
+            a.host_points, a.pairs)
     if a.out:
         Path(a.out).parent.mkdir(parents=True, exist_ok=True)
         Path(a.out).write_text(json.dumps(r, indent=1))
