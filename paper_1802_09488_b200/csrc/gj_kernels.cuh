@@ -344,8 +344,6 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
   const uint32_t* __restrict__ table2 = tb.table;
   const uint32_t qc_shift = ix.qc.shift, qc_mul = ix.qc.mul;
   const uint32_t qc_x0 = ix.qc.x0, qc_y0 = ix.qc.y0, qc_xc = ix.qc.x_clamp, qc_yc = ix.qc.y_clamp;
-  const uint32_t q_index_bits = ix.qc.index_bits, q_index_mask = (1u << q_index_bits) - 1u;
-  const uint32_t q_slow_mark = ix.qc.slow_mark;
   const double2* __restrict__ pts = jp.pts;
   uint32_t* __restrict__ first_id = jp.first_id;
   const uint32_t n = static_cast<uint32_t>(jp.n);  // 1 <= n < 2^index_bits per launch (the bits above are queue flags)
@@ -389,7 +387,8 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
   // nodes = 32 GB and more) between the point index and bit 31 of `iw`.  All
   // 32 lanes go through it together because the record reservations are per warp.
   auto resolve_open = [&](bool mine, uint32_t iw, uint32_t c) {
-    const uint32_t i = iw & q_index_mask;
+    const uint32_t q_index_bits = ix.qc.index_bits, q_slow_mark = ix.qc.slow_mark;
+    const uint32_t i = iw & ((1u << q_index_bits) - 1u);
     const bool flagged = (iw & 0x80000000u) != 0u;
     uint64_t entry = 0;
     if (mine) {
@@ -508,11 +507,12 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
     const bool mine = lane < batch_take;
     const bool lookup = mine && (batch_point & 0x80000000u) == 0u;
     const bool done = settle(batch_code, lookup, batch_point);
-    uint32_t fwd = batch_code, fwd_point = batch_point;  // a slow item travels on as it is (flag + kQueueSlow)
+    // a slow item (bit 31 set in Q2) travels on with kQueueSlow under the full slow mark of Q3
+    uint32_t fwd = batch_code, fwd_point = lookup ? batch_point : batch_point | ix.qc.slow_mark;
     if (lookup && ix.qc.packed && (fwd & kDirLink)) {
       const uint64_t at = static_cast<uint64_t>((fwd & ~kDirLink) - 1u) * kNodeSlots + batch_slot;
       fwd = static_cast<uint32_t>(at);
-      fwd_point |= 0x80000000u | (static_cast<uint32_t>(at >> 32) << q_index_bits);
+      fwd_point |= 0x80000000u | (static_cast<uint32_t>(at >> 32) << ix.qc.index_bits);
     }
     q3_count = enqueue(s_q3, q3_count, mine && !done, fwd_point, fwd);
 #ifdef GJ_EXP_NO_PHASE3  // timing experiment: results are wrong
@@ -610,7 +610,7 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
       const uint32_t qx = min((x >> qc_shift) - qc_x0, qc_xc);
       const uint32_t qy = min((y >> qc_shift) - qc_y0, qc_yc);
       const bool open = live && !emit && !(ok && e == 0xFFFFFFFFu);
-      q2_count = enqueue(s_q2, q2_count, open, ok ? i : i | q_slow_mark, qy * qc_mul + qx);
+      q2_count = enqueue(s_q2, q2_count, open, ok ? i : i | 0x80000000u, qy * qc_mul + qx);
     }
     drain2(false);
   };

@@ -58,7 +58,8 @@ def run_all(n_points: int):
     n_chk = min(n_points, 20_000_000)
     ox = golden_util.oracle_index(golden_util.parse_gjx(path.read_bytes()))
     truth_map, _ = ox.join_count(pts[:n_chk], approx=True, threads=16)
-    for name in VARIANTS:
+    extra = sorted(p.stem[4:] for p in OUT.glob("lib_*.so") if p.stem[4:] not in VARIANTS)  # hand-built A/B libraries
+    for name in list(VARIANTS) + extra:
         lib = OUT / f"lib_{name}.so"
         if not lib.exists():
             continue
