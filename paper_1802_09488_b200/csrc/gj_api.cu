@@ -90,6 +90,10 @@ SmemPlan plan_smem(const gj_index& ix) {
   if (std::getenv("GJ_DEBUG_PLAN")) {
     std::fprintf(stderr, "[gj] K1 smem: 16-bit tier level %d, %zu B; queues at %u; histogram at %u x%u; total %zu\n",
                  30 - ix.dev.dir16.shift, table_bytes, p.queue_off, p.hist_off, p.hist_rep, p.total);
+    const DevDirectory& tb = ix.dev.dirk.n_table ? ix.dev.dirk : (ix.dev.dir2.n_table ? ix.dev.dir2 : ix.dev.dir);
+    std::fprintf(stderr, "[gj] K1 32-bit tier: level %d%s, %u x %u cells (%.1f MB); queue coding %s, tier_shift %u, index bits %u\n",
+                 30 - tb.shift, ix.dev.dirk.n_table ? " (refined)" : "", tb.width, tb.height, tb.n_table * 4e-6,
+                 ix.dev.qc.packed ? "packed" : "unpacked", ix.dev.qc.tier_shift, ix.dev.qc.index_bits);
   }
   return p;
 }

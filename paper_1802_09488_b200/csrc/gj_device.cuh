@@ -44,9 +44,10 @@ struct DevDirectory {
 };
 
 // How K1 codes a point's position in the 32-bit tier `tb` into one queue
-// word.  Packed (the usual case): the word holds the point's cell at level
-// tb.level + 4 relative to the window, (Y << xbits) | X, so the drain gets both
-// the tier index ((Y >> 4) * pitch + (X >> 4)) and the 4 + 4 sub-cell bits that
+// word.  Packed (the usual case): the word holds the point's cell at the level
+// of the NEXT trie-node boundary (tb.level + 4; + 3..1 for a refined tier)
+// relative to the window, (Y << xbits) | X, so the drain gets both the tier
+// index ((Y >> tier_shift) * pitch + (X >> tier_shift)) and the 4 + 4 sub-cell bits that
 // select the slot in the trie node under a link — population 3 then reads the
 // arena without re-reading the point (a random 16-byte read costs a 128-byte
 // DRAM burst).  An arena slot under a link needs 8 + log2(nodes) bits: up to
@@ -65,6 +66,7 @@ struct DevQueueCoding {
   uint32_t mul;             // packed: 1 << xbits, unpacked: tb.pitch
   uint32_t xbits;           // packed only
   uint32_t sub_mask;        // packed only: the sub-cell bits at or above the leaf level (cell_id.cpp:93-94)
+  uint32_t tier_shift;      // packed only: coded level minus the tier's level (4; 3..1 for a refined tier, DevIndex::dirk)
   uint32_t index_bits;      // bits of the first queue word that hold the point index (31, or 30 / 29 for wide arenas)
   uint32_t slow_mark;       // bit 31 and every bit between index_bits and 31: marks a slow point's first word
 };
@@ -124,7 +126,16 @@ struct DevIndex {
   // dir2, otherwise 1 + ((polygon_id << 1) | interior).  K1 stages it instead
   // of `dir` when present; `table` then points at uint16 data.
   DevDirectory dir16;
-  DevQueueCoding qc;  // for the 32-bit tier behind dir16 (dir2 when present, else dir)
+  // Optional refinement of the deepest 32-bit tier for K1 (`dirk`): the same
+  // codes over a window 1-3 grid levels finer than a trie-node boundary.  A
+  // cell resolves here when the aligned run of slots it owns in the node under
+  // its parent's link holds one terminal entry (or nothing); otherwise it
+  // keeps the parent's link.  Built only when most cells of the deepest tier
+  // are links (polygons a few cells across: BASELINE config 4), where every
+  // cell resolved here saves a random 128-byte DRAM burst in the arena.
+  // `chunks` is the parent tier's, so a link is followed exactly as from there.
+  DevDirectory dirk;
+  DevQueueCoding qc;  // for the 32-bit tier behind dir16 (dirk, else dir2, else dir)
   // Optional palette form of every trie node, 128 bytes (one L2 line / DRAM
   // burst) instead of 2 KB: [4 distinct entries (u64) | 256 two-bit codes (64 B) |
   // pad].  A boundary node of a tessellation holds 2-4 distinct entries (two

@@ -230,7 +230,7 @@ struct gj_index {
   gj::DevIndex dev{};
   gj_index_info info{};
   std::vector<uint32_t> ids;  // slot -> polygon id
-  gj::DeviceBuffer d_arena, d_lut, d_ids, d_ring_off, d_ring_len, d_ring_xy, d_dir_table, d_dir_dict, d_dir2_table, d_dir16_table, d_node_pal,
+  gj::DeviceBuffer d_arena, d_lut, d_ids, d_ring_off, d_ring_len, d_ring_xy, d_dir_table, d_dir_dict, d_dir2_table, d_dir16_table, d_dirk_table, d_node_pal,
       d_strip_meta, d_strip_ptr, d_strip_edges;
   int sm_count = 0;
   size_t smem_optin = 0;

@@ -24,6 +24,8 @@ thread_local std::string g_error;
 
 constexpr uint64_t kMaxDirEntries = 32768;         // 128 KB of u32 codes (shared memory)
 constexpr uint64_t kMaxDir2Entries = 16ull << 20;  // 64 MB of u32 codes (stays in the 126 MB L2)
+constexpr uint64_t kMaxDirKEntries = 20ull << 20;  // the refined tier may take a little more: it replaces dir2 in K1
+constexpr double kDirKMinLinkShare = 0.25;         // refine only when at least this share of the deepest tier's cells are links
 // 136 KB of u16 codes: with K1's queues and histogram that stays inside the
 // 196 KB shared-memory carve-out step (60 KB of L1 left for loads in flight);
 // the next step up (228 KB) is a cliff, see plan_smem in gj_api.cu
@@ -91,6 +93,8 @@ struct Analysis {
   HostDirectory dir;           // shared-memory tier
   HostDirectory dir2;          // global-memory (L2-resident) tier, deeper; may be empty
   HostDirectory dir16;         // K1's shared-memory tier (16-bit codes), see build_dir16
+  HostDirectory dirk;          // K1's refined 32-bit tier (DevIndex::dirk); may be empty
+  int dirk_sub = 0;            // its grid levels below the parent tier's (1..3)
   std::vector<uint64_t> dict;  // terminal entries that do not fit a directory code
   uint64_t max_refs = 0;       // most references behind one entry
   uint64_t max_cand_refs = 0;  // most candidate references behind one entry
@@ -347,6 +351,76 @@ int analyse(const gj_index_desc& d, Analysis* out) {
       };
       fill(snap1, dir);
       if (snap2.chunks > snap1.chunks) fill(snap2, out->dir2);
+
+      // K1's refined tier (DevIndex::dirk): the deepest tier again, `sub` grid levels finer.  A cell below a
+      // link owns an aligned run of 4^(4 - sub) slots of the linked node (slots are in Z-order, act.cpp:200-206);
+      // when the run holds one terminal entry, or nothing, the cell resolves here, else it keeps the link.
+      const HostDirectory& base = out->dir2.table.empty() ? dir : out->dir2;
+      if (!base.table.empty() && base.width && base.height) {
+        uint64_t n_links = 0;
+        for (uint32_t y = 0; y < base.height; ++y) {
+          for (uint32_t x = 0; x < base.width; ++x) n_links += (base.table[static_cast<size_t>(y) * base.pitch + x] & kDirLink) != 0;
+        }
+        const int room = std::min(3, d.k_max / 2 - base.level);  // never finer than the leaf level
+        int sub = 0;
+        const double share = static_cast<double>(n_links) / (static_cast<double>(base.width) * base.height);
+        if (share >= kDirKMinLinkShare) {
+          for (int r = 1; r <= room; ++r) {
+            if (((static_cast<uint64_t>(base.width) << r) + 1) * ((static_cast<uint64_t>(base.height) << r) + 1) <= kMaxDirKEntries) sub = r;
+          }
+        }
+        if (const char* e = std::getenv("GJ_TIER_SUB")) sub = std::max(0, std::min(room, std::atoi(e)));  // tuning knob / test hook
+        if (sub > 0) {
+          HostDirectory& hk = out->dirk;
+          out->dirk_sub = sub;
+          hk.chunks = base.chunks;
+          hk.level = base.level + sub;
+          hk.x0 = base.x0 << sub;
+          hk.y0 = base.y0 << sub;
+          hk.width = base.width << sub;
+          hk.height = base.height << sub;
+          hk.pitch = hk.width + 1;
+          hk.table.assign(static_cast<size_t>(hk.pitch) * (hk.height + 1), 0u);
+          const uint32_t side = 1u << sub;
+          const uint32_t run = 1u << (2 * (4 - sub));  // slots per refined cell
+          for (uint32_t y = 0; y < base.height; ++y) {
+            for (uint32_t x = 0; x < base.width; ++x) {
+              const uint32_t c = base.table[static_cast<size_t>(y) * base.pitch + x];
+              const uint64_t* slots = (c & kDirLink) ? d.arena + (static_cast<uint64_t>(c & ~kDirLink) - 1) * kNodeSlots : nullptr;
+              for (uint32_t q = 0; q < side * side; ++q) {
+                uint32_t qx = 0, qy = 0;
+                unzip_pairs(q, sub, &qx, &qy);
+                uint32_t code = c;
+                if (slots) {
+                  const uint64_t* r0 = slots + static_cast<size_t>(q) * run;
+                  const uint64_t e = r0[0];
+                  bool uniform = e == 0 || (e & 3) != 0;
+                  for (uint32_t k = 1; k < run && uniform; ++k) uniform = r0[k] == e;
+                  if (uniform) {
+                    if (e == 0) {
+                      code = 0;
+                    } else {
+                      auto it = code_of.find(e);
+                      if (it == code_of.end()) {
+                        uint32_t nc;
+                        if ((e & 3) == 1 && ((e >> 2) & 0x7fffffffu) < kDirInline) {
+                          nc = kDirInline | static_cast<uint32_t>((e >> 2) & 0x3fffffffu);
+                        } else {
+                          nc = static_cast<uint32_t>(out->dict.size());
+                          out->dict.push_back(e);
+                        }
+                        it = code_of.emplace(e, nc).first;
+                      }
+                      code = it->second;
+                    }
+                  }
+                }
+                hk.table[static_cast<size_t>((y << sub) + qy) * hk.pitch + ((x << sub) + qx)] = code;
+              }
+            }
+          }
+        }
+      }
     }
   }
   if (dir.level > 30 || out->dir2.level > 30) {
@@ -530,6 +604,7 @@ int create_index(const gj_index_desc& d, int device, gj_index** out) {
   if ((rc = upload(ix->d_dir_dict, an.dict.data(), an.dict.size(), &bytes)) != GJ_OK) return rc;
   if ((rc = upload(ix->d_dir2_table, an.dir2.table.data(), an.dir2.table.size(), &bytes)) != GJ_OK) return rc;
   if ((rc = upload(ix->d_dir16_table, an.dir16.table16.data(), an.dir16.table16.size(), &bytes)) != GJ_OK) return rc;
+  if ((rc = upload(ix->d_dirk_table, an.dirk.table.data(), an.dirk.table.size(), &bytes)) != GJ_OK) return rc;
 
   // Palette form of the nodes (DevIndex::node_pal), for K1's deep descents.
   bool have_pal = false;
@@ -603,17 +678,19 @@ int create_index(const gj_index_desc& d, int device, gj_index** out) {
   set_dir(dv.dir, an.dir, ix->d_dir_table.as<uint32_t>());
   set_dir(dv.dir2, an.dir2, ix->d_dir2_table.as<uint32_t>());
   set_dir(dv.dir16, an.dir16, ix->d_dir16_table.as<uint32_t>());
+  set_dir(dv.dirk, an.dirk, ix->d_dirk_table.as<uint32_t>());
   dv.dir16.n_table = static_cast<uint32_t>(an.dir16.table16.size());
   {  // queue coding for the 32-bit tier K1 gathers from
-    const HostDirectory& tb = an.dir2.table.empty() ? an.dir : an.dir2;
+    const HostDirectory& tb = !an.dirk.table.empty() ? an.dirk : (an.dir2.table.empty() ? an.dir : an.dir2);
     const int tb_shift = 30 - tb.level;
+    const int up = 4 - (an.dirk.table.empty() ? 0 : an.dirk_sub);  // grid levels from the tier to the next node boundary
     auto bits_for = [](uint64_t v) {  // smallest b with v <= 2^b
       uint32_t b = 0;
       while ((1ull << b) < v) ++b;
       return b;
     };
-    const uint32_t xbits = bits_for((static_cast<uint64_t>(tb.width) + 1) * 16);
-    const uint32_t ybits = bits_for((static_cast<uint64_t>(tb.height) + 1) * 16);
+    const uint32_t xbits = bits_for((static_cast<uint64_t>(tb.width) + 1) << up);
+    const uint32_t ybits = bits_for((static_cast<uint64_t>(tb.height) + 1) << up);
     DevQueueCoding& qc = dv.qc;
     qc = DevQueueCoding{};
     const bool force_unpacked = std::getenv("GJ_QUEUE_UNPACKED") != nullptr;  // test hook for the fallback coding
@@ -625,18 +702,19 @@ int create_index(const gj_index_desc& d, int device, gj_index** out) {
     }
     qc.index_bits = 31;
     qc.slow_mark = 0x80000000u;
-    if (!force_unpacked && tb_shift >= 2 && xbits + ybits <= 32 && slot_hi_bits <= 2) {  // slots below the kQueueSlow pattern
+    if (!force_unpacked && tb_shift + 2 >= up && xbits + ybits <= 32 && slot_hi_bits <= 2) {  // slots below the kQueueSlow pattern
       qc.packed = 1;
       qc.index_bits = 31 - slot_hi_bits;
       qc.slow_mark = 0x80000000u | (((1u << slot_hi_bits) - 1u) << qc.index_bits);
-      qc.shift = static_cast<uint32_t>(tb_shift + 2 - 4);
-      qc.x0 = tb.x0 * 16;
-      qc.y0 = tb.y0 * 16;
-      qc.x_clamp = tb.width * 16;
-      qc.y_clamp = tb.height * 16;
+      qc.shift = static_cast<uint32_t>(tb_shift + 2 - up);
+      qc.x0 = tb.x0 << up;
+      qc.y0 = tb.y0 << up;
+      qc.x_clamp = tb.width << up;
+      qc.y_clamp = tb.height << up;
       qc.mul = 1u << xbits;
       qc.xbits = xbits;
-      const int below_leaf = tb.level + 4 - d.k_max / 2;  // sub-cell levels finer than the leaf level
+      qc.tier_shift = static_cast<uint32_t>(up);
+      const int below_leaf = tb.level + up - d.k_max / 2;  // sub-cell levels finer than the leaf level
       qc.sub_mask = below_leaf > 0 ? (0xFu & ~((1u << std::min(below_leaf, 4)) - 1u)) : 0xFu;
     } else {
       qc.shift = static_cast<uint32_t>(tb_shift + 2);

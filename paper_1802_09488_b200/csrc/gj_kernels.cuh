@@ -340,7 +340,7 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
   const uint32_t d1_w = ix.dir16.width, d1_h = ix.dir16.height, d1_pitch = ix.dir16.pitch;
   const uint32_t d1_x0 = ix.dir16.x0, d1_y0 = ix.dir16.y0;
   const uint32_t d1_shift = min(static_cast<uint32_t>(ix.dir16.shift) + 2u, 31u);  // on 32-bit-aligned coordinates
-  const DevDirectory& tb = ix.dir2.n_table ? ix.dir2 : ix.dir;  // the 32-bit tier behind it
+  const DevDirectory& tb = ix.dirk.n_table ? ix.dirk : (ix.dir2.n_table ? ix.dir2 : ix.dir);  // the 32-bit tier behind it
   const uint32_t* __restrict__ table2 = tb.table;
   const uint32_t qc_shift = ix.qc.shift, qc_mul = ix.qc.mul;
   const uint32_t qc_x0 = ix.qc.x0, qc_y0 = ix.qc.y0, qc_xc = ix.qc.x_clamp, qc_yc = ix.qc.y_clamp;
@@ -530,7 +530,7 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
     uint32_t idx = item.y;
     if (ix.qc.packed) {  // (Y << xbits) | X at level tb.level + 4, see DevQueueCoding
       const uint32_t X = item.y & (qc_mul - 1u), Y = item.y >> ix.qc.xbits;
-      idx = (Y >> 4) * tb.pitch + (X >> 4);
+      idx = (Y >> ix.qc.tier_shift) * tb.pitch + (X >> ix.qc.tier_shift);
       batch_slot = ((Y & ix.qc.sub_mask) << 4) | (X & ix.qc.sub_mask);  // spread into a node slot in population 3
     }
     batch_code = ldg32_if(table2 + idx, lane < take && (item.x & 0x80000000u) == 0u, kQueueSlow);

@@ -394,6 +394,24 @@ def test_wide_arena_queue_coding_matches_reference(name, hi_bits, monkeypatch):
     b.close()
 
 
+@pytest.mark.parametrize("sub", [1, 2, 3])
+@pytest.mark.parametrize("name", ["cfg2_tess16_approx4m", "cfg3_tess16_exact_trained", "cfg4_tess36_approx1m_k56",
+                                  "cfg5_stars_scaled", "kmax60_sparse_ids", "world_stars", "join_small_exact"])
+def test_refined_tier_matches_reference(name, sub, monkeypatch):
+    """K1's refined 32-bit tier (DevIndex::dirk): the deepest tier again, 1-3 grid
+    levels finer, cells resolved from uniform slot runs of the linked nodes.  Built
+    by itself only for indexes whose deepest tier is mostly links; forced here on
+    every fixture shape, packed and unpacked queue coding.  Results must not change."""
+    monkeypatch.setenv("GJ_TIER_SUB", str(sub))
+    fx = golden_util.load(name)
+    for unpacked in (False, True):
+        if unpacked:
+            monkeypatch.setenv("GJ_QUEUE_UNPACKED", "1")
+        b = join.IndexBundle.load(golden_util.bundle_file(name), device=0)
+        _check_join_against_fixture(b, fx)
+        b.close()
+
+
 def test_arena_beyond_2_24_nodes_matches_reference():
     """A REAL arena of more than 2^24 nodes (34 GB): the nodes of a fixture index
     renumbered to sit above 2^24 empty, unreachable nodes, so every arena slot the

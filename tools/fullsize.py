@@ -48,7 +48,8 @@ def rss_gb() -> float:
 
 
 def run(config: int, scale: float, n_points: int, launch: int, check: int, reps: int, threads: int,
-        want_ids: bool, want_stats: bool, host_points: int, pairs_points: int = 0):
+        want_ids: bool, want_stats: bool, host_points: int, pairs_points: int = 0, save_index: str = "",
+        load_index: str = "", variants: bool = False):
     import torch
     from oracle import ref
 
@@ -62,7 +63,10 @@ def run(config: int, scale: float, n_points: int, launch: int, check: int, reps:
     res["polygon_gen_s"] = round(time.time() - t0, 1)
     log(f"{len(polys)} polygons generated in {res['polygon_gen_s']}s")
     t0 = time.time()
-    if build_bundles.have_bundle(name):
+    if load_index and Path(load_index).exists():
+        rb = ref.RefBundle.load(load_index)
+        res["index_source"] = "GJX1 file written by an earlier run of this tool (reference build_index + IndexBundle::save)"
+    elif build_bundles.have_bundle(name):
         rb = ref.RefBundle.load(build_bundles.bundle_file(name))
         res["index_source"] = "cached GJX1 file (reference build_index + IndexBundle::save), loaded by the reference"
     else:
@@ -72,6 +76,10 @@ def run(config: int, scale: float, n_points: int, launch: int, check: int, reps:
         rb = ref.RefBundle.build(ref.Polygons(polys.ids, polys.vtx_off, polys.latlng), cfg, None)
         res["index_source"] = "reference build_index in this process"
     res["index_build_s"] = round(time.time() - t0, 1)
+    if save_index and not Path(save_index).exists():
+        t0 = time.time()
+        rb.save(save_index)
+        log(f"index saved to {save_index} in {time.time() - t0:.1f}s")
     i = rb.info
     if spec.build_approx and not i.mode_approx:
         raise RuntimeError("approximate build fell back to exact (SURVEY.md trap 11)")
@@ -156,6 +164,59 @@ def run(config: int, scale: float, n_points: int, launch: int, check: int, reps:
     })
     log(f"device-resident join: {ms:.3f} ms per {n} points = {res['gpoints_per_s']:.1f} G points/s")
 
+    def timed(sess_, label, ids, stats_):
+        def one():
+            for a in range(0, n, launch):
+                m = min(launch, n - a)
+                sess_.join_count_device(flat[2 * a:].data_ptr(), m, d_counts.data_ptr(), mode,
+                                        d_stats_ptr=d_stats.data_ptr() if stats_ else 0,
+                                        d_first_id_ptr=d_first[a:].data_ptr() if ids else 0)
+        torch.cuda.synchronize()
+        one()
+        sess_.sync()
+        st = torch.cuda.ExternalStream(sess_.stream)
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(st):
+            a0.record()
+            for _ in range(reps):
+                one()
+            a1.record()
+        sess_.sync()
+        t = a0.elapsed_time(a1) / reps
+        log(f"variant {label}: {t:.3f} ms")
+        return t
+
+    if variants:  # where the time goes: knobs the library reads per launch (environment), then per index
+        v = {}
+        v["ids+counts (no stats)"] = timed(sess, "ids+counts", want_ids, False)
+        v["counts only"] = timed(sess, "counts only", False, False)
+        os.environ["GJ_HIST_REP"] = "0"
+        v["counts only, per-CTA private count copies forced"] = timed(sess, "counts only, private copies", False, False)
+        del os.environ["GJ_HIST_REP"]
+        for sub in (1, 2):
+            os.environ["GJ_TIER_SUB"] = str(sub)
+            os.environ["GJ_DEBUG_PLAN"] = "1"
+            try:
+                b2 = join.IndexBundle.from_arrays(arena, lut, roots, prefixes, pbits, rb.k_max, rb.approx,
+                                                  rp.ids, rp.vtx_off, rp.latlng, device=0)
+            except Exception as ex:  # e.g. out of device memory for the second copy
+                log(f"refined tier {sub}: {ex}")
+                continue
+            finally:
+                del os.environ["GJ_TIER_SUB"]
+            s2 = b2.session()
+            d_counts.zero_()
+            d_stats.zero_()
+            v[f"refined tier +{sub}: ids+counts+stats"] = timed(s2, f"refined tier +{sub}", want_ids, want_stats)
+            torch.cuda.synchronize()
+            res[f"refined_tier_{sub}_counts_equal"] = bool(np.array_equal(
+                (d_counts.cpu().numpy() // (reps + 1)).astype(np.uint64), counts))
+            v[f"refined tier +{sub}: counts only"] = timed(s2, f"refined tier +{sub}, counts only", False, False)
+            s2.close()
+            b2.close()
+            os.environ.pop("GJ_DEBUG_PLAN", None)
+        res["variants_ms"] = v
+
     # ---- host-buffer call (pageable numpy points -> counts) ----
     if host_points:
         hp = min(host_points, n)
@@ -169,6 +230,12 @@ def run(config: int, scale: float, n_points: int, launch: int, check: int, reps:
         if hp == n:
             res["host_counts_equal_device"] = bool(np.array_equal(hc.astype(np.uint64), counts))
 
+    if check <= 0:
+        res["peak_rss_gb"] = rss_gb()
+        print(json.dumps(res), flush=True)
+        sess.close()
+        bundle.close()
+        return res
     # ---- parity: the reference's own CPU join ----
     m = min(check, n)
     t0 = time.time()
@@ -237,10 +304,13 @@ def main():
     ap.add_argument("--no-stats", action="store_true")
     ap.add_argument("--host-points", type=int, default=1 << 62, help="points of the host-buffer call (0 = skip)")
     ap.add_argument("--pairs", type=int, default=0, help="also time gj_join_pairs_host + gj_pairs_copy on this many points")
+    ap.add_argument("--save-index", default="", help="write the built index here (GJX1) for a later --load-index run")
+    ap.add_argument("--load-index", default="", help="load the index from this GJX1 file when it exists")
+    ap.add_argument("--variants", action="store_true", help="extra timings that attribute the time (knobs, refined tiers)")
     ap.add_argument("--out", default="")
     a = ap.parse_args()
     r = run(a.config, a.scale, a.points, a.launch, a.check, a.reps, a.threads, not a.no_ids, not a.no_stats,
-            a.host_points, a.pairs)
+            a.host_points, a.pairs, a.save_index, a.load_index, a.variants)
     if a.out:
         Path(a.out).parent.mkdir(parents=True, exist_ok=True)
         Path(a.out).write_text(json.dumps(r, indent=1))
