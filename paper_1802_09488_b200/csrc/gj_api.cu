@@ -108,10 +108,10 @@ int allow_max_smem(const gj_index& ix, Kernel kernel) {
   return GJ_OK;
 }
 
-template <bool kIds, bool kStats, bool kDense>
+template <bool kIds, bool kStats, bool kDense, bool kLate = false>
 int launch_join_variant(gj_session* s, const JoinParams& jp, const SmemPlan& sp) {
   const gj_index& ix = *s->ix;
-  auto kernel = join_kernel<kIds, kStats, kDense>;
+  auto kernel = join_kernel<kIds, kStats, kDense, kLate>;
   int rc = allow_max_smem(ix, kernel);
   if (rc != GJ_OK) return rc;
   int occ = 0;
@@ -211,8 +211,13 @@ int enqueue_join(gj_session* s, const JoinRequest& rq) {
   jp.n_priv = static_cast<uint32_t>(ix.sm_count);
   jp.exact = rq.exact ? 1 : 0;
 
-  const int variant = (rq.d_first_id ? 4 : 0) | (rq.want_stats ? 2 : 0) | (ix.dev.ids_dense && sp.hist_rep ? 1 : 0);
+  const int variant = (rq.d_first_id && ix.ids_late ? 8 : 0) | (rq.d_first_id ? 4 : 0) | (rq.want_stats ? 2 : 0) |
+                      (ix.dev.ids_dense && sp.hist_rep ? 1 : 0);
   switch (variant) {
+    case 12: rc = launch_join_variant<true, false, false, true>(s, jp, sp); break;
+    case 13: rc = launch_join_variant<true, false, true, true>(s, jp, sp); break;
+    case 14: rc = launch_join_variant<true, true, false, true>(s, jp, sp); break;
+    case 15: rc = launch_join_variant<true, true, true, true>(s, jp, sp); break;
     case 0: rc = launch_join_variant<false, false, false>(s, jp, sp); break;
     case 1: rc = launch_join_variant<false, false, true>(s, jp, sp); break;
     case 2: rc = launch_join_variant<false, true, false>(s, jp, sp); break;

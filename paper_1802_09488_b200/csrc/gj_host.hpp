@@ -234,6 +234,7 @@ struct gj_index {
       d_strip_meta, d_strip_ptr, d_strip_edges;
   int sm_count = 0;
   size_t smem_optin = 0;
+  bool ids_late = false;       // K1 writes first ids where a point is settled (join_kernel's kLate): the 16-bit tier resolves few cells
   uint64_t max_refs = 0;       // most references behind one reachable entry
   uint64_t max_cand_refs = 0;  // most candidate references behind one entry
 };

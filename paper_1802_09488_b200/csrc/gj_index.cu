@@ -590,6 +590,15 @@ int create_index(const gj_index_desc& d, int device, gj_index** out) {
     if (const char* e = std::getenv("GJ_DIR16_LEVEL_MAX")) max_level = std::atoi(e);
     build_dir16(an.dir2.table.empty() ? an.dir : an.dir2, max16, max_level, &an.dir16);
   }
+  {  // first ids written late (join_kernel's kLate) when most of the 16-bit tier says "look in the 32-bit tier"
+    uint64_t open_cells = 0;
+    for (uint32_t y = 0; y < an.dir16.height; ++y) {
+      for (uint32_t x = 0; x < an.dir16.width; ++x) open_cells += an.dir16.table16[static_cast<size_t>(y) * an.dir16.pitch + x] == 0xFFFFu;
+    }
+    const uint64_t cells = static_cast<uint64_t>(an.dir16.width) * an.dir16.height;
+    ix->ids_late = cells != 0 && open_cells * 2 > cells;
+    if (const char* e = std::getenv("GJ_IDS_LATE")) ix->ids_late = std::atoi(e) != 0;  // tuning knob / test hook
+  }
   size_t bytes = 0;
   if ((rc = upload(ix->d_arena, d.arena, d.node_count * kNodeSlots, &bytes)) != GJ_OK) return rc;
   if ((rc = upload(ix->d_lut, d.lut, d.lut_len, &bytes)) != GJ_OK) return rc;

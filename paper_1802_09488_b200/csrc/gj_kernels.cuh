@@ -310,7 +310,12 @@ __device__ __noinline__ uint32_t emit_general(const DevIndex& ix, const JoinPara
 // few active ones; through the queues they always run with full warps.
 // kDense: id == count slot for every polygon AND the histogram is in shared
 // memory (jp.hist_rep != 0), the common case; otherwise the general counting path.
-template <bool kIds, bool kStats, bool kDense>
+// kLate (first ids wanted, and the shared-memory tier resolves few points — DevIndex::ids_late): population 1
+// does not pre-write the first-id words of the points it queues; population 2 writes the word of every point it
+// looks up (whole runs again, because nearly all points of a tile pass through it) and population 3 always writes.
+// Without it such an index writes almost every word twice, the second time as scattered partial sectors (measured
+// on BASELINE config 4 at full size: 9 of 23 ms).
+template <bool kIds, bool kStats, bool kDense, bool kLate = false>
 __global__ void __launch_bounds__(kJoinThreads, GJ_JOIN_MIN_BLOCKS)
 join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinParams jp) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -375,7 +380,13 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
       refined += emit && !(c & 1u);
       cand_refs += emit && !(c & 1u);
     }
-    if (kIds) st32_if(first_id + i, id, emit);
+    if (kIds) {
+      if (kLate) {
+        st32_if(first_id + i, emit ? id : kNoMatch, active);
+      } else {
+        st32_if(first_id + i, id, emit);
+      }
+    }
     return emit || miss;
   };
 
@@ -468,7 +479,7 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
         cand_refs += plan.n_cand;
       }
     }
-    if (kIds && first != kNoMatch) first_id[i] = first;
+    if (kIds && (kLate || first != kNoMatch)) first_id[i] = first;
   };
 
   // Append (a, b) of the lanes with `open` to a warp queue; returns the new count.
@@ -602,14 +613,14 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
       // emits), i.e. whole 128-byte runs per warp; later populations only
       // overwrite words that change, and those 4-byte stores then hit a
       // sector that is still dirty in L2 instead of forcing a 32-byte DRAM fill.
-      if (kIds) st32_if(first_id + i, emit ? id : kNoMatch, live);
+      const bool open = live && !emit && !(ok && e == 0xFFFFFFFFu);
+      if (kIds) st32_if(first_id + i, emit ? id : kNoMatch, kLate ? live && !open : live);
 #ifdef GJ_EXP_PHASE1_ONLY  // timing experiment: results are wrong
       continue;
 #endif
       // what stays open is queued with its position in the 32-bit tier (DevQueueCoding)
       const uint32_t qx = min((x >> qc_shift) - qc_x0, qc_xc);
       const uint32_t qy = min((y >> qc_shift) - qc_y0, qc_yc);
-      const bool open = live && !emit && !(ok && e == 0xFFFFFFFFu);
       q2_count = enqueue(s_q2, q2_count, open, ok ? i : i | 0x80000000u, qy * qc_mul + qx);
     }
     drain2(false);

@@ -109,6 +109,45 @@ def test_first_id_and_overflow(name, kind):
     assert np.array_equal(more & inline, (per_point > 1) & inline)
 
 
+@pytest.mark.parametrize("name", ["join_small_exact", "cfg2_tess16_approx4m", "cfg3_tess16_exact_trained",
+                                  "cfg4_tess36_approx1m_k56", "cfg5_stars_scaled", "world_stars", "empty_index"])
+@pytest.mark.parametrize("tier_sub", [0, 2])
+def test_late_first_ids_equal_early_first_ids(name, tier_sub, monkeypatch):
+    """join_kernel's kLate variant (first-id words written where a point is settled
+    instead of pre-written for every point; chosen by itself when the 16-bit tier
+    resolves few cells) must produce the same first ids, overflow records, counts and
+    stats as the default variant — host-buffer and device-resident calls, both modes,
+    ragged sizes, with and without a refined tier."""
+    import torch
+    fx = golden_util.load(name)
+    pts = np.ascontiguousarray(fx["points"])
+    results = {}
+    for late in ("0", "1"):
+        monkeypatch.setenv("GJ_IDS_LATE", late)
+        monkeypatch.setenv("GJ_TIER_SUB", str(tier_sub))
+        b = join.IndexBundle.load(golden_util.bundle_file(name), device=0)
+        s = b.session()
+        out = []
+        for mode in (capi.GJ_MODE_EXACT, capi.GJ_MODE_APPROX):
+            for n in (len(pts), min(len(pts), 4097), min(len(pts), 31)):
+                st = join.JoinStats()
+                counts, first, (opt, oid) = s.join_count(pts[:n], mode, stats=st, want_ids=True)
+                out += [counts, first, opt, oid, np.array(st.as_tuple())]
+                if n:
+                    d_pts = torch.from_numpy(pts[:n]).cuda()
+                    d_counts = torch.zeros(max(1, len(b.ids)), dtype=torch.int64, device="cuda")
+                    d_first = torch.full((n,), 0x55555555, dtype=torch.int32, device="cuda")
+                    torch.cuda.synchronize()
+                    s.join_count_device(d_pts.data_ptr(), n, d_counts.data_ptr(), mode,
+                                        d_first_id_ptr=d_first.data_ptr(), sync=True)
+                    out += [d_counts.cpu().numpy(), d_first.cpu().numpy()]
+        results[late] = out
+        b.close()
+    assert len(results["0"]) == len(results["1"])
+    for a, c in zip(results["0"], results["1"]):
+        assert np.array_equal(a, c)
+
+
 def test_invalid_point_reports_first_index():
     fx, bundle = setup("join_small_exact")
     pts = fx["points"].copy()
