@@ -238,7 +238,10 @@ GJ_API int gj_join_count_host(gj_session* s, const double* latlng, uint64_t n,
  * and in exact mode a point whose pairs depend on refinement reads
  * GJ_DEFERRED (its pairs are in the counts); use the *_host calls for lists.
  * Errors (invalid point, unknown polygon) are latched in the session and
- * returned by gj_session_sync. */
+ * returned by gj_session_sync.  Any n is accepted: one kernel launch takes up
+ * to 2^31 - 1 points (2^30 - 1 / 2^29 - 1 for indexes of 2^24 / 2^25 trie nodes
+ * and more) and longer calls run as several launches; the error index reported
+ * is the smallest offending one of the whole call. */
 GJ_API int gj_join_count_device(gj_session* s, const double* d_latlng, uint64_t n,
                                 int mode, uint64_t* d_counts, uint64_t* d_stats,
                                 uint32_t* d_first_id, int sync);
