@@ -151,3 +151,69 @@ def test_one_billion_points_in_one_launch():
     tail, _, _ = s.join_count(pts[N_FULL - 12_345:], capi.GJ_MODE_APPROX)
     assert np.array_equal(d_counts.cpu().numpy().astype(np.uint64),
                           d_counts1.cpu().numpy().astype(np.uint64) * reps - tail)
+
+
+def _scaled_bundle(config, scale):
+    name = build_bundles.workload_name(config, scale)
+    if not build_bundles.have_bundle(name):
+        pytest.skip(f"no cached index {name} (tools/build_bundles.py needs the reference)")
+    return build_bundles.bundle_file(name)
+
+
+@pytest.mark.parametrize("config,scale,n,mode", [(4, 0.04, 50_000_000, capi.GJ_MODE_APPROX),
+                                                (5, 0.03, 10_000_000, capi.GJ_MODE_EXACT)])
+def test_density_matched_configs_4_and_5(config, scale, n, mode):
+    """The regimes of BASELINE configs[3] and configs[4] (run at full size by
+    tools/fullsize.py: profiles/fullsize_r01_cfg*.json) on their density-matched
+    stand-ins: 1 600 polygons at 1 m with k_max 56 (an id table beyond the
+    shared-memory histogram when the tier is capped like the full-size box's, first ids
+    written late), and 300 overlapping stars (every probe a lookup-table record, exact).
+    Conservation, JoinStats identities, device-resident == host-buffer results, and
+    — when the compiled reference travelled with the repo — counts and ordered pairs
+    against the reference's own CPU join on a prefix."""
+    import torch
+    path = _scaled_bundle(config, scale)
+    bundle = join.IndexBundle.load(path, device=0)
+    s = bundle.session()
+    polys = None
+    pts = synth.points_for(config, n, polys, scale=scale)
+    st = join.JoinStats()
+    counts, first, (ovf_pt, ovf_id) = s.join_count(pts, mode, stats=st, want_ids=True)
+    probes, pip_tests, false_hits, solely_true, refined, cand_refs = st.as_tuple()
+    assert probes == n and false_hits + solely_true + refined == n
+    if mode == capi.GJ_MODE_APPROX:
+        assert pip_tests == 0
+        assert np.array_equal(counts, _hist(bundle, first, ovf_id))
+    else:
+        assert pip_tests == cand_refs
+    # device-resident call, in pieces that are not multiples of anything
+    d_pts = torch.from_numpy(pts).cuda()
+    d_counts = torch.zeros(len(bundle.ids), dtype=torch.int64, device="cuda")
+    d_stats = torch.zeros(6, dtype=torch.int64, device="cuda")
+    d_first = torch.empty(n, dtype=torch.int32, device="cuda")
+    torch.cuda.synchronize()
+    flat = d_pts.view(-1)
+    piece = 7_654_321
+    for a in range(0, n, piece):
+        s.join_count_device(flat[2 * a:].data_ptr(), min(piece, n - a), d_counts.data_ptr(), mode,
+                            d_stats_ptr=d_stats.data_ptr(), d_first_id_ptr=d_first[a:].data_ptr())
+    s.sync()
+    assert np.array_equal(d_counts.cpu().numpy().astype(np.uint64), counts)
+    assert tuple(int(v) for v in d_stats.cpu().numpy()) == st.as_tuple()
+    if mode == capi.GJ_MODE_APPROX:
+        assert np.array_equal(d_first.cpu().numpy().view(np.uint32), first)
+    # the reference itself on a prefix
+    from oracle import ref
+    if ref.available():
+        rb = ref.RefBundle.load(path)
+        m = 1_000_000
+        got, _, _ = s.join_count(pts[:m], mode)
+        got_map = {int(bundle.ids[k]): int(got[k]) for k in np.nonzero(got)[0]}
+        want = rb.join_exact_count_threads(pts[:m], 8) if mode == capi.GJ_MODE_EXACT else rb.join_count(pts[:m], 8)
+        assert got_map == want
+        mp = 100_000
+        row_ptr, ids = s.join_pairs(pts[:mp], mode)
+        pi, pid, rst = rb.join_pairs(pts[:mp], mode == capi.GJ_MODE_EXACT)
+        gpi = np.repeat(np.arange(mp, dtype=np.uint64), np.diff(row_ptr.astype(np.int64)))
+        assert np.array_equal(gpi, pi) and np.array_equal(ids, pid)
+    bundle.close()
