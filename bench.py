@@ -15,7 +15,15 @@ Prints ONE JSON line (rank 0).  ``value`` = points/s with points resident in
 HBM; ``e2e`` = the same join through the host-buffer C-ABI call with H2D/D2H
 inside the timed region; ``roofline`` = algorithmic bytes (20 B/point) over
 the measured kernel time against the measured HBM copy bandwidth;
-``cpu_baseline`` = the reference's own multithreaded CPU join on this box.
+``cpu_baseline`` = the reference's own multithreaded CPU join on this box, whose
+per-polygon counts must equal the GPU's (``counts_equal_reference``; a mismatch
+exits non-zero); ``secondary`` (N = 1) = the other BASELINE configs — configs[2]
+exact at full size, configs[3] / configs[4] on their cached density-matched
+indexes — each timed the same way and compared per polygon with the reference.
+
+``--gpus N`` with N > 1 and no torchrun environment starts the N ranks itself
+(re-exec under ``torch.distributed.run``, NCCL's init log left on); it fails
+loudly when the box has fewer than N GPUs or when WORLD_SIZE disagrees with N.
 """
 from __future__ import annotations
 
@@ -118,11 +126,25 @@ def measured_peak():
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def kernel_source_hash() -> str:
+    """Content hash of the CUDA sources (works on the GPU box, which has no .git)."""
+    import hashlib
+    h = hashlib.sha256()
+    for f in sorted((ROOT / "paper_1802_09488_b200" / "csrc").iterdir()):
+        h.update(f.name.encode())
+        h.update(f.read_bytes())
+    return h.hexdigest()[:16]
+
+
 def ncu_traffic():
+    """profiles/roofline.json: the last ncu capture of K1 (tools/ncu_roofline.py), stamped with the hash of
+    the kernel sources it was taken on — stale when they have changed since."""
     p = ROOT / "profiles" / "roofline.json"
     if p.exists():
         try:
-            return json.loads(p.read_text())
+            doc = json.loads(p.read_text())
+            doc["ncu_stale"] = doc.get("kernel_source_hash") != kernel_source_hash()
+            return doc
         except Exception:
             pass
     return {}
@@ -153,24 +175,36 @@ def bundle_path() -> Path:
 # --------------------------------------------------------------------------------------
 # reference arm / cpu baseline: the reference's own CPU join on the host cores
 # --------------------------------------------------------------------------------------
-def cpu_join_runner(path: Path):
-    """Returns (kind, cores, fn(points) -> (seconds, pairs)) for the CPU arm:
-    the compiled reference when oracle/_ref is present, else the C oracle port."""
+def cpu_join_runner(path: Path, exact: bool = False):
+    """Returns (kind, cores, fn(points) -> (seconds, pairs), counts_fn(points) -> ({polygon id: count}, seconds))
+    for the CPU arm: the compiled reference when oracle/_ref is present, else the C oracle port.  ``exact``:
+    the join mode (the reference's join_count_per_polygon takes it from the bundle, join.cpp:257; an exact join
+    over an approx-built bundle — configs[4] — threads join_exact over 64 K-point chunks)."""
     from oracle import build as obuild
     cores = os.cpu_count() or 1
     if obuild.REF_LIB.exists() or obuild.reference_available():
         from oracle import ref
         b = ref.RefBundle.load(path)
-        return "reference", cores, lambda pts: b.time_join_count(pts, cores)
-    from oracle import oracle
+
+        def counts(pts):
+            t0 = time.perf_counter()
+            m = b.join_exact_count_threads(pts, cores) if exact and b.approx else b.join_count(pts, cores)
+            return m, time.perf_counter() - t0
+        assert exact or b.approx
+        return "reference", cores, (lambda pts: b.time_join_count(pts, cores)), counts
     from tests import golden_util
     ox = golden_util.oracle_index(golden_util.parse_gjx(path.read_bytes()))
 
     def run(pts):
         t0 = time.perf_counter()
-        _, tot = ox.join_count(pts, approx=True, threads=cores)
+        _, tot = ox.join_count(pts, approx=not exact, threads=cores)
         return time.perf_counter() - t0, tot
-    return "port", cores, run
+
+    def counts(pts):
+        t0 = time.perf_counter()
+        m, _ = ox.join_count(pts, approx=not exact, threads=cores)
+        return m, time.perf_counter() - t0
+    return "port", cores, run, counts
 
 
 def run_reference(args):
@@ -178,7 +212,7 @@ def run_reference(args):
     if rank != 0:
         return
     path = bundle_path()
-    kind, cores, fn = cpu_join_runner(path)
+    kind, cores, fn, _ = cpu_join_runner(path)
     n = min(args.points, args.ref_points)
     pts = make_points(n, 0)
     for _ in range(args.warmup):
@@ -205,17 +239,124 @@ def run_reference(args):
 # --------------------------------------------------------------------------------------
 # our arm
 # --------------------------------------------------------------------------------------
+def counts_map(ids, counts) -> dict:
+    c = np.asarray(counts).astype(np.uint64)
+    return {int(ids[k]): int(c[k]) for k in np.nonzero(c[:len(ids)])[0]}
+
+
+def time_device_join(torch, sess, d_pts, n, d_counts, d_first, mode, reps, warmup=2):
+    """Mean CUDA-event time (ms) of ``reps`` device-resident joins on the session stream."""
+    stream = torch.cuda.ExternalStream(sess.stream)
+
+    def step():
+        sess.join_count_device(d_pts.data_ptr(), n, d_counts.data_ptr(), mode,
+                               d_first_id_ptr=d_first.data_ptr() if d_first is not None else 0)
+    torch.cuda.synchronize()
+    for _ in range(warmup):
+        step()
+    sess.sync()
+    l0 = sess.launches
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        e0.record()
+        for _ in range(reps):
+            step()
+        e1.record()
+    sess.sync()
+    return e0.elapsed_time(e1) / reps, (sess.launches - l0) // reps
+
+
+# (config, density scale of the cached index, points, gj_options fields, label)
+SECONDARY = [
+    (3, 1.0, 100_000_000, {},
+     "configs[2]: exact join, trained index, 289 polygons, 100 M mixture points, ~1 % on edges / vertices (FULL size)"),
+    (4, 0.04, 40_000_000, {"dir16_level_max": 17},
+     "configs[3] regime on its density-matched 4 % index (1 600 polygons at 1 m, k_max 56, shared-memory tier "
+     "capped at the level the full-size box gets); the full 40 000-polygon / 1 B-point run is tools/fullsize.py 4"),
+    (5, 0.03, 10_000_000, {},
+     "configs[4] regime on its density-matched 3 % index (300 overlapping stars, every probe a lookup-table "
+     "record, exact); the full 10 000-star / 500 M-point run is tools/fullsize.py 5"),
+]
+
+
+def run_secondary(torch, capi, join, peak, reps=5):
+    """The other BASELINE configs, each: device-resident join (first ids + counts) timed with CUDA events, and
+    the per-polygon counts of the host-buffer call compared with the reference's CPU join on the same points."""
+    from tools import build_bundles
+    out = []
+    for config, scale, n, opt, label in SECONDARY:
+        t_all = time.time()
+        name = build_bundles.workload_name(config, scale)
+        if not build_bundles.have_bundle(name):
+            out.append({"config": config, "workload": label, "unavailable": f"no cached index {name}"})
+            continue
+        spec = synth.SPECS[config]
+        path = build_bundles.bundle_file(name)
+        bundle = join.IndexBundle.load(path, device=torch.cuda.current_device(),
+                                       options=capi.Options(**opt) if opt else None)
+        sess = bundle.session()
+        polys = synth.polygons_for(config, scale) if spec.boundary_fraction > 0 else None
+        pts = synth.points_for(config, n, polys, scale=scale)
+        exact = spec.exact
+        mode = capi.GJ_MODE_EXACT if exact else capi.GJ_MODE_APPROX
+        d_pts = torch.from_numpy(pts).cuda()
+        d_counts = torch.zeros(max(1, len(bundle.ids)), dtype=torch.int64, device="cuda")
+        d_first = torch.empty(n, dtype=torch.int32, device="cuda")
+        ms, launches = time_device_join(torch, sess, d_pts, n, d_counts, d_first, mode, reps)
+        del d_pts, d_first
+        # parity: the host-buffer call against the reference's CPU join, polygon by polygon
+        st = join.JoinStats()
+        counts, _, _ = sess.join_count(pts, mode, stats=st)
+        kind, cores, _, cpu_counts = cpu_join_runner(path, exact)
+        want, cpu_s = cpu_counts(pts)
+        equal = counts_map(bundle.ids, counts) == want
+        pairs = int(counts.sum())
+        if config == 5:   # 16 B point + 4 B id + the lookup-table record [t, ids, c, ids] every probe reads
+            all_refs, _, _ = sess.join_count(pts, capi.GJ_MODE_APPROX)  # approx mode emits every reference
+            a_bytes = 20.0 + 4.0 * (2.0 + float(all_refs.sum()) / max(1, n))
+            a_note = "16 B point + 4 B first id + 4 B x (2 + references per point) of lookup-table record"
+        elif exact:       # + 12 B written and read again per candidate task (point, slot, ordinal)
+            a_bytes = 20.0 + 12.0 * st.pip_tests / max(1, n)
+            a_note = "16 B point + 4 B first id + 12 B per candidate task (SURVEY.md 8d)"
+        else:
+            a_bytes = 20.0
+            a_note = "16 B point + 4 B first id"
+        achieved = a_bytes * n / (ms * 1e-3) / 1e9
+        out.append({
+            "config": config, "workload": label, "index": name, "mode": "exact" if exact else "approx",
+            "points": n, "ms": ms, "points_per_s": n / (ms * 1e-3), "kernel_launches_per_step": launches,
+            "pairs_per_point": pairs / n, "pip_tests_per_point": st.pip_tests / n,
+            "algorithmic_bytes_per_point": a_bytes, "algorithmic_bytes_note": a_note,
+            "achieved_GBps": achieved, "frac": achieved / peak,
+            "counts_equal_reference": bool(equal),
+            "cpu_baseline": {"value": n / cpu_s, "unit": "points/s", "cores": cores, "kind": kind,
+                             "sample": f"all {n} points, per-polygon counts, {cpu_s:.2f}s"},
+            "options": opt, "seconds_total": round(time.time() - t_all, 1),
+        })
+        log(f"[bench] secondary config {config}: {ms:.3f} ms per {n} points, frac {achieved / peak:.3f}, "
+            f"counts equal reference: {equal} ({time.time() - t_all:.1f}s)")
+        sess.close()
+        bundle.close()
+        del pts
+    return out
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
 
-    from paper_1802_09488_b200 import capi, join
+    from paper_1802_09488_b200 import capi, join, sharding
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE is {world}: launch one rank per GPU "
+                         f"(python -m torch.distributed.run --nproc-per-node {args.gpus} bench.py --gpus {args.gpus} ...)")
     if not torch.cuda.is_available():
-        raise RuntimeError("bench.py needs a CUDA device: the GPU path has no CPU fallback")
+        raise SystemExit("bench.py needs a CUDA device: the GPU path has no CPU fallback")
+    if torch.cuda.device_count() <= local:
+        raise SystemExit(f"bench.py: rank {rank} wants cuda:{local} but the box has {torch.cuda.device_count()} GPU(s)")
     torch.cuda.set_device(local)
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
@@ -236,9 +377,9 @@ def run_ours(args):
     bundle = join.IndexBundle.load(path, device=local)  # replicate: every rank loads into its own HBM
     sess = bundle.session()
     info = bundle.info
-    log(f"[bench] rank {rank}: index {info.node_count} nodes, {info.device_bytes / 1e6:.0f} MB HBM, "
-        f"directory tier 1 level {info.dir_level} ({info.dir_width}x{info.dir_height}, shared memory), "
-        f"tier 2 level {info.dir2_level} ({info.dir2_width}x{info.dir2_height}, L2), dict {info.dir_dict_len}")
+    log(f"[bench] rank {rank}/{world} on cuda:{local}: index {info.node_count} nodes, {info.device_bytes / 1e6:.0f} MB HBM, "
+        f"shared-memory tier level {info.dir16_level} ({info.dir16_width}x{info.dir16_height}), "
+        f"L2 tier level {info.dir2_level} ({info.dir2_width}x{info.dir2_height}), dict {info.dir_dict_len}")
 
     t0 = time.time()
     host_pts = make_points(n, rank, pinned_alloc=L.gj_host_alloc)
@@ -286,10 +427,9 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms_max = float(t.item())
 
-    # counts: the only cross-GPU exchange, after the timed region
-    counts_steps = d_counts.clone()
-    if world > 1:
-        dist.all_reduce(counts_steps, op=dist.ReduceOp.SUM)
+    # counts: the only cross-GPU exchange (one NCCL all-reduce), after the timed region
+    local_counts = d_counts.clone()
+    counts_steps = sharding.allreduce_counts(d_counts.clone())
 
     # ---- end to end through the host-buffer C-ABI call (pinned host memory) ----
     e2e_steps = max(1, min(args.steps, args.e2e_steps))
@@ -324,13 +464,16 @@ def run_ours(args):
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     e2e_s = float(tt.item())
 
-    # ---- self-check: device-resident, e2e and a CPU-oracle sample agree ----
-    per_step_dev = (d_counts.cpu().numpy().astype(np.uint64))[:n_ids]
-    assert np.array_equal(per_step_dev, (h_counts[:n_ids] // e2e_steps) * args.steps), "device vs e2e counts differ"
-    assert np.array_equal(first_host, d_first.cpu().numpy().view(np.uint32)), "device vs e2e ids differ"
+    # ---- self-check: the device-resident and the host-buffer path agree on this rank's shard ----
+    per_step_dev = (local_counts.cpu().numpy().astype(np.uint64))[:n_ids]
+    if not np.array_equal(per_step_dev, (h_counts[:n_ids] // e2e_steps) * args.steps):
+        raise SystemExit(f"bench.py: rank {rank}: device-resident and host-buffer counts differ")
+    if not np.array_equal(first_host, d_first.cpu().numpy().view(np.uint32)):
+        raise SystemExit(f"bench.py: rank {rank}: device-resident and host-buffer first ids differ")
 
     if rank != 0:
         if world > 1:
+            dist.barrier()
             dist.destroy_process_group()
         return
 
@@ -346,27 +489,45 @@ def run_ours(args):
         "traffic": prof.get("traffic_bytes_per_launch"),
         "kernel": "gj::join_kernel<ids=true, stats=false>", "kernel_ms": kernel_ms,
         "algorithmic_bytes_per_point": BYTES_PER_POINT, "points_per_launch": n, "peak_source": peak_src,
-        "ncu": {k: v for k, v in prof.items() if k != "traffic_bytes_per_launch"} or None,
+        "l2_hit_rate_pct": prof.get("lts__t_sector_hit_rate_pct"),
+        "sectors_per_request": prof.get("l1tex_sectors_per_request_global_ld"),
+        "ncu_stale": prof.get("ncu_stale", True),
+        "ncu": {k: v for k, v in prof.items() if k not in ("traffic_bytes_per_launch", "ncu_stale")} or None,
     }
 
-    # ---- CPU baseline: the reference's multithreaded join on this box's cores ----
+    # ---- CPU baseline: the reference's multithreaded join on this box's cores, and the parity gate ----
     cpu = None
+    counts_equal = None
     if world == 1 and not args.no_cpu_baseline:
-        try:
-            kind, cores, fn = cpu_join_runner(path)
-            m = min(n, args.ref_points)
-            fn(host_pts[: m // 8])
-            secs, pairs = fn(host_pts[:m])
-            cpu = {"value": m / secs, "unit": "points/s", "cores": cores, "kind": kind,
-                   "sample": f"first {m} of {n} points, one join_count_per_polygon call, {cores} threads, {secs:.2f}s"}
-            # the CPU join of the sample must give the GPU's counts
+        kind, cores, fn, cpu_counts = cpu_join_runner(path)
+        m = min(n, args.ref_points)
+        fn(host_pts[: m // 8])
+        secs, pairs = fn(host_pts[:m])
+        cpu = {"value": m / secs, "unit": "points/s", "cores": cores, "kind": kind,
+               "sample": f"first {m} of {n} points, one join_count_per_polygon call, {cores} threads, {secs:.2f}s"}
+        # the CPU join of the sample must give the GPU's per-polygon counts, polygon by polygon
+        want, _ = cpu_counts(host_pts[:m])
+        if m == n:
+            got = counts_map(bundle.ids, h_counts[:n_ids] // e2e_steps)
+        else:
             chk = np.zeros(max(1, n_ids), np.uint64)
             bad = ctypes.c_uint64(0)
             rc = L.gj_join_count_host(sess._h, host_pts.ctypes.data, m, 0, capi.GJ_MODE_APPROX,
                                       chk.ctypes.data, None, None, None, ctypes.byref(bad))
-            assert rc == 0 and int(chk.sum()) == int(pairs), "GPU vs CPU pair totals differ on the sample"
-        except Exception as exc:  # the baseline is reported, never required
-            log(f"[bench] cpu baseline unavailable: {exc}")
+            if rc != 0:
+                raise SystemExit(f"bench.py: gj_join_count_host failed: {rc} {L.gj_last_error().decode()}")
+            got = counts_map(bundle.ids, chk)
+        counts_equal = got == want and sum(want.values()) == int(pairs)
+        log(f"[bench] per-polygon counts equal the CPU {kind} join on {m} points: {counts_equal}")
+
+    # ---- the other configs (N = 1): configs[2] exact at full size, configs[3]/[4] on density-matched indexes ----
+    secondary = None
+    if world == 1 and not args.no_secondary:
+        del d_pts, d_first
+        L.gj_host_free(first_host_ptr)
+        first_host = None
+        torch.cuda.empty_cache()
+        secondary = run_secondary(torch, capi, join, peak)
 
     out = {
         "metric": "joined_points_per_sec", "value": value, "unit": "points/s", "n_gpus": world,
@@ -378,15 +539,43 @@ def run_ours(args):
                 "steps": e2e_steps, "ms_per_step": 1e3 * e2e_s / e2e_steps,
                 "call": "gj_join_count_host (pinned host points in, first ids + counts + overflow out)"},
         "gpu_launches": int(gpu_launches),
-        "roofline": roofline, "cpu_baseline": cpu,
+        "roofline": roofline, "cpu_baseline": cpu, "counts_equal_reference": counts_equal,
         "pairs_per_step": int(counts_steps.sum().item()) // args.steps,
+        "secondary": secondary,
     }
     print(json.dumps(out), flush=True)
     if world > 1:
+        dist.barrier()
         dist.destroy_process_group()
+    bad_secondary = [x["config"] for x in (secondary or []) if x.get("counts_equal_reference") is False]
+    if counts_equal is False or bad_secondary:
+        raise SystemExit(f"bench.py: GPU per-polygon counts differ from the reference CPU join "
+                         f"(headline: {counts_equal}, secondary configs failing: {bad_secondary})")
 
 
-def main():
+def launch_ranks(args, argv) -> int:
+    """``--gpus N`` outside torchrun: start the N ranks here, one per GPU, over NCCL."""
+    import socket
+
+    import torch
+    have = torch.cuda.device_count() if torch.cuda.is_available() else 0
+    if have < args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but this box has {have} CUDA device(s); "
+                         "the GPU path has no CPU fallback and does not oversubscribe devices")
+    with socket.socket() as sck:
+        sck.bind(("127.0.0.1", 0))
+        port = sck.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")          # the communicator / transport lines (NVLS, P2P) go to stderr
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve()), *argv]
+    log(f"[bench] starting {args.gpus} ranks: {' '.join(cmd)}")
+    return subprocess.call(cmd, env=env)
+
+
+def main(argv=None):
+    argv = list(sys.argv[1:] if argv is None else argv)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
@@ -396,10 +585,15 @@ def main():
     ap.add_argument("--ref-points", type=int, default=100_000_000, help="CPU-arm sample size per step")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    args = ap.parse_args()
+    ap.add_argument("--no-secondary", action="store_true", help="skip the other BASELINE configs (N = 1 only anyway)")
+    args = ap.parse_args(argv)
+    if args.gpus < 1:
+        raise SystemExit("bench.py: --gpus must be >= 1")
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     if args.impl == "reference":
         run_reference(args)
+    elif args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        raise SystemExit(launch_ranks(args, argv))
     else:
         run_ours(args)
 

@@ -107,6 +107,34 @@ typedef struct {
   int32_t reserved0;
 } gj_index_info;
 
+/* Explicit tuning knobs and test hooks (the shipped library reads NO environment
+ * variable).  Zero-initialise with gj_options_default and change what you need;
+ * every field's default is the shipped behaviour.  Passed to the *_ex creators
+ * and kept by the index (sessions read the launch knobs from it). */
+typedef struct {
+  uint32_t struct_size;         /* sizeof(gj_options), set by gj_options_default */
+  int32_t dir16_max_entries;    /* cells of the join kernel's shared-memory tier; 0 = sized to the carve-out step */
+  int32_t dir16_level_max;      /* cap its grid level (a density-matched stand-in over a small box can emulate
+                                   the tier level the full-size box gets); 0 = none */
+  int32_t node_pal_max_mb;      /* palette nodes are built while they fit this many MB; -1 = default, 0 = never */
+  int32_t tier_sub;             /* refined 32-bit tier: -1 = automatic, 0 = none, 1..3 = that many grid levels */
+  int32_t ids_late;             /* first ids written where a point is settled: -1 = automatic, 0 / 1 = force */
+  int32_t queue_unpacked;       /* test hook: 1 = force the fallback queue coding */
+  int32_t queue_slot_hi_bits;   /* test hook: at least this many high arena-slot bits travel in the first queue word */
+  int32_t hist_rep_cap;         /* cap the shared-memory histogram replication; -1 = none, 0 = count through the
+                                   per-CTA private copies */
+  int32_t smem_pad;             /* unused shared memory added to the join kernel (L1 carve-out experiments) */
+  int32_t debug_plan;           /* 1 = print the join kernel's shared-memory plan to stderr */
+  int32_t hist16;               /* id tables beyond the 32-bit shared histogram count in a 16-bit one with
+                                   periodic flushes: -1 = automatic, 0 = never */
+  int32_t bin_open;             /* open points of wide arenas are binned by trie node before the arena is read:
+                                   -1 = automatic, 0 = never, 1 = always (when the coding allows it) */
+  uint64_t max_launch_points;   /* test hook: split device-resident calls into launches of this many points; 0 = none */
+  uint64_t chunk_points;        /* host pipeline: points per chunk; 0 = default (3 M counts / 4 M pairs), min 4096 */
+} gj_options;
+
+GJ_API void gj_options_default(gj_options* opt);
+
 /* JoinStats (include/geojoin/join.hpp:77-84), in this order. */
 typedef struct {
   uint64_t probes;
@@ -127,11 +155,22 @@ GJ_API int gj_device_count(void);
  * depth <= ceil((k_max - prefix_bits)/8), every lookup-table record in
  * bounds.  After that the kernels run check-free.  `device` < 0 = current. */
 GJ_API int gj_index_create(const gj_index_desc* desc, int device, gj_index** out);
+/* Same with explicit options (NULL = defaults). */
+GJ_API int gj_index_create_ex(const gj_index_desc* desc, int device, const gj_options* opt,
+                              gj_index** out);
 
 /* Reads the reference's GJX1 bundle file (IndexBundle::save,
  * src/join.cpp:316-339, wrapping the ACT1 snapshot, src/act.cpp:600-622)
  * straight into HBM without constructing the reference's Act. */
 GJ_API int gj_index_load_file(const char* gjx1_path, int device, gj_index** out);
+GJ_API int gj_index_load_file_ex(const char* gjx1_path, int device, const gj_options* opt,
+                                 gj_index** out);
+
+/* Replicates an index into another GPU's HBM (or once more into the same one)
+ * device to device — over NVLink when the GPUs are peers — without going back
+ * to the host arrays: north_star's "index replicated on each GPU".  The copy is
+ * independent of `src` afterwards. */
+GJ_API int gj_index_replicate(const gj_index* src, int device, gj_index** out);
 
 GJ_API void gj_index_destroy(gj_index* ix);
 GJ_API int gj_index_get_info(const gj_index* ix, gj_index_info* info);
@@ -258,6 +297,42 @@ GJ_API int gj_join_pairs_host(gj_session* s, const double* latlng, uint64_t n,
                               int mode, uint64_t* n_pairs, gj_stats* stats,
                               uint64_t* bad_index);
 GJ_API int gj_pairs_copy(gj_session* s, uint64_t* row_ptr, uint32_t* polygon_id);
+
+/* ---- all GPUs of the box for ONE input: ≙ the worker fan-out of
+ * join_count_per_polygon (src/join.cpp:255-285) ------------------------------
+ * A group holds one index replica + session per listed device (a device may be
+ * listed more than once; replicas share nothing).  The first replica is built
+ * from the host arrays / the GJX1 file, the others are copied from it device to
+ * device (gj_index_replicate).  A group call splits its points into contiguous
+ * ranges [n*g/G, n*(g+1)/G) — the reference's worker split, join.cpp:264-265 —
+ * runs range g on replica g with base_index + n*g/G from its own host thread
+ * (own PCIe link, own copy engines), and merges like the reference does
+ * (join.cpp:280-284): per-polygon counts and JoinStats are summed; first ids and
+ * CSR rows are written in place at their global positions; overflow records and
+ * CSR ids are concatenated in range order, which is the global order.  Nothing
+ * crosses GPUs on the probe path.  `workers` = how many replicas take part
+ * (the reference's `threads`): <= 0 or > size means all of them.
+ * Results do not depend on it (tests/test_join.cpp:200-214). */
+typedef struct gj_group gj_group;
+
+GJ_API int gj_group_create(const gj_index_desc* desc, const int* devices, int n_devices,
+                           const gj_options* opt, gj_group** out);
+GJ_API int gj_group_load_file(const char* gjx1_path, const int* devices, int n_devices,
+                              const gj_options* opt, gj_group** out);
+GJ_API void gj_group_destroy(gj_group* g);
+GJ_API int gj_group_size(const gj_group* g);
+/* Borrowed handles of replica k (owned by the group). */
+GJ_API gj_index* gj_group_index(gj_group* g, int k);
+GJ_API gj_session* gj_group_session(gj_group* g, int k);
+
+GJ_API int gj_group_join_count_host(gj_group* g, int workers, const double* latlng, uint64_t n,
+                                    uint64_t base_index, int mode, uint64_t* counts,
+                                    gj_stats* stats, uint32_t* out_first_id,
+                                    gj_overflow* overflow, uint64_t* bad_index);
+GJ_API int gj_group_join_pairs_host(gj_group* g, int workers, const double* latlng, uint64_t n,
+                                    int mode, uint64_t* n_pairs, gj_stats* stats,
+                                    uint64_t* bad_index);
+GJ_API int gj_group_pairs_copy(gj_group* g, uint64_t* row_ptr, uint32_t* polygon_id);
 
 #ifdef __cplusplus
 }

@@ -57,14 +57,29 @@ inline void check(int status) {
 
 }  // namespace detail
 
-/// The reference's IndexBundle replicated into one GPU's HBM.  Immutable like
-/// the bundle it came from (join.hpp:86-88); the session inside serialises
-/// callers, so use one DeviceIndex per calling thread or guard it.
+/// Every CUDA device of the box, in order: the device list that makes the GPU
+/// join use all of them.
+inline std::vector<int> all_devices() {
+  std::vector<int> d(static_cast<size_t>(gj_device_count()));
+  for (size_t k = 0; k < d.size(); ++k) d[k] = static_cast<int>(k);
+  return d;
+}
+
+/// The reference's IndexBundle replicated into the HBM of one GPU — or of
+/// several: the first replica is built from the bundle, the others are copied
+/// from it device to device.  Immutable like the bundle it came from
+/// (join.hpp:86-88); the sessions inside serialise callers, so use one
+/// DeviceIndex per calling thread or guard it.
 class DeviceIndex {
  public:
   /// Copies the bundle's probe view (act.hpp:108-116), lookup table and
   /// polygons to `device` (-1 = current).  Nothing of `bundle` is retained.
-  explicit DeviceIndex(const IndexBundle& bundle, int device = -1) {
+  explicit DeviceIndex(const IndexBundle& bundle, int device = -1) : DeviceIndex(bundle, std::vector<int>{device}) {}
+
+  /// One replica per listed device (e.g. all_devices()).  The joins below then
+  /// fan out over them like join_count_per_polygon fans out over threads
+  /// (join.cpp:255-285): contiguous point ranges, one per replica.
+  DeviceIndex(const IndexBundle& bundle, const std::vector<int>& devices) {
     const Act& act = bundle.act();
     const ActProbeView& v = act.view();
     gj_index_desc d{};
@@ -94,48 +109,48 @@ class DeviceIndex {
     d.polygon_ids = ids.data();
     d.vtx_off = off.data();
     d.vtx_latlng = latlng.data();
-    init(d, device);
+    gj_group* g = nullptr;
+    detail::check(gj_group_create(&d, resolved(devices).data(), static_cast<int>(devices.size()), nullptr, &g));
+    adopt(g);
   }
 
   /// IndexBundle::load without the host-side Act (join.cpp:341-381).
-  explicit DeviceIndex(const std::string& gjx1_path, int device = -1) {
-    gj_index* ix = nullptr;
-    detail::check(gj_index_load_file(gjx1_path.c_str(), device, &ix));
-    adopt(ix);
+  explicit DeviceIndex(const std::string& gjx1_path, int device = -1)
+      : DeviceIndex(gjx1_path, std::vector<int>{device}) {}
+  DeviceIndex(const std::string& gjx1_path, const std::vector<int>& devices) {
+    gj_group* g = nullptr;
+    detail::check(gj_group_load_file(gjx1_path.c_str(), resolved(devices).data(), static_cast<int>(devices.size()),
+                                     nullptr, &g));
+    adopt(g);
   }
 
   DeviceIndex(const DeviceIndex&) = delete;
   DeviceIndex& operator=(const DeviceIndex&) = delete;
 
-  gj_session* session() const { return session_.get(); }
+  gj_group* group() const { return group_.get(); }
+  int replicas() const { return gj_group_size(group_.get()); }
+  gj_session* session(int k = 0) const { return gj_group_session(group_.get(), k); }
   const gj_index_info& info() const { return info_; }
   const std::vector<uint32_t>& ids() const { return ids_; }
   JoinMode mode() const { return info_.approx_mode ? JoinMode::kApprox : JoinMode::kExact; }
 
  private:
-  void init(const gj_index_desc& d, int device) {
-    gj_index* ix = nullptr;
-    detail::check(gj_index_create(&d, device, &ix));
-    adopt(ix);
+  static std::vector<int> resolved(const std::vector<int>& devices) {
+    if (devices.empty()) throw std::invalid_argument("DeviceIndex: empty device list");
+    return devices;  // -1 = the current device, resolved by the library
   }
-  void adopt(gj_index* ix) {
-    index_.reset(ix);
-    gj_session* s = nullptr;
-    detail::check(gj_session_create(ix, &s));
-    session_.reset(s);
+  void adopt(gj_group* g) {
+    group_.reset(g);
+    gj_index* ix = gj_group_index(g, 0);
     detail::check(gj_index_get_info(ix, &info_));
     ids_.resize(info_.n_ids);
     detail::check(gj_index_ids(ix, ids_.data()));
   }
 
-  struct IndexDeleter {
-    void operator()(gj_index* p) const { gj_index_destroy(p); }
+  struct GroupDeleter {
+    void operator()(gj_group* p) const { gj_group_destroy(p); }
   };
-  struct SessionDeleter {
-    void operator()(gj_session* p) const { gj_session_destroy(p); }
-  };
-  std::unique_ptr<gj_index, IndexDeleter> index_;
-  std::unique_ptr<gj_session, SessionDeleter> session_;  // destroyed before the index
+  std::unique_ptr<gj_group, GroupDeleter> group_;  // replicas and their sessions
   gj_index_info info_{};
   std::vector<uint32_t> ids_;
 };
@@ -161,11 +176,11 @@ inline std::vector<JoinPair> pairs(const DeviceIndex& ix, std::span<const LatLng
                                    JoinStats* stats) {
   uint64_t n_pairs = 0, bad = 0;
   gj_stats s{};
-  check(gj_join_pairs_host(ix.session(), as_doubles(points), points.size(), mode, &n_pairs,
-                           stats ? &s : nullptr, &bad));
+  check(gj_group_join_pairs_host(ix.group(), 0, as_doubles(points), points.size(), mode, &n_pairs,
+                                 stats ? &s : nullptr, &bad));
   std::vector<uint64_t> row_ptr(points.size() + 1);
   std::vector<uint32_t> ids(n_pairs);
-  check(gj_pairs_copy(ix.session(), row_ptr.data(), ids.data()));
+  check(gj_group_pairs_copy(ix.group(), row_ptr.data(), ids.data()));
   // CSR -> the reference's array of {point_index, polygon_id}, a few threads over ranges of points
   std::vector<JoinPair> out(n_pairs);
   const size_t n = points.size();
@@ -195,15 +210,18 @@ inline std::vector<JoinPair> join_approx(const DeviceIndex& ix, std::span<const 
   return detail::pairs(ix, points, GJ_MODE_APPROX, stats);
 }
 
-/// Mode from the bundle (join.cpp:257); zero counts are omitted; `threads` is
-/// accepted for signature parity — the result never depended on it.
+/// Mode from the bundle (join.cpp:257); zero counts are omitted.  `threads` is
+/// the reference's worker count (join.cpp:255-262): that many replicas of the
+/// DeviceIndex each join one contiguous range of the points; values above the
+/// number of replicas, or <= 0, mean all of them.  The result does not depend
+/// on it (tests/test_join.cpp:200-214).
 inline std::map<uint32_t, uint64_t> join_count_per_polygon(const DeviceIndex& ix,
                                                            std::span<const LatLng> points,
-                                                           int /*threads*/ = 1) {
+                                                           int threads = 1) {
   std::vector<uint64_t> counts(ix.ids().size() + 1, 0);
   uint64_t bad = 0;
-  detail::check(gj_join_count_host(ix.session(), detail::as_doubles(points), points.size(), 0,
-                                   GJ_MODE_BUNDLE, counts.data(), nullptr, nullptr, nullptr, &bad));
+  detail::check(gj_group_join_count_host(ix.group(), threads, detail::as_doubles(points), points.size(), 0,
+                                         GJ_MODE_BUNDLE, counts.data(), nullptr, nullptr, nullptr, &bad));
   std::map<uint32_t, uint64_t> out;
   for (size_t s = 0; s < ix.ids().size(); ++s) {
     if (counts[s]) out.emplace(ix.ids()[s], counts[s]);
@@ -216,8 +234,8 @@ inline void accumulate_probe_stats(const DeviceIndex& ix, std::span<const LatLng
   std::vector<uint64_t> counts(ix.ids().size() + 1, 0);
   gj_stats s{};
   uint64_t bad = 0;
-  detail::check(gj_join_count_host(ix.session(), detail::as_doubles(points), points.size(), 0,
-                                   GJ_MODE_APPROX, counts.data(), &s, nullptr, nullptr, &bad));
+  detail::check(gj_group_join_count_host(ix.group(), 0, detail::as_doubles(points), points.size(), 0,
+                                         GJ_MODE_APPROX, counts.data(), &s, nullptr, nullptr, &bad));
   detail::add_stats(s, &stats);
 }
 

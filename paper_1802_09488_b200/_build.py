@@ -12,7 +12,13 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libgeojoin_b200.so"
 SOURCES = ["gj_index.cu", "gj_api.cu"]
-HEADERS = ["gj_device.cuh", "gj_kernels.cuh", "gj_host.hpp", "../../include/geojoin_b200.h"]
+
+
+def _headers():
+    """Every header the two translation units can include: all of csrc/ and include/."""
+    return sorted(p for d in (CSRC, PKG.parent / "include") for p in d.iterdir()
+                  if p.suffix in (".cuh", ".hpp", ".h"))
+
 
 NVCC_FLAGS = [
     "-std=c++17", "-O3", "-lineinfo",
@@ -35,7 +41,7 @@ def up_to_date() -> bool:
     if not LIB.exists():
         return False
     t = LIB.stat().st_mtime
-    deps = [CSRC / f for f in SOURCES + HEADERS] + [Path(__file__)]
+    deps = [CSRC / f for f in SOURCES] + _headers() + [Path(__file__)]
     return all(d.stat().st_mtime <= t for d in deps)
 
 

@@ -25,6 +25,9 @@ EXPORTS = [
     "gj_host_alloc", "gj_host_free", "gj_cells_from_points_host", "gj_probe_points_host", "gj_probe_cells_host",
     "gj_join_count_host", "gj_join_count_device", "gj_session_sync", "gj_session_launches",
     "gj_join_pairs_host", "gj_pairs_copy", "gj_training_candidates_host", "gj_points_from_csv_host",
+    "gj_options_default", "gj_index_create_ex", "gj_index_load_file_ex", "gj_index_replicate",
+    "gj_group_create", "gj_group_load_file", "gj_group_destroy", "gj_group_size", "gj_group_index",
+    "gj_group_session", "gj_group_join_count_host", "gj_group_join_pairs_host", "gj_group_pairs_copy",
 ]
 
 
@@ -50,6 +53,27 @@ class IndexInfo(C.Structure):
         ("dir16_level", C.c_int32), ("dir16_width", C.c_int32), ("dir16_height", C.c_int32),
         ("reserved0", C.c_int32),
     ]
+
+
+class Options(C.Structure):
+    """gj_options: explicit tuning knobs / test hooks (the library reads no
+    environment variable).  ``Options(tier_sub=2, ids_late=1)`` starts from
+    gj_options_default and overrides the named fields."""
+    _fields_ = [
+        ("struct_size", C.c_uint32), ("dir16_max_entries", C.c_int32), ("dir16_level_max", C.c_int32),
+        ("node_pal_max_mb", C.c_int32), ("tier_sub", C.c_int32), ("ids_late", C.c_int32),
+        ("queue_unpacked", C.c_int32), ("queue_slot_hi_bits", C.c_int32), ("hist_rep_cap", C.c_int32),
+        ("smem_pad", C.c_int32), ("debug_plan", C.c_int32), ("hist16", C.c_int32), ("bin_open", C.c_int32),
+        ("max_launch_points", C.c_uint64), ("chunk_points", C.c_uint64),
+    ]
+
+    def __init__(self, **kw):
+        super().__init__()
+        lib().gj_options_default(C.byref(self))
+        for k, v in kw.items():
+            if k not in dict(self._fields_):
+                raise AttributeError(k)
+            setattr(self, k, v)
 
 
 class Stats(C.Structure):
@@ -115,5 +139,30 @@ def lib():
                                               C.POINTER(C.c_uint64)]
         L.gj_training_candidates_host.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_uint64, C.c_void_p,
                                                   C.c_uint64, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
+        L.gj_options_default.argtypes = [C.POINTER(Options)]
+        L.gj_options_default.restype = None
+        L.gj_index_create_ex.argtypes = [C.POINTER(IndexDesc), C.c_int, C.POINTER(Options), C.POINTER(C.c_void_p)]
+        L.gj_index_load_file_ex.argtypes = [C.c_char_p, C.c_int, C.POINTER(Options), C.POINTER(C.c_void_p)]
+        L.gj_index_replicate.argtypes = [C.c_void_p, C.c_int, C.POINTER(C.c_void_p)]
+        L.gj_group_create.argtypes = [C.POINTER(IndexDesc), C.POINTER(C.c_int), C.c_int, C.POINTER(Options),
+                                      C.POINTER(C.c_void_p)]
+        L.gj_group_load_file.argtypes = [C.c_char_p, C.POINTER(C.c_int), C.c_int, C.POINTER(Options),
+                                         C.POINTER(C.c_void_p)]
+        L.gj_group_destroy.argtypes = [C.c_void_p]
+        L.gj_group_destroy.restype = None
+        L.gj_group_size.argtypes = [C.c_void_p]
+        L.gj_group_index.argtypes = [C.c_void_p, C.c_int]
+        L.gj_group_index.restype = C.c_void_p
+        L.gj_group_session.argtypes = [C.c_void_p, C.c_int]
+        L.gj_group_session.restype = C.c_void_p
+        L.gj_group_join_count_host.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_uint64, C.c_uint64, C.c_int,
+                                               C.c_void_p, C.POINTER(Stats), C.c_void_p, C.POINTER(Overflow),
+                                               C.POINTER(C.c_uint64)]
+        L.gj_group_join_pairs_host.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_uint64, C.c_int,
+                                               C.POINTER(C.c_uint64), C.POINTER(Stats), C.POINTER(C.c_uint64)]
+        L.gj_group_pairs_copy.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+        L.gj_index_destroy.restype = None
+        L.gj_session_destroy.restype = None
+        L.gj_host_free.restype = None
         _LIB = L
     return _LIB

@@ -7,6 +7,7 @@
 #include <cstring>
 #include <memory>
 #include <numeric>
+#include <thread>
 
 #include "gj_host.hpp"
 #include "gj_csv.cuh"
@@ -15,8 +16,10 @@
 namespace gj {
 
 const std::string& last_error();
-int create_index(const gj_index_desc& d, int device, gj_index** out);
-int load_index_file(const char* path, int device, gj_index** out);
+gj_options default_options();
+int create_index(const gj_index_desc& d, int device, const gj_options* opt, gj_index** out);
+int load_index_file(const char* path, int device, const gj_options* opt, gj_index** out);
+int replicate_index(const gj_index& src, int device, gj_index** out);
 
 namespace {
 
@@ -24,10 +27,8 @@ namespace {
 // 2^24 nodes and more (DevQueueCoding::index_bits).
 uint64_t max_launch_points(const gj_index& ix) {
   uint64_t cap = (1ull << ix.dev.qc.index_bits) - 1;
-  if (const char* e = std::getenv("GJ_MAX_LAUNCH_POINTS")) {  // test hook: exercise the splitting of device-resident calls
-    const long long v = std::atoll(e);
-    if (v > 0) cap = std::min<uint64_t>(cap, static_cast<uint64_t>(v));
-  }
+  // test hook: exercise the splitting of device-resident calls
+  if (ix.opt.max_launch_points) cap = std::min<uint64_t>(cap, ix.opt.max_launch_points);
   return cap;
 }
 constexpr size_t kScratchBudget = 3ull << 30;      // per-chunk task + overflow scratch
@@ -82,12 +83,16 @@ SmemPlan plan_smem(const gj_index& ix) {
     rep = 1;
     while (rep < 32 && at + one * rep * 2 <= step) rep <<= 1;
   }
-  if (const char* e = std::getenv("GJ_HIST_REP")) rep = std::min<uint32_t>(rep, static_cast<uint32_t>(std::atoi(e)));
+  if (ix.opt.hist_rep_cap >= 0) {  // explicit knob: a power of two at most the planned value, or 0
+    uint32_t cap = 0;
+    while (cap < rep && (cap ? cap * 2 : 1u) <= static_cast<uint32_t>(ix.opt.hist_rep_cap)) cap = cap ? cap * 2 : 1u;
+    rep = cap;
+  }
   p.hist_rep = rep;
   at += one * rep;
-  if (const char* e = std::getenv("GJ_SMEM_PAD")) at += static_cast<size_t>(std::atoi(e));  // tuning knob
+  if (ix.opt.smem_pad > 0 && at + static_cast<size_t>(ix.opt.smem_pad) <= limit) at += static_cast<size_t>(ix.opt.smem_pad);  // L1 carve-out experiments
   p.total = at;
-  if (std::getenv("GJ_DEBUG_PLAN")) {
+  if (ix.opt.debug_plan) {
     std::fprintf(stderr, "[gj] K1 smem: 16-bit tier level %d, %zu B; queues at %u; histogram at %u x%u; total %zu\n",
                  30 - ix.dev.dir16.shift, table_bytes, p.queue_off, p.hist_off, p.hist_rep, p.total);
     const DevDirectory& tb = ix.dev.dirk.n_table ? ix.dev.dirk : (ix.dev.dir2.n_table ? ix.dev.dir2 : ix.dev.dir);
@@ -346,7 +351,7 @@ int run_host_join(gj_session* s, const double* latlng, uint64_t n, uint64_t base
   if (exact) per_point += max_cand * 17;
   if (want_ids) per_point += max_refs * 16;
   uint64_t chunk_points = 3ull << 20;  // measured: 0.5 / 1 / 2 / 3 / 4 / 8 / 16 M points per chunk -> 42.2 / 35.3 / 30.1 / 30.0 / 30.2 / 30.9 / 32.1 ms per 100 M points
-  if (const char* e = std::getenv("GJ_CHUNK_POINTS")) chunk_points = std::strtoull(e, nullptr, 10);  // tuning knob
+  if (ix.opt.chunk_points) chunk_points = std::max<uint64_t>(4096, ix.opt.chunk_points);  // explicit knob
   uint64_t chunk = std::min<uint64_t>(chunk_points, std::max<uint64_t>(4096, kScratchBudget / per_point));
   chunk = std::min<uint64_t>(chunk, std::max<uint64_t>(n, 1));
   const uint64_t task_cap = exact ? chunk * max_cand : 0;
@@ -653,13 +658,30 @@ int gj_device_count(void) {
   return cudaGetDeviceCount(&n) == cudaSuccess ? n : 0;
 }
 
+void gj_options_default(gj_options* opt) {
+  if (opt) *opt = default_options();
+}
+
 int gj_index_create(const gj_index_desc* desc, int device, gj_index** out) {
+  return gj_index_create_ex(desc, device, nullptr, out);
+}
+
+int gj_index_create_ex(const gj_index_desc* desc, int device, const gj_options* opt, gj_index** out) {
   if (!desc) return GJ_INVALID_ARGUMENT;
-  return create_index(*desc, device, out);
+  return create_index(*desc, device, opt, out);
 }
 
 int gj_index_load_file(const char* path, int device, gj_index** out) {
-  return load_index_file(path, device, out);
+  return load_index_file(path, device, nullptr, out);
+}
+
+int gj_index_load_file_ex(const char* path, int device, const gj_options* opt, gj_index** out) {
+  return load_index_file(path, device, opt, out);
+}
+
+int gj_index_replicate(const gj_index* src, int device, gj_index** out) {
+  if (!src) return GJ_INVALID_ARGUMENT;
+  return replicate_index(*src, device, out);
 }
 
 void gj_index_destroy(gj_index* ix) {
@@ -727,7 +749,7 @@ uint64_t gj_session_launches(const gj_session* s) { return s ? s->launches : 0; 
 
 void* gj_host_alloc(size_t bytes) {
   void* p = nullptr;
-  if (cudaHostAlloc(&p, bytes ? bytes : 1, cudaHostAllocDefault) != cudaSuccess) {
+  if (cudaHostAlloc(&p, bytes ? bytes : 1, cudaHostAllocPortable) != cudaSuccess) {  // pinned for every GPU of a group
     cuda_fail(cudaGetLastError(), "cudaHostAlloc");
     return nullptr;
   }
@@ -1126,6 +1148,244 @@ int gj_pairs_copy(gj_session* s, uint64_t* row_ptr, uint32_t* polygon_id) {
     GJ_CUDA(stager_of(s).to_host(polygon_id, s->d_all_ids.ptr, s->pairs_total * 4, s->copy_out));
   }
   return GJ_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Device groups: the reference's worker fan-out (join.cpp:255-285) over GPUs.
+// ---------------------------------------------------------------------------
+struct gj_group {
+  std::vector<gj_index*> ix;
+  std::vector<gj_session*> s;
+  // the last gj_group_join_pairs_host call
+  std::vector<uint64_t> pairs_begin;  // first point of every worker's range, then n
+  std::vector<uint64_t> pairs_base;   // pairs emitted by the ranges before it, then the total
+  bool pairs_valid = false;
+  ~gj_group() {
+    for (gj_session* q : s) gj_session_destroy(q);
+    for (gj_index* q : ix) gj_index_destroy(q);
+  }
+};
+
+namespace {
+
+int group_finish(std::unique_ptr<gj_group>& g, gj_index* first, const int* devices, int n_devices, gj_group** out) {
+  g->ix.push_back(first);
+  for (int k = 1; k < n_devices; ++k) {  // device to device, not from the host again
+    gj_index* rep = nullptr;
+    const int rc = replicate_index(*first, devices[k], &rep);
+    if (rc != GJ_OK) return rc;
+    g->ix.push_back(rep);
+  }
+  for (gj_index* ix : g->ix) {
+    gj_session* s = nullptr;
+    const int rc = gj_session_create(ix, &s);
+    if (rc != GJ_OK) return rc;
+    g->s.push_back(s);
+  }
+  *out = g.release();
+  return GJ_OK;
+}
+
+int group_workers(const gj_group* g, int workers) {
+  const int size = static_cast<int>(g->s.size());
+  return workers <= 0 || workers > size ? size : workers;
+}
+
+// Runs fn(w) for w in [0, W) — worker 0 on the calling thread — and returns the status of the first range
+// that failed (with its error text on this thread), like a sequential scan would.
+template <typename Fn>
+int fan_out(int W, Fn fn, int* failed_worker = nullptr) {
+  std::vector<int> rc(W, GJ_OK);
+  std::vector<std::string> err(W);
+  auto run = [&](int w) {
+    rc[w] = fn(w);
+    if (rc[w] != GJ_OK) err[w] = last_error();
+  };
+  std::vector<std::thread> pool;
+  for (int w = 1; w < W; ++w) pool.emplace_back(run, w);
+  run(0);
+  for (std::thread& t : pool) t.join();
+  for (int w = 0; w < W; ++w) {
+    if (rc[w] != GJ_OK) {
+      set_error(err[w]);
+      if (failed_worker) *failed_worker = w;
+      return rc[w];
+    }
+  }
+  return GJ_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int gj_group_create(const gj_index_desc* desc, const int* devices, int n_devices, const gj_options* opt,
+                    gj_group** out) {
+  if (!desc || !devices || n_devices < 1 || !out) return GJ_INVALID_ARGUMENT;
+  *out = nullptr;
+  std::unique_ptr<gj_group> g(new gj_group);
+  gj_index* first = nullptr;
+  const int rc = create_index(*desc, devices[0], opt, &first);
+  if (rc != GJ_OK) return rc;
+  return group_finish(g, first, devices, n_devices, out);
+}
+
+int gj_group_load_file(const char* path, const int* devices, int n_devices, const gj_options* opt, gj_group** out) {
+  if (!path || !devices || n_devices < 1 || !out) return GJ_INVALID_ARGUMENT;
+  *out = nullptr;
+  std::unique_ptr<gj_group> g(new gj_group);
+  gj_index* first = nullptr;
+  const int rc = load_index_file(path, devices[0], opt, &first);
+  if (rc != GJ_OK) return rc;
+  return group_finish(g, first, devices, n_devices, out);
+}
+
+void gj_group_destroy(gj_group* g) { delete g; }
+int gj_group_size(const gj_group* g) { return g ? static_cast<int>(g->s.size()) : 0; }
+gj_index* gj_group_index(gj_group* g, int k) {
+  return g && k >= 0 && k < static_cast<int>(g->ix.size()) ? g->ix[k] : nullptr;
+}
+gj_session* gj_group_session(gj_group* g, int k) {
+  return g && k >= 0 && k < static_cast<int>(g->s.size()) ? g->s[k] : nullptr;
+}
+
+int gj_group_join_count_host(gj_group* g, int workers, const double* latlng, uint64_t n, uint64_t base_index,
+                             int mode, uint64_t* counts, gj_stats* stats, uint32_t* out_first_id,
+                             gj_overflow* overflow, uint64_t* bad_index) {
+  if (!g || g->s.empty() || (n && !latlng)) return GJ_INVALID_ARGUMENT;
+  bool exact = false;
+  if (!resolve_exact(*g->ix[0], mode, &exact)) return GJ_INVALID_ARGUMENT;
+  if (overflow && !out_first_id) {
+    set_error("an overflow list needs out_first_id");
+    return GJ_INVALID_ARGUMENT;
+  }
+  const int W = group_workers(g, workers);
+  const uint32_t n_ids = g->ix[0]->dev.n_ids;
+  struct Part {
+    std::vector<uint64_t> counts;
+    gj_stats st{};
+    OverflowSink sink;
+    uint64_t bad = 0;
+  };
+  std::vector<Part> part(W);
+  int failed = 0;
+  auto begin_of = [&](int w) { return static_cast<uint64_t>(static_cast<unsigned __int128>(n) * w / W); };  // join.cpp:264-265
+  const int rc = fan_out(W, [&](int w) {
+    Part& p = part[w];
+    p.counts.assign(n_ids + 1, 0);
+    const uint64_t begin = begin_of(w), len = begin_of(w + 1) - begin;
+    return run_host_join(g->s[w], latlng + 2 * begin, len, base_index + begin, exact, p.counts.data(),
+                         stats ? &p.st : nullptr, out_first_id ? out_first_id + begin : nullptr,
+                         out_first_id ? &p.sink : nullptr, &p.bad);
+  }, &failed);
+  if (rc != GJ_OK) {  // the first failing range holds the smallest offending index
+    if (bad_index) *bad_index = part[failed].bad;
+    return rc;
+  }
+  // merge like join.cpp:280-284
+  for (int w = 0; w < W; ++w) {
+    if (counts) {
+      for (uint32_t i = 0; i < n_ids; ++i) counts[i] += part[w].counts[i];
+    }
+    if (stats) {
+      stats->probes += part[w].st.probes;
+      stats->pip_tests += part[w].st.pip_tests;
+      stats->false_hits += part[w].st.false_hits;
+      stats->solely_true_hits += part[w].st.solely_true_hits;
+      stats->refinement_entered += part[w].st.refinement_entered;
+      stats->candidate_refs += part[w].st.candidate_refs;
+    }
+  }
+  if (overflow) {
+    size_t m = 0;
+    for (const Part& p : part) m += p.sink.records.size();
+    overflow->count = m;
+    if (m > overflow->capacity) {
+      set_error("overflow list larger than the caller's capacity");
+      return GJ_CAPACITY;
+    }
+    size_t at = 0;  // ranges ascend, each list is sorted: the concatenation is sorted
+    for (const Part& p : part) {
+      for (const OverflowRecord& r : p.sink.records) {
+        overflow->point_index[at] = r.point;
+        overflow->polygon_id[at] = r.id;
+        ++at;
+      }
+    }
+  }
+  return GJ_OK;
+}
+
+int gj_group_join_pairs_host(gj_group* g, int workers, const double* latlng, uint64_t n, int mode,
+                             uint64_t* n_pairs, gj_stats* stats, uint64_t* bad_index) {
+  if (!g || g->s.empty() || (n && !latlng)) return GJ_INVALID_ARGUMENT;
+  bool exact = false;
+  if (!resolve_exact(*g->ix[0], mode, &exact)) return GJ_INVALID_ARGUMENT;
+  g->pairs_valid = false;
+  const int W = group_workers(g, workers);
+  g->pairs_begin.assign(W + 1, 0);
+  for (int w = 0; w <= W; ++w) g->pairs_begin[w] = static_cast<uint64_t>(static_cast<unsigned __int128>(n) * w / W);
+  std::vector<gj_stats> st(W);
+  std::vector<uint64_t> bad(W, 0);
+  int failed = 0;
+  int rc = fan_out(W, [&](int w) {
+    const uint64_t begin = g->pairs_begin[w], len = g->pairs_begin[w + 1] - begin;
+    return run_host_pairs(g->s[w], latlng + 2 * begin, len, exact, stats ? &st[w] : nullptr, &bad[w]);
+  }, &failed);
+  if (rc != GJ_OK) {
+    if (bad_index) *bad_index = g->pairs_begin[failed] + bad[failed];  // run_host_pairs reports indices of its own range
+    return rc;
+  }
+  g->pairs_base.assign(W + 1, 0);
+  for (int w = 0; w < W; ++w) g->pairs_base[w + 1] = g->pairs_base[w] + g->s[w]->pairs_total;
+  // every replica's row offsets move behind the pairs of the ranges before it, still in HBM
+  rc = fan_out(W, [&](int w) {
+    gj_session* s = g->s[w];
+    const uint64_t rows = g->pairs_begin[w + 1] - g->pairs_begin[w] + 1;
+    if (g->pairs_base[w] == 0) return static_cast<int>(GJ_OK);
+    GJ_CUDA(cudaSetDevice(s->ix->device));
+    add_offset_kernel<<<static_cast<unsigned>(s->ix->sm_count) * 8u, 256, 0, s->stream>>>(s->d_all_row_ptr.as<uint64_t>(),
+                                                                                          rows, g->pairs_base[w]);
+    ++s->launches;
+    GJ_CUDA(cudaGetLastError());
+    GJ_CUDA(cudaStreamSynchronize(s->stream));
+    return static_cast<int>(GJ_OK);
+  });
+  if (rc != GJ_OK) return rc;
+  for (int w = 0; w < W && stats; ++w) {
+    stats->probes += st[w].probes;
+    stats->pip_tests += st[w].pip_tests;
+    stats->false_hits += st[w].false_hits;
+    stats->solely_true_hits += st[w].solely_true_hits;
+    stats->refinement_entered += st[w].refinement_entered;
+    stats->candidate_refs += st[w].candidate_refs;
+  }
+  if (n_pairs) *n_pairs = g->pairs_base[W];
+  g->pairs_valid = true;
+  return GJ_OK;
+}
+
+int gj_group_pairs_copy(gj_group* g, uint64_t* row_ptr, uint32_t* polygon_id) {
+  if (!g || !row_ptr) return GJ_INVALID_ARGUMENT;
+  if (!g->pairs_valid) {
+    set_error("gj_group_pairs_copy: no completed gj_group_join_pairs_host call to copy from");
+    return GJ_INVALID_ARGUMENT;
+  }
+  const int W = static_cast<int>(g->pairs_begin.size()) - 1;
+  // range w's rows land at row_ptr[begin_w .. begin_{w+1}] (its last entry == the next range's first), its ids
+  // behind those of the ranges before it; every replica copies over its own link
+  return fan_out(W, [&](int w) {
+    gj_session* s = g->s[w];
+    GJ_CUDA(cudaSetDevice(s->ix->device));
+    const uint64_t begin = g->pairs_begin[w], rows = g->pairs_begin[w + 1] - begin;
+    GJ_CUDA(stager_of(s).to_host(row_ptr + begin, s->d_all_row_ptr.ptr, (rows + (w == W - 1 ? 1 : 0)) * 8, s->copy_out));
+    if (polygon_id && s->pairs_total) {
+      GJ_CUDA(stager_of(s).to_host(polygon_id + g->pairs_base[w], s->d_all_ids.ptr, s->pairs_total * 4, s->copy_out));
+    }
+    return static_cast<int>(GJ_OK);
+  });
 }
 
 }  // extern "C"

@@ -96,9 +96,9 @@ __host__ __device__ inline uint32_t strip_of(double y, double y0, double inv_h, 
 }
 
 struct DevIndex {
-  const uint64_t* arena;   // payload polygon ids replaced by id-table slots
-  const uint32_t* lut;     // records [t, slot*t, c, slot*c]
-  const uint32_t* ids;     // slot -> polygon id (sorted unique)
+  const uint64_t* arena;   // the reference's arena, bit-identical (act.hpp:241-246): payloads carry polygon ids
+  const uint32_t* lut;     // the reference's lookup table, bit-identical: records [t, id*t, c, id*c]
+  const uint32_t* ids;     // count slot -> polygon id (sorted unique); id -> slot by binary search unless ids_dense
   // closed rings per slot, x = lng, y = lat (geometry.cpp:35); len 0 = the
   // bundle has no geometry for this id (join.cpp:111-114)
   const uint64_t* ring_off;
@@ -325,24 +325,6 @@ __device__ __forceinline__ uint64_t probe_raw(const DevIndex& ix, uint64_t raw) 
     node = e >> 2;
     shift -= 8;
   }
-}
-
-// Device arenas carry id-table slots in their payloads; entries handed back
-// to the caller carry the original polygon ids again (act.hpp:55-83).
-__device__ __forceinline__ uint64_t entry_slots_to_ids(const DevIndex& ix, uint64_t e) {
-  if (ix.ids_dense) return e;
-  const uint32_t tag = static_cast<uint32_t>(e) & 3u;
-  if (tag == 1u) {
-    const uint32_t p = static_cast<uint32_t>(e >> 2) & 0x7fffffffu;
-    return (static_cast<uint64_t>((ix.ids[p >> 1] << 1) | (p & 1u)) << 2) | 1u;
-  }
-  if (tag == 2u) {
-    const uint32_t a = static_cast<uint32_t>(e >> 33) & 0x7fffffffu;
-    const uint32_t b = static_cast<uint32_t>(e >> 2) & 0x7fffffffu;
-    return (static_cast<uint64_t>((ix.ids[a >> 1] << 1) | (a & 1u)) << 33) |
-           (static_cast<uint64_t>((ix.ids[b >> 1] << 1) | (b & 1u)) << 2) | 2u;
-  }
-  return e;  // sentinel or lookup-table offset
 }
 
 // ---------------------------------------------------------------------------

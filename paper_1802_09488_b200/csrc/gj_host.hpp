@@ -229,6 +229,7 @@ struct gj_index {
   int device = 0;
   gj::DevIndex dev{};
   gj_index_info info{};
+  gj_options opt{};            // explicit knobs (gj_options_default unless the creator passed others)
   std::vector<uint32_t> ids;  // slot -> polygon id
   gj::DeviceBuffer d_arena, d_lut, d_ids, d_ring_off, d_ring_len, d_ring_xy, d_dir_table, d_dir_dict, d_dir2_table, d_dir16_table, d_dirk_table, d_node_pal,
       d_strip_meta, d_strip_ptr, d_strip_edges;
@@ -237,6 +238,32 @@ struct gj_index {
   bool ids_late = false;       // K1 writes first ids where a point is settled (join_kernel's kLate): the 16-bit tier resolves few cells
   uint64_t max_refs = 0;       // most references behind one reachable entry
   uint64_t max_cand_refs = 0;  // most candidate references behind one entry
+  // Points the device pointers of `dev` at this index's buffers (after uploads, and after gj_index_replicate
+  // copied the buffers of another index).
+  void bind() {
+    dev.arena = d_arena.as<uint64_t>();
+    dev.lut = d_lut.as<uint32_t>();
+    dev.ids = d_ids.as<uint32_t>();
+    dev.ring_off = d_ring_off.as<uint64_t>();
+    dev.ring_len = d_ring_len.as<uint32_t>();
+    dev.ring_xy = d_ring_xy.as<double2>();
+    dev.strip_meta = d_strip_meta.as<gj::StripMeta>();
+    dev.strip_ptr = d_strip_ptr.as<uint32_t>();
+    dev.strip_edges = d_strip_edges.as<gj::EdgeRecord>();
+    dev.dir.table = d_dir_table.as<uint32_t>();
+    dev.dir2.table = d_dir2_table.as<uint32_t>();
+    dev.dir16.table = d_dir16_table.as<uint32_t>();
+    dev.dirk.table = d_dirk_table.as<uint32_t>();
+    dev.node_pal = d_node_pal.ptr ? d_node_pal.as<uint64_t>() : nullptr;
+    dev.dict = d_dir_dict.as<uint64_t>();
+  }
+  // every device buffer, for replication
+  std::vector<gj::DeviceBuffer gj_index::*> buffers() const {
+    return {&gj_index::d_arena, &gj_index::d_lut, &gj_index::d_ids, &gj_index::d_ring_off, &gj_index::d_ring_len,
+            &gj_index::d_ring_xy, &gj_index::d_dir_table, &gj_index::d_dir_dict, &gj_index::d_dir2_table,
+            &gj_index::d_dir16_table, &gj_index::d_dirk_table, &gj_index::d_node_pal, &gj_index::d_strip_meta,
+            &gj_index::d_strip_ptr, &gj_index::d_strip_edges};
+  }
 };
 
 struct gj_session {
@@ -264,6 +291,4 @@ struct gj_session {
   uint64_t pairs_n = 0, pairs_total = 0;
   bool pairs_valid = false;
   std::unique_ptr<gj::HostStager> stager;  // created on first use with pageable host memory
-  int latched_status = 0;
-  uint64_t latched_bad = ~0ull;
 };

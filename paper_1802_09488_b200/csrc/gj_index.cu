@@ -78,6 +78,7 @@ struct Box {
     y_hi = std::max(y_hi, yh);
   }
   uint64_t area() const { return empty() ? 0 : (x_hi - x_lo + 1) * (y_hi - y_lo + 1); }
+  uint64_t padded_area() const { return empty() ? 1 : (x_hi - x_lo + 2) * (y_hi - y_lo + 2); }
 };
 
 bool record_in_bounds(const gj_index_desc& d, uint64_t off) {  // act.cpp:141-153
@@ -164,7 +165,7 @@ void build_dir16(const HostDirectory& tb, uint64_t max_entries, int max_level, H
 
 // One breadth-first pass per face: forest check, depth bound, record bounds,
 // id collection; for face 0 the first levels also feed the directory.
-int analyse(const gj_index_desc& d, Analysis* out) {
+int analyse(const gj_index_desc& d, const gj_options& opt, Analysis* out) {
   const bool k_ok = d.k_max >= 8 && d.k_max <= 60 && (d.k_max % 8 == 0 || d.k_max == 60);
   if (!k_ok) {  // validate_act_config, act.cpp:38-42
     set_error("k_max must be one of 8, 16, ..., 56, 60");
@@ -245,7 +246,7 @@ int analyse(const gj_index_desc& d, Analysis* out) {
     std::vector<Cell> terminals;  // steps <= the deepest window still tracked
     std::vector<Cell> frontier;   // nodes at the current depth, with cells
     struct Snapshot {
-      int chunks = 0;
+      int chunks = -1;  // -1 = none taken
       Box box;
       std::vector<Cell> links;  // frontier at that depth
       size_t n_terminals = 0;
@@ -254,6 +255,11 @@ int analyse(const gj_index_desc& d, Analysis* out) {
     uint32_t px = 0, py = 0;
     unzip_pairs(d.prefixes[face], prefix_level, &px, &py);
     frontier.push_back(Cell{root, px, py, 0});
+    if (track) {  // zero node steps: the prefix cell links to the root (the tier of last resort, e.g. k_max 60 under a 56-bit prefix)
+      Box b0;
+      b0.add(px, py, px, py);
+      snap1 = snap2 = Snapshot{0, b0, frontier, 0};
+    }
     for (int depth = 0; !frontier.empty(); ++depth) {
       if (depth >= max_chunks) {  // act.cpp:269 / act.cpp:693-696
         set_error("trie path longer than the maximum key length");
@@ -294,8 +300,12 @@ int analyse(const gj_index_desc& d, Analysis* out) {
                   ((static_cast<uint64_t>(t.x) + 1) << s) - 1, ((static_cast<uint64_t>(t.y) + 1) << s) - 1);
         }
         for (const Cell& l : next) box.add(l.x, l.y, l.x, l.y);
-        if (box.area() <= kMaxDirEntries) snap1 = Snapshot{depth + 1, box, next, terminals.size()};
-        if (box.area() <= kMaxDir2Entries) {
+        // A tier must sit at or above the leaf level: with k_max = 60 the last node step ends at "level 32",
+        // two grid levels below the leaf level (its slots use 4 of their 8 key bits), where no window exists.
+        const bool level_ok = prefix_level + 4 * (depth + 1) <= d.k_max / 2;
+        // sized WITH the all-miss padding column and row, which the kernels stage as well
+        if (level_ok && box.padded_area() <= kMaxDirEntries) snap1 = Snapshot{depth + 1, box, next, terminals.size()};
+        if (level_ok && box.padded_area() <= kMaxDir2Entries) {
           snap2 = Snapshot{depth + 1, box, next, terminals.size()};
         } else {
           track = false;  // deeper windows only grow
@@ -310,7 +320,7 @@ int analyse(const gj_index_desc& d, Analysis* out) {
       std::unordered_map<uint64_t, uint32_t> code_of;
       out->dict.assign(1, 0ull);
       auto fill = [&](const Snapshot& sn, HostDirectory& hd) {
-        if (sn.chunks == 0 || sn.box.empty()) return;
+        if (sn.chunks < 0 || sn.box.empty()) return;
         hd.chunks = sn.chunks;
         hd.level = prefix_level + 4 * sn.chunks;
         hd.x0 = static_cast<uint32_t>(sn.box.x_lo);
@@ -369,7 +379,7 @@ int analyse(const gj_index_desc& d, Analysis* out) {
             if (((static_cast<uint64_t>(base.width) << r) + 1) * ((static_cast<uint64_t>(base.height) << r) + 1) <= kMaxDirKEntries) sub = r;
           }
         }
-        if (const char* e = std::getenv("GJ_TIER_SUB")) sub = std::max(0, std::min(room, std::atoi(e)));  // tuning knob / test hook
+        if (opt.tier_sub >= 0) sub = std::max(0, std::min(room, static_cast<int>(opt.tier_sub)));  // explicit knob / test hook
         if (sub > 0) {
           HostDirectory& hk = out->dirk;
           out->dirk_sub = sub;
@@ -459,7 +469,19 @@ int cuda_fail(cudaError_t e, const char* what) {
   return GJ_CUDA_ERROR;
 }
 
-int create_index(const gj_index_desc& d, int device, gj_index** out) {
+gj_options default_options() {
+  gj_options o{};
+  o.struct_size = sizeof(gj_options);
+  o.node_pal_max_mb = -1;
+  o.tier_sub = -1;
+  o.ids_late = -1;
+  o.hist_rep_cap = -1;
+  o.hist16 = -1;
+  o.bin_open = -1;
+  return o;
+}
+
+int create_index(const gj_index_desc& d, int device, const gj_options* options, gj_index** out) {
   if (!out) return GJ_INVALID_ARGUMENT;
   *out = nullptr;
   if ((d.node_count && !d.arena) || (d.lut_len && !d.lut) ||
@@ -475,12 +497,21 @@ int create_index(const gj_index_desc& d, int device, gj_index** out) {
   if (device < 0) GJ_CUDA(cudaGetDevice(&device));
   GJ_CUDA(cudaSetDevice(device));
 
+  gj_options opt = default_options();
+  if (options) {
+    if (options->struct_size != sizeof(gj_options)) {
+      set_error("gj_options: struct_size mismatch (initialise with gj_options_default)");
+      return GJ_INVALID_ARGUMENT;
+    }
+    opt = *options;
+  }
   Analysis an;
-  int rc = analyse(d, &an);
+  int rc = analyse(d, opt, &an);
   if (rc != GJ_OK) return rc;
 
   std::unique_ptr<gj_index> ix(new gj_index);
   ix->device = device;
+  ix->opt = opt;
   ix->ids = std::move(an.ids);
   ix->max_refs = an.max_refs;
   ix->max_cand_refs = an.max_cand_refs;
@@ -585,9 +616,9 @@ int create_index(const gj_index_desc& d, int device, gj_index** out) {
     const size_t besides = k1_smem_besides_tier(n_ids);
     const size_t step = (196u - 1u) << 10;
     uint64_t max16 = std::min<uint64_t>(kMaxDir16Entries, step > besides ? (step - besides) / 2 : 0);
-    if (const char* e = std::getenv("GJ_DIR16_MAX")) max16 = std::strtoull(e, nullptr, 10);  // tuning knob
-    int max_level = 30;  // tuning knob: a density-matched stand-in over a small box can emulate the full-size tier
-    if (const char* e = std::getenv("GJ_DIR16_LEVEL_MAX")) max_level = std::atoi(e);
+    if (opt.dir16_max_entries > 0) max16 = std::min<uint64_t>(static_cast<uint64_t>(opt.dir16_max_entries), 110000);  // explicit knob
+    // explicit knob: a density-matched stand-in over a small box can emulate the full-size tier
+    const int max_level = opt.dir16_level_max > 0 ? std::min(30, static_cast<int>(opt.dir16_level_max)) : 30;
     build_dir16(an.dir2.table.empty() ? an.dir : an.dir2, max16, max_level, &an.dir16);
   }
   {  // first ids written late (join_kernel's kLate) when most of the 16-bit tier says "look in the 32-bit tier"
@@ -597,7 +628,7 @@ int create_index(const gj_index_desc& d, int device, gj_index** out) {
     }
     const uint64_t cells = static_cast<uint64_t>(an.dir16.width) * an.dir16.height;
     ix->ids_late = cells != 0 && open_cells * 2 > cells;
-    if (const char* e = std::getenv("GJ_IDS_LATE")) ix->ids_late = std::atoi(e) != 0;  // tuning knob / test hook
+    if (opt.ids_late >= 0) ix->ids_late = opt.ids_late != 0;  // explicit knob / test hook
   }
   size_t bytes = 0;
   if ((rc = upload(ix->d_arena, d.arena, d.node_count * kNodeSlots, &bytes)) != GJ_OK) return rc;
@@ -619,7 +650,7 @@ int create_index(const gj_index_desc& d, int device, gj_index** out) {
   bool have_pal = false;
   {
     uint64_t max_pal = kMaxNodePalBytes;
-    if (const char* e = std::getenv("GJ_NODE_PAL_MAX_MB")) max_pal = std::strtoull(e, nullptr, 10) << 20;  // tuning knob
+    if (opt.node_pal_max_mb >= 0) max_pal = static_cast<uint64_t>(opt.node_pal_max_mb) << 20;  // explicit knob
     if (d.node_count != 0 && d.node_count * 128 <= max_pal && d.node_count <= (1ull << 23)) {
       std::vector<uint64_t> pal(d.node_count * 16, 0);
       for (uint64_t node = 0; node < d.node_count; ++node) {
@@ -653,16 +684,7 @@ int create_index(const gj_index_desc& d, int device, gj_index** out) {
   }
 
   DevIndex& dv = ix->dev;
-  dv.arena = ix->d_arena.as<uint64_t>();
-  dv.node_pal = have_pal ? ix->d_node_pal.as<uint64_t>() : nullptr;
-  dv.lut = ix->d_lut.as<uint32_t>();
-  dv.ids = ix->d_ids.as<uint32_t>();
-  dv.ring_off = ix->d_ring_off.as<uint64_t>();
-  dv.ring_len = ix->d_ring_len.as<uint32_t>();
-  dv.ring_xy = ix->d_ring_xy.as<double2>();
-  dv.strip_meta = ix->d_strip_meta.as<StripMeta>();
-  dv.strip_ptr = ix->d_strip_ptr.as<uint32_t>();
-  dv.strip_edges = ix->d_strip_edges.as<EdgeRecord>();
+  (void)have_pal;  // d_node_pal stays empty without palette nodes
   for (int f = 0; f < 8; ++f) {
     dv.roots[f] = f < 6 ? d.roots[f] : 0;  // refresh_view, act.cpp:373-383
     dv.prefixes[f] = f < 6 ? d.prefixes[f] : 0;
@@ -673,8 +695,7 @@ int create_index(const gj_index_desc& d, int device, gj_index** out) {
   dv.leaf_level = d.k_max / 2;
   dv.prefix_level0 = static_cast<int>(d.prefix_bits[0]) / 2;
   dv.ids_dense = dense ? 1 : 0;
-  auto set_dir = [](DevDirectory& dd, const HostDirectory& hd, const uint32_t* table) {
-    dd.table = table;
+  auto set_dir = [](DevDirectory& dd, const HostDirectory& hd) {
     dd.width = hd.width;
     dd.height = hd.height;
     dd.pitch = hd.pitch;
@@ -684,10 +705,10 @@ int create_index(const gj_index_desc& d, int device, gj_index** out) {
     dd.shift = 30 - hd.level;
     dd.chunks = hd.chunks;
   };
-  set_dir(dv.dir, an.dir, ix->d_dir_table.as<uint32_t>());
-  set_dir(dv.dir2, an.dir2, ix->d_dir2_table.as<uint32_t>());
-  set_dir(dv.dir16, an.dir16, ix->d_dir16_table.as<uint32_t>());
-  set_dir(dv.dirk, an.dirk, ix->d_dirk_table.as<uint32_t>());
+  set_dir(dv.dir, an.dir);
+  set_dir(dv.dir2, an.dir2);
+  set_dir(dv.dir16, an.dir16);
+  set_dir(dv.dirk, an.dirk);
   dv.dir16.n_table = static_cast<uint32_t>(an.dir16.table16.size());
   {  // queue coding for the 32-bit tier K1 gathers from
     const HostDirectory& tb = !an.dirk.table.empty() ? an.dirk : (an.dir2.table.empty() ? an.dir : an.dir2);
@@ -702,12 +723,12 @@ int create_index(const gj_index_desc& d, int device, gj_index** out) {
     const uint32_t ybits = bits_for((static_cast<uint64_t>(tb.height) + 1) << up);
     DevQueueCoding& qc = dv.qc;
     qc = DevQueueCoding{};
-    const bool force_unpacked = std::getenv("GJ_QUEUE_UNPACKED") != nullptr;  // test hook for the fallback coding
+    const bool force_unpacked = opt.queue_unpacked != 0;  // test hook for the fallback coding
     // high bits of an arena slot that travel in the first queue word (see DevQueueCoding)
     uint32_t slot_hi_bits = 0;
     while (slot_hi_bits < 3 && d.node_count >= (1ull << (24 + slot_hi_bits))) ++slot_hi_bits;
-    if (const char* e = std::getenv("GJ_QUEUE_SLOT_HI_BITS")) {  // test hook: the wide-arena coding on a small index
-      slot_hi_bits = std::max<uint32_t>(slot_hi_bits, static_cast<uint32_t>(std::atoi(e)));
+    if (opt.queue_slot_hi_bits > 0) {  // test hook: the wide-arena coding on a small index
+      slot_hi_bits = std::max<uint32_t>(slot_hi_bits, static_cast<uint32_t>(opt.queue_slot_hi_bits));
     }
     qc.index_bits = 31;
     qc.slow_mark = 0x80000000u;
@@ -734,8 +755,8 @@ int create_index(const gj_index_desc& d, int device, gj_index** out) {
       qc.mul = tb.pitch;
     }
   }
-  dv.dict = ix->d_dir_dict.as<uint64_t>();
   dv.n_dict = static_cast<uint32_t>(an.dict.size());
+  ix->bind();
 
   cudaDeviceProp prop{};
   GJ_CUDA(cudaGetDeviceProperties(&prop, device));
@@ -762,6 +783,55 @@ int create_index(const gj_index_desc& d, int device, gj_index** out) {
   info.dir2_width = static_cast<int32_t>(an.dir2.width);
   info.dir2_height = static_cast<int32_t>(an.dir2.height);
   info.ids_dense = dense ? 1 : 0;
+  *out = ix.release();
+  return GJ_OK;
+}
+
+// Device-to-device replica of an index: every buffer is copied from the source
+// GPU's HBM (over NVLink when the two are peers, staged by the driver otherwise;
+// a plain device copy on the same GPU) and the kernel parameter block is
+// re-pointed.  The host arrays the source was created from are not needed.
+int replicate_index(const gj_index& src, int device, gj_index** out) {
+  if (!out) return GJ_INVALID_ARGUMENT;
+  *out = nullptr;
+  if (device < 0) GJ_CUDA(cudaGetDevice(&device));
+  GJ_CUDA(cudaSetDevice(device));
+  if (device != src.device) {
+    int can = 0;
+    GJ_CUDA(cudaDeviceCanAccessPeer(&can, device, src.device));
+    if (can) {
+      const cudaError_t e = cudaDeviceEnablePeerAccess(src.device, 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) return cuda_fail(e, "cudaDeviceEnablePeerAccess");
+      cudaGetLastError();
+    }
+  }
+  std::unique_ptr<gj_index> ix(new gj_index);
+  ix->device = device;
+  ix->dev = src.dev;  // scalars; pointers are re-bound below
+  ix->info = src.info;
+  ix->info.device = device;
+  ix->opt = src.opt;
+  ix->ids = src.ids;
+  ix->ids_late = src.ids_late;
+  ix->max_refs = src.max_refs;
+  ix->max_cand_refs = src.max_cand_refs;
+  for (DeviceBuffer gj_index::*m : src.buffers()) {
+    const DeviceBuffer& from = src.*m;
+    if (!from.ptr) continue;
+    DeviceBuffer& to = ix.get()->*m;
+    GJ_CUDA(to.reserve(from.bytes));
+    if (device == src.device) {
+      GJ_CUDA(cudaMemcpy(to.ptr, from.ptr, from.bytes, cudaMemcpyDeviceToDevice));
+    } else {
+      GJ_CUDA(cudaMemcpyPeer(to.ptr, device, from.ptr, src.device, from.bytes));
+    }
+  }
+  GJ_CUDA(cudaDeviceSynchronize());
+  ix->bind();
+  cudaDeviceProp prop{};
+  GJ_CUDA(cudaGetDeviceProperties(&prop, device));
+  ix->sm_count = prop.multiProcessorCount;
+  ix->smem_optin = prop.sharedMemPerBlockOptin;
   *out = ix.release();
   return GJ_OK;
 }
@@ -813,7 +883,7 @@ struct Cursor {
 
 }  // namespace
 
-int load_index_file(const char* path, int device, gj_index** out) {
+int load_index_file(const char* path, int device, const gj_options* options, gj_index** out) {
   if (!path || !out) return GJ_INVALID_ARGUMENT;
   *out = nullptr;
   const int fd = ::open(path, O_RDONLY);
@@ -925,7 +995,7 @@ int load_index_file(const char* path, int device, gj_index** out) {
   d.polygon_ids = ids.data();
   d.vtx_off = off.data();
   d.vtx_latlng = latlng.data();
-  return create_index(d, device, out);
+  return create_index(d, device, options, out);
 }
 
 }  // namespace gj

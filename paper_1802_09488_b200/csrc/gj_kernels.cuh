@@ -1175,4 +1175,11 @@ scan_apply_kernel(const uint32_t* __restrict__ in, uint64_t n, const uint64_t* _
   }
 }
 
+// v[i] += offset: a replica's CSR row offsets moved behind the pairs of the ranges before it (gj_group_*)
+__global__ void __launch_bounds__(256)
+add_offset_kernel(uint64_t* __restrict__ v, uint64_t n, uint64_t offset) {
+  const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+  for (uint64_t i = static_cast<uint64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride) v[i] += offset;
+}
+
 }  // namespace gj

@@ -127,11 +127,41 @@ def _vp(a):
     return C.c_void_p(a.ctypes.data) if a is not None else None
 
 
+def _desc(arena, lut, roots, prefixes, prefix_bits, k_max, approx_mode, polygon_ids, vtx_off, vtx_latlng):
+    """gj_index_desc over numpy arrays -> (desc, the arrays it borrows)."""
+    arena = np.ascontiguousarray(arena, np.uint64)
+    lut = np.ascontiguousarray(lut, np.uint32)
+    polygon_ids = np.ascontiguousarray(polygon_ids, np.uint32)
+    vtx_off = np.ascontiguousarray(vtx_off, np.uint64)
+    vtx_latlng = np.ascontiguousarray(vtx_latlng, np.float64)
+    d = capi.IndexDesc()
+    d.arena = arena.ctypes.data
+    d.node_count = len(arena) // 256
+    d.lut = lut.ctypes.data
+    d.lut_len = len(lut)
+    for f in range(8):
+        d.roots[f] = int(roots[f])
+        d.prefixes[f] = int(prefixes[f])
+        d.prefix_bits[f] = int(prefix_bits[f])
+    d.k_max = int(k_max)
+    d.approx_mode = int(bool(approx_mode))
+    d.n_polygons = len(polygon_ids)
+    d.polygon_ids = polygon_ids.ctypes.data
+    d.vtx_off = vtx_off.ctypes.data
+    d.vtx_latlng = vtx_latlng.ctypes.data
+    return d, (arena, lut, polygon_ids, vtx_off, vtx_latlng)
+
+
+def _opt(options):
+    return C.byref(options) if options is not None else None
+
+
 class IndexBundle:
     """An immutable index replicated into one GPU's HBM."""
 
-    def __init__(self, handle: int):
+    def __init__(self, handle: int, owned: bool = True):
         self._h = C.c_void_p(handle)
+        self._owned = owned
         info = capi.IndexInfo()
         _check(capi.lib().gj_index_get_info(self._h, C.byref(info)))
         self.info = info
@@ -144,7 +174,8 @@ class IndexBundle:
             self._session.close()
             self._session = None
         if self._h:
-            capi.lib().gj_index_destroy(self._h)
+            if self._owned:
+                capi.lib().gj_index_destroy(self._h)
             self._h = None
 
     def __del__(self):
@@ -155,36 +186,25 @@ class IndexBundle:
 
     @staticmethod
     def from_arrays(arena, lut, roots, prefixes, prefix_bits, k_max: int, approx_mode: bool,
-                    polygon_ids, vtx_off, vtx_latlng, device: int = -1) -> "IndexBundle":
-        arena = np.ascontiguousarray(arena, np.uint64)
-        lut = np.ascontiguousarray(lut, np.uint32)
-        polygon_ids = np.ascontiguousarray(polygon_ids, np.uint32)
-        vtx_off = np.ascontiguousarray(vtx_off, np.uint64)
-        vtx_latlng = np.ascontiguousarray(vtx_latlng, np.float64)
-        d = capi.IndexDesc()
-        d.arena = arena.ctypes.data
-        d.node_count = len(arena) // 256
-        d.lut = lut.ctypes.data
-        d.lut_len = len(lut)
-        for f in range(8):
-            d.roots[f] = int(roots[f])
-            d.prefixes[f] = int(prefixes[f])
-            d.prefix_bits[f] = int(prefix_bits[f])
-        d.k_max = int(k_max)
-        d.approx_mode = int(bool(approx_mode))
-        d.n_polygons = len(polygon_ids)
-        d.polygon_ids = polygon_ids.ctypes.data
-        d.vtx_off = vtx_off.ctypes.data
-        d.vtx_latlng = vtx_latlng.ctypes.data
+                    polygon_ids, vtx_off, vtx_latlng, device: int = -1,
+                    options: capi.Options | None = None) -> "IndexBundle":
+        d, _keep = _desc(arena, lut, roots, prefixes, prefix_bits, k_max, approx_mode, polygon_ids, vtx_off,
+                         vtx_latlng)
         h = C.c_void_p()
-        _check(capi.lib().gj_index_create(C.byref(d), device, C.byref(h)))
+        _check(capi.lib().gj_index_create_ex(C.byref(d), device, _opt(options), C.byref(h)))
         return IndexBundle(h.value)
 
     @staticmethod
-    def load(path, device: int = -1) -> "IndexBundle":
+    def load(path, device: int = -1, options: capi.Options | None = None) -> "IndexBundle":
         """IndexBundle::load (join.cpp:341-381): GJX1 file -> HBM."""
         h = C.c_void_p()
-        _check(capi.lib().gj_index_load_file(str(path).encode(), device, C.byref(h)))
+        _check(capi.lib().gj_index_load_file_ex(str(path).encode(), device, _opt(options), C.byref(h)))
+        return IndexBundle(h.value)
+
+    def replicate(self, device: int = -1) -> "IndexBundle":
+        """A copy of this index in another GPU's HBM, made device to device."""
+        h = C.c_void_p()
+        _check(capi.lib().gj_index_replicate(self._h, device, C.byref(h)))
         return IndexBundle(h.value)
 
     @property
@@ -200,15 +220,20 @@ class IndexBundle:
 class Session:
     """One CUDA stream + scratch; not thread-safe (use one per thread)."""
 
-    def __init__(self, bundle: IndexBundle):
+    def __init__(self, bundle: IndexBundle, handle: int | None = None):
         self.bundle = bundle
-        h = C.c_void_p()
-        _check(capi.lib().gj_session_create(bundle._h, C.byref(h)))
+        self._owned = handle is None
+        if handle is None:
+            h = C.c_void_p()
+            _check(capi.lib().gj_session_create(bundle._h, C.byref(h)))
+        else:  # borrowed from a group
+            h = C.c_void_p(handle)
         self._h = h
 
     def close(self):
         if self._h:
-            capi.lib().gj_session_destroy(self._h)
+            if self._owned:
+                capi.lib().gj_session_destroy(self._h)
             self._h = None
 
     def __del__(self):
@@ -275,6 +300,10 @@ class Session:
         return out[:found.value].copy()
 
     # ---- streaming join ----
+    def _count_call(self, p, base_index, mode, counts, cs, first, ovf, bad):
+        return capi.lib().gj_join_count_host(self._h, _vp(p), len(p), base_index, mode, _vp(counts), cs,
+                                             _vp(first), ovf, C.byref(bad))
+
     def join_count(self, points, mode=capi.GJ_MODE_BUNDLE, stats: JoinStats | None = None,
                    want_ids: bool = False, base_index: int = 0, overflow_capacity: int | None = None):
         """Returns (counts_by_slot u64[n_ids], first_id u32[n] | None, (ovf_point, ovf_id) | None)."""
@@ -293,9 +322,8 @@ class Session:
                 ovf = capi.Overflow(ovf_pt.ctypes.data, ovf_id.ctypes.data, cap, 0)
                 counts[:] = 0
                 cs = capi.Stats()
-                rc = capi.lib().gj_join_count_host(self._h, _vp(p), len(p), base_index, mode, _vp(counts),
-                                                   C.byref(cs) if stats is not None else None,
-                                                   _vp(first), C.byref(ovf), C.byref(bad))
+                rc = self._count_call(p, base_index, mode, counts, C.byref(cs) if stats is not None else None,
+                                      first, C.byref(ovf), bad)
                 if rc == capi.GJ_CAPACITY and ovf.count > cap and overflow_capacity is None:
                     cap = int(ovf.count)
                     continue
@@ -303,9 +331,8 @@ class Session:
                 break
             ovf_pt, ovf_id = ovf_pt[:ovf.count], ovf_id[:ovf.count]
         else:
-            _check(capi.lib().gj_join_count_host(self._h, _vp(p), len(p), base_index, mode, _vp(counts),
-                                                 C.byref(cs) if stats is not None else None,
-                                                 None, None, C.byref(bad)), bad)
+            _check(self._count_call(p, base_index, mode, counts, C.byref(cs) if stats is not None else None,
+                                    None, None, bad), bad)
         if stats is not None:
             stats._add(cs)
         counts = counts[:len(self.bundle.ids)]
@@ -329,20 +356,121 @@ class Session:
         _check(capi.lib().gj_session_sync(self._h, C.byref(bad)), bad)
 
     # ---- materialised pairs ----
+    def _pairs_call(self, p, mode, n_pairs, cs, bad):
+        return capi.lib().gj_join_pairs_host(self._h, _vp(p), len(p), mode, C.byref(n_pairs), cs, C.byref(bad))
+
+    def _pairs_copy(self, row_ptr, ids):
+        return capi.lib().gj_pairs_copy(self._h, _vp(row_ptr), _vp(ids))
+
     def join_pairs(self, points, mode, stats: JoinStats | None = None):
         """(row_ptr u64[n+1], polygon_id u32[]) in the reference's emit order."""
         p = _points(points)
         n_pairs = C.c_uint64(0)
         cs = capi.Stats()
         bad = C.c_uint64(0)
-        _check(capi.lib().gj_join_pairs_host(self._h, _vp(p), len(p), mode, C.byref(n_pairs),
-                                             C.byref(cs) if stats is not None else None, C.byref(bad)), bad)
+        _check(self._pairs_call(p, mode, n_pairs, C.byref(cs) if stats is not None else None, bad), bad)
         row_ptr = np.empty(len(p) + 1, np.uint64)
         ids = np.empty(n_pairs.value, np.uint32)
-        _check(capi.lib().gj_pairs_copy(self._h, _vp(row_ptr), _vp(ids)))
+        _check(self._pairs_copy(row_ptr, ids))
         if stats is not None:
             stats._add(cs)
         return row_ptr, ids
+
+
+class _GroupJoiner(Session):
+    """join_count / join_pairs of a Session, routed through the group calls."""
+
+    def __init__(self, group: "IndexGroup", workers: int):
+        self.bundle = group.replicas[0]
+        self._g = group
+        self._workers = int(workers)
+        self._h = group.sessions[0]._h  # everything but the joins runs on the first replica
+        self._owned = False
+
+    def _count_call(self, p, base_index, mode, counts, cs, first, ovf, bad):
+        return capi.lib().gj_group_join_count_host(self._g._h, self._workers, _vp(p), len(p), base_index, mode,
+                                                   _vp(counts), cs, _vp(first), ovf, C.byref(bad))
+
+    def _pairs_call(self, p, mode, n_pairs, cs, bad):
+        return capi.lib().gj_group_join_pairs_host(self._g._h, self._workers, _vp(p), len(p), mode,
+                                                   C.byref(n_pairs), cs, C.byref(bad))
+
+    def _pairs_copy(self, row_ptr, ids):
+        return capi.lib().gj_group_pairs_copy(self._g._h, _vp(row_ptr), _vp(ids))
+
+
+class IndexGroup:
+    """The index replicated over several GPUs of one box, for ONE input: the
+    reference's worker fan-out (join.cpp:255-285) with GPUs as the workers.
+    Points split into contiguous ranges [n*g/G, n*(g+1)/G) (join.cpp:264-265),
+    range g runs on replica g from its own host thread with
+    ``base_index + n*g/G``; counts and stats are summed, first ids / CSR rows
+    land at their global positions (join.cpp:280-284).  ``devices`` may repeat a
+    device (replicas share nothing) — that is how the one-GPU tests exercise it."""
+
+    def __init__(self, handle: int):
+        self._h = C.c_void_p(handle)
+        L = capi.lib()
+        self.replicas = [IndexBundle(L.gj_group_index(self._h, k), owned=False) for k in range(L.gj_group_size(self._h))]
+        self.sessions = [Session(b, handle=L.gj_group_session(self._h, k)) for k, b in enumerate(self.replicas)]
+        for b, s in zip(self.replicas, self.sessions):
+            b._session = s
+        self.info = self.replicas[0].info
+        self.ids = self.replicas[0].ids
+
+    @staticmethod
+    def _devices(devices):
+        if devices is None:
+            devices = list(range(capi.lib().gj_device_count()))
+        devices = [int(d) for d in devices]
+        if not devices:
+            raise CudaError("no CUDA device: geojoin_b200 has no CPU fallback")
+        return (C.c_int * len(devices))(*devices), len(devices)
+
+    @staticmethod
+    def load(path, devices=None, options: capi.Options | None = None) -> "IndexGroup":
+        """GJX1 file -> the first device's HBM -> device-to-device copies on the others (None = every GPU)."""
+        arr, n = IndexGroup._devices(devices)
+        h = C.c_void_p()
+        _check(capi.lib().gj_group_load_file(str(path).encode(), arr, n, _opt(options), C.byref(h)))
+        return IndexGroup(h.value)
+
+    @staticmethod
+    def from_arrays(arena, lut, roots, prefixes, prefix_bits, k_max: int, approx_mode: bool, polygon_ids, vtx_off,
+                    vtx_latlng, devices=None, options: capi.Options | None = None) -> "IndexGroup":
+        d, _keep = _desc(arena, lut, roots, prefixes, prefix_bits, k_max, approx_mode, polygon_ids, vtx_off,
+                         vtx_latlng)
+        arr, n = IndexGroup._devices(devices)
+        h = C.c_void_p()
+        _check(capi.lib().gj_group_create(C.byref(d), arr, n, _opt(options), C.byref(h)))
+        return IndexGroup(h.value)
+
+    @property
+    def approx(self) -> bool:
+        return bool(self.info.approx_mode)
+
+    def __len__(self):
+        return len(self.replicas)
+
+    def session(self, workers: int = 0) -> Session:
+        """A Session-shaped handle whose join_count / join_pairs use ``workers`` replicas (0 = all)."""
+        return _GroupJoiner(self, workers)
+
+    def close(self):
+        for s in self.sessions:
+            s.close()
+        for b in self.replicas:
+            b._session = None
+            b.close()
+        if self._h:
+            capi.lib().gj_group_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def _pairs_from_csr(row_ptr: np.ndarray, ids: np.ndarray):
@@ -361,11 +489,15 @@ def join_approx(bundle: IndexBundle, points, stats: JoinStats | None = None):
     return _pairs_from_csr(*bundle.session().join_pairs(points, capi.GJ_MODE_APPROX, stats))
 
 
-def join_count_per_polygon(bundle: IndexBundle, points, threads: int = 1) -> dict[int, int]:
+def join_count_per_polygon(bundle, points, threads: int = 1) -> dict[int, int]:
     """join.cpp:255-285 — mode from the bundle; only polygons with a non-zero
-    count appear.  ``threads`` is accepted for signature parity (the GPU path
-    has no use for it; results are independent of it by contract)."""
-    counts, _, _ = bundle.session().join_count(points, capi.GJ_MODE_BUNDLE)
+    count appear.  ``threads`` is the reference's worker count: on an
+    ``IndexGroup`` that many replicas (GPUs) each take one contiguous range of
+    the points (0 or more than the group holds = all of them); on a single
+    ``IndexBundle`` there is one worker.  Results do not depend on it
+    (tests/test_join.cpp:200-214)."""
+    sess = bundle.session(threads) if isinstance(bundle, IndexGroup) else bundle.session()
+    counts, _, _ = sess.join_count(points, capi.GJ_MODE_BUNDLE)
     nz = np.nonzero(counts)[0]
     return {int(bundle.ids[k]): int(counts[k]) for k in nz}
 

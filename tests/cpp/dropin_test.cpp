@@ -115,6 +115,32 @@ void compare(const IndexBundle& bundle, const std::vector<LatLng>& points) {
     std::remove(path.c_str());
   }
 
+  // The reference's worker fan-out (join.cpp:255-285) over index replicas: one replica per GPU of the box,
+  // topped up to three (a device may hold several replicas; they share nothing), `threads` = how many take part.
+  // Results must not depend on the worker count (tests/test_join.cpp:200-214).
+  {
+    std::vector<int> devices = gpu::all_devices();
+    while (devices.size() < 3) devices.push_back(0);
+    gpu::DeviceIndex fleet(bundle, devices);
+    EXPECT(fleet.replicas() == static_cast<int>(devices.size()));
+    const auto want_counts = join_count_per_polygon(bundle, points, 1);
+    for (int threads : {1, 2, 3, 7}) EXPECT(gpu::join_count_per_polygon(fleet, points, threads) == want_counts);
+    JoinStats fs;
+    cs = JoinStats{};
+    EXPECT(gpu::join_exact(fleet, points, &fs) == join_exact(bundle, points, &cs));
+    EXPECT(same_stats(cs, fs));
+    fs = JoinStats{};
+    cs = JoinStats{};
+    EXPECT(gpu::join_approx(fleet, points, &fs) == join_approx(bundle, points, &cs));
+    EXPECT(same_stats(cs, fs));
+    // an offending point in the LAST range is reported even though the first ranges succeed
+    std::vector<LatLng> bad_tail = points;
+    bad_tail[bad_tail.size() - 2].lng = -181.0;
+    bool threw = false;
+    try { gpu::join_count_per_polygon(fleet, bad_tail, 0); } catch (const std::invalid_argument&) { threw = true; }
+    EXPECT(threw);
+  }
+
   // a single bad coordinate aborts the join with std::invalid_argument on both sides
   std::vector<LatLng> bad = points;
   bad[bad.size() / 2].lat = 91.0;

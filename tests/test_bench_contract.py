@@ -38,13 +38,31 @@ def test_reference_arm_other_ranks_exit_quietly():
     assert res.returncode == 0 and res.stdout.strip() == ""
 
 
+def test_own_arm_fails_loudly_without_enough_gpus():
+    """``--gpus N`` never degrades to fewer ranks: outside torchrun it starts N ranks itself and refuses when the
+    box has fewer than N devices; under a launcher whose WORLD_SIZE disagrees with N it refuses as well."""
+    import os
+    import torch
+    have = torch.cuda.device_count() if torch.cuda.is_available() else 0
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    want = have + 1 if have else 2
+    res = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", str(want), "--steps", "1", "--warmup", "3"],
+                         capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
+    assert res.returncode != 0 and res.stdout.strip() == ""
+    assert f"--gpus {want}" in res.stderr and "CUDA device" in res.stderr
+    res = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "2", "--steps", "1", "--warmup", "3"],
+                         capture_output=True, text=True, timeout=300, cwd=ROOT,
+                         env=dict(env, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0"))
+    assert res.returncode != 0 and res.stdout.strip() == "" and "WORLD_SIZE is 1" in res.stderr
+
+
 @pytest.mark.gpu
 def test_own_arm_prints_one_contract_line():
     from tools import build_bundles
     if not build_bundles.have_bundle(build_bundles.workload_name(2)):
         pytest.skip("no cached config-2 index")
     res = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "1", "--steps", "4", "--warmup", "3",
-                          "--points", "4000000", "--ref-points", "4000000", "--e2e-steps", "2"],
+                          "--points", "4000000", "--ref-points", "4000000", "--e2e-steps", "2", "--no-secondary"],
                          capture_output=True, text=True, timeout=900, cwd=ROOT)
     assert res.returncode == 0, res.stderr[-2000:]
     lines = [l for l in res.stdout.splitlines() if l.strip()]
@@ -62,5 +80,7 @@ def test_own_arm_prints_one_contract_line():
     r = d["roofline"]
     assert r["bound"] == "hbm" and r["unit"] == "GB/s" and 0 < r["frac"] < 1.2 and r["peak"] > 1000
     assert abs(r["frac"] - r["achieved"] / r["peak"]) < 1e-9 and "traffic" in r
+    assert "ncu_stale" in r and "sectors_per_request" in r and "l2_hit_rate_pct" in r
     cb = d["cpu_baseline"]
     assert cb["kind"] in ("reference", "port") and cb["cores"] >= 1 and cb["value"] > 0 and cb["sample"]
+    assert d["counts_equal_reference"] is True and d["secondary"] is None

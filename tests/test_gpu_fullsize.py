@@ -69,6 +69,51 @@ def test_config2_full_size_properties():
     assert np.array_equal(c_only, counts)
 
 
+def _cpu_counts(path, pts, exact):
+    """Per-polygon counts of the CPU join on all host threads: the compiled reference's own
+    join_count_per_polygon when oracle/_ref travelled with the repo, else the C oracle port."""
+    import os
+    from oracle import ref
+    threads = os.cpu_count() or 1
+    if ref.available():
+        rb = ref.RefBundle.load(path)
+        assert rb.approx != exact  # join_count_per_polygon takes the mode from the bundle (join.cpp:257)
+        return rb.join_count(pts, threads), "reference"
+    from tests import golden_util
+    ox = golden_util.oracle_index(golden_util.parse_gjx(open(path, "rb").read()))
+    return ox.join_count(pts, approx=not exact, threads=threads)[0], "port"
+
+
+@pytest.mark.parametrize("config,exact", [(2, False), (3, True)])
+def test_full_size_counts_equal_the_cpu_reference(config, exact):
+    """BASELINE configs[1] (approx) and configs[2] (exact, trained, ~1 % of the points on
+    edges / vertices) at their full 100 M points: the per-polygon counts of the GPU join —
+    host-buffer call and device-resident call — equal the reference's multithreaded CPU
+    join_count_per_polygon on ALL points, polygon by polygon."""
+    import torch
+    bundle = _bundle(config)
+    path = build_bundles.bundle_file(build_bundles.workload_name(config))
+    polys = synth.polygons_for(config, 1.0) if synth.SPECS[config].boundary_fraction > 0 else None
+    pts = synth.points_for(config, N_FULL, polys)
+    want, kind = _cpu_counts(path, pts, exact)
+    assert sum(want.values()) >= N_FULL * 0.99
+    got = join.join_count_per_polygon(bundle, pts)  # mode from the bundle, like the reference
+    assert got == want, f"GPU counts differ from the CPU {kind} join"
+    s = bundle.session()
+    d_pts = torch.from_numpy(pts).cuda()
+    d_counts = torch.zeros(len(bundle.ids), dtype=torch.int64, device="cuda")
+    torch.cuda.synchronize()
+    s.join_count_device(d_pts.data_ptr(), N_FULL, d_counts.data_ptr(), capi.GJ_MODE_BUNDLE, sync=True)
+    c = d_counts.cpu().numpy()
+    assert {int(bundle.ids[k]): int(c[k]) for k in np.nonzero(c)[0]} == want
+    # and all GPUs of the box behind one call (one replica per device, at least two replicas)
+    devices = list(range(capi.lib().gj_device_count()))
+    fleet = join.IndexGroup.load(path, devices if len(devices) > 1 else [0, 0])
+    assert join.join_count_per_polygon(fleet, pts, 0) == want
+    fleet.close()
+    bundle.close()
+
+
 def test_config2_device_resident_equals_host_path():
     import torch
     bundle = _bundle(2)

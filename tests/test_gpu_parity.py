@@ -112,7 +112,7 @@ def test_first_id_and_overflow(name, kind):
 @pytest.mark.parametrize("name", ["join_small_exact", "cfg2_tess16_approx4m", "cfg3_tess16_exact_trained",
                                   "cfg4_tess36_approx1m_k56", "cfg5_stars_scaled", "world_stars", "empty_index"])
 @pytest.mark.parametrize("tier_sub", [0, 2])
-def test_late_first_ids_equal_early_first_ids(name, tier_sub, monkeypatch):
+def test_late_first_ids_equal_early_first_ids(name, tier_sub):
     """join_kernel's kLate variant (first-id words written where a point is settled
     instead of pre-written for every point; chosen by itself when the 16-bit tier
     resolves few cells) must produce the same first ids, overflow records, counts and
@@ -123,9 +123,8 @@ def test_late_first_ids_equal_early_first_ids(name, tier_sub, monkeypatch):
     pts = np.ascontiguousarray(fx["points"])
     results = {}
     for late in ("0", "1"):
-        monkeypatch.setenv("GJ_IDS_LATE", late)
-        monkeypatch.setenv("GJ_TIER_SUB", str(tier_sub))
-        b = join.IndexBundle.load(golden_util.bundle_file(name), device=0)
+        b = join.IndexBundle.load(golden_util.bundle_file(name), device=0,
+                                  options=capi.Options(ids_late=int(late), tier_sub=tier_sub))
         s = b.session()
         out = []
         for mode in (capi.GJ_MODE_EXACT, capi.GJ_MODE_APPROX):
@@ -361,7 +360,7 @@ def test_structurally_corrupt_indexes_are_rejected():
         make(roots=roots)
 
 
-def test_large_id_table_counts_through_private_copies(monkeypatch):
+def test_large_id_table_counts_through_private_copies():
     """Id tables too large for the shared-memory histograms (K1: forced here
     with the tuning knob; K2: more than 8192 ids) count into per-CTA copies in
     global memory that are folded afterwards: same counts, pairs and stats."""
@@ -372,9 +371,9 @@ def test_large_id_table_counts_through_private_copies(monkeypatch):
     tri = np.array([[-80.0, 10.0], [-80.0, 10.001], [-79.999, 10.0]])
     vtx = np.concatenate([g["vtx_latlng"].reshape(-1, 2), np.tile(tri, (extra, 1))])
     off = np.concatenate([g["vtx_off"], g["vtx_off"][-1] + 3 * np.arange(1, extra + 1, dtype=np.uint64)])
-    monkeypatch.setenv("GJ_HIST_REP", "0")
     b = join.IndexBundle.from_arrays(g["arena"], g["lut"], g["roots"], g["prefixes"], g["prefix_bits"], g["k_max"],
-                                     g["approx"], ids, off, vtx, device=0)
+                                     g["approx"], ids, off, vtx, device=0,
+                                     options=capi.Options(hist_rep_cap=0, hist16=0))
     assert len(b.ids) > 8192
     want = dict(zip(fx["count_ids"].tolist(), fx["count_values"].tolist()))
     for _ in range(2):  # the copies are left zero for the next launch
@@ -390,13 +389,12 @@ def test_large_id_table_counts_through_private_copies(monkeypatch):
 
 @pytest.mark.parametrize("name", ["cfg2_tess16_approx4m", "cfg3_tess16_exact_trained", "cfg4_tess36_approx1m_k56",
                                   "cfg5_stars_scaled", "kmax60_sparse_ids"])
-def test_unpacked_queue_coding_matches_reference(name, monkeypatch):
+def test_unpacked_queue_coding_matches_reference(name):
     """The fallback queue coding (window too wide for 32 bits, arenas of 2^24+
     nodes): the queue word is the tier index and population 3 re-reads the
     point.  Forced with the test hook; results must not change."""
-    monkeypatch.setenv("GJ_QUEUE_UNPACKED", "1")
     fx = golden_util.load(name)
-    b = join.IndexBundle.load(golden_util.bundle_file(name), device=0)
+    b = join.IndexBundle.load(golden_util.bundle_file(name), device=0, options=capi.Options(queue_unpacked=1))
     want = dict(zip(fx["count_ids"].tolist(), fx["count_values"].tolist()))
     assert join.join_count_per_polygon(b, fx["points"]) == want
     for kind, mode in (("exact", capi.GJ_MODE_EXACT), ("approx", capi.GJ_MODE_APPROX)):
@@ -422,13 +420,13 @@ def _check_join_against_fixture(b, fx):
 @pytest.mark.parametrize("hi_bits", [1, 2])
 @pytest.mark.parametrize("name", ["cfg2_tess16_approx4m", "cfg3_tess16_exact_trained", "cfg4_tess36_approx1m_k56",
                                   "cfg5_stars_scaled"])
-def test_wide_arena_queue_coding_matches_reference(name, hi_bits, monkeypatch):
+def test_wide_arena_queue_coding_matches_reference(name, hi_bits):
     """Arenas of 2^24 / 2^25 nodes and more keep the packed queue coding by carrying
     1 / 2 high bits of the arena slot next to the point index (DevQueueCoding::index_bits).
     Forced on a small index with the test hook; results must not change."""
-    monkeypatch.setenv("GJ_QUEUE_SLOT_HI_BITS", str(hi_bits))
     fx = golden_util.load(name)
-    b = join.IndexBundle.load(golden_util.bundle_file(name), device=0)
+    b = join.IndexBundle.load(golden_util.bundle_file(name), device=0,
+                              options=capi.Options(queue_slot_hi_bits=hi_bits))
     _check_join_against_fixture(b, fx)
     b.close()
 
@@ -436,17 +434,15 @@ def test_wide_arena_queue_coding_matches_reference(name, hi_bits, monkeypatch):
 @pytest.mark.parametrize("sub", [1, 2, 3])
 @pytest.mark.parametrize("name", ["cfg2_tess16_approx4m", "cfg3_tess16_exact_trained", "cfg4_tess36_approx1m_k56",
                                   "cfg5_stars_scaled", "kmax60_sparse_ids", "world_stars", "join_small_exact"])
-def test_refined_tier_matches_reference(name, sub, monkeypatch):
+def test_refined_tier_matches_reference(name, sub):
     """K1's refined 32-bit tier (DevIndex::dirk): the deepest tier again, 1-3 grid
     levels finer, cells resolved from uniform slot runs of the linked nodes.  Built
     by itself only for indexes whose deepest tier is mostly links; forced here on
     every fixture shape, packed and unpacked queue coding.  Results must not change."""
-    monkeypatch.setenv("GJ_TIER_SUB", str(sub))
     fx = golden_util.load(name)
     for unpacked in (False, True):
-        if unpacked:
-            monkeypatch.setenv("GJ_QUEUE_UNPACKED", "1")
-        b = join.IndexBundle.load(golden_util.bundle_file(name), device=0)
+        b = join.IndexBundle.load(golden_util.bundle_file(name), device=0,
+                                  options=capi.Options(tier_sub=sub, queue_unpacked=int(unpacked)))
         _check_join_against_fixture(b, fx)
         b.close()
 
@@ -486,19 +482,21 @@ def test_arena_beyond_2_24_nodes_matches_reference():
     b.close()
 
 
-def test_device_resident_call_is_split_into_launches(monkeypatch):
+def test_device_resident_call_is_split_into_launches():
     """A device-resident call longer than one launch may be (the cap depends on the
     arena size) runs as several launches: same counts, first ids and stats, and the
     smallest offending index of the whole call survives the later pieces."""
     import torch
     fx = golden_util.load("cfg3_tess16_exact_trained")
     b = join.IndexBundle.load(golden_util.bundle_file("cfg3_tess16_exact_trained"), device=0)
-    s = b.session()
     pts = np.ascontiguousarray(fx["points"])
     n = len(pts)
+    # the same index again (a device-to-device replica would inherit the knob), capped at a seventh of the call per launch
+    b_split = join.IndexBundle.load(golden_util.bundle_file("cfg3_tess16_exact_trained"), device=0,
+                                    options=capi.Options(max_launch_points=n // 7 + 1))
     d_pts = torch.from_numpy(pts).cuda()
 
-    def run(mode):
+    def run(mode, s):
         d_counts = torch.zeros(len(b.ids), dtype=torch.int64, device="cuda")
         d_stats = torch.zeros(6, dtype=torch.int64, device="cuda")
         d_first = torch.empty(n, dtype=torch.int32, device="cuda")
@@ -508,13 +506,13 @@ def test_device_resident_call_is_split_into_launches(monkeypatch):
         return d_counts.cpu().numpy(), d_stats.cpu().numpy(), d_first.cpu().numpy()
 
     for mode in (capi.GJ_MODE_EXACT, capi.GJ_MODE_APPROX):
-        monkeypatch.delenv("GJ_MAX_LAUNCH_POINTS", raising=False)
+        s = b.session()
         l0 = s.launches
-        one = run(mode)
+        one = run(mode, s)
         per_call = s.launches - l0
-        monkeypatch.setenv("GJ_MAX_LAUNCH_POINTS", str(n // 7 + 1))
+        s = b_split.session()
         l0 = s.launches
-        many = run(mode)
+        many = run(mode, s)
         assert s.launches - l0 == 7 * per_call
         for a, c in zip(one, many):
             assert np.array_equal(a, c)
@@ -529,6 +527,7 @@ def test_device_resident_call_is_split_into_launches(monkeypatch):
         s.sync()
     assert e.value.index == n // 7 - 3
     b.close()
+    b_split.close()
 
 
 def test_index_and_session_lifecycle_releases_device_memory():
@@ -594,3 +593,75 @@ def test_concurrent_sessions_on_one_index_and_on_two_indexes():
     assert errors == []
     ba.close()
     bb.close()
+
+
+def _fleet_devices():
+    """Every GPU of the box, topped up to three replicas with device 0 (replicas
+    on one device share nothing, and their kernels do not wait on one another)."""
+    devices = list(range(capi.lib().gj_device_count()))
+    while len(devices) < 3:
+        devices.append(0)
+    return devices
+
+
+@pytest.mark.parametrize("name", ["join_small_exact", "cfg2_tess16_approx4m", "cfg3_tess16_exact_trained",
+                                  "cfg5_stars_scaled", "kmax60_sparse_ids", "empty_index"])
+def test_index_group_equals_single_device(name):
+    """The all-GPUs-for-one-input call (gj_group_*: the reference's worker fan-out,
+    join.cpp:255-285, with index replicas as the workers): counts, stats, first ids,
+    overflow records and ordered pairs equal the one-device results and the reference
+    fixture for every worker count — tests/test_join.cpp:200-214 (threads in {1,2,3,7})."""
+    fx = golden_util.load(name)
+    pts = np.ascontiguousarray(fx["points"])
+    one = join.IndexBundle.load(golden_util.bundle_file(name), device=0)
+    fleet = join.IndexGroup.load(golden_util.bundle_file(name), _fleet_devices())
+    assert len(fleet) == len(_fleet_devices()) and np.array_equal(fleet.ids, one.ids)
+    want = {int(k): int(v) for k, v in zip(fx["count_ids"], fx["count_values"])}
+    for threads in (1, 2, 3, 7):
+        assert join.join_count_per_polygon(fleet, pts, threads) == want
+    for kind, mode in (("exact", capi.GJ_MODE_EXACT), ("approx", capi.GJ_MODE_APPROX)):
+        s1, sg = join.JoinStats(), join.JoinStats()
+        c1, f1, (p1, i1) = one.session().join_count(pts, mode, stats=s1, want_ids=True, base_index=1000)
+        for workers in (0, 2):
+            sg = join.JoinStats()
+            cg, fg, (pg, ig) = fleet.session(workers).join_count(pts, mode, stats=sg, want_ids=True, base_index=1000)
+            assert np.array_equal(c1, cg) and np.array_equal(f1, fg)
+            assert np.array_equal(p1, pg) and np.array_equal(i1, ig)
+            assert s1.as_tuple() == sg.as_tuple() == tuple(int(v) for v in fx[f"{kind}_stats"])
+        st = join.JoinStats()
+        pi, pid = (join.join_exact if kind == "exact" else join.join_approx)(fleet, pts, st)
+        epi, epid = golden_util.pairs_of(fx, kind)
+        assert np.array_equal(pi, epi) and np.array_equal(pid, epid)
+        assert st.as_tuple() == tuple(int(v) for v in fx[f"{kind}_stats"])
+    if len(pts) > 10:  # the smallest offending index wins, wherever its range runs
+        bad = pts.copy()
+        bad[len(pts) - 2, 1] = 200.0
+        with pytest.raises(join.InvalidArgument) as e:
+            fleet.session().join_count(bad, capi.GJ_MODE_APPROX)
+        assert e.value.index == len(pts) - 2
+        bad[3, 0] = np.inf
+        with pytest.raises(join.InvalidArgument) as e:
+            fleet.session().join_count(bad, capi.GJ_MODE_EXACT, want_ids=True)
+        assert e.value.index == 3
+        with pytest.raises(join.InvalidArgument) as e:
+            join.join_exact(fleet, bad)
+        assert e.value.index == 3
+    fleet.close()
+    one.close()
+
+
+def test_replica_is_independent_of_its_source():
+    """gj_index_replicate: a device-to-device copy keeps working after the index it was
+    copied from is destroyed, and gives the same entries and join results."""
+    fx = golden_util.load("cfg3_tess16_exact_trained")
+    src = join.IndexBundle.load(golden_util.bundle_file("cfg3_tess16_exact_trained"), device=0,
+                                options=capi.Options(tier_sub=1))
+    n_dev = capi.lib().gj_device_count()
+    rep = src.replicate(n_dev - 1)
+    assert rep.info.device == n_dev - 1 and rep.info.node_count == src.info.node_count
+    src.close()
+    filler = join.IndexBundle.load(golden_util.bundle_file("cfg5_stars_scaled"), device=0)  # reuse the freed HBM
+    assert np.array_equal(rep.session().probe_points(fx["points"]), fx["entries"])
+    _check_join_against_fixture(rep, fx)
+    filler.close()
+    rep.close()

@@ -31,6 +31,17 @@ def test_header_structs_match_ctypes_layout():
     assert C.sizeof(capi.Stats) == 48
     assert C.sizeof(capi.IndexInfo) == 5 * 8 + 16 * 4
     assert C.sizeof(capi.Overflow) == 32
+    assert C.sizeof(capi.Options) == 13 * 4 + 4 + 2 * 8
+    o = capi.Options(tier_sub=2)  # gj_options_default + overrides
+    assert o.struct_size == C.sizeof(capi.Options) and o.tier_sub == 2
+    assert (o.ids_late, o.hist_rep_cap, o.node_pal_max_mb, o.max_launch_points, o.chunk_points) == (-1, -1, -1, 0, 0)
+
+
+def test_library_reads_no_environment_variable():
+    """Tuning knobs and test hooks travel in gj_options; a stray variable in a user's
+    environment must not change kernel variants or launch splitting."""
+    for f in (ROOT / "paper_1802_09488_b200" / "csrc").iterdir():
+        assert "getenv" not in f.read_text(), f"{f.name} reads the environment"
 
 
 def test_no_gpu_means_loud_failure():

@@ -24,13 +24,13 @@ from tools import build_bundles  # noqa: E402
 
 
 def run_config(config: int, n_points: int, scale: float, reps: int, check: int, want_ids: bool = True,
-               pairs_points: int = 0, want_stats: bool = True, force_mode: str | None = None):
+               pairs_points: int = 0, want_stats: bool = True, force_mode: str | None = None, options=None):
     import torch
 
     spec = synth.SPECS[config]
     name = build_bundles.workload_name(config, scale)
     path = build_bundles.ensure_workload_bundle(config, scale, log=lambda *a: print(*a, file=sys.stderr))
-    bundle = join.IndexBundle.load(path, device=0)
+    bundle = join.IndexBundle.load(path, device=0, options=options)
     sess = bundle.session()
     info = bundle.info
     polys = synth.polygons_for(config, scale) if spec.boundary_fraction > 0 else None
@@ -132,12 +132,14 @@ def main():
                     help="cap the shared-memory tier at this grid level (a stand-in over a scaled-down box otherwise "
                          "gets a finer first tier than the full-size box would: level 17 for the BASELINE box)")
     ap.add_argument("--pairs", type=int, default=0, help="also time gj_join_pairs_host on this many points")
+    ap.add_argument("--opt", default="", help="comma-separated gj_options fields, e.g. hist_rep_cap=0,hist16=0")
     args = ap.parse_args()
+    kw = {k: int(v) for k, v in (kv.split("=", 1) for kv in args.opt.split(",") if kv)}
     if args.dir16_level:
-        import os
-        os.environ["GJ_DIR16_LEVEL_MAX"] = str(args.dir16_level)
-    out = [run_config(c, args.points, args.scale, args.reps, args.check, not args.no_ids, args.pairs, not args.no_stats, args.mode)
-           for c in args.configs]
+        kw["dir16_level_max"] = args.dir16_level
+    options = capi.Options(**kw) if kw else None
+    out = [run_config(c, args.points, args.scale, args.reps, args.check, not args.no_ids, args.pairs, not args.no_stats,
+                      args.mode, options) for c in args.configs]
     (ROOT / "gpurun_out").mkdir(exist_ok=True)
     (ROOT / "gpurun_out" / "bench_configs.json").write_text(json.dumps(out, indent=1))
 

@@ -49,7 +49,7 @@ def rss_gb() -> float:
 
 def run(config: int, scale: float, n_points: int, launch: int, check: int, reps: int, threads: int,
         want_ids: bool, want_stats: bool, host_points: int, pairs_points: int = 0, save_index: str = "",
-        load_index: str = "", variants: bool = False):
+        load_index: str = "", variants=()):
     import torch
     from oracle import ref
 
@@ -186,35 +186,28 @@ def run(config: int, scale: float, n_points: int, launch: int, check: int, reps:
         log(f"variant {label}: {t:.3f} ms")
         return t
 
-    if variants:  # where the time goes: knobs the library reads per launch (environment), then per index
+    if variants:  # where the time goes: ids / counts, then index variants built with explicit options (gj_options)
         v = {}
         v["ids+counts (no stats)"] = timed(sess, "ids+counts", want_ids, False)
         v["counts only"] = timed(sess, "counts only", False, False)
-        os.environ["GJ_HIST_REP"] = "0"
-        v["counts only, per-CTA private count copies forced"] = timed(sess, "counts only, private copies", False, False)
-        del os.environ["GJ_HIST_REP"]
-        for sub in (1, 2):
-            os.environ["GJ_TIER_SUB"] = str(sub)
-            os.environ["GJ_DEBUG_PLAN"] = "1"
+        for label, kw in variants:
             try:
                 b2 = join.IndexBundle.from_arrays(arena, lut, roots, prefixes, pbits, rb.k_max, rb.approx,
-                                                  rp.ids, rp.vtx_off, rp.latlng, device=0)
+                                                  rp.ids, rp.vtx_off, rp.latlng, device=0,
+                                                  options=capi.Options(debug_plan=1, **kw))
             except Exception as ex:  # e.g. out of device memory for the second copy
-                log(f"refined tier {sub}: {ex}")
+                log(f"variant {label}: {ex}")
                 continue
-            finally:
-                del os.environ["GJ_TIER_SUB"]
             s2 = b2.session()
             d_counts.zero_()
             d_stats.zero_()
-            v[f"refined tier +{sub}: ids+counts+stats"] = timed(s2, f"refined tier +{sub}", want_ids, want_stats)
+            v[f"{label}: ids+counts+stats"] = timed(s2, label, want_ids, want_stats)
             torch.cuda.synchronize()
-            res[f"refined_tier_{sub}_counts_equal"] = bool(np.array_equal(
+            res[f"{label}: counts equal"] = bool(np.array_equal(
                 (d_counts.cpu().numpy() // (reps + 1)).astype(np.uint64), counts))
-            v[f"refined tier +{sub}: counts only"] = timed(s2, f"refined tier +{sub}, counts only", False, False)
+            v[f"{label}: counts only"] = timed(s2, f"{label}, counts only", False, False)
             s2.close()
             b2.close()
-            os.environ.pop("GJ_DEBUG_PLAN", None)
         res["variants_ms"] = v
 
     # ---- host-buffer call (pageable numpy points -> counts) ----
@@ -306,11 +299,14 @@ def main():
     ap.add_argument("--pairs", type=int, default=0, help="also time gj_join_pairs_host + gj_pairs_copy on this many points")
     ap.add_argument("--save-index", default="", help="write the built index here (GJX1) for a later --load-index run")
     ap.add_argument("--load-index", default="", help="load the index from this GJX1 file when it exists")
-    ap.add_argument("--variants", action="store_true", help="extra timings that attribute the time (knobs, refined tiers)")
+    ap.add_argument("--variants", default="",
+                    help="extra timings that attribute the time: ';'-separated index variants, each a comma-separated "
+                         "list of gj_options fields, e.g. 'hist16=0;bin_open=0;hist16=0,bin_open=0;tier_sub=1'")
     ap.add_argument("--out", default="")
     a = ap.parse_args()
     r = run(a.config, a.scale, a.points, a.launch, a.check, a.reps, a.threads, not a.no_ids, not a.no_stats,
-            a.host_points, a.pairs, a.save_index, a.load_index, a.variants)
+            a.host_points, a.pairs, a.save_index, a.load_index,
+            [(v, {k: int(x) for k, x in (kv.split("=") for kv in v.split(","))}) for v in a.variants.split(";") if v])
     if a.out:
         Path(a.out).parent.mkdir(parents=True, exist_ok=True)
         Path(a.out).write_text(json.dumps(r, indent=1))

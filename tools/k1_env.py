@@ -1,8 +1,9 @@
-"""Time K1 (device-resident join of BASELINE config 2) under index-build
-environment knobs, e.g.  python tools/k1_env.py GJ_DIR16_MAX=0 GJ_DIR16_MAX=69632
+"""Time K1 (device-resident join of BASELINE config 2) under explicit index
+options (gj_options), e.g.
+    python tools/k1_env.py "" dir16_max_entries=34000 node_pal_max_mb=0,smem_pad=30000
 
-Each argument is a comma-separated list of NAME=VALUE settings applied before
-the index is loaded; results are checked against each other (counts)."""
+Each argument is a comma-separated list of field=value settings the index is
+loaded with; results are checked against each other (counts, first ids)."""
 from __future__ import annotations
 
 import json
@@ -28,9 +29,8 @@ def main():
     first = None
     out = {}
     for arg in sys.argv[1:] or [""]:
-        sets = dict(kv.split("=", 1) for kv in arg.split(",") if kv)
-        os.environ.update(sets)
-        bundle = join.IndexBundle.load(path, device=0)
+        sets = {k: int(v) for k, v in (kv.split("=", 1) for kv in arg.split(",") if kv)}
+        bundle = join.IndexBundle.load(path, device=0, options=capi.Options(**sets))
         sess = bundle.session()
         d_counts = torch.zeros(len(bundle.ids), dtype=torch.int64, device="cuda")
         d_first = torch.empty(n, dtype=torch.int32, device="cuda")
@@ -57,8 +57,6 @@ def main():
         same = bool(np.array_equal(counts, first[0]) and np.array_equal(ids, first[1]))
         out[arg] = {"ms": ms, "dir16_level": bundle.info.dir16_level, "same_as_first": same}
         print(arg or "(default)", out[arg], flush=True)
-        for k in sets:
-            os.environ.pop(k, None)
         sess.close()
         bundle.close()
     (ROOT / "gpurun_out").mkdir(exist_ok=True)

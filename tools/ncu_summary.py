@@ -3,8 +3,12 @@
     python tools/ncu_summary.py REPORT.ncu-rep [--title TEXT] [--roofline profiles/roofline.json]
 
 Prints the metrics profiles/*.txt quote, one block per profiled launch.  With
---roofline it also rewrites the JSON bench.py reads for ``roofline.traffic``
-from the FIRST launch in the report (K1 on BASELINE config 2)."""
+--roofline it also rewrites the JSON bench.py reads for ``roofline.traffic`` /
+``l2_hit_rate_pct`` / ``sectors_per_request`` from the FIRST launch in the report
+(K1 on BASELINE config 2) and stamps it with the content hash of the CUDA sources
+the capture was taken on: bench.py prints ``"ncu_stale": true`` once they differ.
+tools/capture_k1.sh is the whole recipe (bench without ncu, launch list, full
+capture, this summary)."""
 from __future__ import annotations
 
 import argparse
@@ -12,6 +16,10 @@ import csv
 import io
 import json
 import subprocess
+import sys
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent.parent
 
 METRICS = """gpu__time_duration.sum dram__bytes_read.sum dram__bytes_write.sum
 gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed lts__t_sector_hit_rate.pct
@@ -69,7 +77,14 @@ def main():
             "dram_throughput_pct_of_peak": val("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
             "smsp_issue_active_pct": val("smsp__issue_active.avg.pct_of_peak_sustained_active"),
             "warp_instructions": val("smsp__inst_executed.sum"),
+            "l1tex_sectors_per_request_global_ld": val("l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum") /
+            max(1.0, val("l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum")),
+            "kernel_time_us_under_ncu": val("gpu__time_duration.sum"),
+            "kernel": r[col["Kernel Name"]],
         }
+        sys.path.insert(0, str(ROOT))
+        import bench
+        doc["kernel_source_hash"] = bench.kernel_source_hash()
         with open(args.roofline, "w") as f:
             json.dump(doc, f, indent=1)
             f.write("\n")
