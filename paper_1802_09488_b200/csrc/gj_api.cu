@@ -37,15 +37,28 @@ size_t align16(size_t v) { return (v + 15) & ~size_t{15}; }
 
 struct SmemPlan {
   uint32_t queue_off, hist_off, hist_rep;
+  uint32_t hist16;  // 1 = one 16-bit histogram instead (hist_rep == 0)
   size_t total;
 };
 
+constexpr size_t kHist32MaxRow = 64u << 10;  // a 32-bit histogram row set beyond this is not tried
+constexpr size_t kHist16MaxRow = 96u << 10;
+
 }  // namespace
 
-size_t k1_smem_besides_tier(size_t n_ids) {
+bool k1_uses_hist16(size_t n_ids, const gj_options& opt) {
+  if (opt.hist16 == 0 || n_ids == 0) return false;
+  const size_t row16 = (n_ids + 2) / 2 * 4;
+  if (row16 > kHist16MaxRow) return false;
+  return opt.hist16 > 0 || (n_ids + 1) * 4 > kHist32MaxRow;  // forced, or the 32-bit form does not fit
+}
+
+size_t k1_smem_besides_tier(size_t n_ids, const gj_options& opt) {
   const size_t queues = static_cast<size_t>(kJoinThreads / 32) * kQueueBytesPerWarp;
   const size_t hist_row = (n_ids + 1) * 4;
-  return queues + (hist_row <= (64u << 10) ? hist_row : 0) + 64;  // + alignment slack
+  size_t hist = hist_row <= kHist32MaxRow ? hist_row : 0;
+  if (k1_uses_hist16(n_ids, opt)) hist = (n_ids + 2) / 2 * 4;
+  return queues + hist + 64;  // + alignment slack
 }
 
 namespace {
@@ -72,7 +85,11 @@ SmemPlan plan_smem(const gj_index& ix) {
   uint32_t rep = 0;
   const size_t last_good_step = (196u - 1u) << 10;  // above it: the 228 KB carve-out cliff
   const bool hist_fits = at + one <= limit && (at + one <= last_good_step || at > last_good_step);
-  if (ix.dev.n_ids && hist_fits) {
+  const size_t one16 = (static_cast<size_t>(ix.dev.n_ids) + 2) / 2 * 4;  // two 16-bit counters per word, + the spare
+  if (k1_uses_hist16(ix.dev.n_ids, ix.opt) && at + one16 <= limit) {
+    p.hist16 = 1;
+    at += one16;
+  } else if (ix.dev.n_ids && hist_fits) {
     size_t step = limit;  // carve-out steps hold 1 KB of system shared memory per CTA
     for (size_t kb : {64, 100, 132, 164, 196}) {
       if (at + one <= (kb - 1) << 10) {
@@ -83,7 +100,7 @@ SmemPlan plan_smem(const gj_index& ix) {
     rep = 1;
     while (rep < 32 && at + one * rep * 2 <= step) rep <<= 1;
   }
-  if (ix.opt.hist_rep_cap >= 0) {  // explicit knob: a power of two at most the planned value, or 0
+  if (!p.hist16 && ix.opt.hist_rep_cap >= 0) {  // explicit knob: a power of two at most the planned value, or 0
     uint32_t cap = 0;
     while (cap < rep && (cap ? cap * 2 : 1u) <= static_cast<uint32_t>(ix.opt.hist_rep_cap)) cap = cap ? cap * 2 : 1u;
     rep = cap;
@@ -93,8 +110,9 @@ SmemPlan plan_smem(const gj_index& ix) {
   if (ix.opt.smem_pad > 0 && at + static_cast<size_t>(ix.opt.smem_pad) <= limit) at += static_cast<size_t>(ix.opt.smem_pad);  // L1 carve-out experiments
   p.total = at;
   if (ix.opt.debug_plan) {
-    std::fprintf(stderr, "[gj] K1 smem: 16-bit tier level %d, %zu B; queues at %u; histogram at %u x%u; total %zu\n",
-                 30 - ix.dev.dir16.shift, table_bytes, p.queue_off, p.hist_off, p.hist_rep, p.total);
+    std::fprintf(stderr, "[gj] K1 smem: 16-bit tier level %d, %zu B; queues at %u; histogram at %u x%u%s; total %zu; palette nodes %s\n",
+                 30 - ix.dev.dir16.shift, table_bytes, p.queue_off, p.hist_off, p.hist_rep, p.hist16 ? " (16-bit, flushed)" : "",
+                 p.total, ix.dev.node_pal ? "yes" : "no");
     const DevDirectory& tb = ix.dev.dirk.n_table ? ix.dev.dirk : (ix.dev.dir2.n_table ? ix.dev.dir2 : ix.dev.dir);
     std::fprintf(stderr, "[gj] K1 32-bit tier: level %d%s, %u x %u cells (%.1f MB); queue coding %s, tier_shift %u, index bits %u\n",
                  30 - tb.shift, ix.dev.dirk.n_table ? " (refined)" : "", tb.width, tb.height, tb.n_table * 4e-6,
@@ -200,10 +218,12 @@ int enqueue_join(gj_session* s, const JoinRequest& rq) {
   jp.smem_queue_off = sp.queue_off;
   jp.smem_hist_off = sp.hist_off;
   jp.hist_rep = sp.hist_rep;
+  jp.hist16 = sp.hist16;
   // No room for the histogram in shared memory: count into per-SM copies (at most 1 GB of them)
   const size_t priv_bytes = static_cast<size_t>(ix.sm_count) * n_ids * 4;
   const bool k2_local = static_cast<size_t>(n_ids) * 4 <= (32u << 10);
-  const bool want_priv = n_ids != 0 && priv_bytes <= (1ull << 30) && (sp.hist_rep == 0 || (rq.exact && !k2_local));
+  const bool k1_priv = sp.hist_rep == 0 && !sp.hist16;
+  const bool want_priv = n_ids != 0 && priv_bytes <= (1ull << 30) && (k1_priv || (rq.exact && !k2_local));
   uint32_t* d_priv = nullptr;
   if (want_priv) {
     if (s->d_counts_priv.bytes < priv_bytes) {
@@ -212,7 +232,7 @@ int enqueue_join(gj_session* s, const JoinRequest& rq) {
     }
     d_priv = s->d_counts_priv.as<uint32_t>();
   }
-  jp.counts_priv = sp.hist_rep == 0 ? d_priv : nullptr;
+  jp.counts_priv = k1_priv ? d_priv : nullptr;
   jp.n_priv = static_cast<uint32_t>(ix.sm_count);
   jp.exact = rq.exact ? 1 : 0;
 

@@ -23,7 +23,10 @@ int cuda_fail(cudaError_t e, const char* what);
 // Shared memory K1 needs besides its first tier (per-warp queues, one histogram row set for `n_ids`
 // polygons when that fits), so the index builder can size the tier to stay below the 228 KB carve-out
 // step (defined next to the kernel's launch plan, gj_api.cu).
-size_t k1_smem_besides_tier(size_t n_ids);
+size_t k1_smem_besides_tier(size_t n_ids, const gj_options& opt);
+// Id tables beyond the 32-bit shared-memory histogram (64 KB) count in a 16-bit one that the CTA flushes every
+// kHist16FlushTiles tiles — no counter can overflow in between (join_kernel) — when it fits and the options allow it.
+bool k1_uses_hist16(size_t n_ids, const gj_options& opt);
 
 #define GJ_CUDA(call)                                  \
   do {                                                 \

@@ -12,6 +12,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <memory>
+#include <thread>
 #include <unordered_map>
 
 #include "gj_host.hpp"
@@ -30,7 +31,8 @@ constexpr double kDirKMinLinkShare = 0.25;         // refine only when at least 
 // 196 KB shared-memory carve-out step (60 KB of L1 left for loads in flight);
 // the next step up (228 KB) is a cliff, see plan_smem in gj_api.cu
 constexpr uint64_t kMaxDir16Entries = 69632;
-constexpr uint64_t kMaxNodePalBytes = 32ull << 20;  // palette nodes are only worth it while they stay in L2
+constexpr uint64_t kMaxNodePalBytes = 32ull << 20;  // palette nodes of a tree this small stay in L2 as a whole
+constexpr uint64_t kMaxNodePalLargeBytes = 8ull << 30;  // larger trees: only when most nodes fit the form (create_index)
 constexpr uint64_t kMaxPolygonId = (1u << 30) - 1;
 
 struct Bitmap {
@@ -77,7 +79,6 @@ struct Box {
     x_hi = std::max(x_hi, xh);
     y_hi = std::max(y_hi, yh);
   }
-  uint64_t area() const { return empty() ? 0 : (x_hi - x_lo + 1) * (y_hi - y_lo + 1); }
   uint64_t padded_area() const { return empty() ? 1 : (x_hi - x_lo + 2) * (y_hi - y_lo + 2); }
 };
 
@@ -613,8 +614,10 @@ int create_index(const gj_index_desc& d, int device, const gj_options* options, 
   }
   {
     // the tier, K1's queues and one histogram row set must stay inside the 196 KB carve-out step
-    const size_t besides = k1_smem_besides_tier(n_ids);
-    const size_t step = (196u - 1u) << 10;
+    const size_t besides = k1_smem_besides_tier(n_ids, opt);
+    // (with the 16-bit histogram — tens of thousands of polygons, each a few tier cells across, so the tier
+    // resolves little anyway — everything stays inside the 164 KB step and leaves L1 its 92 KB)
+    const size_t step = ((k1_uses_hist16(n_ids, opt) ? 164u : 196u) - 1u) << 10;
     uint64_t max16 = std::min<uint64_t>(kMaxDir16Entries, step > besides ? (step - besides) / 2 : 0);
     if (opt.dir16_max_entries > 0) max16 = std::min<uint64_t>(static_cast<uint64_t>(opt.dir16_max_entries), 110000);  // explicit knob
     // explicit knob: a density-matched stand-in over a small box can emulate the full-size tier
@@ -646,45 +649,61 @@ int create_index(const gj_index_desc& d, int device, const gj_options* options, 
   if ((rc = upload(ix->d_dir16_table, an.dir16.table16.data(), an.dir16.table16.size(), &bytes)) != GJ_OK) return rc;
   if ((rc = upload(ix->d_dirk_table, an.dirk.table.data(), an.dirk.table.size(), &bytes)) != GJ_OK) return rc;
 
-  // Palette form of the nodes (DevIndex::node_pal), for K1's deep descents.
-  bool have_pal = false;
+  // Palette form of the nodes (DevIndex::node_pal), for K1's deep descents.  Small trees (<= 32 MB of palette
+  // records) always get it: it stays in L2 as a whole.  Large ones (BASELINE config 4: 18.3 M nodes = 2.3 GB of
+  // records next to a 37 GB arena) get it when at least three quarters of the nodes fit the four-entry form: a
+  // random slot read costs one 128-byte DRAM burst either way, but the hot part of the tree is 16x smaller in
+  // this form, and that part does stay in L2.  (Lookup-table-heavy trees — overlapping polygons — rarely fit.)
   {
-    uint64_t max_pal = kMaxNodePalBytes;
+    uint64_t max_pal = kMaxNodePalLargeBytes;
     if (opt.node_pal_max_mb >= 0) max_pal = static_cast<uint64_t>(opt.node_pal_max_mb) << 20;  // explicit knob
-    if (d.node_count != 0 && d.node_count * 128 <= max_pal && d.node_count <= (1ull << 23)) {
+    if (d.node_count != 0 && d.node_count * 128 <= max_pal) {
       std::vector<uint64_t> pal(d.node_count * 16, 0);
-      for (uint64_t node = 0; node < d.node_count; ++node) {
-        const uint64_t* slots = d.arena + node * kNodeSlots;
-        uint64_t* rec = pal.data() + node * 16;
-        uint64_t values[4];
-        int n_values = 0;
-        bool fits = true;
-        for (int sl = 0; sl < kNodeSlots && fits; ++sl) {
-          int code = 0;
-          while (code < n_values && values[code] != slots[sl]) ++code;
-          if (code == n_values) {
-            if (n_values == 4) {
-              fits = false;
-              break;
+      const unsigned n_workers = static_cast<unsigned>(std::max<uint64_t>(
+          1, std::min<uint64_t>({16, std::thread::hardware_concurrency(), d.node_count / 4096 + 1})));
+      std::vector<uint64_t> fit_count(n_workers, 0);
+      auto build_range = [&](unsigned w) {
+        const uint64_t first = d.node_count * w / n_workers, last = d.node_count * (w + 1) / n_workers;
+        for (uint64_t node = first; node < last; ++node) {
+          const uint64_t* slots = d.arena + node * kNodeSlots;
+          uint64_t* rec = pal.data() + node * 16;
+          uint64_t values[4];
+          int n_values = 0;
+          bool fits = true;
+          for (int sl = 0; sl < kNodeSlots && fits; ++sl) {
+            int code = 0;
+            while (code < n_values && values[code] != slots[sl]) ++code;
+            if (code == n_values) {
+              if (n_values == 4) {
+                fits = false;
+                break;
+              }
+              values[n_values++] = slots[sl];
             }
-            values[n_values++] = slots[sl];
+            rec[4 + sl / 32] |= static_cast<uint64_t>(code) << (2 * (sl % 32));
           }
-          rec[4 + sl / 32] |= static_cast<uint64_t>(code) << (2 * (sl % 32));
+          if (fits) {
+            for (int c = 0; c < 4; ++c) rec[c] = c < n_values ? values[c] : 0;
+            ++fit_count[w];
+          } else {
+            for (int w16 = 0; w16 < 16; ++w16) rec[w16] = 0;
+            rec[0] = ~0ull;  // more than 4 distinct entries: read the arena
+          }
         }
-        if (fits) {
-          for (int c = 0; c < 4; ++c) rec[c] = c < n_values ? values[c] : 0;
-        } else {
-          for (int w = 0; w < 16; ++w) rec[w] = 0;
-          rec[0] = ~0ull;  // more than 4 distinct entries: read the arena
-        }
+      };
+      std::vector<std::thread> pool;
+      for (unsigned w = 1; w < n_workers; ++w) pool.emplace_back(build_range, w);
+      build_range(0);
+      for (std::thread& t : pool) t.join();
+      uint64_t fit = 0;
+      for (uint64_t f : fit_count) fit += f;
+      if (d.node_count * 128 <= kMaxNodePalBytes || fit * 4 >= d.node_count * 3 || opt.node_pal_max_mb >= 0) {
+        if ((rc = upload(ix->d_node_pal, pal.data(), pal.size(), &bytes)) != GJ_OK) return rc;
       }
-      if ((rc = upload(ix->d_node_pal, pal.data(), pal.size(), &bytes)) != GJ_OK) return rc;
-      have_pal = true;
     }
   }
 
   DevIndex& dv = ix->dev;
-  (void)have_pal;  // d_node_pal stays empty without palette nodes
   for (int f = 0; f < 8; ++f) {
     dv.roots[f] = f < 6 ? d.roots[f] : 0;  // refresh_view, act.cpp:373-383
     dv.prefixes[f] = f < 6 ? d.prefixes[f] : 0;

@@ -43,6 +43,11 @@ constexpr int kQueue3Cap = 64;
 constexpr int kQueueBytesPerWarp = (kQueue2Cap + kQueue3Cap) * 8;
 constexpr int kChunkPoints = 32 * kPointsPerThread;  // consecutive points a warp owns in a tile
 constexpr int kRefineThreads = 256;
+// The 16-bit histogram (JoinParams::hist16) is flushed by the whole CTA every this many tiles.  Between two
+// flushes a CTA settles at most the points it loaded since (kTile per tile) plus what its queues and in-flight
+// batches carried over (< 32 warps * (kQueue2Cap + kQueue3Cap + 32) = 8192), and a point adds at most 1 to any
+// one polygon: 12 * 4096 + 8192 = 57344 < 65536, so no counter can overflow.
+constexpr uint32_t kHist16FlushTiles = 12;
 
 struct JoinParams {
   const double2* pts;  // (lat, lng) pairs: .x = lat, .y = lng  (latlng.hpp:26-29)
@@ -64,6 +69,7 @@ struct JoinParams {
   uint32_t smem_queue_off;  // bytes: per-warp open-point queues
   uint32_t smem_hist_off;   // bytes
   uint32_t hist_rep;        // replicas per slot (power of two), 0 = not in shared memory
+  uint32_t hist16;          // hist_rep == 0: one 16-bit histogram in shared memory, flushed every kHist16FlushTiles tiles
   uint32_t* counts_priv;    // hist_rep == 0: [n_priv][n_ids] u32 copies, zero on entry; may be null
   uint32_t n_priv;          // CTA b counts into copy b % n_priv
   int32_t exact;
@@ -144,7 +150,8 @@ struct HistRef {
   uint32_t smem;      // shared address of the histogram
   uint32_t rep;       // replicas per slot (power of two), 0 = not in shared memory
   uint32_t lane_rep;  // lane & (rep - 1)
-  uint32_t* priv;     // rep == 0: this SM's copy (null: straight into jp.counts)
+  uint32_t h16;       // rep == 0: 16-bit counters, two per word (JoinParams::hist16)
+  uint32_t* priv;     // rep == 0 && !h16: this SM's copy (null: straight into jp.counts)
 };
 
 template <bool kDense>
@@ -153,6 +160,8 @@ __device__ __forceinline__ void count_slot(const DevIndex& ix, const JoinParams&
   const uint32_t slot = kDense ? id : id_to_slot(ix, id);
   if (h.rep) {
     red_inc_shared_if(h.smem + (slot * h.rep + h.lane_rep) * 4u, true);
+  } else if (h.h16) {  // the half-word's carry cannot happen between two flushes (kHist16FlushTiles)
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(h.smem + (slot >> 1) * 4u), "r"(1u << ((slot & 1u) * 16u)) : "memory");
   } else if (h.priv) {
     atomicAdd(h.priv + slot, 1u);
   } else {
@@ -329,14 +338,14 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
     const uint32_t n4 = (ix.dir16.n_table * 2u + 15u) / 16u;  // buffers are padded to 16 B
     for (uint32_t i = tid; i < n4; i += kJoinThreads) dst[i] = __ldg(src + i);
     uint32_t* hist = reinterpret_cast<uint32_t*>(smem + jp.smem_hist_off);
-    const uint32_t n_hist = (ix.n_ids + 1u) * jp.hist_rep;
+    const uint32_t n_hist = jp.hist16 ? (ix.n_ids + 2u) / 2u : (ix.n_ids + 1u) * jp.hist_rep;
     for (uint32_t i = tid; i < n_hist; i += kJoinThreads) hist[i] = 0;
   }
   __syncthreads();
 
   // loop invariants in registers
   const uint32_t s_table = smem_addr(smem);
-  const HistRef hist{smem_addr(smem + jp.smem_hist_off), jp.hist_rep, lane & (jp.hist_rep ? jp.hist_rep - 1u : 0u),
+  const HistRef hist{smem_addr(smem + jp.smem_hist_off), jp.hist_rep, lane & (jp.hist_rep ? jp.hist_rep - 1u : 0u), jp.hist16,
                      jp.counts_priv ? jp.counts_priv + static_cast<size_t>(blockIdx.x % jp.n_priv) * ix.n_ids : nullptr};
   const uint32_t s_q2 = smem_addr(smem + jp.smem_queue_off) + warp * kQueueBytesPerWarp;
   const uint32_t s_q3 = s_q2 + kQueue2Cap * 8u;
@@ -628,14 +637,39 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
     }
     drain2(false);
   };
+  // 16-bit histogram: add the non-zero counters to the caller's counts and clear them (whole CTA)
+  auto flush_hist16 = [&]() {
+    __syncthreads();
+    uint32_t* words = reinterpret_cast<uint32_t*>(smem + jp.smem_hist_off);
+    for (uint32_t w = tid; w < (ix.n_ids + 1u) / 2u; w += kJoinThreads) {
+      const uint32_t v = words[w];
+      if (v == 0u) continue;
+      words[w] = 0u;
+      if (v & 0xFFFFu) atomicAdd(&jp.counts[2u * w], static_cast<unsigned long long>(v & 0xFFFFu));
+      if ((v >> 16) && 2u * w + 1u < ix.n_ids) atomicAdd(&jp.counts[2u * w + 1u], static_cast<unsigned long long>(v >> 16));
+    }
+    __syncthreads();
+  };
   const uint32_t n_full_tiles = n / kTile;
   uint32_t tile = blockIdx.x;
-  for (; tile < n_full_tiles; tile += gridDim.x) tile_body(tile, std::true_type{});
+  if (jp.hist16) {  // every warp of the CTA runs the same number of tiles, so the barriers inside line up
+    uint32_t since = 0;
+    for (; tile < n_full_tiles; tile += gridDim.x) {
+      tile_body(tile, std::true_type{});
+      if (++since == kHist16FlushTiles) {
+        since = 0;
+        flush_hist16();
+      }
+    }
+  } else {
+    for (; tile < n_full_tiles; tile += gridDim.x) tile_body(tile, std::true_type{});
+  }
   if (tile < n_tiles) tile_body(tile, std::false_type{});  // the partial last tile, in one CTA
   drain2(true);
   settle_batch();
   drain3(true);
 
+  if (jp.hist16) flush_hist16();
   __syncthreads();
   if (jp.hist_rep) {  // fold the replicas, one global add per non-zero slot
     const uint32_t* hist_words = reinterpret_cast<const uint32_t*>(smem + jp.smem_hist_off);

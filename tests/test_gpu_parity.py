@@ -665,3 +665,39 @@ def test_replica_is_independent_of_its_source():
     _check_join_against_fixture(rep, fx)
     filler.close()
     rep.close()
+
+
+@pytest.mark.parametrize("name", ["join_small_exact", "cfg4_tess36_approx1m_k56", "cfg5_stars_scaled", "kmax60_sparse_ids"])
+def test_flushed_16bit_histogram_matches_reference(name):
+    """Id tables beyond the 32-bit shared-memory histogram count in a 16-bit one that the CTA flushes every
+    kHist16FlushTiles tiles (forced here on small tables): the fixture's results, then launches long enough for
+    many flushes per CTA — random points, and the worst case of every point in ONE polygon (a counter that would
+    wrap 30 times without the flushes) — against the default counting path."""
+    import torch
+    fx = golden_util.load(name)
+    b16 = join.IndexBundle.load(golden_util.bundle_file(name), device=0, options=capi.Options(hist16=1))
+    b32 = join.IndexBundle.load(golden_util.bundle_file(name), device=0)
+    _check_join_against_fixture(b16, fx)
+    rng = np.random.default_rng(0x16B1)
+    pts = np.ascontiguousarray(fx["points"])
+    n = 20_000_000
+    big = pts[rng.integers(0, len(pts), n)]
+    hit = pts[np.flatnonzero(b32.session().join_count(pts, capi.GJ_MODE_APPROX, want_ids=True)[1] < capi.GJ_DEFERRED)[0]]
+    same = np.tile(hit, (n, 1))
+    for arr in (big, same):
+        d_pts = torch.from_numpy(arr).cuda()
+        for mode in (capi.GJ_MODE_APPROX, capi.GJ_MODE_EXACT):
+            if mode == capi.GJ_MODE_EXACT and name == "cfg5_stars_scaled":
+                continue  # 2^32 candidate tasks in one launch: the call is refused, see test_device_resident_call_is_split_into_launches
+            res = []
+            for b in (b16, b32):
+                d_counts = torch.zeros(len(b.ids), dtype=torch.int64, device="cuda")
+                d_first = torch.empty(n, dtype=torch.int32, device="cuda")
+                torch.cuda.synchronize()
+                b.session().join_count_device(d_pts.data_ptr(), n, d_counts.data_ptr(), mode,
+                                              d_first_id_ptr=d_first.data_ptr(), sync=True)
+                res.append((d_counts.cpu().numpy(), d_first.cpu().numpy()))
+            assert np.array_equal(res[0][0], res[1][0]) and np.array_equal(res[0][1], res[1][1])
+            assert int(res[0][0].sum()) >= (n if arr is same else 1)
+    b16.close()
+    b32.close()
