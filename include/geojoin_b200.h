@@ -126,9 +126,8 @@ typedef struct {
   int32_t smem_pad;             /* unused shared memory added to the join kernel (L1 carve-out experiments) */
   int32_t debug_plan;           /* 1 = print the join kernel's shared-memory plan to stderr */
   int32_t hist16;               /* id tables beyond the 32-bit shared histogram count in a 16-bit one with
-                                   periodic flushes: -1 = automatic, 0 = never */
-  int32_t bin_open;             /* open points of wide arenas are binned by trie node before the arena is read:
-                                   -1 = automatic, 0 = never, 1 = always (when the coding allows it) */
+                                   periodic flushes: -1 = automatic, 0 = never, 1 = also when the 32-bit one fits */
+  int32_t reserved0;            /* keep 0 */
   uint64_t max_launch_points;   /* test hook: split device-resident calls into launches of this many points; 0 = none */
   uint64_t chunk_points;        /* host pipeline: points per chunk; 0 = default (3 M counts / 4 M pairs), min 4096 */
 } gj_options;
@@ -297,6 +296,26 @@ GJ_API int gj_join_pairs_host(gj_session* s, const double* latlng, uint64_t n,
                               int mode, uint64_t* n_pairs, gj_stats* stats,
                               uint64_t* bad_index);
 GJ_API int gj_pairs_copy(gj_session* s, uint64_t* row_ptr, uint32_t* polygon_id);
+
+/* The same join in ONE call with caller-provided output arrays: row_ptr[n + 1]
+ * and polygon_id[id_capacity].  The pipeline keeps the running pair count on the
+ * device, so chunks follow each other without a host round trip, and chunk c's
+ * rows and ids travel to the caller's arrays while chunk c + 1 runs (directly
+ * when they are pinned, gj_host_alloc).  *n_pairs is always the join's pair
+ * count; when it exceeds id_capacity the call returns GJ_CAPACITY with row_ptr
+ * complete and polygon_id undefined — allocate *n_pairs ids and call again
+ * (id_capacity 0 sizes the output). */
+GJ_API int gj_join_pairs_host_into(gj_session* s, const double* latlng, uint64_t n, int mode,
+                                   uint64_t* row_ptr, uint32_t* polygon_id, uint64_t id_capacity,
+                                   uint64_t* n_pairs, gj_stats* stats, uint64_t* bad_index);
+
+/* CSR without the host detour: points, row offsets and polygon ids all in HBM
+ * (device pointers; d_row_ptr u64[n + 1], d_polygon_id u32[id_capacity]) — what
+ * a multi-GPU CSR pipeline keeps sharded per device (BASELINE configs[4]).
+ * Synchronous; same capacity convention as gj_join_pairs_host_into. */
+GJ_API int gj_join_pairs_device(gj_session* s, const double* d_latlng, uint64_t n, int mode,
+                                uint64_t* d_row_ptr, uint32_t* d_polygon_id, uint64_t id_capacity,
+                                uint64_t* n_pairs, gj_stats* stats, uint64_t* bad_index);
 
 /* ---- all GPUs of the box for ONE input: ≙ the worker fan-out of
  * join_count_per_polygon (src/join.cpp:255-285) ------------------------------

@@ -28,6 +28,7 @@ EXPORTS = [
     "gj_options_default", "gj_index_create_ex", "gj_index_load_file_ex", "gj_index_replicate",
     "gj_group_create", "gj_group_load_file", "gj_group_destroy", "gj_group_size", "gj_group_index",
     "gj_group_session", "gj_group_join_count_host", "gj_group_join_pairs_host", "gj_group_pairs_copy",
+    "gj_join_pairs_host_into", "gj_join_pairs_device",
 ]
 
 
@@ -63,7 +64,7 @@ class Options(C.Structure):
         ("struct_size", C.c_uint32), ("dir16_max_entries", C.c_int32), ("dir16_level_max", C.c_int32),
         ("node_pal_max_mb", C.c_int32), ("tier_sub", C.c_int32), ("ids_late", C.c_int32),
         ("queue_unpacked", C.c_int32), ("queue_slot_hi_bits", C.c_int32), ("hist_rep_cap", C.c_int32),
-        ("smem_pad", C.c_int32), ("debug_plan", C.c_int32), ("hist16", C.c_int32), ("bin_open", C.c_int32),
+        ("smem_pad", C.c_int32), ("debug_plan", C.c_int32), ("hist16", C.c_int32), ("reserved0", C.c_int32),
         ("max_launch_points", C.c_uint64), ("chunk_points", C.c_uint64),
     ]
 
@@ -161,6 +162,9 @@ def lib():
         L.gj_group_join_pairs_host.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_uint64, C.c_int,
                                                C.POINTER(C.c_uint64), C.POINTER(Stats), C.POINTER(C.c_uint64)]
         L.gj_group_pairs_copy.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p]
+        for fn in (L.gj_join_pairs_host_into, L.gj_join_pairs_device):
+            fn.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_int, C.c_void_p, C.c_void_p, C.c_uint64,
+                           C.POINTER(C.c_uint64), C.POINTER(Stats), C.POINTER(C.c_uint64)]
         L.gj_index_destroy.restype = None
         L.gj_session_destroy.restype = None
         L.gj_host_free.restype = None

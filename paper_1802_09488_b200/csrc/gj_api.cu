@@ -627,7 +627,7 @@ int run_host_pairs(gj_session* s, const double* latlng, uint64_t n, bool exact, 
     uint64_t* d_total = s->d_block_sums.as<uint64_t>() + n_blocks_max + 1;
     scan_sums_kernel<<<1, kScanThreads, 0, s->stream>>>(s->d_block_sums.as<uint64_t>(), n_blocks, d_total);
     scan_apply_kernel<<<n_blocks, kScanThreads, 0, s->stream>>>(pp.count, len, s->d_block_sums.as<uint64_t>(), id_base,
-                                                                d_row_all + begin);
+                                                                d_row_all + begin, nullptr, true);
     s->launches += 4;
     GJ_CUDA(cudaGetLastError());
     // stage the next chunk's points while the device works on this one
@@ -642,6 +642,8 @@ int run_host_pairs(gj_session* s, const double* latlng, uint64_t n, bool exact, 
       if ((rc = grow_keep(s, s->d_all_ids, want, id_base * 4)) != GJ_OK) return rc;
     }
     pp.out_id = s->d_all_ids.as<uint32_t>();  // row_ptr already carries the global base
+    pp.out_cap = s->d_all_ids.bytes / 4;
+    pp.out_sub = nullptr;
     pairs_emit_kernel<true><<<wide, 256, 0, s->stream>>>(ix.dev, pp);
     ++s->launches;
     GJ_CUDA(cudaGetLastError());
@@ -660,6 +662,211 @@ int run_host_pairs(gj_session* s, const double* latlng, uint64_t n, bool exact, 
     stats->solely_true_hits += h_stats[3];
     stats->refinement_entered += h_stats[4];
     stats->candidate_refs += h_stats[5];
+  }
+  return GJ_OK;
+}
+
+
+// Where run_pairs_async leaves the CSR: the caller's device arrays (row offsets and ids at their global positions),
+// or the caller's host arrays, streamed chunk by chunk while the next chunk runs.
+struct PairsSink {
+  uint64_t* d_row_ptr = nullptr;  // device output: [n + 1]
+  uint32_t* d_ids = nullptr;      //                [ids_cap]
+  uint64_t* h_row_ptr = nullptr;  // host output:   [n + 1]
+  uint32_t* h_ids = nullptr;      //                [ids_cap]
+  uint64_t ids_cap = 0;
+};
+
+// join_exact / join_approx -> CSR without a host round trip per chunk: the pair count so far lives on the device
+// (the scan of a chunk starts from it, a one-thread kernel advances it), the capacity of the id array is checked
+// by the fill kernel, and — host output — chunk c's rows and ids travel D2H on the copy-out stream while chunk
+// c + 1 runs.  `src` is device memory when `src_on_device`, else host memory copied one chunk ahead.
+int run_pairs_async(gj_session* s, const double* src, bool src_on_device, uint64_t n, bool exact, gj_stats* stats,
+                    const PairsSink& sink, uint64_t* n_pairs, uint64_t* bad_index) {
+  gj_index& ix = *s->ix;
+  GJ_CUDA(cudaSetDevice(ix.device));
+  const bool to_host = sink.h_row_ptr != nullptr;
+  const uint64_t max_cand = std::max<uint64_t>(1, ix.max_cand_refs);
+  const uint64_t max_refs = std::max<uint64_t>(1, ix.max_refs);
+  const uint64_t per_point = 48 + (exact ? max_cand * 13 : 0);
+  uint64_t chunk = std::min<uint64_t>(ix.opt.chunk_points ? std::max<uint64_t>(4096, ix.opt.chunk_points) : 4ull << 20,
+                                      std::max<uint64_t>(4096, kScratchBudget / per_point));
+  if (to_host) chunk = std::min<uint64_t>(chunk, std::max<uint64_t>(4096, (768ull << 20) / (max_refs * 4)));  // chunk-local ids
+  chunk = std::min<uint64_t>(chunk, std::max<uint64_t>(n, 1));
+  const uint64_t task_cap = exact ? chunk * max_cand : 0;
+  if (task_cap >= (1ull << 32)) {
+    set_error("candidate task capacity exceeds 2^32");
+    return GJ_INVALID_ARGUMENT;
+  }
+  int rc;
+  if (exact) {
+    if ((rc = reserve_tasks(s, task_cap)) != GJ_OK) return rc;
+    GJ_CUDA(s->d_task_pass.reserve(task_cap + 16));
+  }
+  const uint32_t n_blocks_max = static_cast<uint32_t>((chunk + kScanTile - 1) / kScanTile);
+  if (!src_on_device) {
+    GJ_CUDA(s->d_points[0].reserve(chunk * 16));
+    GJ_CUDA(s->d_points[1].reserve(chunk * 16));
+  }
+  GJ_CUDA(s->d_entries.reserve(chunk * 8));
+  GJ_CUDA(s->d_nrefs.reserve(chunk * 4));
+  GJ_CUDA(s->d_task_base.reserve(chunk * 4));
+  GJ_CUDA(s->d_pair_count.reserve(chunk * 4));
+  GJ_CUDA(s->d_block_sums.reserve((static_cast<size_t>(n_blocks_max) + 2) * 8));
+  GJ_CUDA(s->d_stats.reserve(6 * 8));
+  GJ_CUDA(s->d_pairs_base.reserve(16));
+  const uint64_t chunk_ids = chunk * max_refs;
+  if (to_host) {
+    for (int b = 0; b < 2; ++b) {
+      GJ_CUDA(s->d_chunk_rows[b].reserve((chunk + 1) * 8));
+      GJ_CUDA(s->d_chunk_ids[b].reserve(chunk_ids * 4 + 16));
+    }
+  }
+  uint64_t* d_base = s->d_pairs_base.as<uint64_t>();
+  GJ_CUDA(cudaMemsetAsync(d_base, 0, 16, s->stream));
+  GJ_CUDA(cudaMemsetAsync(s->d_stats.ptr, 0, 6 * 8, s->stream));
+  DevStatus* d_status = s->d_status.as<DevStatus>() + 3;
+  if ((rc = reset_status(s, d_status)) != GJ_OK) return rc;
+  const size_t probe_smem = align16(std::max<size_t>(ix.dev.dir.n_table * 4, 16));
+  if (int rc_attr = allow_max_smem(ix, probe_points_kernel)) return rc_attr;
+  const unsigned wide = static_cast<unsigned>(ix.sm_count) * 8u;
+  uint64_t* h_total = reinterpret_cast<uint64_t*>(s->h_status + 4);  // pinned: [2] chunk totals (host output)
+
+  auto copy_in = [&](uint64_t begin, int b) -> int {  // host chunk at `begin` -> point buffer b, on the copy stream
+    const uint64_t len = std::min(chunk, n - begin);
+    GJ_CUDA(cudaStreamWaitEvent(s->copy_in, s->ev_done[b], 0));  // the kernels that read buffer b last
+    GJ_CUDA(stager_of(s).to_device(s->d_points[b].ptr, src + 2 * begin, len * 16, s->copy_in));
+    GJ_CUDA(cudaEventRecord(s->ev_in[b], s->copy_in));
+    return GJ_OK;
+  };
+  GJ_CUDA(cudaEventRecord(s->ev_done[0], s->stream));
+  GJ_CUDA(cudaEventRecord(s->ev_done[1], s->stream));
+  GJ_CUDA(cudaEventRecord(s->ev_out[0], s->copy_out));
+  GJ_CUDA(cudaEventRecord(s->ev_out[1], s->copy_out));
+  if (!src_on_device && n && (rc = copy_in(0, 0)) != GJ_OK) return rc;
+
+  uint64_t host_base = 0;     // pairs of the chunks already handed to the copy-out stream
+  bool host_full = false;     // the caller's id array ran out: rows still come back, ids stop
+  auto copy_out = [&](uint64_t begin, int b) -> int {  // host output: chunk at `begin` (buffers b) -> the caller's arrays
+    const uint64_t len = std::min(chunk, n - begin);
+    GJ_CUDA(cudaEventSynchronize(s->ev_total[b]));  // its pair count is on the host
+    const uint64_t total = h_total[b];
+    GJ_CUDA(cudaStreamWaitEvent(s->copy_out, s->ev_total[b], 0));
+    GJ_CUDA(stager_of(s).to_host_async(sink.h_row_ptr + begin, s->d_chunk_rows[b].ptr, len * 8, s->copy_out));
+    if (host_base + total > sink.ids_cap) host_full = true;
+    if (!host_full && total) {
+      GJ_CUDA(stager_of(s).to_host_async(sink.h_ids + host_base, s->d_chunk_ids[b].ptr, total * 4, s->copy_out));
+    }
+    GJ_CUDA(cudaEventRecord(s->ev_out[b], s->copy_out));
+    host_base += total;
+    return GJ_OK;
+  };
+
+  int b = 0;
+  for (uint64_t begin = 0; begin < n; begin += chunk, b ^= 1) {
+    const uint64_t len = std::min(chunk, n - begin);
+    const uint32_t n_blocks = static_cast<uint32_t>((len + kScanTile - 1) / kScanTile);
+    const double2* d_pts;
+    if (src_on_device) {
+      d_pts = reinterpret_cast<const double2*>(src) + begin;
+    } else {
+      GJ_CUDA(cudaStreamWaitEvent(s->stream, s->ev_in[b], 0));
+      d_pts = s->d_points[b].as<double2>();
+    }
+    if (to_host) GJ_CUDA(cudaStreamWaitEvent(s->stream, s->ev_out[b], 0));  // chunk c - 2 has left these buffers
+    GJ_CUDA(cudaMemsetAsync(&d_status->task_count, 0, sizeof(unsigned long long), s->stream));
+    probe_points_kernel<<<static_cast<unsigned>(std::min<uint64_t>((len + 255) / 256, ix.sm_count * 4ull)), 256,
+                          probe_smem, s->stream>>>(ix.dev, d_pts, len, begin, s->d_entries.as<uint64_t>(), d_status);
+    uint64_t* d_rows = to_host ? s->d_chunk_rows[b].as<uint64_t>() : sink.d_row_ptr + begin;
+    PairsParams pp{};
+    pp.entries = s->d_entries.as<uint64_t>();
+    pp.n = len;
+    pp.base_index = begin;
+    pp.n_refs = s->d_nrefs.as<uint32_t>();
+    pp.task_base = s->d_task_base.as<uint32_t>();
+    pp.task_point = s->d_task_point.as<uint32_t>();
+    pp.task_slot = s->d_task_slot.as<uint32_t>();
+    pp.task_ord = s->d_task_ord.as<uint32_t>();
+    pp.task_cap = task_cap;
+    pp.task_pass = s->d_task_pass.as<uint8_t>();
+    pp.count = s->d_pair_count.as<uint32_t>();
+    pp.row_ptr = d_rows;
+    pp.out_id = to_host ? s->d_chunk_ids[b].as<uint32_t>() : sink.d_ids;
+    pp.out_cap = to_host ? chunk_ids : sink.ids_cap;
+    pp.out_sub = to_host ? d_base : nullptr;
+    pp.stats = stats ? s->d_stats.as<unsigned long long>() : nullptr;
+    pp.status = d_status;
+    pp.exact = exact ? 1 : 0;
+    pairs_plan_kernel<<<wide, 256, 0, s->stream>>>(ix.dev, pp);
+    s->launches += 2;
+    if (exact) {
+      RefineParams rp{};
+      rp.pts = d_pts;
+      rp.base_index = begin;
+      rp.task_point = pp.task_point;
+      rp.task_slot = pp.task_slot;
+      rp.task_ord = pp.task_ord;
+      rp.task_cap = task_cap;
+      rp.task_pass = s->d_task_pass.as<uint8_t>();
+      rp.status = d_status;
+      int per_sm = 0;
+      GJ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, refine_kernel, kRefineThreads, 0));
+      refine_kernel<<<static_cast<unsigned>(ix.sm_count) * static_cast<unsigned>(std::max(per_sm, 1)), kRefineThreads, 0,
+                      s->stream>>>(ix.dev, rp);
+      ++s->launches;
+    }
+    if (!src_on_device) GJ_CUDA(cudaEventRecord(s->ev_done[b], s->stream));  // the point buffer is free again
+    uint64_t* d_sums = s->d_block_sums.as<uint64_t>();
+    uint64_t* d_total = d_sums + n_blocks_max + 1;
+    pairs_emit_kernel<false><<<wide, 256, 0, s->stream>>>(ix.dev, pp);
+    scan_block_sums_kernel<<<n_blocks, kScanThreads, 0, s->stream>>>(pp.count, len, d_sums);
+    scan_sums_kernel<<<1, kScanThreads, 0, s->stream>>>(d_sums, n_blocks, d_total);
+    scan_apply_kernel<<<n_blocks, kScanThreads, 0, s->stream>>>(pp.count, len, d_sums, 0, d_rows, d_base, true);
+    pairs_emit_kernel<true><<<wide, 256, 0, s->stream>>>(ix.dev, pp);
+    if (to_host) GJ_CUDA(cudaMemcpyAsync(&h_total[b], d_total, 8, cudaMemcpyDeviceToHost, s->stream));
+    advance_base_kernel<<<1, 1, 0, s->stream>>>(d_base, d_total);
+    s->launches += 6;
+    GJ_CUDA(cudaGetLastError());
+    if (to_host) GJ_CUDA(cudaEventRecord(s->ev_total[b], s->stream));
+    // stage the next chunk's points, then send the previous chunk's results home, while the device works on this one
+    if (!src_on_device && begin + chunk < n && (rc = copy_in(begin + chunk, b ^ 1)) != GJ_OK) return rc;
+    if (to_host && begin != 0 && (rc = copy_out(begin - chunk, b ^ 1)) != GJ_OK) return rc;
+  }
+  if (to_host && n) {  // the last chunk
+    const uint64_t last = (n - 1) / chunk * chunk;
+    if ((rc = copy_out(last, static_cast<int>((last / chunk) & 1))) != GJ_OK) return rc;
+  }
+  uint64_t total = 0;
+  GJ_CUDA(cudaMemcpyAsync(&s->h_status[3], d_status, sizeof(DevStatus), cudaMemcpyDeviceToHost, s->stream));
+  GJ_CUDA(cudaMemcpyAsync(&h_total[0], d_base, 8, cudaMemcpyDeviceToHost, s->stream));
+  GJ_CUDA(cudaStreamSynchronize(s->stream));
+  total = h_total[0];
+  if (to_host) {
+    GJ_CUDA(stager_of(s).drain());
+    GJ_CUDA(cudaStreamSynchronize(s->copy_out));
+    sink.h_row_ptr[n] = total;
+  } else if (n == 0) {
+    GJ_CUDA(cudaMemsetAsync(sink.d_row_ptr, 0, 8, s->stream));
+    GJ_CUDA(cudaStreamSynchronize(s->stream));
+  }
+  if (n_pairs) *n_pairs = total;
+  DevStatus st = s->h_status[3];
+  const bool ids_short = (st.flags & kErrOverflowCap) != 0 || host_full || total > sink.ids_cap;
+  st.flags &= ~kErrOverflowCap;
+  if ((rc = status_to_code(st, bad_index)) != GJ_OK) return rc;
+  if (stats) {
+    unsigned long long h_stats[6];
+    GJ_CUDA(cudaMemcpy(h_stats, s->d_stats.ptr, sizeof h_stats, cudaMemcpyDeviceToHost));
+    stats->probes += h_stats[0];
+    stats->pip_tests += h_stats[1];
+    stats->false_hits += h_stats[2];
+    stats->solely_true_hits += h_stats[3];
+    stats->refinement_entered += h_stats[4];
+    stats->candidate_refs += h_stats[5];
+  }
+  if (ids_short) {
+    set_error("polygon id array too small for the join's pairs (n_pairs holds the size needed)");
+    return GJ_CAPACITY;
   }
   return GJ_OK;
 }
@@ -735,8 +942,9 @@ int gj_session_create(gj_index* ix, gj_session** out) {
     GJ_CUDA(cudaEventCreateWithFlags(&s->ev_in[b], cudaEventDisableTiming));
     GJ_CUDA(cudaEventCreateWithFlags(&s->ev_done[b], cudaEventDisableTiming));
     GJ_CUDA(cudaEventCreateWithFlags(&s->ev_out[b], cudaEventDisableTiming));
+    GJ_CUDA(cudaEventCreateWithFlags(&s->ev_total[b], cudaEventDisableTiming));
   }
-  GJ_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&s->h_status), 4 * sizeof(DevStatus), cudaHostAllocDefault));
+  GJ_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&s->h_status), 5 * sizeof(DevStatus), cudaHostAllocDefault));  // [4]: scratch words
   GJ_CUDA(s->d_status.reserve(4 * sizeof(DevStatus)));
   // No L2 persistence window for the second directory tier: it is hot enough
   // to stay resident by itself (98 % hit rate with and without a window), and a
@@ -756,6 +964,7 @@ void gj_session_destroy(gj_session* s) {
     if (s->ev_in[b]) cudaEventDestroy(s->ev_in[b]);
     if (s->ev_done[b]) cudaEventDestroy(s->ev_done[b]);
     if (s->ev_out[b]) cudaEventDestroy(s->ev_out[b]);
+    if (s->ev_total[b]) cudaEventDestroy(s->ev_total[b]);
   }
   if (s->h_status) cudaFreeHost(s->h_status);
   cudaStreamDestroy(s->stream);
@@ -1152,6 +1361,32 @@ int gj_join_pairs_host(gj_session* s, const double* latlng, uint64_t n, int mode
   }
   if (n_pairs) *n_pairs = s->pairs_total;
   return GJ_OK;
+}
+
+int gj_join_pairs_device(gj_session* s, const double* d_latlng, uint64_t n, int mode, uint64_t* d_row_ptr,
+                         uint32_t* d_polygon_id, uint64_t id_capacity, uint64_t* n_pairs, gj_stats* stats,
+                         uint64_t* bad_index) {
+  if (!s || (n && !d_latlng) || !d_row_ptr || (id_capacity && !d_polygon_id)) return GJ_INVALID_ARGUMENT;
+  bool exact = false;
+  if (!resolve_exact(*s->ix, mode, &exact)) return GJ_INVALID_ARGUMENT;
+  PairsSink sink;
+  sink.d_row_ptr = d_row_ptr;
+  sink.d_ids = d_polygon_id;
+  sink.ids_cap = id_capacity;
+  return run_pairs_async(s, d_latlng, true, n, exact, stats, sink, n_pairs, bad_index);
+}
+
+int gj_join_pairs_host_into(gj_session* s, const double* latlng, uint64_t n, int mode, uint64_t* row_ptr,
+                            uint32_t* polygon_id, uint64_t id_capacity, uint64_t* n_pairs, gj_stats* stats,
+                            uint64_t* bad_index) {
+  if (!s || (n && !latlng) || !row_ptr || (id_capacity && !polygon_id)) return GJ_INVALID_ARGUMENT;
+  bool exact = false;
+  if (!resolve_exact(*s->ix, mode, &exact)) return GJ_INVALID_ARGUMENT;
+  PairsSink sink;
+  sink.h_row_ptr = row_ptr;
+  sink.h_ids = polygon_id;
+  sink.ids_cap = id_capacity;
+  return run_pairs_async(s, latlng, false, n, exact, stats, sink, n_pairs, bad_index);
 }
 
 int gj_pairs_copy(gj_session* s, uint64_t* row_ptr, uint32_t* polygon_id) {

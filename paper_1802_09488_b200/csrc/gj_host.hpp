@@ -177,6 +177,13 @@ class HostStager {
     }
     return e;
   }
+  // Pinned destination: enqueued on `st` and left in flight (synchronise `st` before reading).  Pageable
+  // destination: staged like to_host, i.e. complete on return (the device keeps running what is already queued).
+  cudaError_t to_host_async(void* h_dst, const void* d_src, size_t bytes, cudaStream_t st) {
+    if (is_pinned(h_dst)) return cudaMemcpyAsync(h_dst, d_src, bytes, cudaMemcpyDeviceToHost, st);
+    return to_host(h_dst, d_src, bytes, st);
+  }
+  cudaError_t drain() { return cudaSuccess; }  // staged copies complete inside to_host_async
   // Blocking: the data is in h_dst on return.
   cudaError_t to_host(void* h_dst, const void* d_src, size_t bytes, cudaStream_t st) {
     if (bytes < (4u << 20) || is_pinned(h_dst)) {
@@ -283,7 +290,10 @@ struct gj_session {
   gj::DeviceBuffer d_task_point, d_task_slot, d_task_ord, d_task_pass;
   // CSR pairs pipeline
   gj::DeviceBuffer d_nrefs, d_task_base, d_pair_count, d_row_ptr, d_block_sums;
-  cudaEvent_t ev_in[3]{}, ev_done[3]{}, ev_out[3]{};
+  cudaEvent_t ev_in[3]{}, ev_done[3]{}, ev_out[3]{}, ev_total[3]{};
+  // CSR pipeline without per-chunk host round trips (run_pairs_async): the pair count so far, and — host output —
+  // two chunk-local row / id buffers that drain D2H while the next chunk runs
+  gj::DeviceBuffer d_pairs_base, d_chunk_rows[2], d_chunk_ids[2];
   gj::DevStatus* h_status = nullptr;   // pinned
   // materialised pairs of the last gj_join_pairs_host call, kept in HBM for gj_pairs_copy:
   // row_ptr[n + 1] (global offsets) and the polygon ids

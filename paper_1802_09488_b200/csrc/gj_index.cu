@@ -32,7 +32,6 @@ constexpr double kDirKMinLinkShare = 0.25;         // refine only when at least 
 // the next step up (228 KB) is a cliff, see plan_smem in gj_api.cu
 constexpr uint64_t kMaxDir16Entries = 69632;
 constexpr uint64_t kMaxNodePalBytes = 32ull << 20;  // palette nodes of a tree this small stay in L2 as a whole
-constexpr uint64_t kMaxNodePalLargeBytes = 8ull << 30;  // larger trees: only when most nodes fit the form (create_index)
 constexpr uint64_t kMaxPolygonId = (1u << 30) - 1;
 
 struct Bitmap {
@@ -478,7 +477,6 @@ gj_options default_options() {
   o.ids_late = -1;
   o.hist_rep_cap = -1;
   o.hist16 = -1;
-  o.bin_open = -1;
   return o;
 }
 
@@ -649,13 +647,15 @@ int create_index(const gj_index_desc& d, int device, const gj_options* options, 
   if ((rc = upload(ix->d_dir16_table, an.dir16.table16.data(), an.dir16.table16.size(), &bytes)) != GJ_OK) return rc;
   if ((rc = upload(ix->d_dirk_table, an.dirk.table.data(), an.dirk.table.size(), &bytes)) != GJ_OK) return rc;
 
-  // Palette form of the nodes (DevIndex::node_pal), for K1's deep descents.  Small trees (<= 32 MB of palette
-  // records) always get it: it stays in L2 as a whole.  Large ones (BASELINE config 4: 18.3 M nodes = 2.3 GB of
-  // records next to a 37 GB arena) get it when at least three quarters of the nodes fit the four-entry form: a
-  // random slot read costs one 128-byte DRAM burst either way, but the hot part of the tree is 16x smaller in
-  // this form, and that part does stay in L2.  (Lookup-table-heavy trees — overlapping polygons — rarely fit.)
+  // Palette form of the nodes (DevIndex::node_pal), for K1's deep descents: built while the whole tree fits
+  // 32 MB in this form and so stays in L2.  Larger trees do not get it by default: measured on BASELINE config 4 at
+  // full size (18.3 M nodes, 2.3 GB of palette records next to the 37 GB arena) the join took 24.3 instead of
+  // 18.1 ms per 1 B points with it — a random slot read costs one 128-byte DRAM burst either way, the hot part of
+  // the tree does not stay in L2 even in this form, a quarter of the boundary nodes (three polygons meeting) hold
+  // more than four distinct entries and pay a second burst in the arena, and the record costs three dependent
+  // loads instead of one.  gj_options.node_pal_max_mb forces it.
   {
-    uint64_t max_pal = kMaxNodePalLargeBytes;
+    uint64_t max_pal = kMaxNodePalBytes;
     if (opt.node_pal_max_mb >= 0) max_pal = static_cast<uint64_t>(opt.node_pal_max_mb) << 20;  // explicit knob
     if (d.node_count != 0 && d.node_count * 128 <= max_pal) {
       std::vector<uint64_t> pal(d.node_count * 16, 0);
@@ -697,9 +697,8 @@ int create_index(const gj_index_desc& d, int device, const gj_options* options, 
       for (std::thread& t : pool) t.join();
       uint64_t fit = 0;
       for (uint64_t f : fit_count) fit += f;
-      if (d.node_count * 128 <= kMaxNodePalBytes || fit * 4 >= d.node_count * 3 || opt.node_pal_max_mb >= 0) {
-        if ((rc = upload(ix->d_node_pal, pal.data(), pal.size(), &bytes)) != GJ_OK) return rc;
-      }
+      (void)fit;
+      if ((rc = upload(ix->d_node_pal, pal.data(), pal.size(), &bytes)) != GJ_OK) return rc;
     }
   }
 

@@ -319,11 +319,14 @@ __device__ __noinline__ uint32_t emit_general(const DevIndex& ix, const JoinPara
 // few active ones; through the queues they always run with full warps.
 // kDense: id == count slot for every polygon AND the histogram is in shared
 // memory (jp.hist_rep != 0), the common case; otherwise the general counting path.
-// kLate (first ids wanted, and the shared-memory tier resolves few points — DevIndex::ids_late): population 1
+// kLate (first ids wanted, and the shared-memory tier resolves few points — gj_index::ids_late): population 1
 // does not pre-write the first-id words of the points it queues; population 2 writes the word of every point it
 // looks up (whole runs again, because nearly all points of a tile pass through it) and population 3 always writes.
 // Without it such an index writes almost every word twice, the second time as scattered partial sectors (measured
-// on BASELINE config 4 at full size: 9 of 23 ms).
+// on BASELINE config 4 at full size: 9 of 23 ms).  (Tried for the same indexes and dropped: a "direct" population 1
+// that skips the shared-memory tier and Q2 and has every lane gather the 32-bit tier codes of its own four points —
+// bit-exact, but 1.25 instead of 1.00 ms per 100 M points on the config-4 stand-in: the gathers' L2 latency is
+// exposed in every tile, where the queued batch is issued one tile ahead of its use.)
 template <bool kIds, bool kStats, bool kDense, bool kLate = false>
 __global__ void __launch_bounds__(kJoinThreads, GJ_JOIN_MIN_BLOCKS)
 join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinParams jp) {
@@ -439,6 +442,10 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
             from_arena = first == ~0ull;
             entry = v;
           }
+#ifdef GJ_EXP_NO_ARENA  // timing experiment: results are wrong
+          from_arena = false;
+          if (!ix.node_pal) entry = 0;
+#endif
           if (from_arena) entry = ld_arena(ix.arena + at);
           walk = (entry & 3u) == 0u && entry != 0u;  // a link again: deeper than the queued bits reach
           node = entry >> 2;
@@ -459,7 +466,11 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
     }
     const bool single = (static_cast<uint32_t>(entry) & 3u) == 1u &&
                         ((static_cast<uint32_t>(entry >> 2) & 1u) != 0u || !jp.exact);  // one payload that emits
-    const bool general = mine && entry != 0 && !single;
+    // two inlined payloads that both emit now (approximate mode, or two true hits), and no overflow record to write:
+    // the boundary cells between two polygons of a tessellation — a quarter of all points on BASELINE config 4
+    const bool pair_now = (static_cast<uint32_t>(entry) & 3u) == 2u && (!kIds || jp.ovf_discard) &&
+                          (!jp.exact || ((entry >> 33) & (entry >> 2) & 1u) != 0u);
+    const bool general = mine && entry != 0 && !single && !pair_now;
     EntryPlan plan{};
     if (general) plan = plan_entry<kIds>(ix, jp.exact != 0, entry);
     unsigned long long ovf_base = 0, task_base = 0;
@@ -482,6 +493,17 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
         solely_true += interior;
         refined += !interior;
         cand_refs += !interior;
+      }
+    } else if (pair_now) {
+      const uint32_t pa = static_cast<uint32_t>(entry >> 33) & 0x7fffffffu, pb = static_cast<uint32_t>(entry >> 2) & 0x7fffffffu;
+      first = (pa >> 1) | kMoreFlag;  // the second pair exists only as this flag (the overflow list is discarded)
+      count_slot<kDense>(ix, jp, hist, pa >> 1);
+      count_slot<kDense>(ix, jp, hist, pb >> 1);
+      if (kStats) {
+        const uint32_t n_cand = 2u - ((pa & 1u) + (pb & 1u));
+        solely_true += n_cand == 0u;
+        refined += n_cand != 0u;
+        cand_refs += n_cand;
       }
     } else {
       first = emit_general<kIds, kDense>(ix, jp, hist, entry, i, plan, ovf_base, task_base);
@@ -556,7 +578,12 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
       idx = (Y >> ix.qc.tier_shift) * tb.pitch + (X >> ix.qc.tier_shift);
       batch_slot = ((Y & ix.qc.sub_mask) << 4) | (X & ix.qc.sub_mask);  // spread into a node slot in population 3
     }
+#ifdef GJ_EXP_NO_TB  // timing experiment: results are wrong (no gather into the 32-bit tier: every lookup misses)
+    batch_code = (lane < take && (item.x & 0x80000000u) == 0u) ? 0u : kQueueSlow;
+    (void)idx;
+#else
     batch_code = ldg32_if(table2 + idx, lane < take && (item.x & 0x80000000u) == 0u, kQueueSlow);
+#endif
     batch_open = true;
   };
 
@@ -1021,6 +1048,8 @@ struct PairsParams {
   uint32_t* count;          // [n] out (count): pairs of the point
   const uint64_t* row_ptr;  // [n + 1] (fill)
   uint32_t* out_id;         // (fill)
+  uint64_t out_cap;         // (fill) ids that fit out_id; a row ending beyond it is not written (kErrOverflowCap)
+  const uint64_t* out_sub;  // (fill) optional: *out_sub is subtracted from the row offsets (chunk-local id buffers)
   unsigned long long* stats;  // [6] or null
   DevStatus* status;
   int32_t exact;
@@ -1112,7 +1141,15 @@ pairs_emit_kernel(const __grid_constant__ DevIndex ix, PairsParams pp) {
         off = static_cast<uint32_t>(entry >> 2) & 0x7fffffffu;
         t = __ldg(ix.lut + off);
       }
-      const uint64_t out = kFill ? pp.row_ptr[i] : 0;
+      uint64_t out = kFill ? pp.row_ptr[i] : 0;
+      if (kFill) {
+        const uint64_t sub = pp.out_sub ? *pp.out_sub : 0;
+        out -= sub;
+        if (pp.row_ptr[i + 1] - sub > pp.out_cap) {  // (row_ptr[i + 1] exists: the scan writes the end offset too)
+          atomicOr(&pp.status->flags, kErrOverflowCap);  // the caller's id array is too small: sizes still come back
+          continue;
+        }
+      }
       uint32_t cand = 0;
       const uint32_t task_base = pp.exact ? pp.task_base[i] : 0u;
       for (uint32_t k = 0; k < n_refs; ++k) {
@@ -1189,10 +1226,14 @@ scan_sums_kernel(uint64_t* __restrict__ block_sums, uint32_t n_blocks, uint64_t*
   if (threadIdx.x == 0) *grand_total = carry;
 }
 
+// out[i] = offset (+ *running when given: a total kept on the device) + exclusive prefix of in[0..i); with
+// `write_end` the element after the last one gets the inclusive total (the n + 1-th row offset).
 __global__ void __launch_bounds__(kScanThreads)
 scan_apply_kernel(const uint32_t* __restrict__ in, uint64_t n, const uint64_t* __restrict__ block_sums,
-                  uint64_t offset, uint64_t* __restrict__ out) {
+                  uint64_t offset, uint64_t* __restrict__ out, const uint64_t* __restrict__ running = nullptr,
+                  bool write_end = false) {
   __shared__ uint64_t s_total;
+  if (running) offset += *running;
   const uint64_t base = static_cast<uint64_t>(blockIdx.x) * kScanTile + threadIdx.x * kScanItems;
   uint32_t item[kScanItems];
   uint64_t v = 0;
@@ -1206,8 +1247,13 @@ scan_apply_kernel(const uint32_t* __restrict__ in, uint64_t n, const uint64_t* _
   for (int k = 0; k < kScanItems; ++k) {
     if (base + k < n) out[base + k] = run;
     run += item[k];
+    if (write_end && base + k + 1 == n) out[n] = run;
   }
 }
+
+// *running += *chunk_total (one thread): the pair count so far, kept on the device so that consecutive chunks of
+// the CSR pipeline need no host round trip.
+__global__ void advance_base_kernel(uint64_t* running, const uint64_t* chunk_total) { *running += *chunk_total; }
 
 // v[i] += offset: a replica's CSR row offsets moved behind the pairs of the ranges before it (gj_group_*)
 __global__ void __launch_bounds__(256)

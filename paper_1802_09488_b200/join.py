@@ -377,6 +377,60 @@ class Session:
         return row_ptr, ids
 
 
+    def join_pairs_into(self, points, mode, row_ptr: np.ndarray, ids: np.ndarray, stats: JoinStats | None = None) -> int:
+        """ONE call, caller-provided arrays (``row_ptr`` u64[n+1], ``ids`` u32[capacity]; pinned
+        memory from ``pinned_array`` is copied to directly): chunk c's rows and ids stream home while
+        chunk c+1 runs.  Returns the pair count; raises ``CapacityError`` (``.needed`` = pair count)
+        when ``ids`` is too small — ``row_ptr`` is complete then."""
+        p = _points(points)
+        assert row_ptr.dtype == np.uint64 and len(row_ptr) >= len(p) + 1 and ids.dtype == np.uint32
+        n_pairs, cs, bad = C.c_uint64(0), capi.Stats(), C.c_uint64(0)
+        rc = capi.lib().gj_join_pairs_host_into(self._h, _vp(p), len(p), mode, _vp(row_ptr), _vp(ids), len(ids),
+                                                C.byref(n_pairs), C.byref(cs) if stats is not None else None,
+                                                C.byref(bad))
+        if rc == capi.GJ_CAPACITY:
+            err = CapacityError(capi.lib().gj_last_error().decode())
+            err.needed = int(n_pairs.value)
+            raise err
+        _check(rc, bad)
+        if stats is not None:
+            stats._add(cs)
+        return int(n_pairs.value)
+
+    def join_pairs_device(self, d_points_ptr: int, n: int, mode, d_row_ptr: int, d_ids_ptr: int, id_capacity: int,
+                          stats: JoinStats | None = None) -> int:
+        """CSR entirely in HBM (raw device pointers: points f64[n, 2] in, row offsets u64[n+1] and
+        polygon ids u32[id_capacity] out).  Synchronous.  Returns the pair count; ``CapacityError``
+        (``.needed``) when the id array is too small."""
+        n_pairs, cs, bad = C.c_uint64(0), capi.Stats(), C.c_uint64(0)
+        rc = capi.lib().gj_join_pairs_device(self._h, C.c_void_p(d_points_ptr), n, mode, C.c_void_p(d_row_ptr),
+                                             C.c_void_p(d_ids_ptr) if d_ids_ptr else None, id_capacity,
+                                             C.byref(n_pairs), C.byref(cs) if stats is not None else None,
+                                             C.byref(bad))
+        if rc == capi.GJ_CAPACITY:
+            err = CapacityError(capi.lib().gj_last_error().decode())
+            err.needed = int(n_pairs.value)
+            raise err
+        _check(rc, bad)
+        if stats is not None:
+            stats._add(cs)
+        return int(n_pairs.value)
+
+
+def pinned_array(n: int, dtype) -> np.ndarray:
+    """A numpy array over pinned host memory (gj_host_alloc): the *_host calls copy to and from it
+    directly, without the stager.  The memory is released when the array is garbage-collected."""
+    import weakref
+    dt = np.dtype(dtype)
+    ptr = capi.lib().gj_host_alloc(max(1, n) * dt.itemsize)
+    if not ptr:
+        raise CudaError(capi.lib().gj_last_error().decode())
+    buf = (C.c_char * (max(1, n) * dt.itemsize)).from_address(ptr)
+    arr = np.frombuffer(buf, dtype=dt, count=n)
+    weakref.finalize(buf, capi.lib().gj_host_free, ptr)
+    return arr
+
+
 class _GroupJoiner(Session):
     """join_count / join_pairs of a Session, routed through the group calls."""
 

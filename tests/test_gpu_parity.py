@@ -701,3 +701,61 @@ def test_flushed_16bit_histogram_matches_reference(name):
             assert int(res[0][0].sum()) >= (n if arr is same else 1)
     b16.close()
     b32.close()
+
+
+@pytest.mark.parametrize("name", ["join_small_exact", "cfg3_tess16_exact_trained", "cfg5_stars_scaled", "empty_index"])
+@pytest.mark.parametrize("chunk", [0, 4096])
+def test_csr_into_caller_arrays_host_and_device(name, chunk):
+    """join_exact / join_approx -> CSR in ONE call: gj_join_pairs_host_into (caller's host arrays, pageable and
+    pinned, streamed chunk by chunk) and gj_join_pairs_device (points, row offsets and ids all in HBM) give the
+    fixture's ordered pairs and stats, with many small chunks as well; an id array that is too small returns the
+    size needed and complete row offsets."""
+    import torch
+    fx = golden_util.load(name)
+    pts = np.ascontiguousarray(fx["points"])
+    n = len(pts)
+    b = join.IndexBundle.load(golden_util.bundle_file(name), device=0,
+                              options=capi.Options(chunk_points=chunk) if chunk else None)
+    s = b.session()
+    for kind, mode in (("exact", capi.GJ_MODE_EXACT), ("approx", capi.GJ_MODE_APPROX)):
+        epi, epid = golden_util.pairs_of(fx, kind)
+        want_rows = np.concatenate([[0], np.cumsum(np.bincount(epi.astype(np.int64), minlength=n))]).astype(np.uint64)
+        want_stats = tuple(int(v) for v in fx[f"{kind}_stats"])
+        for pinned in (False, True):
+            row_ptr = join.pinned_array(n + 1, np.uint64) if pinned else np.empty(n + 1, np.uint64)
+            ids = join.pinned_array(len(epid) + 5, np.uint32) if pinned else np.empty(len(epid) + 5, np.uint32)
+            st = join.JoinStats()
+            total = s.join_pairs_into(pts, mode, row_ptr, ids, st)
+            assert total == len(epid) and np.array_equal(row_ptr, want_rows) and np.array_equal(ids[:total], epid)
+            assert st.as_tuple() == want_stats
+        if len(epid) > 3:  # too small: the size comes back, and the rows
+            row_ptr = np.zeros(n + 1, np.uint64)
+            with pytest.raises(join.CapacityError) as e:
+                s.join_pairs_into(pts, mode, row_ptr, np.empty(len(epid) // 2, np.uint32))
+            assert e.value.needed == len(epid) and np.array_equal(row_ptr, want_rows)
+        # everything in HBM
+        d_pts = torch.from_numpy(pts).cuda() if n else torch.zeros((1, 2), dtype=torch.float64, device="cuda")
+        d_rows = torch.full((n + 1,), -1, dtype=torch.int64, device="cuda")
+        d_ids = torch.full((len(epid) + 7,), -1, dtype=torch.int32, device="cuda")
+        torch.cuda.synchronize()
+        st = join.JoinStats()
+        total = s.join_pairs_device(d_pts.data_ptr(), n, mode, d_rows.data_ptr(), d_ids.data_ptr(), len(d_ids), st)
+        assert total == len(epid) and st.as_tuple() == want_stats
+        assert np.array_equal(d_rows.cpu().numpy().view(np.uint64), want_rows)
+        got = d_ids.cpu().numpy().view(np.uint32)
+        assert np.array_equal(got[:total], epid) and np.all(got[total:] == 0xFFFFFFFF)  # nothing written past the end
+        if len(epid) > 3:
+            with pytest.raises(join.CapacityError) as e:
+                s.join_pairs_device(d_pts.data_ptr(), n, mode, d_rows.data_ptr(), d_ids.data_ptr(), len(epid) - 1)
+            assert e.value.needed == len(epid)
+            with pytest.raises(join.CapacityError) as e:  # sizing call
+                s.join_pairs_device(d_pts.data_ptr(), n, mode, d_rows.data_ptr(), 0, 0)
+            assert e.value.needed == len(epid)
+            assert np.array_equal(d_rows.cpu().numpy().view(np.uint64), want_rows)
+    if n > 10:
+        bad = pts.copy()
+        bad[n // 2, 0] = -90.5
+        with pytest.raises(join.InvalidArgument) as e:
+            s.join_pairs_into(bad, capi.GJ_MODE_EXACT, np.empty(n + 1, np.uint64), np.empty(16, np.uint32))
+        assert e.value.index == n // 2
+    b.close()

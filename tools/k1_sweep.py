@@ -29,6 +29,8 @@ VARIANTS = {
     "ppt6": ["GJ_PPT=6"],
     "exp_phase1_only": ["GJ_EXP_PHASE1_ONLY"],
     "exp_no_phase3": ["GJ_EXP_NO_PHASE3"],
+    "exp_no_arena": ["GJ_EXP_NO_ARENA"],
+    "exp_no_tb": ["GJ_EXP_NO_TB", "GJ_EXP_NO_PHASE3"],
 }
 
 
@@ -40,15 +42,16 @@ def build_all():
         print(f"built {name} in {time.time() - t0:.1f}s")
 
 
-def run_all(n_points: int):
+def run_all(n_points: int, config: int = 2, scale: float = 1.0, opt: dict | None = None, want_ids: bool = True,
+            only=None):
     import numpy as np
     import torch
 
     from paper_1802_09488_b200 import capi, join, synth
     from tools import build_bundles
 
-    path = build_bundles.bundle_file(build_bundles.workload_name(2))
-    pts = synth.uniform_points(n_points, synth.seed_for(2, 2))
+    path = build_bundles.bundle_file(build_bundles.workload_name(config, scale))
+    pts = synth.points_for(config, n_points, None, scale=scale)
     d_pts = torch.from_numpy(pts).cuda()
     results = {}
     ref_counts = None
@@ -61,12 +64,12 @@ def run_all(n_points: int):
     extra = sorted(p.stem[4:] for p in OUT.glob("lib_*.so") if p.stem[4:] not in VARIANTS)  # hand-built A/B libraries
     for name in list(VARIANTS) + extra:
         lib = OUT / f"lib_{name}.so"
-        if not lib.exists():
+        if not lib.exists() or (only and name not in only):
             continue
         capi._LIB = None
         _build.LIB = lib
         capi._build.LIB = lib
-        bundle = join.IndexBundle.load(path, device=0)
+        bundle = join.IndexBundle.load(path, device=0, options=capi.Options(**opt) if opt else None)
         sess = bundle.session()
         d_counts = torch.zeros(len(bundle.ids), dtype=torch.int64, device="cuda")
         d_first = torch.empty(n_points, dtype=torch.int32, device="cuda")
@@ -74,7 +77,7 @@ def run_all(n_points: int):
 
         def step():
             sess.join_count_device(d_pts.data_ptr(), n_points, d_counts.data_ptr(), capi.GJ_MODE_APPROX,
-                                   d_first_id_ptr=d_first.data_ptr())
+                                   d_first_id_ptr=d_first.data_ptr() if want_ids else 0)
         truth = np.zeros(len(bundle.ids), np.int64)
         for k, v in truth_map.items():
             truth[np.searchsorted(bundle.ids, k)] = v
@@ -113,11 +116,23 @@ def run_all(n_points: int):
         sess.close()
         bundle.close()
     (ROOT / "gpurun_out").mkdir(exist_ok=True)
-    (ROOT / "gpurun_out" / "k1_sweep.json").write_text(json.dumps(results, indent=1))
+    tag = f"cfg{config}" + ("" if want_ids else "_noids")
+    (ROOT / "gpurun_out" / f"k1_sweep_{tag}.json").write_text(json.dumps(results, indent=1))
 
 
 if __name__ == "__main__":
     if sys.argv[1] == "build":
         build_all()
     else:
-        run_all(int(sys.argv[2]) if len(sys.argv) > 2 else 100_000_000)
+        import argparse
+        ap = argparse.ArgumentParser()
+        ap.add_argument("cmd")
+        ap.add_argument("points", nargs="?", type=int, default=100_000_000)
+        ap.add_argument("--config", type=int, default=2)
+        ap.add_argument("--scale", type=float, default=1.0)
+        ap.add_argument("--opt", default="", help="comma-separated gj_options fields")
+        ap.add_argument("--no-ids", action="store_true")
+        ap.add_argument("--only", default="", help="comma-separated variant names")
+        a = ap.parse_args()
+        run_all(a.points, a.config, a.scale, {k: int(v) for k, v in (kv.split("=") for kv in a.opt.split(",") if kv)},
+                not a.no_ids, set(a.only.split(",")) if a.only else None)
