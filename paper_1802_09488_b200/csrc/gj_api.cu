@@ -131,10 +131,10 @@ int allow_max_smem(const gj_index& ix, Kernel kernel) {
   return GJ_OK;
 }
 
-template <bool kIds, bool kStats, bool kDense, bool kLate = false>
-int launch_join_variant(gj_session* s, const JoinParams& jp, const SmemPlan& sp) {
+template <bool kIds, bool kStats, bool kDense, bool kLate, bool kPipe3>
+int launch_join_kernel(gj_session* s, const JoinParams& jp, const SmemPlan& sp) {
   const gj_index& ix = *s->ix;
-  auto kernel = join_kernel<kIds, kStats, kDense, kLate>;
+  auto kernel = join_kernel<kIds, kStats, kDense, kLate, kPipe3>;
   int rc = allow_max_smem(ix, kernel);
   if (rc != GJ_OK) return rc;
   int occ = 0;
@@ -151,6 +151,17 @@ int launch_join_variant(gj_session* s, const JoinParams& jp, const SmemPlan& sp)
   ++s->launches;
   GJ_CUDA(cudaGetLastError());
   return GJ_OK;
+}
+
+// Trees without palette nodes (arenas beyond L2) run the instantiation that pipelines population 3's arena reads —
+// except with JoinStats: there the batch in flight pushes two instantiations into keeping thread-local copies of
+// the parameter blocks (680-byte stack frames; measured 9.7 instead of 1.3 ms per 100 M points).
+template <bool kIds, bool kStats, bool kDense, bool kLate = false>
+int launch_join_variant(gj_session* s, const JoinParams& jp, const SmemPlan& sp) {
+  if (!kStats && s->ix->dev.node_pal == nullptr && s->ix->info.node_count != 0 && s->ix->opt.pipe3 != 0) {
+    return launch_join_kernel<kIds, false, kDense, kLate, true>(s, jp, sp);
+  }
+  return launch_join_kernel<kIds, kStats, kDense, kLate, false>(s, jp, sp);
 }
 
 int reset_status(gj_session* s, DevStatus* d_status) {

@@ -477,6 +477,7 @@ gj_options default_options() {
   o.ids_late = -1;
   o.hist_rep_cap = -1;
   o.hist16 = -1;
+  o.pipe3 = -1;
   return o;
 }
 

@@ -327,7 +327,10 @@ __device__ __noinline__ uint32_t emit_general(const DevIndex& ix, const JoinPara
 // that skips the shared-memory tier and Q2 and has every lane gather the 32-bit tier codes of its own four points —
 // bit-exact, but 1.25 instead of 1.00 ms per 100 M points on the config-4 stand-in: the gathers' L2 latency is
 // exposed in every tile, where the queued batch is issued one tile ahead of its use.)
-template <bool kIds, bool kStats, bool kDense, bool kLate = false>
+// kPipe3 (trees without palette nodes, i.e. arenas beyond L2): population 3's arena reads are software-pipelined
+// across batches (drain3); a compile-time choice because the batch in flight costs six registers the other
+// instantiations — the headline one among them — would otherwise spill.
+template <bool kIds, bool kStats, bool kDense, bool kLate = false, bool kPipe3 = false>
 __global__ void __launch_bounds__(kJoinThreads, GJ_JOIN_MIN_BLOCKS)
 join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinParams jp) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -409,7 +412,23 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
   // under a link: its low 32 bits in `c`, the bits above them (arenas of 2^24
   // nodes = 32 GB and more) between the point index and bit 31 of `iw`.  All
   // 32 lanes go through it together because the record reservations are per warp.
-  auto resolve_open = [&](bool mine, uint32_t iw, uint32_t c) {
+  // The arena slot a flagged queue item names (see above).
+  auto queued_slot = [&](uint32_t iw, uint32_t c) -> uint64_t {
+    const uint32_t slot = (spread4((c >> 4) & 0xFu) << 1) | spread4(c & 0xFu);  // chunk_slot
+    return (static_cast<uint64_t>((iw & 0x7FFFFFFFu) >> ix.qc.index_bits) << 32) | (static_cast<uint64_t>(c) & ~0xFFull) | slot;
+  };
+  // Stage 1 of a batch, for trees without palette nodes (large arenas: every slot read is a DRAM burst): only
+  // ISSUES the arena read of a flagged item.  The value is first touched in resolve_open, which drain3 runs one
+  // batch later, so the DRAM latency hides behind the emit work of the batch before.
+  auto fetch_open = [&](bool mine, uint32_t iw, uint32_t c) -> uint64_t {
+    uint64_t v = 0;
+    const bool slow = c == kQueueSlow && (iw & ix.qc.slow_mark) == ix.qc.slow_mark;
+    if (mine && (iw & 0x80000000u) != 0u && !slow) {
+      asm volatile("ld.global.nc.u64 %0, [%1];" : "=l"(v) : "l"(ix.arena + queued_slot(iw, c)));
+    }
+    return v;
+  };
+  auto resolve_open = [&](bool mine, uint32_t iw, uint32_t c, bool fetched, uint64_t fetched_entry) {
     const uint32_t q_index_bits = ix.qc.index_bits, q_slow_mark = ix.qc.slow_mark;
     const uint32_t i = iw & ((1u << q_index_bits) - 1u);
     const bool flagged = (iw & 0x80000000u) != 0u;
@@ -430,11 +449,11 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
         int level = walk_level;
         bool walk = true;
         if (flagged) {  // the word is (node - 1) * 256 + (y sub-cell bits << 4 | x sub-cell bits)
-          const uint32_t slot = (spread4((c >> 4) & 0xFu) << 1) | spread4(c & 0xFu);  // chunk_slot
-          const uint64_t at = (static_cast<uint64_t>((iw & 0x7FFFFFFFu) >> q_index_bits) << 32) |
-                              (static_cast<uint64_t>(c) & ~0xFFull) | slot;
-          bool from_arena = true;
-          if (ix.node_pal) {  // the node's 128-byte palette form, usually an L2 hit
+          const uint64_t at = queued_slot(iw, c);
+          const uint32_t slot = static_cast<uint32_t>(at) & 0xFFu;
+          bool from_arena = !fetched;
+          entry = fetched_entry;
+          if (!fetched && ix.node_pal) {  // the node's 128-byte palette form, usually an L2 hit
             const uint64_t* rec = ix.node_pal + (at >> 8) * 16u;
             const uint32_t codes = __ldg(reinterpret_cast<const uint32_t*>(rec + 4) + (slot >> 4));
             const uint64_t v = __ldg(rec + ((codes >> ((slot & 15u) * 2u)) & 3u));
@@ -523,6 +542,12 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
     return count + __popc(mask);
   };
 
+  // Q3 items 32 at a time.  Without palette nodes the batch is software-pipelined like population 2's: its arena
+  // reads are issued when it is taken off the queue and it is resolved when the NEXT batch is taken (or at the
+  // final flush), so a warp always has one batch of DRAM reads in flight behind the emit work of another.
+  bool open_pending = false;  // warp-uniform
+  uint32_t open_take = 0, open_iw = 0, open_c = 0;
+  uint64_t open_entry = 0;
   auto drain3 = [&](bool flush) {
     __syncwarp();
     while (q3_count >= 32u || (flush && q3_count)) {
@@ -530,7 +555,21 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
       q3_count -= take;
       const uint2 item = lds64(s_q3 + (q3_count + min(lane, take - 1u)) * 8u);
       __syncwarp();
-      resolve_open(lane < take, item.x, item.y);
+      if (!kPipe3) {
+        resolve_open(lane < take, item.x, item.y, false, 0);
+        continue;
+      }
+      const uint64_t v = fetch_open(lane < take, item.x, item.y);
+      if (open_pending) resolve_open(lane < open_take, open_iw, open_c, true, open_entry);
+      open_pending = true;
+      open_take = take;
+      open_iw = item.x;
+      open_c = item.y;
+      open_entry = v;
+    }
+    if (kPipe3 && flush && open_pending) {
+      open_pending = false;
+      resolve_open(lane < open_take, open_iw, open_c, true, open_entry);
     }
   };
 

@@ -301,7 +301,7 @@ def main():
     ap.add_argument("--load-index", default="", help="load the index from this GJX1 file when it exists")
     ap.add_argument("--variants", default="",
                     help="extra timings that attribute the time: ';'-separated index variants, each a comma-separated "
-                         "list of gj_options fields, e.g. 'hist16=0;bin_open=0;hist16=0,bin_open=0;tier_sub=1'")
+                         "list of gj_options fields, e.g. 'hist16=0;node_pal_max_mb=4096;tier_sub=1'")
     ap.add_argument("--out", default="")
     a = ap.parse_args()
     r = run(a.config, a.scale, a.points, a.launch, a.check, a.reps, a.threads, not a.no_ids, not a.no_stats,
