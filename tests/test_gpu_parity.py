@@ -14,6 +14,7 @@ JOIN_FIXTURES = [
     "join_small_exact", "join_small_approx", "acceptance_exact20", "cfg1_tess5_approx60m",
     "cfg2_tess16_approx4m", "cfg3_tess16_exact_trained", "cfg4_tess36_approx1m_k56",
     "cfg5_stars_scaled", "kmax60_sparse_ids", "world_stars", "empty_index",
+    "kmax60_tiny_a", "kmax60_tiny_b",  # k_max 60 under a 48-bit prefix: the last node step ends below the leaf level
 ]
 
 _cache = {}

@@ -13,7 +13,7 @@ from tests import golden_util
 JOIN_FIXTURES = [
     "join_small_exact", "acceptance_exact20", "cfg1_tess5_approx60m", "cfg2_tess16_approx4m",
     "cfg3_tess16_exact_trained", "cfg4_tess36_approx1m_k56", "cfg5_stars_scaled", "kmax60_sparse_ids",
-    "world_stars", "empty_index",
+    "world_stars", "empty_index", "kmax60_tiny_a", "kmax60_tiny_b",
 ]
 
 
