@@ -276,11 +276,30 @@ __device__ __noinline__ uint32_t emit_general(const DevIndex& ix, const JoinPara
   if (e.tag == 3u) {  // record [t, true ids, c, candidate ids]: two plain loops (overlapping polygon sets live here)
     const uint32_t* true_ids = ix.lut + e.off + 1;
     const uint32_t* cand_ids = ix.lut + e.off + 2;  // indexed by k as well
-    for (uint32_t k = 0; k < e.t; ++k) emit_pair(__ldg(true_ids + k), k);
+    // four independent loads in flight per step: a lane walks its own record, so consecutive words share a sector
+    // but each word is its own load, and one load's latency per reference adds up over ~17 references
+    uint32_t k = 0;
+    for (; k + 4u <= e.t; k += 4u) {
+      const uint32_t a = __ldg(true_ids + k), b = __ldg(true_ids + k + 1u), c = __ldg(true_ids + k + 2u),
+                     d = __ldg(true_ids + k + 3u);
+      emit_pair(a, k);
+      emit_pair(b, k + 1u);
+      emit_pair(c, k + 2u);
+      emit_pair(d, k + 3u);
+    }
+    for (; k < e.t; ++k) emit_pair(__ldg(true_ids + k), k);
     if (exact) {
-      for (uint32_t k = e.t; k < e.n_refs; ++k) emit_task(__ldg(cand_ids + k), k);
+      for (; k < e.n_refs; ++k) emit_task(__ldg(cand_ids + k), k);
     } else {
-      for (uint32_t k = e.t; k < e.n_refs; ++k) emit_pair(__ldg(cand_ids + k), k);
+      for (; k + 4u <= e.n_refs; k += 4u) {
+        const uint32_t a = __ldg(cand_ids + k), b = __ldg(cand_ids + k + 1u), c = __ldg(cand_ids + k + 2u),
+                       d = __ldg(cand_ids + k + 3u);
+        emit_pair(a, k);
+        emit_pair(b, k + 1u);
+        emit_pair(c, k + 2u);
+        emit_pair(d, k + 3u);
+      }
+      for (; k < e.n_refs; ++k) emit_pair(__ldg(cand_ids + k), k);
     }
   } else {
     for (uint32_t k = 0; k < e.n_refs; ++k) {
