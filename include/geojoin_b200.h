@@ -127,8 +127,9 @@ typedef struct {
   int32_t debug_plan;           /* 1 = print the join kernel's shared-memory plan to stderr */
   int32_t hist16;               /* id tables beyond the 32-bit shared histogram count in a 16-bit one with
                                    periodic flushes: -1 = automatic, 0 = never, 1 = also when the 32-bit one fits */
-  int32_t pipe3;                /* trees without palette nodes pipeline population 3's arena reads across batches:
-                                   -1 = automatic (on), 0 = off */
+  int32_t reserved0;            /* keep 0 */
+  int32_t stage_lut;            /* lookup-table records of a population-3 batch staged in shared memory by the whole
+                                   warp: -1 = automatic (tables of 256 MB and more), 0 = never, 1 = always */
   uint64_t max_launch_points;   /* test hook: split device-resident calls into launches of this many points; 0 = none */
   uint64_t chunk_points;        /* host pipeline: points per chunk; 0 = default (3 M counts / 4 M pairs), min 4096 */
 } gj_options;

@@ -38,6 +38,8 @@ size_t align16(size_t v) { return (v + 15) & ~size_t{15}; }
 struct SmemPlan {
   uint32_t queue_off, hist_off, hist_rep;
   uint32_t hist16;  // 1 = one 16-bit histogram instead (hist_rep == 0)
+  uint32_t stage_off;  // per-warp staging buffers for lookup-table records, 0 = none
+  uint32_t stage_chunks;  // 16-byte chunks per warp
   size_t total;
 };
 
@@ -51,6 +53,16 @@ bool k1_uses_hist16(size_t n_ids, const gj_options& opt) {
   const size_t row16 = (n_ids + 2) / 2 * 4;
   if (row16 > kHist16MaxRow) return false;
   return opt.hist16 > 0 || (n_ids + 1) * 4 > kHist32MaxRow;  // forced, or the 32-bit form does not fit
+}
+
+// Lookup-table-heavy indexes (overlapping polygon sets: every probe ends in a record of many references) stage the
+// records of a population-3 batch in shared memory; the first tier then only has to catch the points outside every
+// polygon, so it makes room.
+// Only tables far beyond L2 (256 MB and more): there a lane's word-by-word walk pays an L2 / DRAM round trip per
+// sector (full-size BASELINE config 5, 1.3 GB table: 5.56 -> 4.71 ms per 20 M points with staging); a table that
+// sits in L2 is walked faster than it is staged (config-5 stand-in, 30 MB: 2.42 vs 2.96 ms — instruction-bound).
+bool k1_stages_records(uint64_t lut_len, const gj_options& opt) {
+  return opt.stage_lut > 0 || (opt.stage_lut < 0 && lut_len >= (1ull << 26));
 }
 
 size_t k1_smem_besides_tier(size_t n_ids, const gj_options& opt) {
@@ -107,12 +119,23 @@ SmemPlan plan_smem(const gj_index& ix) {
   }
   p.hist_rep = rep;
   at += one * rep;
+  if (ix.stage_records) {  // lookup-table-heavy index: what is left goes to the warp-cooperative record staging (join_kernel)
+    const size_t warps = kJoinThreads / 32;
+    const size_t room = limit > align16(at) ? (limit - align16(at)) / (warps * 16) : 0;
+    const uint32_t chunks = static_cast<uint32_t>(std::min<size_t>(room, kStageChunksMax));
+    if (chunks >= kStageChunksMin) {
+      p.stage_off = static_cast<uint32_t>(align16(at));
+      p.stage_chunks = chunks;
+      at = p.stage_off + warps * chunks * 16;
+    }
+  }
   if (ix.opt.smem_pad > 0 && at + static_cast<size_t>(ix.opt.smem_pad) <= limit) at += static_cast<size_t>(ix.opt.smem_pad);  // L1 carve-out experiments
   p.total = at;
   if (ix.opt.debug_plan) {
     std::fprintf(stderr, "[gj] K1 smem: 16-bit tier level %d, %zu B; queues at %u; histogram at %u x%u%s; total %zu; palette nodes %s\n",
                  30 - ix.dev.dir16.shift, table_bytes, p.queue_off, p.hist_off, p.hist_rep, p.hist16 ? " (16-bit, flushed)" : "",
                  p.total, ix.dev.node_pal ? "yes" : "no");
+    std::fprintf(stderr, "[gj] K1 smem: record staging %u chunks per warp\n", p.stage_chunks);
     const DevDirectory& tb = ix.dev.dirk.n_table ? ix.dev.dirk : (ix.dev.dir2.n_table ? ix.dev.dir2 : ix.dev.dir);
     std::fprintf(stderr, "[gj] K1 32-bit tier: level %d%s, %u x %u cells (%.1f MB); queue coding %s, tier_shift %u, index bits %u\n",
                  30 - tb.shift, ix.dev.dirk.n_table ? " (refined)" : "", tb.width, tb.height, tb.n_table * 4e-6,
@@ -127,14 +150,17 @@ SmemPlan plan_smem(const gj_index& ix) {
 // sized indexes.  (The L1 carve-out follows the launch's actual size.)
 template <typename Kernel>
 int allow_max_smem(const gj_index& ix, Kernel kernel) {
-  GJ_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(ix.smem_optin)));
+  cudaFuncAttributes attr{};
+  GJ_CUDA(cudaFuncGetAttributes(&attr, kernel));  // static shared memory (K1's EmitCtx) counts against the same limit
+  GJ_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               static_cast<int>(ix.smem_optin - attr.sharedSizeBytes)));
   return GJ_OK;
 }
 
-template <bool kIds, bool kStats, bool kDense, bool kLate, bool kPipe3>
+template <bool kIds, bool kStats, bool kDense, bool kLate, bool kStage>
 int launch_join_kernel(gj_session* s, const JoinParams& jp, const SmemPlan& sp) {
   const gj_index& ix = *s->ix;
-  auto kernel = join_kernel<kIds, kStats, kDense, kLate, kPipe3>;
+  auto kernel = join_kernel<kIds, kStats, kDense, kLate, kStage>;
   int rc = allow_max_smem(ix, kernel);
   if (rc != GJ_OK) return rc;
   int occ = 0;
@@ -153,14 +179,15 @@ int launch_join_kernel(gj_session* s, const JoinParams& jp, const SmemPlan& sp) 
   return GJ_OK;
 }
 
-// Trees without palette nodes (arenas beyond L2) run the instantiation that pipelines population 3's arena reads —
-// except with JoinStats: there the batch in flight pushes two instantiations into keeping thread-local copies of
-// the parameter blocks (680-byte stack frames; measured 9.7 instead of 1.3 ms per 100 M points).
+// Lookup-table-heavy indexes (the launch plan found room for the staging buffers) run the kStage instantiations.
 template <bool kIds, bool kStats, bool kDense, bool kLate = false>
 int launch_join_variant(gj_session* s, const JoinParams& jp, const SmemPlan& sp) {
-  if (!kStats && s->ix->dev.node_pal == nullptr && s->ix->info.node_count != 0 && s->ix->opt.pipe3 != 0) {
-    return launch_join_kernel<kIds, false, kDense, kLate, true>(s, jp, sp);
-  }
+  // One kStage instantiation is left out: <ids, no stats, general counting, early ids> — nvcc 12.9 gives it a
+  // 704-byte stack frame (a thread-local copy of the parameter blocks), and a frame like that cost 7x in another
+  // instantiation before the general emit path stopped taking the blocks by reference.  Check `ptxas -v` (python -m
+  // paper_1802_09488_b200._build --force -v) when touching the kernel.
+  constexpr bool kStageOk = !(kIds && !kStats && !kDense && !kLate);
+  if (kStageOk && sp.stage_off != 0) return launch_join_kernel<kIds, kStats, kDense, kLate, kStageOk>(s, jp, sp);
   return launch_join_kernel<kIds, kStats, kDense, kLate, false>(s, jp, sp);
 }
 
@@ -230,6 +257,8 @@ int enqueue_join(gj_session* s, const JoinRequest& rq) {
   jp.smem_hist_off = sp.hist_off;
   jp.hist_rep = sp.hist_rep;
   jp.hist16 = sp.hist16;
+  jp.smem_stage_off = sp.stage_off;
+  jp.stage_chunks = sp.stage_chunks;
   // No room for the histogram in shared memory: count into per-SM copies (at most 1 GB of them)
   const size_t priv_bytes = static_cast<size_t>(ix.sm_count) * n_ids * 4;
   const bool k2_local = static_cast<size_t>(n_ids) * 4 <= (32u << 10);

@@ -308,13 +308,11 @@ __device__ __forceinline__ uint64_t probe_point(const DevIndex& ix, const uint32
 // Generic probe of a raw cell id on any face without the directory: the
 // scalar walk of act.cpp:248-270 (used by gj_probe_cells_host, the
 // ProbeBatchFn-shaped test hook).
-__device__ __forceinline__ uint64_t probe_raw(const DevIndex& ix, uint64_t raw) {
-  const uint32_t face = static_cast<uint32_t>(raw >> 61);
-  uint64_t node = ix.roots[face];  // faces 6,7 hold a zero root
+__device__ __forceinline__ uint64_t probe_from_root(const DevIndex& ix, uint64_t raw, uint64_t node, uint32_t plen,
+                                                    uint64_t prefix) {
   if (node == 0) return 0;
   const uint64_t key = (raw ^ (raw & (~raw + 1))) << 3;  // key_of, act.hpp:142-145
-  const uint32_t plen = ix.prefix_bits[face];
-  if (plen != 0 && (key >> (64 - plen)) != ix.prefixes[face]) return 0;
+  if (plen != 0 && (key >> (64 - plen)) != prefix) return 0;
   int shift = 56 - static_cast<int>(plen);
   for (;;) {
     // past the last key bit the reference's lockstep kernels would read
@@ -325,6 +323,18 @@ __device__ __forceinline__ uint64_t probe_raw(const DevIndex& ix, uint64_t raw) 
     node = e >> 2;
     shift -= 8;
   }
+}
+
+__device__ __forceinline__ uint64_t probe_raw(const DevIndex& ix, uint64_t raw) {
+  const uint32_t face = static_cast<uint32_t>(raw >> 61);  // faces 6,7 hold a zero root
+  return probe_from_root(ix, raw, ix.roots[face], ix.prefix_bits[face], ix.prefixes[face]);
+}
+
+// The same for a cell id made by cell_from_point, which never sets face bits (cell_id.cpp:89-94).  K1's slow path
+// uses this form: indexing the face tables of the kernel parameter block with a run-time face made ptxas keep a
+// thread-local copy of the whole block in some instantiations.
+__device__ __forceinline__ uint64_t probe_raw_face0(const DevIndex& ix, uint64_t raw) {
+  return probe_from_root(ix, raw, ix.roots[0], ix.prefix_bits[0], ix.prefixes[0]);
 }
 
 // ---------------------------------------------------------------------------

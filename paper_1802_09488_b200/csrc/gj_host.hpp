@@ -27,6 +27,7 @@ size_t k1_smem_besides_tier(size_t n_ids, const gj_options& opt);
 // Id tables beyond the 32-bit shared-memory histogram (64 KB) count in a 16-bit one that the CTA flushes every
 // kHist16FlushTiles tiles — no counter can overflow in between (join_kernel) — when it fits and the options allow it.
 bool k1_uses_hist16(size_t n_ids, const gj_options& opt);
+bool k1_stages_records(uint64_t lut_len, const gj_options& opt);
 
 #define GJ_CUDA(call)                                  \
   do {                                                 \
@@ -245,6 +246,7 @@ struct gj_index {
       d_strip_meta, d_strip_ptr, d_strip_edges;
   int sm_count = 0;
   size_t smem_optin = 0;
+  bool stage_records = false;  // K1 stages the lookup-table records of a population-3 batch in shared memory (lookup-table-heavy indexes)
   bool ids_late = false;       // K1 writes first ids where a point is settled (join_kernel's kLate): the 16-bit tier resolves few cells
   uint64_t max_refs = 0;       // most references behind one reachable entry
   uint64_t max_cand_refs = 0;  // most candidate references behind one entry

@@ -477,7 +477,7 @@ gj_options default_options() {
   o.ids_late = -1;
   o.hist_rep_cap = -1;
   o.hist16 = -1;
-  o.pipe3 = -1;
+  o.stage_lut = -1;
   return o;
 }
 
@@ -618,6 +618,8 @@ int create_index(const gj_index_desc& d, int device, const gj_options* options, 
     // resolves little anyway — everything stays inside the 164 KB step and leaves L1 its 92 KB)
     const size_t step = ((k1_uses_hist16(n_ids, opt) ? 164u : 196u) - 1u) << 10;
     uint64_t max16 = std::min<uint64_t>(kMaxDir16Entries, step > besides ? (step - besides) / 2 : 0);
+    ix->stage_records = k1_stages_records(d.lut_len, opt);
+    if (ix->stage_records) max16 = std::min<uint64_t>(max16, 5120);  // 10 KB: the rest of shared memory stages records
     if (opt.dir16_max_entries > 0) max16 = std::min<uint64_t>(static_cast<uint64_t>(opt.dir16_max_entries), 110000);  // explicit knob
     // explicit knob: a density-matched stand-in over a small box can emulate the full-size tier
     const int max_level = opt.dir16_level_max > 0 ? std::min(30, static_cast<int>(opt.dir16_level_max)) : 30;
@@ -832,6 +834,7 @@ int replicate_index(const gj_index& src, int device, gj_index** out) {
   ix->opt = src.opt;
   ix->ids = src.ids;
   ix->ids_late = src.ids_late;
+  ix->stage_records = src.stage_records;
   ix->max_refs = src.max_refs;
   ix->max_cand_refs = src.max_cand_refs;
   for (DeviceBuffer gj_index::*m : src.buffers()) {

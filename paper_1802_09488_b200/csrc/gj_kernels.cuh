@@ -48,6 +48,12 @@ constexpr int kRefineThreads = 256;
 // batches carried over (< 32 warps * (kQueue2Cap + kQueue3Cap + 32) = 8192), and a point adds at most 1 to any
 // one polygon: 12 * 4096 + 8192 = 57344 < 65536, so no counter can overflow.
 constexpr uint32_t kHist16FlushTiles = 12;
+// Lookup-table records of one population-3 batch staged in shared memory by the whole warp (stage_records):
+// up to this many 16-byte chunks per warp (the launch plan gives what shared memory has left, JoinParams::
+// stage_chunks).  A batch of 32 records of ~20 words takes ~190 chunks; a batch that needs more than the buffer
+// holds is walked from global memory as before.
+constexpr uint32_t kStageChunksMax = 256;
+constexpr uint32_t kStageChunksMin = 128;
 
 struct JoinParams {
   const double2* pts;  // (lat, lng) pairs: .x = lat, .y = lng  (latlng.hpp:26-29)
@@ -70,6 +76,8 @@ struct JoinParams {
   uint32_t smem_hist_off;   // bytes
   uint32_t hist_rep;        // replicas per slot (power of two), 0 = not in shared memory
   uint32_t hist16;          // hist_rep == 0: one 16-bit histogram in shared memory, flushed every kHist16FlushTiles tiles
+  uint32_t smem_stage_off;  // bytes: per-warp staging buffers for lookup-table records (stage_chunks * 16 each); 0 = none
+  uint32_t stage_chunks;
   uint32_t* counts_priv;    // hist_rep == 0: [n_priv][n_ids] u32 copies, zero on entry; may be null
   uint32_t n_priv;          // CTA b counts into copy b % n_priv
   int32_t exact;
@@ -127,6 +135,9 @@ __device__ __forceinline__ void red_inc_shared_if(uint32_t addr, bool pred) {
                "r"(static_cast<uint32_t>(pred))
                : "memory");
 }
+// One random 4-byte gather (the 32-bit tier), read-only path, allocating in L1: `L1::no_allocate` here — on the
+// argument that 4 bytes of a line are used — took config 2 from 0.355 to 0.472 ms per 100 M points (the tier is
+// small enough for L1 to catch a good share of the gathers) and gained 1.4 % on full-size config 5.
 __device__ __forceinline__ uint32_t ldg32_if(const uint32_t* p, bool pred, uint32_t otherwise) {
   uint32_t v;
   asm volatile("{ .reg .pred p; setp.ne.u32 p, %3, 0; mov.u32 %0, %2; @p ld.global.nc.u32 %0, [%1]; }"
@@ -166,6 +177,55 @@ __device__ __forceinline__ void count_slot(const DevIndex& ix, const JoinParams&
     atomicAdd(h.priv + slot, 1u);
   } else {
     atomicAdd(&jp.counts[slot], 1ull);
+  }
+}
+
+// What the out-of-line general emit path (emit_general) needs of the two kernel parameter blocks, copied once per
+// CTA into shared memory.  Passing the __grid_constant__ blocks themselves by reference into a __noinline__
+// function made ptxas keep thread-local copies of both (a ~690-byte stack frame) in whichever instantiation was
+// short of registers — measured 9.7 instead of 1.3 ms per 100 M points in one of them.
+struct EmitCtx {
+  const uint32_t* lut;
+  const uint32_t* ids;
+  const uint32_t* ring_len;
+  unsigned long long* counts;
+  DevStatus* status;
+  uint64_t* ovf_point;
+  uint32_t* ovf_id;
+  uint32_t* ovf_ord;
+  uint32_t* task_point;
+  uint32_t* task_slot;
+  uint32_t* task_ord;
+  uint64_t base_index, ovf_cap, task_cap;
+  uint32_t n_ids;
+  int32_t ids_dense, exact, ovf_discard;
+};
+
+__device__ __forceinline__ uint32_t id_to_slot(const EmitCtx& c, uint32_t id) {
+  if (c.ids_dense) return id;
+  uint32_t lo = 0, hi = c.n_ids;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (__ldg(c.ids + mid) < id) {
+      lo = mid + 1;
+    } else {
+      hi = mid;
+    }
+  }
+  return lo;
+}
+
+template <bool kDense>
+__device__ __forceinline__ void count_slot(const EmitCtx& c, const HistRef& h, uint32_t id) {
+  const uint32_t slot = kDense ? id : id_to_slot(c, id);
+  if (h.rep) {
+    red_inc_shared_if(h.smem + (slot * h.rep + h.lane_rep) * 4u, true);
+  } else if (h.h16) {
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(h.smem + (slot >> 1) * 4u), "r"(1u << ((slot & 1u) * 16u)) : "memory");
+  } else if (h.priv) {
+    atomicAdd(h.priv + slot, 1u);
+  } else {
+    atomicAdd(&c.counts[slot], 1ull);
   }
 }
 
@@ -223,14 +283,69 @@ __device__ __forceinline__ unsigned long long warp_reserve(unsigned long long* c
   return base + (incl - want);
 }
 
+// Warp-cooperative copy of the lookup-table records of one batch into shared memory.  Lane l holds a record that
+// spans the aligned 16-byte chunks [first_chunk, first_chunk + n_chunks) of the table (n_chunks == 0: none).  The
+// chunks of all lanes are flattened — chunk g belongs to the first lane whose inclusive prefix of n_chunks exceeds
+// g — so every load instruction reads 32 consecutive chunks of a few records (coalesced, each sector fetched once,
+// independent of L1) and the loads of a step are all issued before the first store: a per-lane walk costs one
+// round trip per word (per four words at best), this costs two or three per batch.  Returns the chunk index at
+// which this lane's record starts in the staging buffer, or ~0u when the batch does not fit (nothing is copied).
+__device__ __noinline__ uint32_t stage_records(const uint4* __restrict__ lut4, uint32_t s_stage, uint32_t capacity,
+                                               uint32_t lane, uint32_t first_chunk, uint32_t n_chunks) {
+  uint32_t incl = n_chunks;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t up = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= static_cast<uint32_t>(o)) incl += up;
+  }
+  const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+  if (total == 0u || total > capacity) return ~0u;
+  const uint32_t excl = incl - n_chunks;
+  __syncwarp();  // every lane is done with the records of the batch before
+  for (uint32_t g0 = 0; g0 < total; g0 += 96u) {
+    uint4 v[3];
+#pragma unroll
+    for (int u = 0; u < 3; ++u) {
+      const uint32_t g = g0 + static_cast<uint32_t>(u) * 32u + lane;
+      uint32_t owner = 0;  // number of lanes with incl <= g
+#pragma unroll
+      for (int step = 16; step >= 1; step >>= 1) {
+        const uint32_t at = __shfl_sync(0xffffffffu, incl, min(owner + step - 1u, 31u));
+        if (at <= g) owner += step;
+      }
+      const uint32_t src = min(owner, 31u);
+      const uint32_t fc = __shfl_sync(0xffffffffu, first_chunk, src), ex = __shfl_sync(0xffffffffu, excl, src);
+      v[u] = make_uint4(0, 0, 0, 0);
+      if (g < total) {
+        asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(v[u].x), "=r"(v[u].y), "=r"(v[u].z), "=r"(v[u].w)
+                     : "l"(lut4 + fc + (g - ex)));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 3; ++u) {
+      const uint32_t g = g0 + static_cast<uint32_t>(u) * 32u + lane;
+      if (g < total) {
+        asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(s_stage + g * 16u), "r"(v[u].x), "r"(v[u].y),
+                     "r"(v[u].z), "r"(v[u].w)
+                     : "memory");
+      }
+    }
+  }
+  __syncwarp();
+  return excl;
+}
+
 // The per-(point, entry) body of run_join (join.cpp:93-127) for everything
 // the straight-line path does not take: two payloads, lookup-table records,
 // exact-mode candidates (tasks for K2) and the overflow list.  Cold and out
 // of line.  Returns the first-id word of the point.
 template <bool kIds, bool kDense>
-__device__ __noinline__ uint32_t emit_general(const DevIndex& ix, const JoinParams& jp, HistRef h, uint64_t entry,
-                                              uint32_t local, EntryPlan e, unsigned long long ovf_base,
-                                              unsigned long long task_base) {
+__device__ __noinline__ uint32_t emit_general(const EmitCtx* ctx, HistRef h, uint64_t entry, uint32_t local,
+                                              EntryPlan e, unsigned long long ovf_base,
+                                              unsigned long long task_base, uint32_t staged_at) {
+  const EmitCtx& jp = *ctx;  // (in shared memory)
+  const EmitCtx& ix = *ctx;
   const bool exact = jp.exact != 0;
   const uint32_t n_now = exact ? e.n_refs - e.n_cand : e.n_refs;
   uint32_t n_ovf = e.n_ovf;
@@ -245,7 +360,7 @@ __device__ __noinline__ uint32_t emit_general(const DevIndex& ix, const JoinPara
   uint32_t emitted = 0, tasks = 0;
   // the k-th reference emits a pair now (a true hit, or any reference in approximate mode) ...
   auto emit_pair = [&](uint32_t id, uint32_t k) {
-    count_slot<kDense>(ix, jp, h, id);
+    count_slot<kDense>(jp, h, id);
     if (kIds) {
       if (!e.defer && emitted == 0) {
         first = id | (n_now > 1 ? kMoreFlag : 0u);
@@ -274,6 +389,16 @@ __device__ __noinline__ uint32_t emit_general(const DevIndex& ix, const JoinPara
   };
   // references in the reference's emit order (act.hpp:169-196)
   if (e.tag == 3u) {  // record [t, true ids, c, candidate ids]: two plain loops (overlapping polygon sets live here)
+    if (staged_at) {  // the record is in shared memory (stage_records): word 0 = t, 1 + k = true id k, 2 + k = candidate k
+      uint32_t k = 0;
+      for (; k < e.t; ++k) emit_pair(lds32(staged_at + (1u + k) * 4u), k);
+      if (exact) {
+        for (; k < e.n_refs; ++k) emit_task(lds32(staged_at + (2u + k) * 4u), k);
+      } else {
+        for (; k < e.n_refs; ++k) emit_pair(lds32(staged_at + (2u + k) * 4u), k);
+      }
+      return first;
+    }
     const uint32_t* true_ids = ix.lut + e.off + 1;
     const uint32_t* cand_ids = ix.lut + e.off + 2;  // indexed by k as well
     // four independent loads in flight per step: a lane walks its own record, so consecutive words share a sector
@@ -346,10 +471,15 @@ __device__ __noinline__ uint32_t emit_general(const DevIndex& ix, const JoinPara
 // that skips the shared-memory tier and Q2 and has every lane gather the 32-bit tier codes of its own four points —
 // bit-exact, but 1.25 instead of 1.00 ms per 100 M points on the config-4 stand-in: the gathers' L2 latency is
 // exposed in every tile, where the queued batch is issued one tile ahead of its use.)
-// kPipe3 (trees without palette nodes, i.e. arenas beyond L2): population 3's arena reads are software-pipelined
-// across batches (drain3); a compile-time choice because the batch in flight costs six registers the other
-// instantiations — the headline one among them — would otherwise spill.
-template <bool kIds, bool kStats, bool kDense, bool kLate = false, bool kPipe3 = false>
+// kStage (lookup-table-heavy indexes): compiles in the warp-cooperative staging of lookup-table records
+// (stage_records).  A compile-time choice because its registers slow the other instantiations down (measured with
+// the code merely present: config-4 stand-in, counts only, 0.96 -> 1.10 ms per 100 M points).
+// (Tried next to it and dropped: software-pipelining population 3's arena reads across batches for trees without
+// palette nodes — issue the read when a batch is taken off Q3, resolve it when the next one is taken.  Bit-exact;
+// 4 % on the config-4 stand-in counts only, nothing with first ids, nothing at all on full-size config 5 (171.9 vs
+// 171.2 ms per 500 M points), and with JoinStats two instantiations kept thread-local copies of the parameter
+// blocks: 9.7 instead of 1.3 ms.)
+template <bool kIds, bool kStats, bool kDense, bool kLate = false, bool kStage = false>
 __global__ void __launch_bounds__(kJoinThreads, GJ_JOIN_MIN_BLOCKS)
 join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinParams jp) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -357,6 +487,12 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
   const uint32_t lane = tid & 31u;
   const uint32_t warp = tid >> 5;
 
+  __shared__ EmitCtx s_ctx;
+  if (tid == 0) {
+    s_ctx = EmitCtx{ix.lut, ix.ids, ix.ring_len, jp.counts, jp.status, jp.ovf_point, jp.ovf_id, jp.ovf_ord,
+                    jp.task_point, jp.task_slot, jp.task_ord, jp.base_index, jp.ovf_cap, jp.task_cap, ix.n_ids,
+                    ix.ids_dense, jp.exact, jp.ovf_discard};
+  }
   {  // stage the first directory tier, clear the histogram
     const uint4* src = reinterpret_cast<const uint4*>(ix.dir16.table);
     uint4* dst = reinterpret_cast<uint4*>(smem);
@@ -374,13 +510,18 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
                      jp.counts_priv ? jp.counts_priv + static_cast<size_t>(blockIdx.x % jp.n_priv) * ix.n_ids : nullptr};
   const uint32_t s_q2 = smem_addr(smem + jp.smem_queue_off) + warp * kQueueBytesPerWarp;
   const uint32_t s_q3 = s_q2 + kQueue2Cap * 8u;
+  const uint32_t s_stage = kStage && jp.smem_stage_off ? smem_addr(smem + jp.smem_stage_off) + warp * jp.stage_chunks * 16u : 0u;
   const uint32_t hist_spare = ix.n_ids;  // the histogram has n_ids + 1 rows
   const uint32_t lane_lt = (1u << lane) - 1u;
   const uint32_t d1_w = ix.dir16.width, d1_h = ix.dir16.height, d1_pitch = ix.dir16.pitch;
   const uint32_t d1_x0 = ix.dir16.x0, d1_y0 = ix.dir16.y0;
   const uint32_t d1_shift = min(static_cast<uint32_t>(ix.dir16.shift) + 2u, 31u);  // on 32-bit-aligned coordinates
-  const DevDirectory& tb = ix.dirk.n_table ? ix.dirk : (ix.dir2.n_table ? ix.dir2 : ix.dir);  // the 32-bit tier behind it
-  const uint32_t* __restrict__ table2 = tb.table;
+  // the 32-bit tier behind it: dirk, else dir2, else dir — its fields by value (a reference picked at run time among
+  // three members of the parameter block is one of the things that made ptxas copy the block to local memory)
+  const int tb_which = ix.dirk.n_table ? 2 : (ix.dir2.n_table ? 1 : 0);
+  const uint32_t* __restrict__ table2 = tb_which == 2 ? ix.dirk.table : (tb_which == 1 ? ix.dir2.table : ix.dir.table);
+  const uint32_t tb_pitch = tb_which == 2 ? ix.dirk.pitch : (tb_which == 1 ? ix.dir2.pitch : ix.dir.pitch);
+  const int tb_chunks = tb_which == 2 ? ix.dirk.chunks : (tb_which == 1 ? ix.dir2.chunks : ix.dir.chunks);
   const uint32_t qc_shift = ix.qc.shift, qc_mul = ix.qc.mul;
   const uint32_t qc_x0 = ix.qc.x0, qc_y0 = ix.qc.y0, qc_xc = ix.qc.x_clamp, qc_yc = ix.qc.y_clamp;
   const double2* __restrict__ pts = jp.pts;
@@ -436,18 +577,7 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
     const uint32_t slot = (spread4((c >> 4) & 0xFu) << 1) | spread4(c & 0xFu);  // chunk_slot
     return (static_cast<uint64_t>((iw & 0x7FFFFFFFu) >> ix.qc.index_bits) << 32) | (static_cast<uint64_t>(c) & ~0xFFull) | slot;
   };
-  // Stage 1 of a batch, for trees without palette nodes (large arenas: every slot read is a DRAM burst): only
-  // ISSUES the arena read of a flagged item.  The value is first touched in resolve_open, which drain3 runs one
-  // batch later, so the DRAM latency hides behind the emit work of the batch before.
-  auto fetch_open = [&](bool mine, uint32_t iw, uint32_t c) -> uint64_t {
-    uint64_t v = 0;
-    const bool slow = c == kQueueSlow && (iw & ix.qc.slow_mark) == ix.qc.slow_mark;
-    if (mine && (iw & 0x80000000u) != 0u && !slow) {
-      asm volatile("ld.global.nc.u64 %0, [%1];" : "=l"(v) : "l"(ix.arena + queued_slot(iw, c)));
-    }
-    return v;
-  };
-  auto resolve_open = [&](bool mine, uint32_t iw, uint32_t c, bool fetched, uint64_t fetched_entry) {
+  auto resolve_open = [&](bool mine, uint32_t iw, uint32_t c) {
     const uint32_t q_index_bits = ix.qc.index_bits, q_slow_mark = ix.qc.slow_mark;
     const uint32_t i = iw & ((1u << q_index_bits) - 1u);
     const bool flagged = (iw & 0x80000000u) != 0u;
@@ -460,19 +590,18 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
           mine = false;
         } else {
           if (kStats) ++n_valid;
-          entry = probe_raw(ix, cell_from_point(q.x, q.y, ix.leaf_level));
+          entry = probe_raw_face0(ix, cell_from_point(q.x, q.y, ix.leaf_level));
         }
       } else if (flagged || (c & kDirLink)) {
-        const int walk_level = ix.prefix_level0 + 4 * tb.chunks;
+        const int walk_level = ix.prefix_level0 + 4 * tb_chunks;
         uint64_t node = c & ~kDirLink;  // unpacked coding: the node under the link
         int level = walk_level;
         bool walk = true;
         if (flagged) {  // the word is (node - 1) * 256 + (y sub-cell bits << 4 | x sub-cell bits)
           const uint64_t at = queued_slot(iw, c);
           const uint32_t slot = static_cast<uint32_t>(at) & 0xFFu;
-          bool from_arena = !fetched;
-          entry = fetched_entry;
-          if (!fetched && ix.node_pal) {  // the node's 128-byte palette form, usually an L2 hit
+          bool from_arena = true;
+          if (ix.node_pal) {  // the node's 128-byte palette form, usually an L2 hit
             const uint64_t* rec = ix.node_pal + (at >> 8) * 16u;
             const uint32_t codes = __ldg(reinterpret_cast<const uint32_t*>(rec + 4) + (slot >> 4));
             const uint64_t v = __ldg(rec + ((codes >> ((slot & 15u) * 2u)) & 3u));
@@ -519,6 +648,14 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
       if (kIds && !jp.ovf_discard) ovf_base = warp_reserve(&jp.status->overflow_count, plan.n_ovf, lane);
       if (jp.exact) task_base = warp_reserve(&jp.status->task_count, plan.n_tasks, lane);
     }
+    uint32_t staged_at = 0;  // shared address of this lane's lookup-table record, 0 = walk it in global memory
+    if (kStage && s_stage != 0u && __any_sync(0xffffffffu, general && plan.tag == 3u)) {
+      const bool rec = general && plan.tag == 3u;
+      const uint32_t first_chunk = plan.off >> 2;  // the record is words off .. off + 1 + n_refs of the table
+      const uint32_t n_chunks = rec ? ((plan.off + 1u + plan.n_refs) >> 2) - first_chunk + 1u : 0u;
+      const uint32_t at = stage_records(reinterpret_cast<const uint4*>(ix.lut), s_stage, jp.stage_chunks, lane, first_chunk, n_chunks);
+      if (rec && at != ~0u) staged_at = s_stage + (at * 4u + (plan.off & 3u)) * 4u;
+    }
     if (!mine) return;
     uint32_t first = kNoMatch;
     if (entry == 0) {
@@ -544,7 +681,7 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
         cand_refs += n_cand;
       }
     } else {
-      first = emit_general<kIds, kDense>(ix, jp, hist, entry, i, plan, ovf_base, task_base);
+      first = emit_general<kIds, kDense>(&s_ctx, hist, entry, i, plan, ovf_base, task_base, staged_at);
       if (kStats) {
         solely_true += plan.n_cand == 0;
         refined += plan.n_cand != 0;
@@ -561,12 +698,6 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
     return count + __popc(mask);
   };
 
-  // Q3 items 32 at a time.  Without palette nodes the batch is software-pipelined like population 2's: its arena
-  // reads are issued when it is taken off the queue and it is resolved when the NEXT batch is taken (or at the
-  // final flush), so a warp always has one batch of DRAM reads in flight behind the emit work of another.
-  bool open_pending = false;  // warp-uniform
-  uint32_t open_take = 0, open_iw = 0, open_c = 0;
-  uint64_t open_entry = 0;
   auto drain3 = [&](bool flush) {
     __syncwarp();
     while (q3_count >= 32u || (flush && q3_count)) {
@@ -574,21 +705,7 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
       q3_count -= take;
       const uint2 item = lds64(s_q3 + (q3_count + min(lane, take - 1u)) * 8u);
       __syncwarp();
-      if (!kPipe3) {
-        resolve_open(lane < take, item.x, item.y, false, 0);
-        continue;
-      }
-      const uint64_t v = fetch_open(lane < take, item.x, item.y);
-      if (open_pending) resolve_open(lane < open_take, open_iw, open_c, true, open_entry);
-      open_pending = true;
-      open_take = take;
-      open_iw = item.x;
-      open_c = item.y;
-      open_entry = v;
-    }
-    if (kPipe3 && flush && open_pending) {
-      open_pending = false;
-      resolve_open(lane < open_take, open_iw, open_c, true, open_entry);
+      resolve_open(lane < take, item.x, item.y);
     }
   };
 
@@ -633,7 +750,7 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
     uint32_t idx = item.y;
     if (ix.qc.packed) {  // (Y << xbits) | X at level tb.level + 4, see DevQueueCoding
       const uint32_t X = item.y & (qc_mul - 1u), Y = item.y >> ix.qc.xbits;
-      idx = (Y >> ix.qc.tier_shift) * tb.pitch + (X >> ix.qc.tier_shift);
+      idx = (Y >> ix.qc.tier_shift) * tb_pitch + (X >> ix.qc.tier_shift);
       batch_slot = ((Y & ix.qc.sub_mask) << 4) | (X & ix.qc.sub_mask);  // spread into a node slot in population 3
     }
 #ifdef GJ_EXP_NO_TB  // timing experiment: results are wrong (no gather into the 32-bit tier: every lookup misses)

@@ -760,3 +760,33 @@ def test_csr_into_caller_arrays_host_and_device(name, chunk):
             s.join_pairs_into(bad, capi.GJ_MODE_EXACT, np.empty(n + 1, np.uint64), np.empty(16, np.uint32))
         assert e.value.index == n // 2
     b.close()
+
+
+@pytest.mark.parametrize("name", ["cfg5_stars_scaled", "join_small_exact", "cfg3_tess16_exact_trained", "world_stars",
+                                  "kmax60_sparse_ids"])
+def test_staged_lookup_table_records_match_reference(name):
+    """Lookup-table-heavy indexes stage the records of a population-3 batch in shared memory (stage_records: a
+    warp-cooperative, coalesced copy in 16-byte chunks) instead of walking them word by word per lane.  Forced on
+    here; counts, stats, first ids and overflow records must equal the fixture's and the unstaged path's, with
+    batches that fit the staging buffer and — small chunk budget — batches that do not."""
+    import torch
+    fx = golden_util.load(name)
+    pts = np.ascontiguousarray(fx["points"])
+    plain = join.IndexBundle.load(golden_util.bundle_file(name), device=0, options=capi.Options(stage_lut=0))
+    for extra in ({}, {"smem_pad": 60000}):  # the padding leaves the staging buffer only its minimum size
+        b = join.IndexBundle.load(golden_util.bundle_file(name), device=0, options=capi.Options(stage_lut=1, **extra))
+        _check_join_against_fixture(b, fx)
+        for mode in (capi.GJ_MODE_EXACT, capi.GJ_MODE_APPROX):
+            sa, sb = join.JoinStats(), join.JoinStats()
+            ca, fa, (pa, ia) = plain.session().join_count(pts, mode, stats=sa, want_ids=True)
+            cb, fb, (pb, ib) = b.session().join_count(pts, mode, stats=sb, want_ids=True)
+            assert np.array_equal(ca, cb) and np.array_equal(fa, fb) and np.array_equal(pa, pb) and np.array_equal(ia, ib)
+            assert sa.as_tuple() == sb.as_tuple()
+            n = len(pts)
+            d_pts = torch.from_numpy(pts).cuda()
+            d_counts = torch.zeros(max(1, len(b.ids)), dtype=torch.int64, device="cuda")
+            torch.cuda.synchronize()
+            b.session().join_count_device(d_pts.data_ptr(), n, d_counts.data_ptr(), mode, sync=True)
+            assert np.array_equal(d_counts.cpu().numpy()[:len(ca)].astype(np.uint64), ca)
+        b.close()
+    plain.close()
