@@ -127,7 +127,8 @@ typedef struct {
   int32_t debug_plan;           /* 1 = print the join kernel's shared-memory plan to stderr */
   int32_t hist16;               /* id tables beyond the 32-bit shared histogram count in a 16-bit one with
                                    periodic flushes: -1 = automatic, 0 = never, 1 = also when the 32-bit one fits */
-  int32_t reserved0;            /* keep 0 */
+  int32_t strip_index;          /* the refine kernel's strip lists hold vertex indices instead of 32-byte edge records:
+                                   -1 = automatic (polygon sets whose records would exceed 32 MB), 0 = never, 1 = always */
   int32_t stage_lut;            /* lookup-table records of a population-3 batch staged in shared memory by the whole
                                    warp: -1 = automatic (tables of 256 MB and more), 0 = never, 1 = always */
   uint64_t max_launch_points;   /* test hook: split device-resident calls into launches of this many points; 0 = none */

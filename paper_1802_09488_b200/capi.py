@@ -64,7 +64,7 @@ class Options(C.Structure):
         ("struct_size", C.c_uint32), ("dir16_max_entries", C.c_int32), ("dir16_level_max", C.c_int32),
         ("node_pal_max_mb", C.c_int32), ("tier_sub", C.c_int32), ("ids_late", C.c_int32),
         ("queue_unpacked", C.c_int32), ("queue_slot_hi_bits", C.c_int32), ("hist_rep_cap", C.c_int32),
-        ("smem_pad", C.c_int32), ("debug_plan", C.c_int32), ("hist16", C.c_int32), ("reserved0", C.c_int32), ("stage_lut", C.c_int32),
+        ("smem_pad", C.c_int32), ("debug_plan", C.c_int32), ("hist16", C.c_int32), ("strip_index", C.c_int32), ("stage_lut", C.c_int32),
         ("max_launch_points", C.c_uint64), ("chunk_points", C.c_uint64),
     ]
 

@@ -191,6 +191,22 @@ int launch_join_variant(gj_session* s, const JoinParams& jp, const SmemPlan& sp)
   return launch_join_kernel<kIds, kStats, kDense, kLate, false>(s, jp, sp);
 }
 
+// K2 on a persistent grid: exactly the blocks that are resident at once (a partial second wave of a grid-stride
+// kernel only adds a tail).  The instantiation follows the form of the index's strip lists.
+int launch_refine(gj_session* s, const RefineParams& rp, size_t smem) {
+  const gj_index& ix = *s->ix;
+  auto launch = [&](auto kernel) -> int {
+    int per_sm = 0;
+    GJ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kRefineThreads, smem));
+    const unsigned blocks = static_cast<unsigned>(ix.sm_count) * static_cast<unsigned>(std::max(per_sm, 1));
+    kernel<<<blocks, kRefineThreads, smem, s->stream>>>(ix.dev, rp);
+    ++s->launches;
+    GJ_CUDA(cudaGetLastError());
+    return GJ_OK;
+  };
+  return ix.dev.strip_eidx ? launch(refine_kernel<true>) : launch(refine_kernel<false>);
+}
+
 int reset_status(gj_session* s, DevStatus* d_status) {
   static const DevStatus init{kNoBadIndex, 0, 0, 0, 0};
   GJ_CUDA(cudaMemcpyAsync(d_status, &init, sizeof init, cudaMemcpyHostToDevice, s->stream));
@@ -314,15 +330,7 @@ int enqueue_join(gj_session* s, const JoinRequest& rq) {
     rp.smem_counts = counts_smem <= (32u << 10) ? 1 : 0;
     rp.counts_priv = rp.smem_counts ? nullptr : d_priv;
     rp.n_priv = static_cast<uint32_t>(ix.sm_count);
-    // persistent grid: exactly the blocks that are resident at once (a partial
-    // second wave of a grid-stride kernel only adds a tail)
-    int per_sm = 0;
-    GJ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, refine_kernel, kRefineThreads,
-                                                          rp.smem_counts ? counts_smem : 0));
-    const unsigned blocks = static_cast<unsigned>(ix.sm_count) * static_cast<unsigned>(std::max(per_sm, 1));
-    refine_kernel<<<blocks, kRefineThreads, rp.smem_counts ? counts_smem : 0, s->stream>>>(ix.dev, rp);
-    ++s->launches;
-    GJ_CUDA(cudaGetLastError());
+    if ((rc = launch_refine(s, rp, rp.smem_counts ? counts_smem : 0)) != GJ_OK) return rc;
   }
   if (d_priv) {
     fold_private_counts_kernel<<<std::max(1u, std::min((n_ids + 255u) / 256u, static_cast<unsigned>(ix.sm_count) * 8u)), 256, 0,
@@ -655,11 +663,7 @@ int run_host_pairs(gj_session* s, const double* latlng, uint64_t n, bool exact, 
       rp.task_cap = task_cap;
       rp.task_pass = s->d_task_pass.as<uint8_t>();
       rp.status = d_status;
-      int per_sm = 0;
-      GJ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, refine_kernel, kRefineThreads, 0));
-      refine_kernel<<<static_cast<unsigned>(ix.sm_count) * static_cast<unsigned>(std::max(per_sm, 1)), kRefineThreads, 0,
-                      s->stream>>>(ix.dev, rp);
-      ++s->launches;
+      if ((rc = launch_refine(s, rp, 0)) != GJ_OK) return rc;
     }
     GJ_CUDA(cudaEventRecord(s->ev_done[b], s->stream));  // the point buffer is free again
     pairs_emit_kernel<false><<<wide, 256, 0, s->stream>>>(ix.dev, pp);
@@ -849,11 +853,7 @@ int run_pairs_async(gj_session* s, const double* src, bool src_on_device, uint64
       rp.task_cap = task_cap;
       rp.task_pass = s->d_task_pass.as<uint8_t>();
       rp.status = d_status;
-      int per_sm = 0;
-      GJ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, refine_kernel, kRefineThreads, 0));
-      refine_kernel<<<static_cast<unsigned>(ix.sm_count) * static_cast<unsigned>(std::max(per_sm, 1)), kRefineThreads, 0,
-                      s->stream>>>(ix.dev, rp);
-      ++s->launches;
+      if ((rc = launch_refine(s, rp, 0)) != GJ_OK) return rc;
     }
     if (!src_on_device) GJ_CUDA(cudaEventRecord(s->ev_done[b], s->stream));  // the point buffer is free again
     uint64_t* d_sums = s->d_block_sums.as<uint64_t>();

@@ -107,6 +107,11 @@ struct DevIndex {
   const StripMeta* strip_meta;     // [n_ids]
   const uint32_t* strip_ptr;       // per polygon k + 1 offsets into strip_edges
   const EdgeRecord* strip_edges;
+  // Compact form of the strip lists for large polygon sets (null otherwise): per listed edge the index of its
+  // first vertex in ring_xy (closed rings: the edge is ring_xy[v], ring_xy[v + 1]) instead of a 32-byte record.
+  // The lists shrink 8x and the rings they point into are a few MB, so both stay in L2 where 140 MB of edge records
+  // (10 000 polygons of BASELINE config 5) do not.
+  const uint32_t* strip_eidx;
   uint64_t roots[8];
   uint64_t prefixes[8];
   uint32_t prefix_bits[8];
@@ -399,6 +404,17 @@ __device__ __forceinline__ uint32_t pip_edge_classify(double qx, double qy, doub
 // One edge record with a single 256-bit load (sm_100+).
 __device__ __forceinline__ void load_edge(const EdgeRecord* rec, double* ax, double* ay, double* bx, double* by) {
   asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(*ax), "=d"(*ay), "=d"(*bx), "=d"(*by) : "l"(rec));
+}
+
+// The same edge through the compact strip lists: two 16-byte vertex loads (vertex pairs are not 32-byte aligned).
+__device__ __forceinline__ void load_edge_indexed(const double2* ring_xy, const uint32_t* eidx, uint32_t e, double* ax,
+                                                  double* ay, double* bx, double* by) {
+  const double2* v = ring_xy + __ldg(eidx + e);
+  const double2 a = __ldg(v), b = __ldg(v + 1);
+  *ax = a.x;
+  *ay = a.y;
+  *bx = b.x;
+  *by = b.y;
 }
 
 // geometry.cpp:186-193: on an edge or vertex

@@ -243,7 +243,7 @@ struct gj_index {
   gj_options opt{};            // explicit knobs (gj_options_default unless the creator passed others)
   std::vector<uint32_t> ids;  // slot -> polygon id
   gj::DeviceBuffer d_arena, d_lut, d_ids, d_ring_off, d_ring_len, d_ring_xy, d_dir_table, d_dir_dict, d_dir2_table, d_dir16_table, d_dirk_table, d_node_pal,
-      d_strip_meta, d_strip_ptr, d_strip_edges;
+      d_strip_meta, d_strip_ptr, d_strip_edges, d_strip_eidx;
   int sm_count = 0;
   size_t smem_optin = 0;
   bool stage_records = false;  // K1 stages the lookup-table records of a population-3 batch in shared memory (lookup-table-heavy indexes)
@@ -262,6 +262,7 @@ struct gj_index {
     dev.strip_meta = d_strip_meta.as<gj::StripMeta>();
     dev.strip_ptr = d_strip_ptr.as<uint32_t>();
     dev.strip_edges = d_strip_edges.as<gj::EdgeRecord>();
+    dev.strip_eidx = d_strip_eidx.ptr ? d_strip_eidx.as<uint32_t>() : nullptr;
     dev.dir.table = d_dir_table.as<uint32_t>();
     dev.dir2.table = d_dir2_table.as<uint32_t>();
     dev.dir16.table = d_dir16_table.as<uint32_t>();
@@ -274,7 +275,7 @@ struct gj_index {
     return {&gj_index::d_arena, &gj_index::d_lut, &gj_index::d_ids, &gj_index::d_ring_off, &gj_index::d_ring_len,
             &gj_index::d_ring_xy, &gj_index::d_dir_table, &gj_index::d_dir_dict, &gj_index::d_dir2_table,
             &gj_index::d_dir16_table, &gj_index::d_dirk_table, &gj_index::d_node_pal, &gj_index::d_strip_meta,
-            &gj_index::d_strip_ptr, &gj_index::d_strip_edges};
+            &gj_index::d_strip_ptr, &gj_index::d_strip_edges, &gj_index::d_strip_eidx};
   }
 };
 

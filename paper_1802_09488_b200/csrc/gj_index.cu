@@ -33,6 +33,7 @@ constexpr double kDirKMinLinkShare = 0.25;         // refine only when at least 
 constexpr uint64_t kMaxDir16Entries = 69632;
 constexpr uint64_t kMaxNodePalBytes = 32ull << 20;  // palette nodes of a tree this small stay in L2 as a whole
 constexpr uint64_t kMaxPolygonId = (1u << 30) - 1;
+constexpr uint64_t kMaxEdgeRecordBytes = 32ull << 20;  // beyond this (estimated) size K2's strip lists hold vertex indices
 
 struct Bitmap {
   std::vector<uint64_t> w;
@@ -478,6 +479,7 @@ gj_options default_options() {
   o.hist_rep_cap = -1;
   o.hist16 = -1;
   o.stage_lut = -1;
+  o.strip_index = -1;
   return o;
 }
 
@@ -558,6 +560,13 @@ int create_index(const gj_index_desc& d, int device, const gj_options* options, 
   std::vector<StripMeta> strip_meta(n_ids);
   std::vector<uint32_t> strip_ptr;
   std::vector<EdgeRecord> strip_edges;
+  std::vector<uint32_t> strip_eidx;  // the compact form (DevIndex::strip_eidx), filled instead when the records get large
+  // two strips per edge, ~3 listed edges per strip: ~6 records of 32 bytes per polygon edge
+  const bool strips_indexed = opt.strip_index > 0 || (opt.strip_index < 0 && total * 6 * sizeof(EdgeRecord) > kMaxEdgeRecordBytes);
+  if (strips_indexed && total >= (1ull << 32)) {
+    set_error("polygon set exceeds 2^32 vertices");
+    return GJ_INVALID_ARGUMENT;
+  }
   {
     const double margin = 1e-9;  // pip_edge's rejection margin
     std::vector<std::vector<uint32_t>> lists;
@@ -592,14 +601,18 @@ int create_index(const gj_index_desc& d, int device, const gj_options* options, 
         for (uint32_t st = first; st <= last; ++st) lists[st].push_back(e);
       }
       for (uint32_t st = 0; st < m.k; ++st) {
-        strip_ptr.push_back(static_cast<uint32_t>(strip_edges.size()));
+        strip_ptr.push_back(static_cast<uint32_t>(strips_indexed ? strip_eidx.size() : strip_edges.size()));
         for (uint32_t e : lists[st]) {
-          const double2 a = v[e], b = v[e + 1];
-          strip_edges.push_back(EdgeRecord{a.x, a.y, b.x, b.y});
+          if (strips_indexed) {
+            strip_eidx.push_back(static_cast<uint32_t>(ring_off[s] + e));
+          } else {
+            const double2 a = v[e], b = v[e + 1];
+            strip_edges.push_back(EdgeRecord{a.x, a.y, b.x, b.y});
+          }
         }
       }
-      strip_ptr.push_back(static_cast<uint32_t>(strip_edges.size()));
-      if (strip_edges.size() >= (1ull << 32)) {
+      strip_ptr.push_back(static_cast<uint32_t>(strips_indexed ? strip_eidx.size() : strip_edges.size()));
+      if (std::max(strip_edges.size(), strip_eidx.size()) >= (1ull << 32)) {
         set_error("polygon strip table exceeds 2^32 edge records");
         return GJ_INVALID_ARGUMENT;
       }
@@ -644,6 +657,7 @@ int create_index(const gj_index_desc& d, int device, const gj_options* options, 
   if ((rc = upload(ix->d_strip_meta, strip_meta.data(), strip_meta.size(), &bytes)) != GJ_OK) return rc;
   if ((rc = upload(ix->d_strip_ptr, strip_ptr.data(), strip_ptr.size(), &bytes)) != GJ_OK) return rc;
   if ((rc = upload(ix->d_strip_edges, strip_edges.data(), strip_edges.size(), &bytes)) != GJ_OK) return rc;
+  if (strips_indexed && (rc = upload(ix->d_strip_eidx, strip_eidx.data(), strip_eidx.size(), &bytes)) != GJ_OK) return rc;
   if ((rc = upload(ix->d_dir_table, an.dir.table.data(), an.dir.table.size(), &bytes)) != GJ_OK) return rc;
   if ((rc = upload(ix->d_dir_dict, an.dict.data(), an.dict.size(), &bytes)) != GJ_OK) return rc;
   if ((rc = upload(ix->d_dir2_table, an.dir2.table.data(), an.dir2.table.size(), &bytes)) != GJ_OK) return rc;

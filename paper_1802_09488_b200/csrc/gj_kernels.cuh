@@ -1049,6 +1049,8 @@ struct RefineParams {
   uint32_t n_priv;
 };
 
+// kIndexed: the strip lists hold vertex indices (DevIndex::strip_eidx) instead of 32-byte edge records.
+template <bool kIndexed>
 __global__ void __launch_bounds__(kRefineThreads, 4)
 refine_kernel(const __grid_constant__ DevIndex ix, RefineParams rp) {
   constexpr int kWarps = kRefineThreads / 32;
@@ -1104,7 +1106,11 @@ refine_kernel(const __grid_constant__ DevIndex ix, RefineParams rp) {
       const double oy = __shfl_sync(0xffffffffu, qy, owner);
       if (lane < take) {
         double ax, ay, bx, by;
-        load_edge(ix.strip_edges + item.x, &ax, &ay, &bx, &by);
+        if (kIndexed) {
+          load_edge_indexed(ix.ring_xy, ix.strip_eidx, item.x, &ax, &ay, &bx, &by);
+        } else {
+          load_edge(ix.strip_edges + item.x, &ax, &ay, &bx, &by);
+        }
         if ((item.y & 1u) && pip_edge_on_boundary(ox, oy, ax, ay, bx, by)) atomicOr(&s_result[warp][owner], 1u);
         if ((item.y & 2u) && pip_edge_crosses(ox, oy, ax, ay, bx, by)) atomicXor(&s_result[warp][owner], 2u);
       }
@@ -1138,7 +1144,11 @@ refine_kernel(const __grid_constant__ DevIndex ix, RefineParams rp) {
       uint32_t kinds = 0;
       if (real) {
         double ax, ay, bx, by;
-        load_edge(ix.strip_edges + e, &ax, &ay, &bx, &by);
+        if (kIndexed) {
+          load_edge_indexed(ix.ring_xy, ix.strip_eidx, e, &ax, &ay, &bx, &by);
+        } else {
+          load_edge(ix.strip_edges + e, &ax, &ay, &bx, &by);
+        }
         kinds = pip_edge_classify(ox, oy, ax, ay, bx, by);
       }
       if (kinds & 4u) atomicXor(&s_result[warp][src], 2u);  // crosses for certain: no division

@@ -790,3 +790,20 @@ def test_staged_lookup_table_records_match_reference(name):
             assert np.array_equal(d_counts.cpu().numpy()[:len(ca)].astype(np.uint64), ca)
         b.close()
     plain.close()
+
+
+@pytest.mark.parametrize("name", ["join_small_exact", "acceptance_exact20", "cfg3_tess16_exact_trained", "cfg5_stars_scaled",
+                                  "kmax60_sparse_ids", "world_stars", "kmax60_tiny_a"])
+def test_indexed_strip_lists_match_reference(name):
+    """Large polygon sets give the refine kernel strip lists of vertex indices instead of 32-byte edge records
+    (gj_options.strip_index; automatic beyond ~32 MB of records).  Forced here: exact pairs, counts and stats must
+    equal the fixture's."""
+    fx = golden_util.load(name)
+    b = join.IndexBundle.load(golden_util.bundle_file(name), device=0, options=capi.Options(strip_index=1))
+    _check_join_against_fixture(b, fx)
+    st = join.JoinStats()
+    pi, pid = pairs_from_csr(*b.session().join_pairs(fx["points"], capi.GJ_MODE_EXACT, st))
+    epi, epid = golden_util.pairs_of(fx, "exact")
+    assert np.array_equal(pi, epi) and np.array_equal(pid, epid)
+    assert st.as_tuple() == tuple(int(v) for v in fx["exact_stats"])
+    b.close()

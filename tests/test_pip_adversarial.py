@@ -86,10 +86,11 @@ def test_oracle_pip_equals_live_reference_polygon_by_polygon(ref_available):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("strip_index", [0, 1])  # K2's strip lists as 32-byte edge records / as vertex indices
 @pytest.mark.parametrize("name", ["special"] + FIXTURES)
-def test_gpu_exact_join_on_adversarial_points(name):
+def test_gpu_exact_join_on_adversarial_points(name, strip_index):
     path, g, pts, gold, name = _case(name)
-    bundle = join.IndexBundle.load(path, device=0)
+    bundle = join.IndexBundle.load(path, device=0, options=capi.Options(strip_index=strip_index))
     s = bundle.session()
     st = join.JoinStats()
     row_ptr, pid = s.join_pairs(pts, capi.GJ_MODE_EXACT, st)
