@@ -17,9 +17,11 @@
  * Everything is plain C: pointers and sizes, no C++/torch types.  The index
  * is built OFFLINE by the reference's own build_index (src/join.cpp:152-235)
  * or read from its GJX1 bundle file (src/join.cpp:316-381); this library
- * copies it into one GPU's HBM and runs the probe path there.  There is no CPU
- * fallback: every entry point needs a CUDA device and fails with
- * GJ_CUDA_ERROR otherwise.
+ * copies it into a GPU's HBM — or replicates it into the HBM of several
+ * (gj_group_*, gj_index_replicate) — and runs the probe path there.  There is
+ * no CPU fallback: every entry point needs a CUDA device and fails with
+ * GJ_CUDA_ERROR otherwise.  The library reads no environment variable; tuning
+ * knobs and test hooks are the fields of gj_options.
  *
  * Threading: a gj_index is immutable after creation (like the reference's
  * IndexBundle, include/geojoin/join.hpp:86-88).  A gj_session owns one CUDA

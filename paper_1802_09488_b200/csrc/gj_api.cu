@@ -2,6 +2,7 @@
 // plumbing and the host-buffer pipelines (H2D / kernels / D2H overlapped on
 // three streams).
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -150,10 +151,17 @@ SmemPlan plan_smem(const gj_index& ix) {
 // sized indexes.  (The L1 carve-out follows the launch's actual size.)
 template <typename Kernel>
 int allow_max_smem(const gj_index& ix, Kernel kernel) {
+  // once per kernel and device: the host pipelines launch a chunk every few hundred microseconds
+  static std::mutex m;
+  static std::vector<std::pair<const void*, int>> done;
+  const std::pair<const void*, int> key{reinterpret_cast<const void*>(kernel), ix.device};
+  std::lock_guard<std::mutex> lk(m);
+  if (std::find(done.begin(), done.end(), key) != done.end()) return GJ_OK;
   cudaFuncAttributes attr{};
   GJ_CUDA(cudaFuncGetAttributes(&attr, kernel));  // static shared memory (K1's EmitCtx) counts against the same limit
   GJ_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                static_cast<int>(ix.smem_optin - attr.sharedSizeBytes)));
+  done.push_back(key);
   return GJ_OK;
 }
 
