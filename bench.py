@@ -323,13 +323,36 @@ def run_secondary(torch, capi, join, peak, reps=5):
             a_bytes = 20.0
             a_note = "16 B point + 4 B first id"
         achieved = a_bytes * n / (ms * 1e-3) / 1e9
+        csr = None
+        if config == 5:  # configs[4]'s own output form: every covering polygon per point, as CSR, left in HBM
+            d_pts = torch.from_numpy(pts).cuda()
+            d_rows = torch.empty(n + 1, dtype=torch.int64, device="cuda")
+            d_ids = torch.empty(pairs, dtype=torch.int32, device="cuda")
+            torch.cuda.synchronize()
+            sess.join_pairs_device(d_pts.data_ptr(), n, mode, d_rows.data_ptr(), d_ids.data_ptr(), pairs)  # warm-up
+            t0 = time.perf_counter()
+            total = sess.join_pairs_device(d_pts.data_ptr(), n, mode, d_rows.data_ptr(), d_ids.data_ptr(), pairs)
+            csr_s = time.perf_counter() - t0  # synchronous call: returns when row offsets and ids are in HBM
+            m = min(n, 200_000)
+            pairs_equal = None
+            if kind == "reference":
+                from oracle import ref
+                rpi, rpid, _ = ref.RefBundle.load(path).join_pairs(pts[:m], exact)
+                rows = d_rows[:m + 1].cpu().numpy().astype(np.int64)
+                gpi = np.repeat(np.arange(m, dtype=np.uint64), np.diff(rows))
+                pairs_equal = bool(np.array_equal(gpi, rpi) and
+                                   np.array_equal(d_ids[:rows[-1]].cpu().numpy().view(np.uint32), rpid))
+            csr = {"call": "gj_join_pairs_device (points, row offsets and polygon ids in HBM)", "ms": 1e3 * csr_s,
+                   "pairs": int(total), "pairs_per_s": total / csr_s,
+                   "ordered_pairs_equal_reference_on_prefix": pairs_equal, "prefix": m}
+            del d_pts, d_rows, d_ids
         out.append({
             "config": config, "workload": label, "index": name, "mode": "exact" if exact else "approx",
             "points": n, "ms": ms, "points_per_s": n / (ms * 1e-3), "kernel_launches_per_step": launches,
             "pairs_per_point": pairs / n, "pip_tests_per_point": st.pip_tests / n,
             "algorithmic_bytes_per_point": a_bytes, "algorithmic_bytes_note": a_note,
             "achieved_GBps": achieved, "frac": achieved / peak,
-            "counts_equal_reference": bool(equal),
+            "counts_equal_reference": bool(equal), "csr": csr,
             "cpu_baseline": {"value": n / cpu_s, "unit": "points/s", "cores": cores, "kind": kind,
                              "sample": f"all {n} points, per-polygon counts, {cpu_s:.2f}s"},
             "options": opt, "seconds_total": round(time.time() - t_all, 1),
@@ -548,7 +571,8 @@ def run_ours(args):
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
-    bad_secondary = [x["config"] for x in (secondary or []) if x.get("counts_equal_reference") is False]
+    bad_secondary = [x["config"] for x in (secondary or []) if x.get("counts_equal_reference") is False or
+                     (x.get("csr") or {}).get("ordered_pairs_equal_reference_on_prefix") is False]
     if counts_equal is False or bad_secondary:
         raise SystemExit(f"bench.py: GPU per-polygon counts differ from the reference CPU join "
                          f"(headline: {counts_equal}, secondary configs failing: {bad_secondary})")

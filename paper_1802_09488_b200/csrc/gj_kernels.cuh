@@ -721,8 +721,7 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
   uint32_t batch_code = 0;      // the gather in flight
   uint32_t batch_slot = 0;      // packed coding: the node slot under a link
 
-  auto settle_batch = [&]() {
-    if (!batch_open) return;
+  auto settle_batch = [&]() {  // requires batch_open; appends to Q3 (the caller drains it)
     batch_open = false;
     const bool mine = lane < batch_take;
     const bool lookup = mine && (batch_point & 0x80000000u) == 0u;
@@ -738,7 +737,6 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
 #ifdef GJ_EXP_NO_PHASE3  // timing experiment: results are wrong
     q3_count = 0;
 #endif
-    drain3(false);
   };
 
   auto issue_batch = [&](uint32_t take) {  // requires !batch_open
@@ -762,12 +760,19 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
     batch_open = true;
   };
 
+  // One loop with ONE settle site and ONE Q3 drain site: population 3's code (resolve_open) is large, and with the
+  // drains inlined at every settle it was instantiated nine times per kernel — 15 K SASS instructions, and
+  // instruction-cache stalls to match on the lookup-table-heavy configs.
   auto drain2 = [&](bool flush) {
     __syncwarp();
-    settle_batch();  // the batch issued one tile ago
-    while (q2_count >= 32u || (flush && q2_count)) {
+    for (;;) {
+      const bool had = batch_open;  // first turn: the batch issued one tile ago
+      if (had) settle_batch();
+      const bool more = q2_count >= 32u || (flush && q2_count != 0u);
+      if (had || (flush && !more)) drain3(flush && !more);  // Q3 holds < 32 + 32 items at this point
+      if (!more) break;
       issue_batch(min(q2_count, 32u));
-      if (q2_count >= 32u || flush) settle_batch();  // more to take: no point in deferring
+      if (!(q2_count >= 32u || flush)) break;  // nothing more to take: leave the batch in flight for a tile
     }
   };
 
@@ -867,9 +872,7 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
     for (; tile < n_full_tiles; tile += gridDim.x) tile_body(tile, std::true_type{});
   }
   if (tile < n_tiles) tile_body(tile, std::false_type{});  // the partial last tile, in one CTA
-  drain2(true);
-  settle_batch();
-  drain3(true);
+  drain2(true);  // settles what is in flight and flushes both queues
 
   if (jp.hist16) flush_hist16();
   __syncthreads();
