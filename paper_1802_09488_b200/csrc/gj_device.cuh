@@ -269,11 +269,11 @@ __device__ __forceinline__ uint64_t ld_arena(const uint64_t* p) { return __ldg(p
 // Trie descent from `node`, whose slots resolve the 4 grid levels below
 // `level_above` (act.cpp:258-268).  The index was validated at create time
 // (forest, depth bound), so the loop needs no bound of its own.
-__device__ __forceinline__ uint64_t walk_from(const DevIndex& ix, uint64_t node, int level_above,
+__device__ __forceinline__ uint64_t walk_from(const uint64_t* __restrict__ arena, uint64_t node, int level_above,
                                               uint32_t xl, uint32_t yl) {
   for (;;) {
     const uint32_t slot = chunk_slot(xl, yl, level_above);
-    const uint64_t e = ld_arena(ix.arena + (node - 1) * kNodeSlots + slot);
+    const uint64_t e = ld_arena(arena + (node - 1) * kNodeSlots + slot);
     if ((e & 3u) != 0u || e == 0u) return e;
     node = e >> 2;
     level_above += 4;
@@ -307,14 +307,14 @@ __device__ __forceinline__ uint64_t probe_point(const DevIndex& ix, const uint32
   if ((code & kDirLink) == 0) return __ldg(ix.dict + code);
   // truncate to the leaf level (cell_id.cpp:93-94), left-align to 32 bits
   const uint32_t keep = ~((1u << (30 - ix.leaf_level)) - 1u);
-  return walk_from(ix, code & ~kDirLink, ix.prefix_level0 + 4 * chunks, (x & keep) << 2, (y & keep) << 2);
+  return walk_from(ix.arena, code & ~kDirLink, ix.prefix_level0 + 4 * chunks, (x & keep) << 2, (y & keep) << 2);
 }
 
 // Generic probe of a raw cell id on any face without the directory: the
 // scalar walk of act.cpp:248-270 (used by gj_probe_cells_host, the
 // ProbeBatchFn-shaped test hook).
-__device__ __forceinline__ uint64_t probe_from_root(const DevIndex& ix, uint64_t raw, uint64_t node, uint32_t plen,
-                                                    uint64_t prefix) {
+__device__ __forceinline__ uint64_t probe_from_root(const uint64_t* __restrict__ arena, uint64_t raw, uint64_t node,
+                                                    uint32_t plen, uint64_t prefix) {
   if (node == 0) return 0;
   const uint64_t key = (raw ^ (raw & (~raw + 1))) << 3;  // key_of, act.hpp:142-145
   if (plen != 0 && (key >> (64 - plen)) != prefix) return 0;
@@ -323,7 +323,7 @@ __device__ __forceinline__ uint64_t probe_from_root(const DevIndex& ix, uint64_t
     // past the last key bit the reference's lockstep kernels would read
     // zeros; a validated index never gets there
     const uint32_t slot = shift >= 0 ? static_cast<uint32_t>(key >> shift) & 0xffu : 0u;
-    const uint64_t e = ld_arena(ix.arena + (node - 1) * kNodeSlots + slot);
+    const uint64_t e = ld_arena(arena + (node - 1) * kNodeSlots + slot);
     if ((e & 3u) != 0u || e == 0u) return e;
     node = e >> 2;
     shift -= 8;
@@ -332,14 +332,17 @@ __device__ __forceinline__ uint64_t probe_from_root(const DevIndex& ix, uint64_t
 
 __device__ __forceinline__ uint64_t probe_raw(const DevIndex& ix, uint64_t raw) {
   const uint32_t face = static_cast<uint32_t>(raw >> 61);  // faces 6,7 hold a zero root
-  return probe_from_root(ix, raw, ix.roots[face], ix.prefix_bits[face], ix.prefixes[face]);
+  return probe_from_root(ix.arena, raw, ix.roots[face], ix.prefix_bits[face], ix.prefixes[face]);
 }
 
 // The same for a cell id made by cell_from_point, which never sets face bits (cell_id.cpp:89-94).  K1's slow path
 // uses this form: indexing the face tables of the kernel parameter block with a run-time face made ptxas keep a
 // thread-local copy of the whole block in some instantiations.
+// (Tried and dropped: K1's two rare paths — this one and the deep walk, four IEEE divisions between them — as
+// __noinline__ functions to shrink population 3's code by another 450 instructions: the calls cost more in the
+// register allocation around them than the footprint gained, config-5 stand-in 2.26 -> 2.48 ms per 20 M points.)
 __device__ __forceinline__ uint64_t probe_raw_face0(const DevIndex& ix, uint64_t raw) {
-  return probe_from_root(ix, raw, ix.roots[0], ix.prefix_bits[0], ix.prefixes[0]);
+  return probe_from_root(ix.arena, raw, ix.roots[0], ix.prefix_bits[0], ix.prefixes[0]);
 }
 
 // ---------------------------------------------------------------------------

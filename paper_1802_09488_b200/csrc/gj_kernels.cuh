@@ -623,7 +623,7 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
           uint32_t x, y;
           grid_xy(q.x, q.y, &x, &y);
           const uint32_t leaf_keep = ~((1u << (30 - ix.leaf_level)) - 1u);  // cell_id.cpp:93-94
-          entry = walk_from(ix, node, level, (x & leaf_keep) << 2, (y & leaf_keep) << 2);
+          entry = walk_from(ix.arena, node, level, (x & leaf_keep) << 2, (y & leaf_keep) << 2);
         }
       } else if (c & kDirInline) {
         entry = (static_cast<uint64_t>(c & 0x3FFFFFFFu) << 2) | 1u;  // exact-mode candidate
@@ -859,17 +859,15 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
   };
   const uint32_t n_full_tiles = n / kTile;
   uint32_t tile = blockIdx.x;
-  if (jp.hist16) {  // every warp of the CTA runs the same number of tiles, so the barriers inside line up
-    uint32_t since = 0;
-    for (; tile < n_full_tiles; tile += gridDim.x) {
-      tile_body(tile, std::true_type{});
-      if (++since == kHist16FlushTiles) {
-        since = 0;
-        flush_hist16();
-      }
+  // (one loop for both counting forms: a second copy of the tile body is 2 500 instructions of cache footprint)
+  uint32_t since = 0;
+  for (; tile < n_full_tiles; tile += gridDim.x) {
+    tile_body(tile, std::true_type{});
+    // every warp of the CTA runs the same number of tiles, so the barriers inside the flush line up
+    if (jp.hist16 && ++since == kHist16FlushTiles) {
+      since = 0;
+      flush_hist16();
     }
-  } else {
-    for (; tile < n_full_tiles; tile += gridDim.x) tile_body(tile, std::true_type{});
   }
   if (tile < n_tiles) tile_body(tile, std::false_type{});  // the partial last tile, in one CTA
   drain2(true);  // settles what is in flight and flushes both queues
