@@ -382,18 +382,35 @@ def run_ours(args):
     if torch.cuda.device_count() <= local:
         raise SystemExit(f"bench.py: rank {rank} wants cuda:{local} but the box has {torch.cuda.device_count()} GPU(s)")
     torch.cuda.set_device(local)
-    if world > 1:
+    # under a launcher (torchrun sets RANK / MASTER_*) the NCCL group is created even for one rank, so that the
+    # rendezvous, the barriers and the all-reduces below run through the same code whatever N is
+    use_dist = world > 1 or ("RANK" in os.environ and "MASTER_PORT" in os.environ)
+    if use_dist:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # NCCL's communicator / transport lines (NVLS, P2P) stay on, on stderr: stdout carries the one JSON line
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        # (NCCL logs to stdout: fd 1 points at stderr while the communicator comes up and runs its first collective)
+        sys.stdout.flush()
+        saved_stdout = os.dup(1)
+        os.dup2(2, 1)
+        try:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+            dist.barrier()
+            torch.cuda.synchronize()
+        finally:
+            os.dup2(saved_stdout, 1)
+            os.close(saved_stdout)
+        log(f"[bench] rank {rank}: NCCL process group of {dist.get_world_size()} rank(s) up")
 
     def barrier():
-        if world > 1:
+        if use_dist:
             dist.barrier()
         torch.cuda.synchronize()
 
     n = args.points
     path = bundle_path() if rank == 0 else None
-    if world > 1:
+    if use_dist:
         dist.barrier()
         from tools import build_bundles
         path = build_bundles.bundle_file(build_bundles.workload_name(CONFIG))
@@ -447,7 +464,7 @@ def run_ours(args):
     total_ms = ev[0].elapsed_time(ev[-1])
     step_ms = [ev[k].elapsed_time(ev[k + 1]) for k in range(args.steps)]
     t = torch.tensor([total_ms], dtype=torch.float64, device="cuda")
-    if world > 1:
+    if use_dist:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms_max = float(t.item())
 
@@ -484,7 +501,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     te = time.perf_counter() - te0
     tt = torch.tensor([te], dtype=torch.float64, device="cuda")
-    if world > 1:
+    if use_dist:
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     e2e_s = float(tt.item())
 
@@ -496,9 +513,8 @@ def run_ours(args):
         raise SystemExit(f"bench.py: rank {rank}: device-resident and host-buffer first ids differ")
 
     if rank != 0:
-        if world > 1:
-            dist.barrier()
-            dist.destroy_process_group()
+        dist.barrier()
+        dist.destroy_process_group()
         return
 
     clocks = sampler.stop(wall0, wall1)
@@ -568,7 +584,7 @@ def run_ours(args):
         "secondary": secondary,
     }
     print(json.dumps(out), flush=True)
-    if world > 1:
+    if use_dist:
         dist.barrier()
         dist.destroy_process_group()
     bad_secondary = [x["config"] for x in (secondary or []) if x.get("counts_equal_reference") is False or
@@ -591,7 +607,7 @@ def launch_ranks(args, argv) -> int:
         sck.bind(("127.0.0.1", 0))
         port = sck.getsockname()[1]
     env = dict(os.environ)
-    env.setdefault("NCCL_DEBUG", "INFO")          # the communicator / transport lines (NVLS, P2P) go to stderr
+    env.setdefault("NCCL_DEBUG", "INFO")  # from process start; the ranks keep whatever NCCL prints off stdout (run_ours)
     env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
            "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve()), *argv]
@@ -611,14 +627,16 @@ def main(argv=None):
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-secondary", action="store_true", help="skip the other BASELINE configs (N = 1 only anyway)")
+    ap.add_argument("--spawn", action="store_true",
+                    help="start the ranks through torch.distributed.run even for --gpus 1 (what --gpus N > 1 does by itself)")
     args = ap.parse_args(argv)
     if args.gpus < 1:
         raise SystemExit("bench.py: --gpus must be >= 1")
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     if args.impl == "reference":
         run_reference(args)
-    elif args.gpus > 1 and "WORLD_SIZE" not in os.environ:
-        raise SystemExit(launch_ranks(args, argv))
+    elif (args.gpus > 1 or args.spawn) and "WORLD_SIZE" not in os.environ:
+        raise SystemExit(launch_ranks(args, [a for a in argv if a != "--spawn"]))
     else:
         run_ours(args)
 

@@ -39,7 +39,7 @@ def allreduce_counts(counts):
     """Sum a per-polygon count tensor over all ranks, in place.  A no-op
     without an initialised process group."""
     d = _dist()
-    if d and d.get_world_size() > 1:
+    if d:  # also with one rank: the collective then runs (trivially) through the same backend
         d.all_reduce(counts, op=d.ReduceOp.SUM)
     return counts
 

@@ -84,3 +84,21 @@ def test_own_arm_prints_one_contract_line():
     cb = d["cpu_baseline"]
     assert cb["kind"] in ("reference", "port") and cb["cores"] >= 1 and cb["value"] > 0 and cb["sample"]
     assert d["counts_equal_reference"] is True and d["secondary"] is None
+
+
+@pytest.mark.gpu
+def test_own_arm_through_its_own_launcher_and_nccl():
+    """``--spawn`` takes the route ``--gpus N > 1`` takes by itself — re-exec under torch.distributed.run, NCCL
+    process group, barriers, max-over-ranks timing, the counts all-reduce — with the one rank a one-GPU box allows."""
+    from tools import build_bundles
+    if not build_bundles.have_bundle(build_bundles.workload_name(2)):
+        pytest.skip("no cached config-2 index")
+    res = subprocess.run([sys.executable, str(ROOT / "bench.py"), "--gpus", "1", "--spawn", "--steps", "3", "--warmup", "3",
+                          "--points", "3000000", "--ref-points", "3000000", "--e2e-steps", "1", "--no-secondary"],
+                         capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert res.returncode == 0, res.stderr[-3000:]
+    lines = [l for l in res.stdout.splitlines() if l.strip()]
+    assert len(lines) == 1, res.stdout[-2000:]  # stdout carries the JSON line and nothing else
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 1 and d["gpu_launches"] == 3 and d["counts_equal_reference"] is True
+    assert "torch.distributed.run" in res.stderr and "NCCL process group of 1 rank(s) up" in res.stderr
