@@ -131,6 +131,7 @@ struct DevIndex {
   // dir2, otherwise 1 + ((polygon_id << 1) | interior).  K1 stages it instead
   // of `dir` when present; `table` then points at uint16 data.
   DevDirectory dir16;
+  int32_t dir16_live;  // 0: (almost) every cell of dir16 says "look in the 32-bit tier" — K1's kLate form skips the lookup
   // Optional refinement of the deepest 32-bit tier for K1 (`dirk`): the same
   // codes over a window 1-3 grid levels finer than a trie-node boundary.  A
   // cell resolves here when the aligned run of slots it owns in the node under

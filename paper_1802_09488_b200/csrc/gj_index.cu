@@ -645,6 +645,7 @@ int create_index(const gj_index_desc& d, int device, const gj_options* options, 
     }
     const uint64_t cells = static_cast<uint64_t>(an.dir16.width) * an.dir16.height;
     ix->ids_late = cells != 0 && open_cells * 2 > cells;
+    ix->dev.dir16_live = !(cells != 0 && open_cells * 20 > cells * 19);  // dead when more than 95 % of the cells are open
     if (opt.ids_late >= 0) ix->ids_late = opt.ids_late != 0;  // explicit knob / test hook
   }
   size_t bytes = 0;

@@ -512,6 +512,7 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
   const uint32_t s_q3 = s_q2 + kQueue2Cap * 8u;
   const uint32_t s_stage = kStage && jp.smem_stage_off ? smem_addr(smem + jp.smem_stage_off) + warp * jp.stage_chunks * 16u : 0u;
   const uint32_t hist_spare = ix.n_ids;  // the histogram has n_ids + 1 rows
+  const bool tier_live = ix.dir16_live != 0;
   const uint32_t lane_lt = (1u << lane) - 1u;
   const uint32_t d1_w = ix.dir16.width, d1_h = ix.dir16.height, d1_pitch = ix.dir16.pitch;
   const uint32_t d1_x0 = ix.dir16.x0, d1_y0 = ix.dir16.y0;
@@ -812,8 +813,9 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
       const bool ok = grid_xy_try(p[j].x, p[j].y, &x, &y) && live;  // valid, coordinates exact
       const uint32_t cx = min((x >> d1_shift) - d1_x0, d1_w);  // clamps into the all-miss padding
       const uint32_t cy = min((y >> d1_shift) - d1_y0, d1_h);
-      // 0 = miss, 0xFFFF = look in the 32-bit tier, else 1 + payload
-      const uint32_t e = lds16(s_table + (cy * d1_pitch + cx) * 2u) - 1u;
+      // 0 = miss, 0xFFFF = look in the 32-bit tier, else 1 + payload.  (kLate, dead tier — polygons smaller than its
+      // cells, BASELINE config 4: the answer is "look in the 32-bit tier" anyway, so the lookup is skipped.)
+      const uint32_t e = (kLate && !tier_live) ? 0xFFFEu : lds16(s_table + (cy * d1_pitch + cx) * 2u) - 1u;
       const bool emit = ok && e < 0xFFFEu && (e & need_interior) == need_interior;
       const uint32_t id = e >> 1;
       if (kDense) {  // unconditional: lanes that do not emit count into a spare row past the last slot

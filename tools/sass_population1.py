@@ -2,7 +2,7 @@
 
     python tools/sass_population1.py > profiles/sass_rNN_k1_population1.txt
 
-Instantiation join_kernel<kIds=true, kStats=false, kDense=true, kLate=false, kPipe3=false> — the kernel bench.py times.  The
+Instantiation join_kernel<kIds=true, kStats=false, kDense=true, kLate=false, kStage=false> — the kernel bench.py times.  The
 excerpt runs from the L2 prefetch + the four 16-byte evict-first point loads to the fourth queue append, i.e. the
 straight-line code every point passes through (grid coordinates in two DFMAs, 16-bit tier lookup, histogram
 increment, first-id store, ballot/popc queue append); what follows it in the kernel (queue drains, populations 2
