@@ -106,7 +106,7 @@ typedef struct {
   int32_t dir16_level;        /* the join kernel's shared-memory tier (16-bit codes) */
   int32_t dir16_width;
   int32_t dir16_height;
-  int32_t reserved0;
+  int32_t link_records;       /* link cells of the deepest tier that got a refinement record (0 = none built) */
 } gj_index_info;
 
 /* Explicit tuning knobs and test hooks (the shipped library reads NO environment
@@ -133,6 +133,14 @@ typedef struct {
                                    -1 = automatic (polygon sets whose records would exceed 32 MB), 0 = never, 1 = always */
   int32_t stage_lut;            /* lookup-table records of a population-3 batch staged in shared memory by the whole
                                    warp: -1 = automatic (tables of 256 MB and more), 0 = never, 1 = always */
+  int32_t link_sub;             /* sparse refinement of the deepest 32-bit tier for the join kernel: one 64-byte record
+                                   per LINK cell, 16 codes two grid levels finer, each resolved when the aligned run of
+                                   16 slots it owns in the linked node is uniform: -1 = automatic (trees too large for
+                                   palette nodes whose records stay L2-resident), 0 = never, 1 = always */
+  int32_t direct;               /* the join kernel's direct form — every point gathers its own code of the 32-bit tier,
+                                   asynchronously into shared memory, instead of being queued for it: -1 = automatic
+                                   (indexes whose shared-memory tier resolves nothing), 0 = never, 1 = whenever possible */
+  int32_t reserved1;
   uint64_t max_launch_points;   /* test hook: split device-resident calls into launches of this many points; 0 = none */
   uint64_t chunk_points;        /* host pipeline: points per chunk; 0 = default (3 M counts / 4 M pairs), min 4096 */
 } gj_options;

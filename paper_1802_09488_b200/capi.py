@@ -52,7 +52,7 @@ class IndexInfo(C.Structure):
         ("dir_dict_len", C.c_int32), ("dir2_level", C.c_int32), ("dir2_width", C.c_int32),
         ("dir2_height", C.c_int32), ("ids_dense", C.c_int32),
         ("dir16_level", C.c_int32), ("dir16_width", C.c_int32), ("dir16_height", C.c_int32),
-        ("reserved0", C.c_int32),
+        ("link_records", C.c_int32),
     ]
 
 
@@ -65,6 +65,7 @@ class Options(C.Structure):
         ("node_pal_max_mb", C.c_int32), ("tier_sub", C.c_int32), ("ids_late", C.c_int32),
         ("queue_unpacked", C.c_int32), ("queue_slot_hi_bits", C.c_int32), ("hist_rep_cap", C.c_int32),
         ("smem_pad", C.c_int32), ("debug_plan", C.c_int32), ("hist16", C.c_int32), ("strip_index", C.c_int32), ("stage_lut", C.c_int32),
+        ("link_sub", C.c_int32), ("direct", C.c_int32), ("reserved1", C.c_int32),
         ("max_launch_points", C.c_uint64), ("chunk_points", C.c_uint64),
     ]
 

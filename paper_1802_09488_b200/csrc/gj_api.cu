@@ -84,10 +84,11 @@ namespace {
 // it only takes what is left inside the carve-out step the rest already needs.
 SmemPlan plan_smem(const gj_index& ix) {
   SmemPlan p{};
-  const size_t table_bytes = static_cast<size_t>(ix.dev.dir16.n_table) * 2;
+  // (the direct form stages no tier, and its per-warp area is two staging buffers + a longer Q3)
+  const size_t table_bytes = ix.direct ? 0 : static_cast<size_t>(ix.dev.dir16.n_table) * 2;
   size_t at = align16(std::max<size_t>(table_bytes, 16));
   p.queue_off = static_cast<uint32_t>(at);
-  at += static_cast<size_t>(kJoinThreads / 32) * kQueueBytesPerWarp;
+  at += static_cast<size_t>(kJoinThreads / 32) * (ix.direct ? kDirectBytesPerWarp : kQueueBytesPerWarp);
   p.hist_off = static_cast<uint32_t>(at);
 #ifdef GJ_SMEM_LIMIT_KB  // tuning: leave room for more than one CTA per SM
   const size_t limit = static_cast<size_t>(GJ_SMEM_LIMIT_KB) << 10;
@@ -165,10 +166,10 @@ int allow_max_smem(const gj_index& ix, Kernel kernel) {
   return GJ_OK;
 }
 
-template <bool kIds, bool kStats, bool kDense, bool kLate, bool kStage>
+template <bool kIds, bool kStats, bool kDense, bool kLate, bool kStage, bool kDirect = false>
 int launch_join_kernel(gj_session* s, const JoinParams& jp, const SmemPlan& sp) {
   const gj_index& ix = *s->ix;
-  auto kernel = join_kernel<kIds, kStats, kDense, kLate, kStage>;
+  auto kernel = join_kernel<kIds, kStats, kDense, kLate, kStage, kDirect>;
   int rc = allow_max_smem(ix, kernel);
   if (rc != GJ_OK) return rc;
   int occ = 0;
@@ -300,6 +301,21 @@ int enqueue_join(gj_session* s, const JoinRequest& rq) {
   jp.n_priv = static_cast<uint32_t>(ix.sm_count);
   jp.exact = rq.exact ? 1 : 0;
 
+  // The direct form (join_kernel's kDirect): every point gathers its own code of the 32-bit tier; decided at index
+  // creation (gj_index::direct), the shared-memory plan above follows it.
+  if (ix.direct) {
+    const int variant = (rq.d_first_id ? 4 : 0) | (rq.want_stats ? 2 : 0) | (ix.dev.ids_dense && sp.hist_rep ? 1 : 0);
+    switch (variant) {
+      case 0: rc = launch_join_kernel<false, false, false, false, false, true>(s, jp, sp); break;
+      case 1: rc = launch_join_kernel<false, false, true, false, false, true>(s, jp, sp); break;
+      case 2: rc = launch_join_kernel<false, true, false, false, false, true>(s, jp, sp); break;
+      case 3: rc = launch_join_kernel<false, true, true, false, false, true>(s, jp, sp); break;
+      case 4: rc = launch_join_kernel<true, false, false, true, false, true>(s, jp, sp); break;
+      case 5: rc = launch_join_kernel<true, false, true, true, false, true>(s, jp, sp); break;
+      case 6: rc = launch_join_kernel<true, true, false, true, false, true>(s, jp, sp); break;
+      default: rc = launch_join_kernel<true, true, true, true, false, true>(s, jp, sp); break;
+    }
+  } else {
   const int variant = (rq.d_first_id && ix.ids_late ? 8 : 0) | (rq.d_first_id ? 4 : 0) | (rq.want_stats ? 2 : 0) |
                       (ix.dev.ids_dense && sp.hist_rep ? 1 : 0);
   switch (variant) {
@@ -315,6 +331,7 @@ int enqueue_join(gj_session* s, const JoinRequest& rq) {
     case 5: rc = launch_join_variant<true, false, true>(s, jp, sp); break;
     case 6: rc = launch_join_variant<true, true, false>(s, jp, sp); break;
     default: rc = launch_join_variant<true, true, true>(s, jp, sp); break;
+  }
   }
   if (rc != GJ_OK) return rc;
 

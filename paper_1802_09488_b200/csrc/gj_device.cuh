@@ -150,6 +150,17 @@ struct DevIndex {
   // burst).  Nodes with more than 4 distinct entries keep word 0 == ~0 and are
   // read from the arena.  Null when absent.
   const uint64_t* node_pal;
+  // Optional SPARSE refinement of the deepest 32-bit tier for K1 (trees too large for palette nodes: BASELINE
+  // config 4 at full size, 18 M nodes = 37 GB, where every open point costs a random 128-byte DRAM burst in the
+  // arena).  Only the tier's LINK cells are refined: link cell number j (1-based, in `tier_links`, a copy of the
+  // tier whose link codes hold j instead of the node) owns the 64-byte record link_sub[(j - 1) * 16 ..]: one code
+  // per aligned run of 16 slots (= one 128-byte line, a 4 x 4 block of cells two grid levels finer) of the linked
+  // node, in slot order.  A run that holds one terminal entry (or nothing) resolves there with the tier's own code
+  // forms; any other run keeps kDirLink | node and is read from the arena as before.  The records of a tier whose
+  // cells are a fifth links are a few tens of MB — they stay in L2 where the same refinement as a dense grid
+  // (`dirk`, 16x the tier) does not.  Null when absent; never together with `dirk`, only with the packed coding.
+  const uint32_t* link_sub;
+  const uint32_t* tier_links;
   const uint64_t* dict;  // [n_dict], dict[0] == 0
   uint32_t n_dict;
 };

@@ -243,11 +243,12 @@ struct gj_index {
   gj_options opt{};            // explicit knobs (gj_options_default unless the creator passed others)
   std::vector<uint32_t> ids;  // slot -> polygon id
   gj::DeviceBuffer d_arena, d_lut, d_ids, d_ring_off, d_ring_len, d_ring_xy, d_dir_table, d_dir_dict, d_dir2_table, d_dir16_table, d_dirk_table, d_node_pal,
-      d_strip_meta, d_strip_ptr, d_strip_edges, d_strip_eidx;
+      d_link_sub, d_tier_links, d_strip_meta, d_strip_ptr, d_strip_edges, d_strip_eidx;
   int sm_count = 0;
   size_t smem_optin = 0;
   bool stage_records = false;  // K1 stages the lookup-table records of a population-3 batch in shared memory (lookup-table-heavy indexes)
   bool ids_late = false;       // K1 writes first ids where a point is settled (join_kernel's kLate): the 16-bit tier resolves few cells
+  bool direct = false;         // K1 runs its direct form (join_kernel's kDirect): the 16-bit tier resolves (almost) nothing
   uint64_t max_refs = 0;       // most references behind one reachable entry
   uint64_t max_cand_refs = 0;  // most candidate references behind one entry
   // Points the device pointers of `dev` at this index's buffers (after uploads, and after gj_index_replicate
@@ -268,13 +269,16 @@ struct gj_index {
     dev.dir16.table = d_dir16_table.as<uint32_t>();
     dev.dirk.table = d_dirk_table.as<uint32_t>();
     dev.node_pal = d_node_pal.ptr ? d_node_pal.as<uint64_t>() : nullptr;
+    dev.link_sub = d_link_sub.ptr ? d_link_sub.as<uint32_t>() : nullptr;
+    dev.tier_links = d_tier_links.ptr ? d_tier_links.as<uint32_t>() : nullptr;
     dev.dict = d_dir_dict.as<uint64_t>();
   }
   // every device buffer, for replication
   std::vector<gj::DeviceBuffer gj_index::*> buffers() const {
     return {&gj_index::d_arena, &gj_index::d_lut, &gj_index::d_ids, &gj_index::d_ring_off, &gj_index::d_ring_len,
             &gj_index::d_ring_xy, &gj_index::d_dir_table, &gj_index::d_dir_dict, &gj_index::d_dir2_table,
-            &gj_index::d_dir16_table, &gj_index::d_dirk_table, &gj_index::d_node_pal, &gj_index::d_strip_meta,
+            &gj_index::d_dir16_table, &gj_index::d_dirk_table, &gj_index::d_node_pal, &gj_index::d_link_sub, &gj_index::d_tier_links,
+            &gj_index::d_strip_meta,
             &gj_index::d_strip_ptr, &gj_index::d_strip_edges, &gj_index::d_strip_eidx};
   }
 };

@@ -26,6 +26,8 @@ thread_local std::string g_error;
 constexpr uint64_t kMaxDirEntries = 32768;         // 128 KB of u32 codes (shared memory)
 constexpr uint64_t kMaxDir2Entries = 16ull << 20;  // 64 MB of u32 codes (stays in the 126 MB L2)
 constexpr uint64_t kMaxDirKEntries = 20ull << 20;  // the refined tier may take a little more: it replaces dir2 in K1
+// sparse refinement records + the tier they hang off: what stays in the 126 MB L2 next to the point stream
+constexpr uint64_t kMaxLinkSubBytes = 96ull << 20;
 constexpr double kDirKMinLinkShare = 0.25;         // refine only when at least this share of the deepest tier's cells are links
 // 136 KB of u16 codes: with K1's queues and histogram that stays inside the
 // 196 KB shared-memory carve-out step (60 KB of L1 left for loads in flight);
@@ -97,6 +99,8 @@ struct Analysis {
   HostDirectory dir16;         // K1's shared-memory tier (16-bit codes), see build_dir16
   HostDirectory dirk;          // K1's refined 32-bit tier (DevIndex::dirk); may be empty
   int dirk_sub = 0;            // its grid levels below the parent tier's (1..3)
+  std::vector<uint32_t> link_sub;    // K1's sparse refinement records (DevIndex::link_sub); may be empty
+  std::vector<uint32_t> tier_links;  // the deepest tier with record numbers in its link codes (DevIndex::tier_links)
   std::vector<uint64_t> dict;  // terminal entries that do not fit a directory code
   uint64_t max_refs = 0;       // most references behind one entry
   uint64_t max_cand_refs = 0;  // most candidate references behind one entry
@@ -431,6 +435,56 @@ int analyse(const gj_index_desc& d, const gj_options& opt, Analysis* out) {
             }
           }
         }
+        // K1's sparse refinement (DevIndex::link_sub): the same idea for the link cells ONLY — 16 codes per link
+        // cell, one per 128-byte line of the linked node (a 4 x 4 block two grid levels finer).  Automatic for
+        // trees that get no palette nodes (the arena is far beyond L2, every open point a DRAM burst) when the
+        // records stay L2-resident next to the tier; create_index drops it again if the queue coding ends up unpacked.
+        bool want_links = sub == 0 && n_links != 0;
+        if (want_links && opt.link_sub < 0) {
+          uint64_t max_pal = kMaxNodePalBytes;
+          if (opt.node_pal_max_mb >= 0) max_pal = static_cast<uint64_t>(opt.node_pal_max_mb) << 20;
+          want_links = d.node_count * 128 > max_pal && n_links * 64 + base.table.size() * 4 <= kMaxLinkSubBytes;
+        } else if (opt.link_sub == 0) {
+          want_links = false;
+        }
+        if (want_links) {
+          out->tier_links = base.table;
+          out->link_sub.reserve(n_links * 16);
+          uint32_t next_record = 0;
+          for (uint32_t y = 0; y < base.height; ++y) {
+            for (uint32_t x = 0; x < base.width; ++x) {
+              const size_t cell = static_cast<size_t>(y) * base.pitch + x;
+              const uint32_t c = base.table[cell];
+              if (!(c & kDirLink)) continue;
+              out->tier_links[cell] = kDirLink | ++next_record;
+              const uint64_t* slots = d.arena + (static_cast<uint64_t>(c & ~kDirLink) - 1) * kNodeSlots;
+              for (uint32_t q = 0; q < 16; ++q) {
+                const uint64_t* r0 = slots + q * 16u;
+                const uint64_t e = r0[0];
+                bool uniform = e == 0 || (e & 3) != 0;
+                for (uint32_t k = 1; k < 16 && uniform; ++k) uniform = r0[k] == e;
+                uint32_t code = c;  // mixed run: the node itself, read from the arena
+                if (uniform && e == 0) {
+                  code = 0;
+                } else if (uniform) {
+                  auto it = code_of.find(e);
+                  if (it == code_of.end()) {
+                    uint32_t nc;
+                    if ((e & 3) == 1 && ((e >> 2) & 0x7fffffffu) < kDirInline) {
+                      nc = kDirInline | static_cast<uint32_t>((e >> 2) & 0x3fffffffu);
+                    } else {
+                      nc = static_cast<uint32_t>(out->dict.size());
+                      out->dict.push_back(e);
+                    }
+                    it = code_of.emplace(e, nc).first;
+                  }
+                  code = it->second;
+                }
+                out->link_sub.push_back(code);
+              }
+            }
+          }
+        }
       }
     }
   }
@@ -479,6 +533,8 @@ gj_options default_options() {
   o.hist_rep_cap = -1;
   o.hist16 = -1;
   o.stage_lut = -1;
+  o.link_sub = -1;
+  o.direct = -1;
   o.strip_index = -1;
   return o;
 }
@@ -647,6 +703,8 @@ int create_index(const gj_index_desc& d, int device, const gj_options* options, 
     ix->ids_late = cells != 0 && open_cells * 2 > cells;
     ix->dev.dir16_live = !(cells != 0 && open_cells * 20 > cells * 19);  // dead when more than 95 % of the cells are open
     if (opt.ids_late >= 0) ix->ids_late = opt.ids_late != 0;  // explicit knob / test hook
+    // the direct form: every point gathers its own code of the 32-bit tier (no record staging in that form)
+    ix->direct = (opt.direct > 0 || (opt.direct < 0 && !ix->dev.dir16_live && n_ids != 0)) && !ix->stage_records;
   }
   size_t bytes = 0;
   if ((rc = upload(ix->d_arena, d.arena, d.node_count * kNodeSlots, &bytes)) != GJ_OK) return rc;
@@ -792,6 +850,12 @@ int create_index(const gj_index_desc& d, int device, const gj_options* options, 
     }
   }
   dv.n_dict = static_cast<uint32_t>(an.dict.size());
+  // K1's sparse refinement: items reach population 3 as (record, slot) only under the packed coding
+  if (dv.qc.packed && !an.link_sub.empty()) {
+    if ((rc = upload(ix->d_link_sub, an.link_sub.data(), an.link_sub.size(), &bytes)) != GJ_OK) return rc;
+    if ((rc = upload(ix->d_tier_links, an.tier_links.data(), an.tier_links.size(), &bytes)) != GJ_OK) return rc;
+    ix->info.link_records = static_cast<int32_t>(an.link_sub.size() / 16);
+  }
   ix->bind();
 
   cudaDeviceProp prop{};
@@ -849,6 +913,7 @@ int replicate_index(const gj_index& src, int device, gj_index** out) {
   ix->opt = src.opt;
   ix->ids = src.ids;
   ix->ids_late = src.ids_late;
+  ix->direct = src.direct;
   ix->stage_records = src.stage_records;
   ix->max_refs = src.max_refs;
   ix->max_cand_refs = src.max_cand_refs;

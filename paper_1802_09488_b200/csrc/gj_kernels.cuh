@@ -37,10 +37,16 @@ constexpr int kPointsPerThread = GJ_PPT;
 #define GJ_PF_DIST 1
 #endif
 constexpr uint32_t kQueueSlow = 0xFFFFFFFFu;  // queue word of a point population 1 would not decide
+constexpr uint32_t kDirectSkip = 0xFFFFFFFEu;  // kDirect: the staged code of a lane past the end of the points
 constexpr uint32_t kPrefetchTiles = GJ_PF_DIST;  // K1: L2 prefetch distance in tiles, 0 = off
 constexpr int kQueue2Cap = 32 * (kPointsPerThread + 1);
 constexpr int kQueue3Cap = 64;
 constexpr int kQueueBytesPerWarp = (kQueue2Cap + kQueue3Cap) * 8;
+// The direct form (join_kernel's kDirect) has no Q2: per warp two staging buffers of 128 codes + 128 node slots,
+// and a Q3 that takes what a whole tile can leave open (< 32 left over + 4 x 32).
+constexpr int kDirectBufBytes = 32 * kPointsPerThread * 5;
+constexpr int kDirectQueue3Cap = 32 * (kPointsPerThread + 1);
+constexpr int kDirectBytesPerWarp = 2 * kDirectBufBytes + kDirectQueue3Cap * 8;
 constexpr int kChunkPoints = 32 * kPointsPerThread;  // consecutive points a warp owns in a tile
 constexpr int kRefineThreads = 256;
 // The 16-bit histogram (JoinParams::hist16) is flushed by the whole CTA every this many tiles.  Between two
@@ -130,6 +136,11 @@ __device__ __forceinline__ void sts64_if(uint32_t addr, uint32_t x, uint32_t y, 
                "r"(y), "r"(static_cast<uint32_t>(pred))
                : "memory");
 }
+__device__ __forceinline__ void red_add_shared_if(uint32_t addr, uint32_t v, bool pred) {
+  asm volatile("{ .reg .pred p; setp.ne.u32 p, %2, 0; @p red.shared.add.u32 [%0], %1; }" ::"r"(addr), "r"(v),
+               "r"(static_cast<uint32_t>(pred))
+               : "memory");
+}
 __device__ __forceinline__ void red_inc_shared_if(uint32_t addr, bool pred) {
   asm volatile("{ .reg .pred p; setp.ne.u32 p, %1, 0; @p red.shared.add.u32 [%0], 1; }" ::"r"(addr),
                "r"(static_cast<uint32_t>(pred))
@@ -143,6 +154,25 @@ __device__ __forceinline__ uint32_t ldg32_if(const uint32_t* p, bool pred, uint3
   asm volatile("{ .reg .pred p; setp.ne.u32 p, %3, 0; mov.u32 %0, %2; @p ld.global.nc.u32 %0, [%1]; }"
                : "=r"(v)
                : "l"(p), "r"(otherwise), "r"(static_cast<uint32_t>(pred)));
+  return v;
+}
+// The same gather issued as an asynchronous copy into shared memory (LDGSTS): no register waits for it.
+__device__ __forceinline__ void cp_async4_if(uint32_t dst, const uint32_t* p, bool pred) {
+  asm volatile("{ .reg .pred p; setp.ne.u32 p, %2, 0; @p cp.async.ca.shared.global [%0], [%1], 4; }" ::"r"(dst), "l"(p),
+               "r"(static_cast<uint32_t>(pred))
+               : "memory");
+}
+__device__ __forceinline__ void sts32_if(uint32_t addr, uint32_t v, bool pred) {
+  asm volatile("{ .reg .pred p; setp.ne.u32 p, %2, 0; @p st.shared.u32 [%0], %1; }" ::"r"(addr), "r"(v),
+               "r"(static_cast<uint32_t>(pred))
+               : "memory");
+}
+__device__ __forceinline__ void sts8(uint32_t addr, uint32_t v) {
+  asm volatile("st.shared.u8 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ uint32_t lds8(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
   return v;
 }
 __device__ __forceinline__ void st32_if(uint32_t* p, uint32_t v, bool pred) {
@@ -479,7 +509,7 @@ __device__ __noinline__ uint32_t emit_general(const EmitCtx* ctx, HistRef h, uin
 // 4 % on the config-4 stand-in counts only, nothing with first ids, nothing at all on full-size config 5 (171.9 vs
 // 171.2 ms per 500 M points), and with JoinStats two instantiations kept thread-local copies of the parameter
 // blocks: 9.7 instead of 1.3 ms.)
-template <bool kIds, bool kStats, bool kDense, bool kLate = false, bool kStage = false>
+template <bool kIds, bool kStats, bool kDense, bool kLate = false, bool kStage = false, bool kDirect = false>
 __global__ void __launch_bounds__(kJoinThreads, GJ_JOIN_MIN_BLOCKS)
 join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinParams jp) {
   extern __shared__ __align__(16) unsigned char smem[];
@@ -493,10 +523,10 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
                     jp.task_point, jp.task_slot, jp.task_ord, jp.base_index, jp.ovf_cap, jp.task_cap, ix.n_ids,
                     ix.ids_dense, jp.exact, jp.ovf_discard};
   }
-  {  // stage the first directory tier, clear the histogram
+  {  // stage the first directory tier (the direct form does not use it), clear the histogram
     const uint4* src = reinterpret_cast<const uint4*>(ix.dir16.table);
     uint4* dst = reinterpret_cast<uint4*>(smem);
-    const uint32_t n4 = (ix.dir16.n_table * 2u + 15u) / 16u;  // buffers are padded to 16 B
+    const uint32_t n4 = kDirect ? 0u : (ix.dir16.n_table * 2u + 15u) / 16u;  // buffers are padded to 16 B
     for (uint32_t i = tid; i < n4; i += kJoinThreads) dst[i] = __ldg(src + i);
     uint32_t* hist = reinterpret_cast<uint32_t*>(smem + jp.smem_hist_off);
     const uint32_t n_hist = jp.hist16 ? (ix.n_ids + 2u) / 2u : (ix.n_ids + 1u) * jp.hist_rep;
@@ -508,10 +538,11 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
   const uint32_t s_table = smem_addr(smem);
   const HistRef hist{smem_addr(smem + jp.smem_hist_off), jp.hist_rep, lane & (jp.hist_rep ? jp.hist_rep - 1u : 0u), jp.hist16,
                      jp.counts_priv ? jp.counts_priv + static_cast<size_t>(blockIdx.x % jp.n_priv) * ix.n_ids : nullptr};
-  const uint32_t s_q2 = smem_addr(smem + jp.smem_queue_off) + warp * kQueueBytesPerWarp;
-  const uint32_t s_q3 = s_q2 + kQueue2Cap * 8u;
+  const uint32_t s_q2 = smem_addr(smem + jp.smem_queue_off) + warp * (kDirect ? kDirectBytesPerWarp : kQueueBytesPerWarp);
+  const uint32_t s_q3 = s_q2 + (kDirect ? 2u * kDirectBufBytes : kQueue2Cap * 8u);
   const uint32_t s_stage = kStage && jp.smem_stage_off ? smem_addr(smem + jp.smem_stage_off) + warp * jp.stage_chunks * 16u : 0u;
   const uint32_t hist_spare = ix.n_ids;  // the histogram has n_ids + 1 rows
+  const bool hist16_dense = !kDense && jp.hist16 != 0u && ix.ids_dense != 0;
   const bool tier_live = ix.dir16_live != 0;
   const uint32_t lane_lt = (1u << lane) - 1u;
   const uint32_t d1_w = ix.dir16.width, d1_h = ix.dir16.height, d1_pitch = ix.dir16.pitch;
@@ -520,7 +551,9 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
   // the 32-bit tier behind it: dirk, else dir2, else dir — its fields by value (a reference picked at run time among
   // three members of the parameter block is one of the things that made ptxas copy the block to local memory)
   const int tb_which = ix.dirk.n_table ? 2 : (ix.dir2.n_table ? 1 : 0);
-  const uint32_t* __restrict__ table2 = tb_which == 2 ? ix.dirk.table : (tb_which == 1 ? ix.dir2.table : ix.dir.table);
+  // (with the sparse refinement the tier is read from its copy whose link codes number the refinement records)
+  const uint32_t* __restrict__ table2 =
+      ix.link_sub ? ix.tier_links : (tb_which == 2 ? ix.dirk.table : (tb_which == 1 ? ix.dir2.table : ix.dir.table));
   const uint32_t tb_pitch = tb_which == 2 ? ix.dirk.pitch : (tb_which == 1 ? ix.dir2.pitch : ix.dir.pitch);
   const int tb_chunks = tb_which == 2 ? ix.dirk.chunks : (tb_which == 1 ? ix.dir2.chunks : ix.dir.chunks);
   const uint32_t qc_shift = ix.qc.shift, qc_mul = ix.qc.mul;
@@ -547,6 +580,8 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
     const uint32_t id = (c >> 1) & 0x1FFFFFFFu;
     if (kDense) {
       red_inc_shared_if(hist.smem + (id * hist.rep + hist.lane_rep) * 4u, emit);
+    } else if (hist16_dense) {  // the 16-bit histogram with id == slot: one predicated add, no branch per lane
+      red_add_shared_if(hist.smem + (id >> 1) * 4u, 1u << ((id & 1u) * 16u), emit);
     } else if (emit) {
       count_slot<kDense>(ix, jp, hist, id);
     }
@@ -599,10 +634,21 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
         int level = walk_level;
         bool walk = true;
         if (flagged) {  // the word is (node - 1) * 256 + (y sub-cell bits << 4 | x sub-cell bits)
-          const uint64_t at = queued_slot(iw, c);
+          uint64_t at = queued_slot(iw, c);
           const uint32_t slot = static_cast<uint32_t>(at) & 0xFFu;
           bool from_arena = true;
-          if (ix.node_pal) {  // the node's 128-byte palette form, usually an L2 hit
+          if (ix.link_sub) {
+            // sparse refinement: `at >> 8` numbers the link cell's record, not a node.  The code of the 16-slot run
+            // holding `slot` (an L2 hit) is a terminal in the tier's own forms, or the link to the node itself.
+            const uint32_t c2 = __ldg(ix.link_sub + static_cast<size_t>(at >> 8) * 16u + (slot >> 4));
+            if (c2 & kDirLink) {
+              at = static_cast<uint64_t>((c2 & ~kDirLink) - 1u) * kNodeSlots + slot;
+            } else {
+              from_arena = false;
+              entry = c2 == 0u ? 0ull
+                               : ((c2 & kDirInline) ? (static_cast<uint64_t>(c2 & 0x3FFFFFFFu) << 2) | 1u : __ldg(ix.dict + c2));
+            }
+          } else if (ix.node_pal) {  // the node's 128-byte palette form, usually an L2 hit
             const uint64_t* rec = ix.node_pal + (at >> 8) * 16u;
             const uint32_t codes = __ldg(reinterpret_cast<const uint32_t*>(rec + 4) + (slot >> 4));
             const uint64_t v = __ldg(rec + ((codes >> ((slot & 15u) * 2u)) & 3u));
@@ -859,10 +905,102 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
     }
     __syncthreads();
   };
+  // ---- kDirect: the form for indexes whose shared-memory tier is dead (polygons smaller than its cells: BASELINE
+  // config 4).  There EVERY point has to be looked up in the 32-bit tier, and sending all of them through Q2 —
+  // compact, store, load, decode, gather, settle — was 150 of the 240 instructions a point cost.  Here a lane gathers
+  // the codes of its own four points where it loads them, as asynchronous copies into shared memory (LDGSTS, no
+  // register waits for them), and settles them one tile LATER from there, so the gathers' L2 latency hides behind a
+  // whole tile of work (issued and consumed in the same tile it was exposed: 1.25 instead of 1.00 ms per 100 M
+  // points).  Instead of Q2 a warp has two staging buffers: 128 codes + 128 node slots (the 4 + 4 sub-cell bits
+  // under a link) = 640 bytes each.  Populations 1 and 2 collapse into ~70 instructions;
+  // population 3 is unchanged (resolve_open; its queue takes a whole tile's open points, so a tile settles in four
+  // straight-line rounds and ONE drain).  First ids are written as in the kLate form.
+  static_assert(!kDirect || (kLate == kIds && !kStage), "kDirect writes first ids late and does not stage records");
+  auto direct_issue = [&](uint32_t tile, uint32_t buf, auto full_tag) {
+    constexpr bool kFull = decltype(full_tag)::value;
+    const uint32_t base = tile * kTile + warp * kChunkPoints + lane;
+    prefetch_chunk(tile + kPrefetchTiles * gridDim.x);
+    double2 p[kPointsPerThread];
+#pragma unroll
+    for (int j = 0; j < kPointsPerThread; ++j) {
+      p[j] = __ldcs(pts + (kFull ? base + j * 32u : min(base + j * 32u, n - 1u)));
+    }
+    const uint32_t s_code = s_q2 + buf * kDirectBufBytes + lane * 4u;
+    const uint32_t s_slot = s_q2 + buf * kDirectBufBytes + kChunkPoints * 4u + lane;
+    const uint32_t tier_shift = ix.qc.tier_shift, sub_mask = ix.qc.sub_mask;
+#pragma unroll
+    for (int j = 0; j < kPointsPerThread; ++j) {
+      const bool live = kFull || base + j * 32u < n;
+      uint32_t x, y;  // left-aligned to 32 bits
+      const bool ok = grid_xy_try(p[j].x, p[j].y, &x, &y) && live;
+      const uint32_t qx = min((x >> qc_shift) - qc_x0, qc_xc);  // clamps into the all-miss padding
+      const uint32_t qy = min((y >> qc_shift) - qc_y0, qc_yc);
+      // packed coding: (qx, qy) is the cell at the next node boundary, tier_shift levels below the tier's; unpacked:
+      // the tier's own cell (tier_shift = 0, sub_mask = 0)
+      const uint32_t idx = (qy >> tier_shift) * tb_pitch + (qx >> tier_shift);
+      cp_async4_if(s_code + j * 128u, table2 + idx, ok);
+      // not looked up: a slow point (decided in population 3), or a lane past the end
+      sts32_if(s_code + j * 128u, live ? kQueueSlow : kDirectSkip, !ok);
+      sts8(s_slot + j * 32u, ((qy & sub_mask) << 4) | (qx & sub_mask));
+      if (kStats) n_valid += ok;
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  // Settles the tile staged in `buf` (its gathers have landed: the caller waited for the copy group): four
+  // straight-line rounds, then ONE Q3 drain site.
+  auto direct_settle = [&](uint32_t tile, uint32_t buf) {
+    const uint32_t base = tile * kTile + warp * kChunkPoints + lane;
+    const uint32_t s_code = s_q2 + buf * kDirectBufBytes + lane * 4u;
+    const uint32_t s_slot = s_q2 + buf * kDirectBufBytes + kChunkPoints * 4u + lane;
+    const uint32_t q_packed = ix.qc.packed, q_index_bits = ix.qc.index_bits, q_slow_mark = ix.qc.slow_mark;
+#pragma unroll
+    for (int j = 0; j < kPointsPerThread; ++j) {
+      const uint32_t i = base + j * 32u;
+      const uint32_t c = lds32(s_code + j * 128u);
+      const uint32_t slot = lds8(s_slot + j * 32u);
+      const bool mine = c != kDirectSkip;
+      const bool lookup = c < kDirectSkip;  // neither marker
+      const bool done = settle(c, lookup, i);
+      uint32_t fwd = c, fwd_point = lookup ? i : i | q_slow_mark;
+      if (lookup && q_packed && (c & kDirLink)) {  // as settle_batch: the arena slot under the link travels on
+        const uint64_t at = static_cast<uint64_t>((c & ~kDirLink) - 1u) * kNodeSlots + slot;
+        fwd = static_cast<uint32_t>(at);
+        fwd_point |= 0x80000000u | (static_cast<uint32_t>(at >> 32) << q_index_bits);
+      }
+      q3_count = enqueue(s_q3, q3_count, mine && !done, fwd_point, fwd);
+    }
+    drain3(false);  // Q3 holds < 32 items again
+  };
+
   const uint32_t n_full_tiles = n / kTile;
   uint32_t tile = blockIdx.x;
   // (one loop for both counting forms: a second copy of the tile body is 2 500 instructions of cache footprint)
   uint32_t since = 0;
+  if constexpr (kDirect) {
+    uint32_t prev = ~0u, buf = 0;  // the tile staged one turn ago, the buffer the next tile goes to
+    for (; tile < n_tiles; tile += gridDim.x) {  // (at most one CTA meets the partial last tile, as its last)
+      if (tile < n_full_tiles) {
+        direct_issue(tile, buf, std::true_type{});
+      } else {
+        direct_issue(tile, buf, std::false_type{});
+      }
+      if (prev != ~0u) {
+        asm volatile("cp.async.wait_group 1;" ::: "memory");  // all but the group just committed
+        direct_settle(prev, buf ^ 1u);
+      }
+      prev = tile;
+      buf ^= 1u;
+      // every warp of the CTA settles the same tiles, so the barriers inside the flush line up
+      if (jp.hist16 && ++since == kHist16FlushTiles) {
+        since = 0;
+        flush_hist16();
+      }
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncwarp();
+    if (prev != ~0u) direct_settle(prev, buf ^ 1u);
+    drain3(true);
+  } else {
   for (; tile < n_full_tiles; tile += gridDim.x) {
     tile_body(tile, std::true_type{});
     // every warp of the CTA runs the same number of tiles, so the barriers inside the flush line up
@@ -873,6 +1011,7 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
   }
   if (tile < n_tiles) tile_body(tile, std::false_type{});  // the partial last tile, in one CTA
   drain2(true);  // settles what is in flight and flushes both queues
+  }
 
   if (jp.hist16) flush_hist16();
   __syncthreads();

@@ -448,6 +448,90 @@ def test_refined_tier_matches_reference(name, sub):
         b.close()
 
 
+def _everything(b, pts):
+    """Every result form of the join, both modes, host-buffer and device-resident calls, ragged sizes."""
+    import torch
+    s = b.session()
+    out = []
+    for mode in (capi.GJ_MODE_EXACT, capi.GJ_MODE_APPROX):
+        for n in (len(pts), min(len(pts), 4097), min(len(pts), 31)):
+            st = join.JoinStats()
+            counts, first, (opt, oid) = s.join_count(pts[:n], mode, stats=st, want_ids=True)
+            out += [counts, first, opt, oid, np.array(st.as_tuple())]
+            counts2, _, _ = s.join_count(pts[:n], mode)
+            out += [counts2]
+            if n:
+                d_pts = torch.from_numpy(pts[:n]).cuda()
+                d_counts = torch.zeros(max(1, len(b.ids)), dtype=torch.int64, device="cuda")
+                d_first = torch.full((n,), 0x55555555, dtype=torch.int32, device="cuda")
+                torch.cuda.synchronize()
+                s.join_count_device(d_pts.data_ptr(), n, d_counts.data_ptr(), mode, d_first_id_ptr=d_first.data_ptr(), sync=True)
+                out += [d_counts.cpu().numpy(), d_first.cpu().numpy()]
+        row_ptr, ids = s.join_pairs(pts, mode)
+        out += [row_ptr, ids]
+    return out
+
+
+@pytest.mark.parametrize("name", ["cfg1_tess5_approx60m", "cfg2_tess16_approx4m", "cfg3_tess16_exact_trained",
+                                  "cfg4_tess36_approx1m_k56", "cfg5_stars_scaled", "kmax60_sparse_ids", "world_stars",
+                                  "join_small_exact", "join_small_approx", "kmax60_tiny_a", "kmax60_tiny_b", "empty_index"])
+def test_direct_form_matches_reference(name):
+    """join_kernel's direct form (kDirect): every point gathers its own code of the 32-bit
+    tier as an asynchronous copy into shared memory and is settled one tile later; chosen
+    by itself when the shared-memory tier resolves nothing (BASELINE config 4).  Forced here
+    on every fixture shape — the replicated histogram, general counting (hist_rep_cap=0 takes
+    the histogram away), the 16-bit flushed histogram, packed / wide / unpacked queue codings,
+    with the sparse refinement behind it — against the queued form.  Results must not change."""
+    fx = golden_util.load(name)
+    pts = np.ascontiguousarray(fx["points"])
+    base = dict(tier_sub=0)
+    plain = join.IndexBundle.load(golden_util.bundle_file(name), device=0, options=capi.Options(direct=0, link_sub=0, **base))
+    want = _everything(plain, pts)
+    plain.close()
+    for extra in ({}, {"hist_rep_cap": 0}, {"hist16": 1}, {"link_sub": 1}, {"link_sub": 1, "hist16": 1, "queue_slot_hi_bits": 2},
+                  {"queue_unpacked": 1, "hist_rep_cap": 0}):
+        b = join.IndexBundle.load(golden_util.bundle_file(name), device=0, options=capi.Options(direct=1, **{**base, **extra}))
+        _check_join_against_fixture(b, fx)
+        got = _everything(b, pts)
+        assert len(got) == len(want)
+        for k, (a, c) in enumerate(zip(want, got)):
+            assert np.array_equal(a, c), (extra, k)
+        b.close()
+
+
+@pytest.mark.parametrize("name", ["cfg2_tess16_approx4m", "cfg3_tess16_exact_trained", "cfg4_tess36_approx1m_k56",
+                                  "cfg5_stars_scaled", "kmax60_sparse_ids", "world_stars", "join_small_exact",
+                                  "kmax60_tiny_a", "kmax60_tiny_b"])
+def test_sparse_refinement_matches_reference(name):
+    """K1's sparse refinement (DevIndex::link_sub): one 64-byte record per LINK cell of
+    the deepest tier, a code per 16-slot run of the linked node.  Built by itself only for
+    trees too large for palette nodes (BASELINE config 4 at full size); forced here on
+    every fixture shape, with and without palette nodes behind it, with the wide-arena
+    queue coding, and with the unpacked coding (where it must be dropped).  Results must
+    not change."""
+    fx = golden_util.load(name)
+    pts = np.ascontiguousarray(fx["points"])
+    everything = lambda b: _everything(b, pts)
+    plain = join.IndexBundle.load(golden_util.bundle_file(name), device=0, options=capi.Options(link_sub=0, tier_sub=0))
+    assert plain.info.link_records == 0
+    want = everything(plain)
+    plain.close()
+    built = 0
+    for extra in ({}, {"node_pal_max_mb": 0}, {"queue_slot_hi_bits": 2}, {"queue_unpacked": 1}, {"ids_late": 1}):
+        b = join.IndexBundle.load(golden_util.bundle_file(name), device=0, options=capi.Options(link_sub=1, tier_sub=0, **extra))
+        if extra.get("queue_unpacked"):
+            assert b.info.link_records == 0
+        built += b.info.link_records
+        _check_join_against_fixture(b, fx)
+        got = everything(b)
+        assert len(got) == len(want)
+        for a, c in zip(want, got):
+            assert np.array_equal(a, c)
+        b.close()
+    if name.startswith("cfg"):
+        assert built > 0  # the fixture does exercise the records
+
+
 def test_arena_beyond_2_24_nodes_matches_reference():
     """A REAL arena of more than 2^24 nodes (34 GB): the nodes of a fixture index
     renumbered to sit above 2^24 empty, unreachable nodes, so every arena slot the

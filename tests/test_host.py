@@ -31,7 +31,7 @@ def test_header_structs_match_ctypes_layout():
     assert C.sizeof(capi.Stats) == 48
     assert C.sizeof(capi.IndexInfo) == 5 * 8 + 16 * 4
     assert C.sizeof(capi.Overflow) == 32
-    assert C.sizeof(capi.Options) == 14 * 4 + 2 * 8
+    assert C.sizeof(capi.Options) == 17 * 4 + 4 + 2 * 8  # 17 words, padding, two u64
     o = capi.Options(tier_sub=2)  # gj_options_default + overrides
     assert o.struct_size == C.sizeof(capi.Options) and o.tier_sub == 2
     assert (o.ids_late, o.hist_rep_cap, o.node_pal_max_mb, o.max_launch_points, o.chunk_points) == (-1, -1, -1, 0, 0)
