@@ -272,8 +272,9 @@ SECONDARY = [
      "configs[2]: exact join, trained index, 289 polygons, 100 M mixture points, ~1 % on edges / vertices (FULL size)"),
     (4, 0.04, 40_000_000, {"dir16_level_max": 17, "hist16": 1},
      "configs[3] regime on its density-matched 4 % index (1 600 polygons at 1 m, k_max 56; shared-memory tier capped "
-     "at the level the full-size box gets and the 16-bit flushed histogram the full config's 40 000 ids force); the "
-     "full 40 000-polygon / 1 B-point run is tools/fullsize.py 4 (profiles/fullsize_r02_cfg4.json)"),
+     "at the level the full-size box gets and the 16-bit flushed histogram the full config's 40 000 ids force; the join "
+     "kernel runs its direct form with the sparse refinement of the tier's link cells, as at full size); the "
+     "full 40 000-polygon / 1 B-point run is tools/fullsize.py 4 (profiles/fullsize_r02_cfg4_direct.json)"),
     (5, 0.03, 10_000_000, {},
      "configs[4] regime on its density-matched 3 % index (300 overlapping stars, every probe a lookup-table "
      "record, exact); the full 10 000-star / 500 M-point run is tools/fullsize.py 5 (profiles/fullsize_r02_cfg5.json)"),
@@ -355,7 +356,8 @@ def run_secondary(torch, capi, join, peak, reps=5):
             "counts_equal_reference": bool(equal), "csr": csr,
             "cpu_baseline": {"value": n / cpu_s, "unit": "points/s", "cores": cores, "kind": kind,
                              "sample": f"all {n} points, per-polygon counts, {cpu_s:.2f}s"},
-            "options": opt, "seconds_total": round(time.time() - t_all, 1),
+            "options": opt, "k1_direct_form": int(bundle.info.k1_direct), "link_records": int(bundle.info.link_records),
+            "seconds_total": round(time.time() - t_all, 1),
         })
         log(f"[bench] secondary config {config}: {ms:.3f} ms per {n} points, frac {achieved / peak:.3f}, "
             f"counts equal reference: {equal} ({time.time() - t_all:.1f}s)")

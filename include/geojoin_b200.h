@@ -107,6 +107,8 @@ typedef struct {
   int32_t dir16_width;
   int32_t dir16_height;
   int32_t link_records;       /* link cells of the deepest tier that got a refinement record (0 = none built) */
+  int32_t k1_direct;          /* 1 when the join kernel runs its direct form on this index (gj_options.direct) */
+  int32_t reserved0;
 } gj_index_info;
 
 /* Explicit tuning knobs and test hooks (the shipped library reads NO environment

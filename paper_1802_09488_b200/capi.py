@@ -52,7 +52,7 @@ class IndexInfo(C.Structure):
         ("dir_dict_len", C.c_int32), ("dir2_level", C.c_int32), ("dir2_width", C.c_int32),
         ("dir2_height", C.c_int32), ("ids_dense", C.c_int32),
         ("dir16_level", C.c_int32), ("dir16_width", C.c_int32), ("dir16_height", C.c_int32),
-        ("link_records", C.c_int32),
+        ("link_records", C.c_int32), ("k1_direct", C.c_int32), ("reserved0", C.c_int32),
     ]
 
 

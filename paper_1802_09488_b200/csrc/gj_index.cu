@@ -883,6 +883,7 @@ int create_index(const gj_index_desc& d, int device, const gj_options* options, 
   info.dir2_width = static_cast<int32_t>(an.dir2.width);
   info.dir2_height = static_cast<int32_t>(an.dir2.height);
   info.ids_dense = dense ? 1 : 0;
+  info.k1_direct = ix->direct ? 1 : 0;
   *out = ix.release();
   return GJ_OK;
 }

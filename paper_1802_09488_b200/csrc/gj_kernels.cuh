@@ -44,9 +44,13 @@ constexpr int kQueue3Cap = 64;
 constexpr int kQueueBytesPerWarp = (kQueue2Cap + kQueue3Cap) * 8;
 // The direct form (join_kernel's kDirect) has no Q2: per warp two staging buffers of 128 codes + 128 node slots,
 // and a Q3 that takes what a whole tile can leave open (< 32 left over + 4 x 32).
+// Its queue area is shared by Q3, growing up from the bottom (< 32 left over + 2 x 32 per half tile), and Q4,
+// growing down from the top: the few open points whose walk goes deeper than the queued sub-cell bits reach
+// (< 32 left over + at most what a Q3 batch hands over, which Q3 has just given up).
 constexpr int kDirectBufBytes = 32 * kPointsPerThread * 5;
-constexpr int kDirectQueue3Cap = 32 * (kPointsPerThread + 1);
+constexpr int kDirectQueue3Cap = 128;
 constexpr int kDirectBytesPerWarp = 2 * kDirectBufBytes + kDirectQueue3Cap * 8;
+static_assert(kPointsPerThread % 2 == 0 && 31 + 32 * (kPointsPerThread / 2) + 31 <= kDirectQueue3Cap, "Q3 + Q4 share the area");
 constexpr int kChunkPoints = 32 * kPointsPerThread;  // consecutive points a warp owns in a tile
 constexpr int kRefineThreads = 256;
 // The 16-bit histogram (JoinParams::hist16) is flushed by the whole CTA every this many tiles.  Between two
@@ -568,7 +572,7 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
   const uint32_t emit_bits = kDirInline | need_interior;
 
   uint32_t n_valid = 0, false_hits = 0, solely_true = 0, refined = 0, cand_refs = 0;
-  uint32_t q2_count = 0, q3_count = 0;  // warp-uniform
+  uint32_t q2_count = 0, q3_count = 0, q4_count = 0;  // warp-uniform
 
   // One resolved 32-bit directory code of a point of population 2: count,
   // stats, first id.  Returns true when the point is finished (inlined emit or
@@ -613,12 +617,26 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
     const uint32_t slot = (spread4((c >> 4) & 0xFu) << 1) | spread4(c & 0xFu);  // chunk_slot
     return (static_cast<uint64_t>((iw & 0x7FFFFFFFu) >> ix.qc.index_bits) << 32) | (static_cast<uint64_t>(c) & ~0xFFull) | slot;
   };
-  auto resolve_open = [&](bool mine, uint32_t iw, uint32_t c) {
+  // `deep` (kDirect only, warp-uniform): the batch comes from Q4 — items (point, node) whose walk continues below
+  // the sub-cell bits the queue word carried.  In the queued form such a lane walks on inside its Q3 batch; here
+  // it is set aside, because ONE such lane makes the whole batch wait for two more dependent DRAM round trips (the
+  // point, then the deeper node) and run 75 more instructions — 2.5 % of the open points of BASELINE config 4, but
+  // 85 % of its batches.
+  auto resolve_open = [&](bool mine, uint32_t iw, uint32_t c, bool deep) {
     const uint32_t q_index_bits = ix.qc.index_bits, q_slow_mark = ix.qc.slow_mark;
-    const uint32_t i = iw & ((1u << q_index_bits) - 1u);
+    const uint32_t i = (kDirect && deep) ? iw : iw & ((1u << q_index_bits) - 1u);
     const bool flagged = (iw & 0x80000000u) != 0u;
     uint64_t entry = 0;
-    if (mine) {
+    bool defer = false;
+    if (kDirect && deep) {
+      if (mine) {
+        const double2 q = __ldg(pts + i);
+        uint32_t x, y;
+        grid_xy(q.x, q.y, &x, &y);
+        const uint32_t leaf_keep = ~((1u << (30 - ix.leaf_level)) - 1u);  // cell_id.cpp:93-94
+        entry = walk_from(ix.arena, c, ix.prefix_level0 + 4 * tb_chunks + 4, (x & leaf_keep) << 2, (y & leaf_keep) << 2);
+      }
+    } else if (mine) {
       if (c == kQueueSlow && (iw & q_slow_mark) == q_slow_mark) {  // nothing decided yet: the reference's own sequence
         const double2 q = __ldg(pts + i);
         if (!latlng_valid(q.x, q.y)) {
@@ -664,6 +682,11 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
           walk = (entry & 3u) == 0u && entry != 0u;  // a link again: deeper than the queued bits reach
           node = entry >> 2;
           level += 4;
+          if (kDirect && walk) {  // goes to Q4 as (point, node)
+            defer = true;
+            walk = false;
+            c = static_cast<uint32_t>(node);
+          }
         }
         if (walk) {
           const double2 q = __ldg(pts + i);
@@ -676,6 +699,15 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
         entry = (static_cast<uint64_t>(c & 0x3FFFFFFFu) << 2) | 1u;  // exact-mode candidate
       } else {
         entry = __ldg(ix.dict + c);
+      }
+    }
+    if (kDirect && !deep) {  // (a Q4 batch adds nothing: walk_from ends in a terminal entry)
+      const uint32_t mask = __ballot_sync(0xffffffffu, defer);
+      sts64_if(s_q3 + (kDirectQueue3Cap - 1u - (q4_count + __popc(mask & lane_lt))) * 8u, i, c, defer);
+      q4_count += __popc(mask);
+      if (defer) {
+        mine = false;
+        entry = 0;
       }
     }
     const bool single = (static_cast<uint32_t>(entry) & 3u) == 1u &&
@@ -745,14 +777,24 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
     return count + __popc(mask);
   };
 
-  auto drain3 = [&](bool flush) {
+  auto drain3 = [&](bool flush) {  // ONE resolve_open site for both queues
     __syncwarp();
-    while (q3_count >= 32u || (flush && q3_count)) {
-      const uint32_t take = min(q3_count, 32u);
-      q3_count -= take;
-      const uint2 item = lds64(s_q3 + (q3_count + min(lane, take - 1u)) * 8u);
+    for (;;) {
+      const bool deep = kDirect && (q4_count >= 32u || (flush && q3_count == 0u && q4_count != 0u));
+      if (!deep && !(q3_count >= 32u || (flush && q3_count))) break;
+      uint32_t take, at;
+      if (deep) {
+        take = min(q4_count, 32u);
+        q4_count -= take;
+        at = kDirectQueue3Cap - 1u - (q4_count + min(lane, take - 1u));
+      } else {
+        take = min(q3_count, 32u);
+        q3_count -= take;
+        at = q3_count + min(lane, take - 1u);
+      }
+      const uint2 item = lds64(s_q3 + at * 8u);
       __syncwarp();
-      resolve_open(lane < take, item.x, item.y);
+      resolve_open(lane < take, item.x, item.y, deep);
     }
   };
 
@@ -913,8 +955,8 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
   // whole tile of work (issued and consumed in the same tile it was exposed: 1.25 instead of 1.00 ms per 100 M
   // points).  Instead of Q2 a warp has two staging buffers: 128 codes + 128 node slots (the 4 + 4 sub-cell bits
   // under a link) = 640 bytes each.  Populations 1 and 2 collapse into ~70 instructions;
-  // population 3 is unchanged (resolve_open; its queue takes a whole tile's open points, so a tile settles in four
-  // straight-line rounds and ONE drain).  First ids are written as in the kLate form.
+  // population 3 is resolve_open as before, except that walks below the queued sub-cell bits wait in a queue of
+  // their own (Q4, see resolve_open).  First ids are written as in the kLate form.
   static_assert(!kDirect || (kLate == kIds && !kStage), "kDirect writes first ids late and does not stage records");
   auto direct_issue = [&](uint32_t tile, uint32_t buf, auto full_tag) {
     constexpr bool kFull = decltype(full_tag)::value;
@@ -946,30 +988,34 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
-  // Settles the tile staged in `buf` (its gathers have landed: the caller waited for the copy group): four
-  // straight-line rounds, then ONE Q3 drain site.
+  // Settles the tile staged in `buf` (its gathers have landed: the caller waited for the copy group): twice two
+  // straight-line rounds and the drain site.
   auto direct_settle = [&](uint32_t tile, uint32_t buf) {
     const uint32_t base = tile * kTile + warp * kChunkPoints + lane;
     const uint32_t s_code = s_q2 + buf * kDirectBufBytes + lane * 4u;
     const uint32_t s_slot = s_q2 + buf * kDirectBufBytes + kChunkPoints * 4u + lane;
     const uint32_t q_packed = ix.qc.packed, q_index_bits = ix.qc.index_bits, q_slow_mark = ix.qc.slow_mark;
+#pragma unroll 1
+    for (uint32_t half = 0; half < kPointsPerThread / 2u; ++half) {  // two rounds, then the drain site
 #pragma unroll
-    for (int j = 0; j < kPointsPerThread; ++j) {
-      const uint32_t i = base + j * 32u;
-      const uint32_t c = lds32(s_code + j * 128u);
-      const uint32_t slot = lds8(s_slot + j * 32u);
-      const bool mine = c != kDirectSkip;
-      const bool lookup = c < kDirectSkip;  // neither marker
-      const bool done = settle(c, lookup, i);
-      uint32_t fwd = c, fwd_point = lookup ? i : i | q_slow_mark;
-      if (lookup && q_packed && (c & kDirLink)) {  // as settle_batch: the arena slot under the link travels on
-        const uint64_t at = static_cast<uint64_t>((c & ~kDirLink) - 1u) * kNodeSlots + slot;
-        fwd = static_cast<uint32_t>(at);
-        fwd_point |= 0x80000000u | (static_cast<uint32_t>(at >> 32) << q_index_bits);
+      for (uint32_t jj = 0; jj < 2u; ++jj) {
+        const uint32_t j = half * 2u + jj;
+        const uint32_t i = base + j * 32u;
+        const uint32_t c = lds32(s_code + j * 128u);
+        const uint32_t slot = lds8(s_slot + j * 32u);
+        const bool mine = c != kDirectSkip;
+        const bool lookup = c < kDirectSkip;  // neither marker
+        const bool done = settle(c, lookup, i);
+        uint32_t fwd = c, fwd_point = lookup ? i : i | q_slow_mark;
+        if (lookup && q_packed && (c & kDirLink)) {  // as settle_batch: the arena slot under the link travels on
+          const uint64_t at = static_cast<uint64_t>((c & ~kDirLink) - 1u) * kNodeSlots + slot;
+          fwd = static_cast<uint32_t>(at);
+          fwd_point |= 0x80000000u | (static_cast<uint32_t>(at >> 32) << q_index_bits);
+        }
+        q3_count = enqueue(s_q3, q3_count, mine && !done, fwd_point, fwd);
       }
-      q3_count = enqueue(s_q3, q3_count, mine && !done, fwd_point, fwd);
+      drain3(false);  // Q3 and Q4 hold < 32 items each again
     }
-    drain3(false);  // Q3 holds < 32 items again
   };
 
   const uint32_t n_full_tiles = n / kTile;

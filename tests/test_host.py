@@ -29,7 +29,7 @@ def test_library_exports_every_declared_symbol():
 def test_header_structs_match_ctypes_layout():
     assert C.sizeof(capi.IndexDesc) == 8 + 8 + 8 + 8 + 3 * 64 + 4 + 4 + 8 + 3 * 8
     assert C.sizeof(capi.Stats) == 48
-    assert C.sizeof(capi.IndexInfo) == 5 * 8 + 16 * 4
+    assert C.sizeof(capi.IndexInfo) == 5 * 8 + 18 * 4
     assert C.sizeof(capi.Overflow) == 32
     assert C.sizeof(capi.Options) == 17 * 4 + 4 + 2 * 8  # 17 words, padding, two u64
     o = capi.Options(tier_sub=2)  # gj_options_default + overrides

@@ -104,7 +104,7 @@ def run_config(config: int, n_points: int, scale: float, reps: int, check: int, 
         "ms": ms, "gpoints_per_s": n / ms / 1e6, "launches_per_step": (launches1 - launches0) // reps, "ids": want_ids, "stats_collected": want_stats,
         "index_nodes": int(info.node_count), "index_mb": info.device_bytes / 1e6, "n_polygons": int(info.n_polygons),
         "dir1_level": info.dir_level, "dir2_level": info.dir2_level, "dir16_level": info.dir16_level,
-        "link_records": int(info.link_records), "dir16_cells": [info.dir16_width, info.dir16_height], "dir2_cells": [info.dir2_width, info.dir2_height],
+        "link_records": int(info.link_records), "k1_direct": int(info.k1_direct), "dir16_cells": [info.dir16_width, info.dir16_height], "dir2_cells": [info.dir2_width, info.dir2_height],
         "stats": dict(zip(["probes", "pip_tests", "false_hits", "solely_true_hits", "refinement_entered",
                            "candidate_refs"], stats)),
         "pairs_per_point": float(counts.sum()) / n,

@@ -97,10 +97,10 @@ def run(config: int, scale: float, n_points: int, launch: int, check: int, reps:
         "index_nodes": int(info.node_count), "index_lut_words": int(i.lut_len), "index_device_gb": info.device_bytes / 1e9,
         "n_polygons": int(info.n_polygons), "k_max": int(rb.k_max), "bound_m": float(i.achieved_precision_m),
         "dir1_level": info.dir_level, "dir2_level": info.dir2_level, "dir16_level": info.dir16_level,
-        "link_records": int(info.link_records),
+        "link_records": int(info.link_records), "k1_direct": int(info.k1_direct),
     })
     log(f"device index created in {res['index_create_s']}s: {res['index_device_gb']:.2f} GB in HBM, tiers "
-        f"{info.dir16_level}/{info.dir_level}/{info.dir2_level}, {info.link_records} sparse refinement records")
+        f"{info.dir16_level}/{info.dir_level}/{info.dir2_level}, {info.link_records} sparse refinement records, direct form {info.k1_direct}")
 
     # ---- points ----
     n = min(n_points, spec.n_points)
