@@ -519,7 +519,9 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
   extern __shared__ __align__(16) unsigned char smem[];
   const uint32_t tid = threadIdx.x;
   const uint32_t lane = tid & 31u;
-  const uint32_t warp = tid >> 5;
+  // (through a shuffle the compiler knows the warp index is warp-uniform, and keeps what derives from it — queue
+  // addresses, tile bases — in uniform registers, outside the 64 registers a thread has here)
+  const uint32_t warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
 
   __shared__ EmitCtx s_ctx;
   if (tid == 0) {
