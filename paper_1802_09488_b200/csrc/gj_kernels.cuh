@@ -42,22 +42,32 @@ constexpr uint32_t kPrefetchTiles = GJ_PF_DIST;  // K1: L2 prefetch distance in 
 constexpr int kQueue2Cap = 32 * (kPointsPerThread + 1);
 constexpr int kQueue3Cap = 64;
 constexpr int kQueueBytesPerWarp = (kQueue2Cap + kQueue3Cap) * 8;
-// The direct form (join_kernel's kDirect) has no Q2: per warp two staging buffers of 128 codes + 128 node slots,
-// and a Q3 that takes what a whole tile can leave open (< 32 left over + 4 x 32).
-// Its queue area is shared by Q3, growing up from the bottom (< 32 left over + 2 x 32 per half tile), and Q4,
-// growing down from the top: the few open points whose walk goes deeper than the queued sub-cell bits reach
-// (< 32 left over + at most what a Q3 batch hands over, which Q3 has just given up).
+// The direct form (join_kernel's kDirect) has no Q2: per warp two staging buffers of 128 codes + 128 node slots
+// and one queue area shared by Q3, growing up from the bottom (< 32 left over + 32 per settle round between two
+// visits of the drain site), and Q4, growing down from the top: the few open points whose walk goes deeper than the
+// queued sub-cell bits reach (< 32 left over + at most what a Q3 batch hands over, which Q3 has just given up).
+// Two rounds per drain visit, not four: four straight rounds are 7 % faster on an index with a small histogram
+// (0.672 vs 0.724 ms per 100 M points, config-4 stand-in), but their 192-entry area pushes BASELINE config 4 at full
+// size (80 KB of 16-bit histogram) over the 164 KB carve-out step, where they lose 5 % instead (0.791 vs 0.750 ms
+// with the stand-in padded to that size; profiles/k1_sweep_r02_cfg4_standin_direct_rounds_padded.json).
+#ifndef GJ_DIRECT_ROUNDS
+#define GJ_DIRECT_ROUNDS 2
+#endif
+constexpr int kDirectRounds = GJ_DIRECT_ROUNDS;  // settle rounds between two visits of the drain site
 constexpr int kDirectBufBytes = 32 * kPointsPerThread * 5;
-constexpr int kDirectQueue3Cap = 128;
+constexpr int kDirectQueue3Cap = 64 + 32 * kDirectRounds;
 constexpr int kDirectBytesPerWarp = 2 * kDirectBufBytes + kDirectQueue3Cap * 8;
-static_assert(kPointsPerThread % 2 == 0 && 31 + 32 * (kPointsPerThread / 2) + 31 <= kDirectQueue3Cap, "Q3 + Q4 share the area");
+static_assert(kPointsPerThread % kDirectRounds == 0 && 31 + 32 * kDirectRounds + 31 <= kDirectQueue3Cap, "Q3 + Q4 share the area");
 constexpr int kChunkPoints = 32 * kPointsPerThread;  // consecutive points a warp owns in a tile
 constexpr int kRefineThreads = 256;
 // The 16-bit histogram (JoinParams::hist16) is flushed by the whole CTA every this many tiles.  Between two
 // flushes a CTA settles at most the points it loaded since (kTile per tile) plus what its queues and in-flight
-// batches carried over (< 32 warps * (kQueue2Cap + kQueue3Cap + 32) = 8192), and a point adds at most 1 to any
-// one polygon: 12 * 4096 + 8192 = 57344 < 65536, so no counter can overflow.
+// batches carried over (< 32 warps * (kQueue2Cap + kQueue3Cap + 32) = 8192; direct form: the staged tile, 4096,
+// + 32 warps * kDirectQueue3Cap = 4096), and a point adds at most 1 to any one polygon: 12 * 4096 + 8192 = 57344
+// < 65536, so no counter can overflow.
 constexpr uint32_t kHist16FlushTiles = 12;
+static_assert(kHist16FlushTiles * GJ_JOIN_THREADS * GJ_PPT + GJ_JOIN_THREADS * GJ_PPT + (GJ_JOIN_THREADS / 32) * kDirectQueue3Cap < 65536,
+              "16-bit counters between two flushes, direct form");
 // Lookup-table records of one population-3 batch staged in shared memory by the whole warp (stage_records):
 // up to this many 16-byte chunks per warp (the launch plan gives what shared memory has left, JoinParams::
 // stage_chunks).  A batch of 32 records of ~20 words takes ~190 chunks; a batch that needs more than the buffer
@@ -998,10 +1008,10 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
     const uint32_t s_slot = s_q2 + buf * kDirectBufBytes + kChunkPoints * 4u + lane;
     const uint32_t q_packed = ix.qc.packed, q_index_bits = ix.qc.index_bits, q_slow_mark = ix.qc.slow_mark;
 #pragma unroll 1
-    for (uint32_t half = 0; half < kPointsPerThread / 2u; ++half) {  // two rounds, then the drain site
+    for (uint32_t half = 0; half < kPointsPerThread / kDirectRounds; ++half) {  // a few rounds, then the drain site
 #pragma unroll
-      for (uint32_t jj = 0; jj < 2u; ++jj) {
-        const uint32_t j = half * 2u + jj;
+      for (uint32_t jj = 0; jj < kDirectRounds; ++jj) {
+        const uint32_t j = half * kDirectRounds + jj;
         const uint32_t i = base + j * 32u;
         const uint32_t c = lds32(s_code + j * 128u);
         const uint32_t slot = lds8(s_slot + j * 32u);
