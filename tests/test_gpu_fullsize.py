@@ -205,9 +205,13 @@ def _scaled_bundle(config, scale):
     return build_bundles.bundle_file(name)
 
 
-@pytest.mark.parametrize("config,scale,n,mode", [(4, 0.04, 50_000_000, capi.GJ_MODE_APPROX),
-                                                (5, 0.03, 10_000_000, capi.GJ_MODE_EXACT)])
-def test_density_matched_configs_4_and_5(config, scale, n, mode):
+@pytest.mark.parametrize("config,scale,n,mode,opts", [
+    (4, 0.04, 50_000_000, capi.GJ_MODE_APPROX, {}),
+    # the full-size box's regime: shared-memory tier capped at its level (dead there), 16-bit flushed histogram ->
+    # K1 picks its direct form and the sparse refinement by itself, as it does on the 37 GB index
+    (4, 0.04, 50_000_000, capi.GJ_MODE_APPROX, {"dir16_level_max": 17, "hist16": 1}),
+    (5, 0.03, 10_000_000, capi.GJ_MODE_EXACT, {})])
+def test_density_matched_configs_4_and_5(config, scale, n, mode, opts):
     """The regimes of BASELINE configs[3] and configs[4] (run at full size by
     tools/fullsize.py: profiles/fullsize_r01_cfg*.json) on their density-matched
     stand-ins: 1 600 polygons at 1 m with k_max 56 (an id table beyond the
@@ -218,7 +222,9 @@ def test_density_matched_configs_4_and_5(config, scale, n, mode):
     against the reference's own CPU join on a prefix."""
     import torch
     path = _scaled_bundle(config, scale)
-    bundle = join.IndexBundle.load(path, device=0)
+    bundle = join.IndexBundle.load(path, device=0, options=capi.Options(**opts) if opts else None)
+    if opts:
+        assert bundle.info.k1_direct == 1 and bundle.info.link_records > 0
     s = bundle.session()
     polys = None
     pts = synth.points_for(config, n, polys, scale=scale)
@@ -251,7 +257,7 @@ def test_density_matched_configs_4_and_5(config, scale, n, mode):
     from oracle import ref
     if ref.available():
         rb = ref.RefBundle.load(path)
-        m = 1_000_000
+        m = 10_000_000 if opts else 1_000_000
         got, _, _ = s.join_count(pts[:m], mode)
         got_map = {int(bundle.ids[k]): int(got[k]) for k in np.nonzero(got)[0]}
         want = rb.join_exact_count_threads(pts[:m], 8) if mode == capi.GJ_MODE_EXACT else rb.join_count(pts[:m], 8)
