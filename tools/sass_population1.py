@@ -2,7 +2,7 @@
 
     python tools/sass_population1.py > profiles/sass_rNN_k1_population1.txt
 
-Instantiation join_kernel<kIds=true, kStats=false, kDense=true, kLate=false, kStage=false> — the kernel bench.py times.  The
+Instantiation join_kernel<kIds=true, kStats=false, kDense=true, kLate=false, kStage=false, kDirect=false> — the kernel bench.py times.  The
 excerpt runs from the L2 prefetch + the four 16-byte evict-first point loads to the fourth queue append, i.e. the
 straight-line code every point passes through (grid coordinates in two DFMAs, 16-bit tier lookup, histogram
 increment, first-id store, ballot/popc queue append); what follows it in the kernel (queue drains, populations 2
@@ -16,7 +16,7 @@ from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent.parent
 LIB = ROOT / "paper_1802_09488_b200" / "libgeojoin_b200.so"
-KERNEL = "_ZN2gj11join_kernelILb1ELb0ELb1ELb0ELb0EEEvNS_8DevIndexENS_10JoinParamsE"
+KERNEL = "_ZN2gj11join_kernelILb1ELb0ELb1ELb0ELb0ELb0EEEvNS_8DevIndexENS_10JoinParamsE"
 
 
 def main():
