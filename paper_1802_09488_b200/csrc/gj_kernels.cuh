@@ -790,8 +790,8 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
   };
 
   auto drain3 = [&](bool flush) {  // ONE resolve_open site for both queues
-    __syncwarp();
     for (;;) {
+      __syncwarp();  // queue words appended by other lanes — to Q3 by the caller, to Q4 by the batch before — are visible
       const bool deep = kDirect && (q4_count >= 32u || (flush && q3_count == 0u && q4_count != 0u));
       if (!deep && !(q3_count >= 32u || (flush && q3_count))) break;
       uint32_t take, at;
