@@ -270,11 +270,12 @@ def time_device_join(torch, sess, d_pts, n, d_counts, d_first, mode, reps, warmu
 SECONDARY = [
     (3, 1.0, 100_000_000, {},
      "configs[2]: exact join, trained index, 289 polygons, 100 M mixture points, ~1 % on edges / vertices (FULL size)"),
-    (4, 0.04, 40_000_000, {"dir16_level_max": 17, "hist16": 1},
+    (4, 0.04, 40_000_000, {"dir16_level_max": 17, "hist16": 1, "smem_pad": 78700},
      "configs[3] regime on its density-matched 4 % index (1 600 polygons at 1 m, k_max 56; shared-memory tier capped "
-     "at the level the full-size box gets and the 16-bit flushed histogram the full config's 40 000 ids force; the join "
-     "kernel runs its direct form with the sparse refinement of the tier's link cells, as at full size); the "
-     "full 40 000-polygon / 1 B-point run is tools/fullsize.py 4 (profiles/fullsize_r02_cfg4_direct.json)"),
+     "at the level the full-size box gets, the 16-bit flushed histogram the full config's 40 000 ids force, shared "
+     "memory padded to the 154 KB the full config's 80 KB histogram makes it; the join kernel runs its direct form "
+     "with the sparse refinement of the tier's link cells, as at full size); the full 40 000-polygon / 1 B-point "
+     "run is tools/fullsize.py 4 (profiles/fullsize_r02_cfg4_direct_form_final.json)"),
     (5, 0.03, 10_000_000, {},
      "configs[4] regime on its density-matched 3 % index (300 overlapping stars, every probe a lookup-table "
      "record, exact); the full 10 000-star / 500 M-point run is tools/fullsize.py 5 (profiles/fullsize_r02_cfg5.json)"),
