@@ -966,9 +966,9 @@ join_kernel(const __grid_constant__ DevIndex ix, const __grid_constant__ JoinPar
   // register waits for them), and settles them one tile LATER from there, so the gathers' L2 latency hides behind a
   // whole tile of work (issued and consumed in the same tile it was exposed: 1.25 instead of 1.00 ms per 100 M
   // points).  Instead of Q2 a warp has two staging buffers: 128 codes + 128 node slots (the 4 + 4 sub-cell bits
-  // under a link) = 640 bytes each.  Populations 1 and 2 collapse into ~70 instructions;
-  // population 3 is resolve_open as before, except that walks below the queued sub-cell bits wait in a queue of
-  // their own (Q4, see resolve_open).  First ids are written as in the kLate form.
+  // under a link) = 640 bytes each.  Populations 1 and 2 collapse into ~33 instructions per point to issue and ~62
+  // to settle; population 3 is resolve_open as before, except that walks below the queued sub-cell bits wait in a
+  // queue of their own (Q4, see resolve_open).  First ids are written as in the kLate form.
   static_assert(!kDirect || (kLate == kIds && !kStage), "kDirect writes first ids late and does not stage records");
   auto direct_issue = [&](uint32_t tile, uint32_t buf, auto full_tag) {
     constexpr bool kFull = decltype(full_tag)::value;
